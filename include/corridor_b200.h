@@ -1,0 +1,194 @@
+/*
+ * corridor_b200.h — C ABI of the B200-native EI-ZO hot path.
+ *
+ * One shared library (paper_2504_10783_b200/_lib/libcorridor_b200.so) exports
+ * the entry points below.  Signatures use plain pointers, sizes and enums
+ * only (no torch types).  Every call returns an ez_status; nothing is thrown
+ * across the ABI.  ez_last_error() returns a thread-local message for the
+ * last non-OK status.
+ *
+ * Each entry point replaces one interface of the reference Python package
+ * (`corridor`, /root/reference/pkg/src/corridor).  The reference binds no
+ * native code; the ctypes binding a maintainer would add is shown in
+ * INTEGRATION.md and implemented in paper_2504_10783_b200/_native.py.
+ *
+ * Pointer conventions: arguments named d_* are CUDA device pointers (the
+ * Python shim passes torch.Tensor.data_ptr()); h_* are host pointers;
+ * plain structs are read on the host during the call.  `stream` is a
+ * cudaStream_t (NULL = legacy default stream).
+ */
+#ifndef CORRIDOR_B200_H
+#define CORRIDOR_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define EZ_ABI_VERSION 1
+
+/* ---- status codes: mapped 1:1 onto corridor.errors (errors.py:4-64) ---- */
+typedef enum ez_status {
+    EZ_OK = 0,
+    EZ_DIMENSION_MISMATCH = 1,   /* DimensionMismatch                       */
+    EZ_EMPTY_CHORD = 2,          /* EmptyChord       (cpoly.py:167-168)      */
+    EZ_SEED_OUTSIDE = 3,         /* SeedOutside      (cpoly.py:158-159)      */
+    EZ_GRADIENT_UNDEFINED = 4,   /* GradientUndefined (inflation.py:423-424) */
+    EZ_SEGMENT_IN_COLLISION = 5, /* SegmentInCollision (inflation.py:303-310)*/
+    EZ_SEED_OUTSIDE_DOMAIN = 6,  /* SeedOutsideDomain (inflation.py:276-277) */
+    EZ_GRID_MISMATCH = 7,        /* GridMismatch     (drm.py:269-270)        */
+    EZ_INVALID_ARGUMENT = 8,     /* ValueError                               */
+    EZ_CUDA_ERROR = 9,           /* CUDA runtime/driver failure              */
+    EZ_UNSUPPORTED = 10,         /* model feature not implemented natively   */
+    EZ_CAPACITY = 11             /* a device capacity limit was exceeded     */
+} ez_status;
+
+enum { EZ_JOINT_FIXED = 0, EZ_JOINT_REVOLUTE = 1, EZ_JOINT_PRISMATIC = 2 };
+enum { EZ_GEOM_SPHERE = 0, EZ_GEOM_BOX = 1 };
+enum { EZ_F32 = 0, EZ_F64 = 1 };          /* element type / arithmetic precision */
+enum { EZ_RNG_COUNTER = 0, EZ_RNG_PHILOX = 1 };
+
+typedef struct ez_world ez_world;          /* opaque, device-resident */
+typedef struct ez_roadmap ez_roadmap;      /* opaque, device-resident */
+
+/* Robot description (host arrays, read during ez_world_create).
+ * Mirrors world.RobotModel (world.py:122-167): joints in chain order with
+ * joint j's child link j, geometries in link-major global order. */
+typedef struct ez_robot_desc {
+    int32_t dim;                  /* task-space dimension: 2 or 3            */
+    int32_t n_joints;             /* == number of links                      */
+    const int32_t* joint_kind;    /* [n_joints] EZ_JOINT_*                   */
+    const int32_t* joint_parent;  /* [n_joints] parent link, -1 = world      */
+    const double* joint_rot;      /* [n_joints][dim][dim] origin rotation    */
+    const double* joint_trans;    /* [n_joints][dim]      origin translation */
+    const double* joint_axis;     /* [n_joints][dim] axis (zeros if unused)  */
+    int32_t n_geoms;
+    const int32_t* geom_link;     /* [n_geoms] owning link                   */
+    const int32_t* geom_kind;     /* [n_geoms] EZ_GEOM_*                     */
+    const double* geom_rot;       /* [n_geoms][dim][dim] local rotation      */
+    const double* geom_trans;     /* [n_geoms][dim]      local translation   */
+    const double* geom_radius;    /* [n_geoms] sphere radius                 */
+    const double* geom_half;      /* [n_geoms][dim] box half extents         */
+    int32_t n_pairs;
+    const int32_t* pairs;         /* [n_pairs][2] global geometry indices    */
+} ez_robot_desc;
+
+/* Obstacles: static geometry posed in the world plus one voxel map
+ * (world.py:369-391, 441-463).  Voxel i is the sphere of radius
+ * 0.5*side*sqrt(dim) centred at origin + (idx_i + 0.5)*side. */
+typedef struct ez_scene_desc {
+    int32_t n_static;
+    const int32_t* static_kind;   /* [n_static] EZ_GEOM_*                    */
+    const double* static_rot;     /* [n_static][dim][dim]                    */
+    const double* static_trans;   /* [n_static][dim]                         */
+    const double* static_radius;  /* [n_static]                              */
+    const double* static_half;    /* [n_static][dim]                         */
+    int64_t n_voxels;             /* 0 = no voxel map                        */
+    const int32_t* h_voxel_idx;   /* [n_voxels][dim] occupied lattice cells  */
+    const double* voxel_origin;   /* [dim]                                   */
+    double voxel_side;
+} ez_scene_desc;
+
+/* Summary of the device obstacle structure (for tests and benchmarks). */
+typedef struct ez_world_info {
+    int32_t dof, n_links, n_spheres, n_pairs, n_static;
+    int64_t n_voxels;
+    int32_t grid_dims[3];         /* cells of the voxel distance grid        */
+    double cell_side;             /* h = voxel side / subdivision            */
+    int64_t list_entries;         /* candidate-list entries (incl. sentinels)*/
+    int64_t device_bytes;         /* bytes held on the device                */
+} ez_world_info;
+
+/* EI-ZO parameters: inflation.InflationParams (inflation.py:55-95). */
+typedef struct ez_eizo_params {
+    double delta, eps, tau, delta_max, t_col;
+    int32_t n_p, n_f, n_b, n_ms;  /* n_b resolved by the caller (>= 1)      */
+    int32_t n_it;                 /* 0 = unlimited                           */
+} ez_eizo_params;
+
+/* inflation.InflationReport (inflation.py:99-108) + timing. */
+typedef struct ez_eizo_report {
+    int32_t iterations;
+    int32_t hyperplanes_added;
+    int64_t collision_checks;
+    int32_t terminated_by;        /* 0 = test_accepted, 1 = max_iterations   */
+    int32_t n_faces;              /* rows written to A_out/b_out             */
+    double device_ms;             /* GPU time of the whole inflation         */
+} ez_eizo_report;
+
+/* ---------------- library ---------------- */
+int32_t ez_abi_version(void);
+const char* ez_last_error(void);
+int32_t ez_device_count(void);
+/* FP32 FMA throughput of `device` (TFLOP/s), the roofline denominator of the
+ * FP32-bound checker; measured with a dependent-chain-free FMA kernel. */
+int32_t ez_fp32_peak(int32_t device, double* tflops, double* ms);
+
+/* ---------------- world / collision checker ----------------
+ * ez_world_create  replaces CollisionChecker.__init__   (world.py:441-463)
+ * ez_check_batch   replaces CollisionChecker.check_batch (world.py:483-495)
+ * ez_fk_batch      replaces fk_batch                     (world.py:195-223)
+ */
+int32_t ez_world_create(const ez_robot_desc* robot, const ez_scene_desc* scene,
+                        double margin, int32_t device, ez_world** out);
+int32_t ez_world_destroy(ez_world* world);
+int32_t ez_world_get_info(const ez_world* world, ez_world_info* out);
+
+/* Free mask (1 = collision-free) for n configurations.  d_q points at n rows
+ * of `dof` values of type q_dtype with row stride ld (elements).  precision
+ * selects the arithmetic (EZ_F32: parity outside a 1e-5 contact band;
+ * EZ_F64: the reference's FP64 arithmetic). */
+int32_t ez_check_batch(ez_world* world, const void* d_q, int32_t q_dtype, int64_t n,
+                       int64_t ld, uint8_t* d_free, int32_t precision, void* stream);
+/* Same, from host memory: pipelined H2D / kernel / D2H over an internal
+ * pinned ring, synchronous on return.  This is what a ctypes binding of the
+ * numpy-facing check_batch calls. */
+int32_t ez_check_batch_host(ez_world* world, const double* h_q, int64_t n, int64_t ld,
+                            uint8_t* h_free, int32_t precision);
+/* Link frames: d_frames[n][n_links][12] = row-major R (9) then t (3),
+ * embedded in 3-D for planar models. */
+int32_t ez_fk_batch(ez_world* world, const double* d_q, int64_t n, double* d_frames,
+                    void* stream);
+
+/* ---------------- hit-and-run (cpoly.py:127-173) ----------------
+ * count walks of n_ms steps inside {x | A x <= b}; walk i starts at
+ * d_seeds[i % n_seeds] and uses stream (seed, walk_offset + i). */
+int32_t ez_hit_and_run(const double* d_A, const double* d_b, int32_t n_faces, int32_t dim,
+                       const double* d_seeds, int64_t n_seeds, int64_t count, int32_t n_ms,
+                       uint64_t seed, uint64_t walk_offset, int32_t rng, double* d_out,
+                       void* stream);
+
+/* ---------------- EI-ZO (inflation.py:262-325) ----------------
+ * Host inputs: segment endpoints h_v1/h_v2 [dim], domain h_A0 [n_faces0][dim],
+ * h_b0 [n_faces0].  Writes the result polytope to h_A_out/h_b_out (capacity
+ * face_cap rows) and the report.  Samples never leave the device. */
+int32_t ez_inflate_edge(ez_world* world, const double* h_v1, const double* h_v2, int32_t dim,
+                        const double* h_A0, const double* h_b0, int32_t n_faces0,
+                        const ez_eizo_params* params, uint64_t seed, int32_t precision,
+                        int32_t rng, ez_eizo_report* report, double* h_A_out, double* h_b_out,
+                        int32_t face_cap);
+
+/* ---------------- DRM online phase ----------------
+ * ez_voxelize        replaces voxelize_point_cloud (world.py:315-328): unique
+ *                    occupied bins floor((p - origin)/side), lexicographically
+ *                    sorted, written to d_idx_out[*n_out][dim] (capacity = n).
+ * ez_roadmap_create  uploads the CSR voxel->node map (drm.py:108-131).
+ * ez_collision_set   replaces collision_set (drm.py:262-296): d_blocked_bits
+ *                    receives the node bitmap (ceil(n_nodes/32) words),
+ *                    *n_blocked its popcount. */
+int32_t ez_voxelize(const double* d_points, int64_t n, int32_t dim, const double* h_origin,
+                    double side, int32_t* d_idx_out, int64_t* n_out, void* stream);
+int32_t ez_roadmap_create(const int64_t* h_cmap_offsets, const int32_t* h_cmap_ids,
+                          int64_t n_voxels, int64_t n_nodes, int32_t dim,
+                          const double* h_origin, double side, const int32_t* h_extents,
+                          int32_t device, ez_roadmap** out);
+int32_t ez_roadmap_destroy(ez_roadmap* roadmap);
+int32_t ez_collision_set(ez_roadmap* roadmap, const int32_t* d_vox_idx, int64_t n_vox,
+                         const double* h_vmap_origin, double vmap_side, int32_t same_grid,
+                         uint32_t* d_blocked_bits, int64_t* n_blocked, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CORRIDOR_B200_H */

@@ -1,0 +1,245 @@
+"""Generate golden vectors by running the REFERENCE itself — TEST INFRASTRUCTURE.
+
+Imports the read-only reference package from /root/reference/pkg/src (only
+possible in the build container; the GPU box has no /root/reference) and
+writes small fixtures to tests/golden/.  The oracle (oracle/ref.py) and the
+GPU path are both checked against these files.
+
+    PYTHONDONTWRITEBYTECODE=1 python -m oracle.gen_goldens
+"""
+
+from __future__ import annotations
+
+import json
+import sys
+import tempfile
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parents[1]
+GOLDEN = ROOT / "tests" / "golden"
+REF_SRC = Path("/root/reference/pkg/src")
+
+
+def _import_reference():
+    sys.dont_write_bytecode = True
+    if str(REF_SRC) not in sys.path:
+        sys.path.insert(0, str(REF_SRC))
+    import corridor  # noqa: F401
+
+    return corridor
+
+
+def _to_ref_world(world, C):
+    """Convert one of our World objects into a reference World through scene JSON."""
+    from paper_2504_10783_b200.scene import save_scene
+
+    with tempfile.TemporaryDirectory() as td:
+        p = Path(td) / "scene.json"
+        save_scene(p, world)
+        rw = C.world.load_scene(p)
+    if world.vmap is not None:
+        occ = frozenset(map(tuple, world.vmap.index_array().tolist()))
+        rw = rw.with_vmap(C.world.VoxelMap(world.vmap.origin, world.vmap.side, occ))
+    return rw
+
+
+def _oracle_clearance(world, Q, margin=0.0):
+    from oracle.ref import OracleChecker
+
+    return OracleChecker(world, margin).clearance(Q)
+
+
+def gen_checks(C):
+    from paper_2504_10783_b200 import fixtures as fx
+    from paper_2504_10783_b200.scene import VoxelMap, World
+
+    cases = {
+        "franka7": (fx.franka7_world(), 20_000, 0.0),
+        "franka7_m02": (fx.franka7_world(), 5_000, 0.02),
+        "bimanual14": (fx.bimanual14_world(), 4_000, 0.0),
+        "arm3": (fx.arm3_world(), 20_000, 0.0),
+    }
+    # forest scene: discs + reference-voxelised cloud (point robot)
+    centers = fx.forest_centers(7)
+    ref_vm = C.world.voxelize_point_cloud(fx.disc_point_cloud(centers), 0.02, np.array([-5.0, -5.0]))
+    vm = VoxelMap(ref_vm.origin, ref_vm.side, np.array(sorted(ref_vm.occupied), dtype=np.int64))
+    forest = fx.disc_world(centers).with_vmap(vm)
+    cases["forest7"] = (forest, 20_000, 0.0)
+    for name, (world, n, margin) in cases.items():
+        rng = np.random.default_rng(0)
+        lo, hi = world.lower, world.upper
+        Q = rng.uniform(lo, hi, size=(n, len(lo))).astype(np.float32)
+        rw = _to_ref_world(world, C)
+        free = rw.checker(margin=margin).check_batch(Q.astype(np.float64))
+        clr = _oracle_clearance(world, Q.astype(np.float64), margin)
+        extra = {}
+        if name == "forest7":
+            extra["vox_idx"] = vm.index_array()
+        np.savez_compressed(GOLDEN / f"check_{name}.npz", Q=Q, free=free, clearance=clr, margin=margin, **extra)
+        print(f"check_{name}: n={n} free={free.mean():.3f} band(1e-5)={np.mean(np.abs(clr) < 1e-5):.2e}")
+
+
+def gen_fk(C):
+    from paper_2504_10783_b200 import fixtures as fx
+
+    out = {}
+    for name, world in (("franka7", fx.franka7_world(False)), ("bimanual14", fx.bimanual14_world(False)),
+                        ("arm3", fx.arm3_world())):
+        rw = _to_ref_world(world, C)
+        rng = np.random.default_rng(1)
+        Q = rng.uniform(world.lower, world.upper, size=(64, len(world.lower)))
+        rots, trans = C.world.fk_batch(rw.model, Q)
+        out[f"{name}_Q"] = Q
+        out[f"{name}_rot"] = np.stack(rots, axis=1)
+        out[f"{name}_trans"] = np.stack(trans, axis=1)
+    np.savez_compressed(GOLDEN / "fk.npz", **out)
+    print("fk: ok")
+
+
+def _poly7():
+    rng = np.random.default_rng(11)
+    from paper_2504_10783_b200.fixtures import HOME7
+
+    lo = np.array([-2.8973, -1.7628, -2.8973, -3.0718, -2.8973, -0.0175, -2.8973])
+    hi = np.array([2.8973, 1.7628, 2.8973, -0.0698, 2.8973, 3.7525, 2.8973])
+    A = [np.eye(7), -np.eye(7)]
+    b = [hi, -lo]
+    extra_a = rng.normal(size=(8, 7))
+    extra_a /= np.linalg.norm(extra_a, axis=1, keepdims=True)
+    extra_b = extra_a @ HOME7 + rng.uniform(0.2, 0.6, size=8)
+    return np.vstack(A + [extra_a]), np.concatenate(b + [extra_b]), HOME7
+
+
+def gen_hnr(C):
+    cases = {}
+    box2 = C.cpoly.HPolytope.from_bounds(np.zeros(2), np.ones(2))
+    cases["box2"] = (box2, np.array([[0.5, 0.5]]), 2000, 30, 9, 0)
+    box3 = C.cpoly.HPolytope.from_bounds([-2, 0, 1], [3, 4, 2])
+    cases["box3"] = (box3, np.array([[0.0, 2.0, 1.5]]), 600, 15, 77, 0)
+    A7, b7, s7 = _poly7()
+    p7 = C.cpoly.HPolytope(A7, b7)
+    cases["poly7"] = (p7, s7[None, :], 1000, 60, 5, 123)
+    out = {}
+    for name, (poly, seeds, count, n_ms, seed, off) in cases.items():
+        sb = C.cpoly.hit_and_run_sample(poly, seeds, count, n_ms, seed, off)
+        out[f"{name}_A"] = poly.A
+        out[f"{name}_b"] = poly.b
+        out[f"{name}_seeds"] = seeds
+        out[f"{name}_meta"] = np.array([count, n_ms, seed, off], dtype=np.int64)
+        out[f"{name}_X"] = sb.points
+    np.savez_compressed(GOLDEN / "hnr.npz", **out)
+    print("hnr: ok")
+
+
+def gen_inflate(C):
+    from paper_2504_10783_b200 import fixtures as fx
+
+    records = []
+    arm = fx.arm3_world()
+    rarm = _to_ref_world(arm, C)
+    v1, v2 = fx.ARM3_SEGMENT
+    dom = C.cpoly.HPolytope.from_bounds(arm.lower, arm.upper)
+    for seed in (0, 1, 2):
+        rep = C.inflation.inflate_edge(C.inflation.Segment(v1, v2), dom, C.inflation.InflationParams(),
+                                       rarm.checker(), seed=seed)
+        records.append(("arm3", seed, {}, v1, v2, rep))
+    disc_cases = [("disc_0_3", [[0.0, 3.0]], 1.0, 0, {}), ("disc_0_2", [[0.0, 2.0]], 0.6, 11, {}),
+                  ("disc_two", [[0.0, 2.0], [0.0, -2.0]], 0.7, 2, {}),
+                  ("disc_nit", [[0.0, 1.2], [0.0, -1.2], [2.0, 1.2]], 0.5, 5, {"n_it": 1})]
+    for name, centers, radius, seed, kw in disc_cases:
+        w = fx.disc_world(centers, radius)
+        rw = _to_ref_world(w, C)
+        dom2 = C.cpoly.HPolytope.from_bounds([-5, -5], [5, 5])
+        a, bb = np.array([-1.0, 0.0]), np.array([1.0, 0.0])
+        rep = C.inflation.inflate_edge(C.inflation.Segment(a, bb), dom2, C.inflation.InflationParams(**kw),
+                                       rw.checker(), seed=seed)
+        records.append((name, seed, kw, a, bb, rep))
+    out = {}
+    index = []
+    for name, seed, kw, a, bb, rep in records:
+        key = f"{name}_s{seed}"
+        index.append({"key": key, "scene": name, "seed": seed, "params": kw, "iterations": rep.iterations,
+                      "hyperplanes_added": rep.hyperplanes_added, "collision_checks": rep.collision_checks,
+                      "terminated_by": rep.terminated_by})
+        out[f"{key}_A"] = rep.polytope.A
+        out[f"{key}_b"] = rep.polytope.b
+        out[f"{key}_v"] = np.stack([a, bb])
+        print(f"inflate {key}: it={rep.iterations} faces={rep.hyperplanes_added} checks={rep.collision_checks}")
+    out["index"] = np.array(json.dumps(index))
+    np.savez_compressed(GOLDEN / "inflate.npz", **out)
+
+
+def gen_voxelize(C):
+    rng = np.random.default_rng(5)
+    out = {}
+    pts3 = rng.normal(size=(20_000, 3)) * 0.3
+    pts3[:50] = np.round(pts3[:50] / 0.02) * 0.02  # exactly on bin boundaries
+    org3 = np.array([-1.0, -1.0, -1.0])
+    vm3 = C.world.voxelize_point_cloud(pts3, 0.02, org3)
+    out["p3"], out["o3"], out["idx3"] = pts3, org3, np.array(sorted(vm3.occupied), dtype=np.int64)
+    pts2 = rng.uniform(-2, 2, size=(5_000, 2))
+    pts2[:10] = np.array([[1.0, 0.2]] * 10)
+    org2 = np.zeros(2)
+    vm2 = C.world.voxelize_point_cloud(pts2, 0.5, org2)
+    out["p2"], out["o2"], out["idx2"] = pts2, org2, np.array(sorted(vm2.occupied), dtype=np.int64)
+    np.savez_compressed(GOLDEN / "voxelize.npz", **out)
+    print(f"voxelize: {out['idx3'].shape[0]} / {out['idx2'].shape[0]} voxels")
+
+
+def gen_drm(C):
+    from paper_2504_10783_b200 import fixtures as fx
+
+    out = {}
+    # 2-D forest roadmap of the reference tests (test_drm.py:15-23)
+    grid = C.drm.Grid(np.array([-5.0, -5.0]), 0.25, (40, 40))
+    base = C.world.World(C.bench.point_robot_model())
+    d2 = C.drm.build_drm(base.model, base.checker(), base.lower, base.upper, 200, 10, 10.0, 10.0, grid, seed=8)
+    out["f_off"], out["f_ids"] = d2.cmap_offsets, d2.cmap_ids
+    rng = np.random.default_rng(5)
+    maps = []
+    for case in range(20):
+        occ = frozenset((int(rng.integers(0, 40)), int(rng.integers(0, 40))) for _ in range(rng.integers(1, 30)))
+        vm = C.world.VoxelMap(grid.origin, grid.side, occ)
+        blocked = np.array(sorted(C.drm.collision_set(d2, vm).blocked), dtype=np.int64)
+        maps.append((np.array(sorted(occ), dtype=np.int64), grid.origin, grid.side, blocked))
+    fine = C.world.VoxelMap(grid.origin, 0.1, frozenset({(3, 3), (24, 17)}))
+    maps.append((np.array(sorted(fine.occupied), dtype=np.int64), fine.origin, 0.1,
+                 np.array(sorted(C.drm.collision_set(d2, fine).blocked), dtype=np.int64)))
+    for i, (idx, org, side, blocked) in enumerate(maps):
+        out[f"f{i}_idx"], out[f"f{i}_org"], out[f"f{i}_side"], out[f"f{i}_blocked"] = idx, org, side, blocked
+    out["f_nmaps"] = len(maps)
+    # 3-D Franka roadmap on the config-5 grid (small node count)
+    w7 = fx.franka7_world(False)
+    rw7 = _to_ref_world(w7, C)
+    g3 = C.drm.Grid(np.array([-0.75, -1.02, -0.36]), 0.06, (25, 34, 26))
+    d3 = C.drm.build_drm(rw7.model, rw7.checker(), rw7.model.lower, rw7.model.upper, 300, 10, 10.0, 10.0, g3, seed=0)
+    out["g_nodes"], out["g_off"], out["g_ids"] = d3.nodes, d3.cmap_offsets, d3.cmap_ids
+    cloud = fx.cloud10k()
+    pts = cloud.centers()
+    vm_same = C.world.voxelize_point_cloud(pts, 0.06, g3.origin)
+    vm_fine = C.world.voxelize_point_cloud(pts[::7], 0.02, np.array([-1.0, -1.0, 0.0]))
+    for tag, vm in (("same", vm_same), ("fine", vm_fine)):
+        out[f"g_{tag}_idx"] = np.array(sorted(vm.occupied), dtype=np.int64)
+        out[f"g_{tag}_org"], out[f"g_{tag}_side"] = vm.origin, vm.side
+        out[f"g_{tag}_blocked"] = np.array(sorted(C.drm.collision_set(d3, vm).blocked), dtype=np.int64)
+        print(f"drm franka {tag}: {len(vm.occupied)} voxels -> {out[f'g_{tag}_blocked'].shape[0]} blocked")
+    np.savez_compressed(GOLDEN / "drm.npz", **out)
+
+
+def main(which=None):
+    GOLDEN.mkdir(parents=True, exist_ok=True)
+    C = _import_reference()
+    import corridor.bench, corridor.cpoly, corridor.drm, corridor.inflation, corridor.world  # noqa: E401,F401
+
+    steps = {"checks": gen_checks, "fk": gen_fk, "hnr": gen_hnr, "inflate": gen_inflate,
+             "voxelize": gen_voxelize, "drm": gen_drm}
+    for name, fn in steps.items():
+        if which and name not in which:
+            continue
+        fn(C)
+
+
+if __name__ == "__main__":
+    main(sys.argv[1:] or None)

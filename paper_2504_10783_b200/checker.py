@@ -1,0 +1,81 @@
+"""GPU collision checker: the drop-in for ``corridor.world.CollisionChecker``.
+
+Same protocol as the reference (``corridor/world.py:430-501``): ``check``,
+``check_batch`` (True = free, order independent), ``check_segment`` and the
+``calls`` counter (one per configuration passed in).  Every call runs the
+fused FK + collision kernel (``ez_check_batch`` / ``ez_check_batch_host``).
+
+``precision="fp32"`` (default) evaluates kinematics and distances in fp32:
+flags agree with the reference's fp64 oracle wherever the contact distance
+exceeds 1e-5.  ``precision="fp64"`` uses the reference's fp64 arithmetic.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from .errors import DimensionMismatch
+from .native_world import NativeWorld, precision_code
+
+
+def segment_samples(v1, v2, step: float) -> np.ndarray:
+    """ceil(len/step)+1 evenly spaced configurations on conv{v1, v2} (world.py:568-582)."""
+    v1 = np.asarray(v1, dtype=float)
+    v2 = np.asarray(v2, dtype=float)
+    if v1.shape != v2.shape:
+        raise DimensionMismatch("segment endpoints differ in dimension")
+    length = float(np.linalg.norm(v2 - v1))
+    if length == 0.0:
+        return v1[None, :]
+    n = int(np.ceil(length / step))
+    ts = np.linspace(0.0, 1.0, n + 1)
+    return v1[None, :] + ts[:, None] * (v2 - v1)[None, :]
+
+
+class CollisionChecker:
+    """Conservative collision oracle for one world and margin, evaluated on the GPU."""
+
+    def __init__(self, world, margin: float = 0.0, precision: str = "fp32"):
+        self.world = world
+        self.model = world.model
+        self.margin = float(margin)
+        self.precision = precision
+        precision_code(precision)
+        self.calls = 0
+        self._native: NativeWorld | None = None
+
+    @property
+    def native(self) -> NativeWorld:
+        if self._native is None:
+            self._native = NativeWorld(self.model, self.world.static, self.world.vmap, self.margin)
+        return self._native
+
+    def check(self, q) -> bool:
+        return bool(self.check_batch(np.asarray(q, dtype=float)[None, :])[0])
+
+    def check_batch(self, Q):
+        """Free mask of a batch.  numpy in -> numpy bool out; a CUDA tensor in -> CUDA bool tensor out."""
+        if hasattr(Q, "is_cuda") and Q.is_cuda:
+            Qt = Q if Q.dim() == 2 else Q.reshape(1, -1)
+            if Qt.shape[0] == 0:
+                return Qt.new_zeros((0,), dtype=bool)
+            if Qt.shape[1] != self.model.dof:
+                raise DimensionMismatch(
+                    f"batch has {Qt.shape[1]} columns, robot has {self.model.dof} dof")
+            self.calls += int(Qt.shape[0])
+            return self.native.check_device(Qt, precision=self.precision).bool()
+        Q = np.asarray(Q, dtype=float)
+        if Q.ndim != 2:
+            Q = np.atleast_2d(Q)
+        if Q.shape[0] == 0:
+            return np.zeros(0, dtype=bool)
+        if Q.shape[1] != self.model.dof:
+            raise DimensionMismatch(f"batch has {Q.shape[1]} columns, robot has {self.model.dof} dof")
+        self.calls += Q.shape[0]
+        return self.native.check_host(Q, precision=self.precision).view(bool)
+
+    def check_segment(self, v1, v2, step: float) -> bool:
+        """True iff every sample at spacing <= step (endpoints included) is free."""
+        if step <= 0.0:
+            raise ValueError("step must be positive")
+        return bool(np.all(self.check_batch(segment_samples(v1, v2, step))))

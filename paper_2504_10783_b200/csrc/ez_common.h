@@ -1,0 +1,124 @@
+// ez_common.h — host+device shared definitions for the corridor_b200 library.
+#pragma once
+
+#include <cstdint>
+#include <cstdio>
+#include <string>
+
+#include <cuda_runtime.h>
+
+#include "../../include/corridor_b200.h"
+
+namespace ez {
+
+// ---------------------------------------------------------------------------
+// error plumbing: thread-local last error + status propagation
+// ---------------------------------------------------------------------------
+void set_error(const std::string& msg);
+int32_t fail(int32_t status, const std::string& msg);
+int32_t cuda_fail(cudaError_t err, const char* what, const char* file, int line);
+
+#define EZ_CUDA(call)                                                        \
+    do {                                                                     \
+        cudaError_t _e = (call);                                             \
+        if (_e != cudaSuccess) return ::ez::cuda_fail(_e, #call, __FILE__, __LINE__); \
+    } while (0)
+
+#define EZ_TRY(call)                                                         \
+    do {                                                                     \
+        int32_t _s = (call);                                                 \
+        if (_s != EZ_OK) return _s;                                          \
+    } while (0)
+
+// ---------------------------------------------------------------------------
+// device-side model records.  All kinematics are embedded in 3-D; a planar
+// model is the z = 0 slice (revolute about z, boxes with zero z half-extent).
+//
+// Frames are "modified" frames G_j = (Rg_j, t_j) with the true link frame
+// F_j = (Rg_j * Q_j^T, t_j), where Q_j maps e_z onto joint j's revolute axis.
+// Every child constant is pre-rotated by Q^T on the host, so a revolute
+// motion is always a right-multiplication by Rz(q) (world.py:64-69 Rodrigues
+// rewritten as P Rz(q) P^T).
+// ---------------------------------------------------------------------------
+constexpr int kMaxJoints = 64;
+constexpr int kMaxSpheres = 1024;
+constexpr int kMaxStore = 8;   // links whose frame is reused by a non-consecutive child
+
+template <typename T>
+struct alignas(16) JointRec {
+    T R[9];     // Q_parent^T * R_origin * P_j
+    T t[3];     // Q_parent^T * t_origin
+    T ax[3];    // prismatic axis (joint frame), zeros otherwise
+    int32_t kind;        // EZ_JOINT_*
+    int32_t parent;      // parent link, -1 = world
+    int32_t qidx;        // configuration column, -1 for fixed
+    int32_t store_slot;  // >= 0: save this link's frame for a later child
+    int32_t parent_slot; // >= 0: parent frame comes from this slot
+    int32_t sph_begin, sph_end;  // spheres attached to this link
+    int32_t pad_;
+};
+
+template <typename T>
+struct alignas(16) SphereRec {
+    T p[3];     // Q_link^T * local translation
+    T r;        // radius
+    T rvox;     // (r + r_vox) + margin  (world.py:532)
+    T rmar;     // r + margin            (world.py:535)
+    T pad_[2];
+};
+
+struct alignas(16) GroupRec {   // self pairs grouped by first sphere
+    int32_t a, begin, end, pad_;
+};
+
+template <typename T>
+struct alignas(8) PairRec {     // second sphere + (ra + rb + margin)^2  (world.py:557)
+    int32_t b;
+    int32_t pad_;
+    T thr2;
+};
+
+template <typename T>
+struct alignas(16) StaticSphereRec {  // world.py:449-451, 522-528
+    T c[3];
+    T r;
+};
+
+template <typename T>
+struct alignas(16) StaticBoxRec {     // world.py:394-398, 533-535
+    T Rt[9];    // transposed world rotation
+    T t[3];
+    T he[3];
+    T pad_;
+};
+
+// Voxel-sphere obstacle structure: a uint32 word per cell of a grid of side
+// h = voxel_side / sub aligned with the voxel lattice.  Bits 31..24 hold a
+// floor-quantised nearest-voxel-centre distance q (d(g) in [q dq, (q+1) dq),
+// 255 = farther than the list radius); bits 23..0 the offset of the cell's
+// candidate list (voxel lattice indices sorted by distance to the cell
+// centre, terminated by a +inf sentinel).
+template <typename T>
+struct VoxGrid {
+    const uint32_t* cells;
+    const int4* lists;
+    int32_t n[3];
+    int32_t present;
+    T org[3];       // corner of cell (0,0,0)
+    T h, inv_h;
+    T dq;           // quantisation step
+    T eps;          // rounding guard of the filter (precision dependent)
+    T vorg[3];      // voxel lattice origin
+    T vside;
+};
+
+template <typename T>
+struct ModelDev {
+    const uint8_t* blob;      // device: joints | spheres | groups | pairs | ssph | sbox
+    uint32_t blob_bytes;      // multiple of 16
+    int32_t n_joints, dof, n_spheres, n_groups, n_pairs, n_ssph, n_sbox, n_store;
+    uint32_t off_spheres, off_groups, off_pairs, off_ssph, off_sbox;
+    VoxGrid<T> vox;
+};
+
+}  // namespace ez

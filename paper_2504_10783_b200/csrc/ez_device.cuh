@@ -1,0 +1,286 @@
+// ez_device.cuh — device building blocks of the fused FK + collision check.
+//
+// Reference semantics (corridor/world.py):
+//   fk_batch            195-223   per-joint T_child = T_parent * Origin * Motion(q)
+//   _check_chunk        505-517   OR over robot-vs-obstacle tests and self pairs
+//   _sphere_vs_obstacles 519-536  static spheres, voxel spheres (nearest centre), static boxes
+//   _pair               554-557   sphere-sphere self pairs
+// Touching counts as collision everywhere (<=), the margin enters every
+// radius sum.  T = float (default; parity outside a 1e-5 contact band) or
+// double (the reference's FP64 arithmetic).
+#pragma once
+
+#include "ez_common.h"
+
+namespace ez {
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+// One elected thread moves `bytes` (multiple of 16, 16-B aligned) from global
+// to shared memory with the TMA bulk-copy engine (cp.async.bulk + mbarrier
+// transaction count); every thread of the CTA waits on the barrier.
+__device__ __forceinline__ void tma_stage(void* dst, const void* src, uint32_t bytes,
+                                          uint64_t* bar) {
+    if (threadIdx.x == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
+                     ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+            ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+    }
+    __syncthreads();
+    uint32_t done = 0;
+    while (!done) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(done) : "r"(smem_u32(bar)) : "memory");
+    }
+}
+
+// ---------------------------------------------------------------------------
+// scalar helpers
+// ---------------------------------------------------------------------------
+template <typename T> __device__ __forceinline__ T tsqrt(T x);
+template <> __device__ __forceinline__ float tsqrt<float>(float x) { return sqrtf(x); }
+template <> __device__ __forceinline__ double tsqrt<double>(double x) { return sqrt(x); }
+
+// sin/cos of a joint value.  fp32 arithmetic on an fp64 input keeps the
+// residual q - float(q) as a first-order correction, so rounding the sample
+// to fp32 costs no accuracy.
+template <typename T, typename Q> struct Angle;
+template <> struct Angle<float, float> {
+    __device__ static __forceinline__ void sc(float q, float& s, float& c) { sincosf(q, &s, &c); }
+};
+template <> struct Angle<float, double> {
+    __device__ static __forceinline__ void sc(double q, float& s, float& c) {
+        const float hi = static_cast<float>(q);
+        const float lo = static_cast<float>(q - static_cast<double>(hi));
+        float s0, c0;
+        sincosf(hi, &s0, &c0);
+        s = fmaf(c0, lo, s0);
+        c = fmaf(-s0, lo, c0);
+    }
+};
+template <> struct Angle<double, double> {
+    __device__ static __forceinline__ void sc(double q, double& s, double& c) { sincos(q, &s, &c); }
+};
+template <> struct Angle<double, float> {
+    __device__ static __forceinline__ void sc(float q, double& s, double& c) {
+        sincos(static_cast<double>(q), &s, &c);
+    }
+};
+
+// voxel centre origin + (idx + 0.5) * side, rounded exactly like the
+// reference's numpy expression (world.py:311-312) in fp64 mode.
+__device__ __forceinline__ float lattice_centre(float org, int idx, float side) {
+    return fmaf(static_cast<float>(idx) + 0.5f, side, org);
+}
+__device__ __forceinline__ double lattice_centre(double org, int idx, double side) {
+    return __dadd_rn(org, __dmul_rn(static_cast<double>(idx) + 0.5, side));
+}
+
+// ---------------------------------------------------------------------------
+// forward kinematics: all sphere centres of one configuration
+// ---------------------------------------------------------------------------
+// q: the configuration (dof values, any stride 1 memory), cen: sphere centre
+// store, element (s, k) at cen[(3 s + k) * stride].
+template <typename T, typename Q>
+__device__ __forceinline__ void fk_sphere_centres(const JointRec<T>* __restrict__ J, int nj,
+                                                  const SphereRec<T>* __restrict__ S,
+                                                  const Q* __restrict__ q, T* __restrict__ cen,
+                                                  int stride) {
+    T R[9] = {T(1), T(0), T(0), T(0), T(1), T(0), T(0), T(0), T(1)};
+    T t[3] = {T(0), T(0), T(0)};
+    T store[kMaxStore][12];
+    for (int j = 0; j < nj; ++j) {
+        const JointRec<T>& jr = J[j];
+        if (jr.parent != j - 1) {
+            if (jr.parent < 0) {
+#pragma unroll
+                for (int k = 0; k < 9; ++k) R[k] = (k % 4 == 0) ? T(1) : T(0);
+                t[0] = t[1] = t[2] = T(0);
+            } else {
+#pragma unroll
+                for (int k = 0; k < 9; ++k) R[k] = store[jr.parent_slot][k];
+#pragma unroll
+                for (int k = 0; k < 3; ++k) t[k] = store[jr.parent_slot][9 + k];
+            }
+        }
+        T N[9], tn[3];
+#pragma unroll
+        for (int r = 0; r < 3; ++r) {
+#pragma unroll
+            for (int c = 0; c < 3; ++c)
+                N[3 * r + c] = R[3 * r] * jr.R[c] + R[3 * r + 1] * jr.R[3 + c] + R[3 * r + 2] * jr.R[6 + c];
+            tn[r] = t[r] + (R[3 * r] * jr.t[0] + R[3 * r + 1] * jr.t[1] + R[3 * r + 2] * jr.t[2]);
+        }
+        if (jr.kind == EZ_JOINT_REVOLUTE) {
+            T s, c;
+            Angle<T, Q>::sc(q[jr.qidx], s, c);
+#pragma unroll
+            for (int r = 0; r < 3; ++r) {
+                const T n0 = N[3 * r], n1 = N[3 * r + 1];
+                N[3 * r] = n0 * c + n1 * s;
+                N[3 * r + 1] = n1 * c - n0 * s;
+            }
+        } else if (jr.kind == EZ_JOINT_PRISMATIC) {
+            const T qq = static_cast<T>(q[jr.qidx]);
+#pragma unroll
+            for (int r = 0; r < 3; ++r)
+                tn[r] += (N[3 * r] * jr.ax[0] + N[3 * r + 1] * jr.ax[1] + N[3 * r + 2] * jr.ax[2]) * qq;
+        }
+#pragma unroll
+        for (int k = 0; k < 9; ++k) R[k] = N[k];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) t[k] = tn[k];
+        if (jr.store_slot >= 0) {
+#pragma unroll
+            for (int k = 0; k < 9; ++k) store[jr.store_slot][k] = R[k];
+#pragma unroll
+            for (int k = 0; k < 3; ++k) store[jr.store_slot][9 + k] = t[k];
+        }
+        for (int s = jr.sph_begin; s < jr.sph_end; ++s) {
+            const SphereRec<T>& sp = S[s];
+#pragma unroll
+            for (int r = 0; r < 3; ++r)
+                cen[(3 * s + r) * stride] =
+                    t[r] + (R[3 * r] * sp.p[0] + R[3 * r + 1] * sp.p[1] + R[3 * r + 2] * sp.p[2]);
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// self pairs (world.py:514-516, 554-557)
+// ---------------------------------------------------------------------------
+template <typename T>
+__device__ __forceinline__ bool self_collides(const GroupRec* __restrict__ G, int ng,
+                                              const PairRec<T>* __restrict__ P,
+                                              const T* __restrict__ cen, int stride) {
+    for (int g = 0; g < ng; ++g) {
+        const GroupRec gr = G[g];
+        const T ax = cen[(3 * gr.a) * stride], ay = cen[(3 * gr.a + 1) * stride],
+                az = cen[(3 * gr.a + 2) * stride];
+        for (int p = gr.begin; p < gr.end; ++p) {
+            const PairRec<T> pr = P[p];
+            const T dx = ax - cen[(3 * pr.b) * stride];
+            const T dy = ay - cen[(3 * pr.b + 1) * stride];
+            const T dz = az - cen[(3 * pr.b + 2) * stride];
+            if (dx * dx + dy * dy + dz * dz <= pr.thr2) return true;
+        }
+    }
+    return false;
+}
+
+// ---------------------------------------------------------------------------
+// voxel spheres: "nearest voxel centre within r + r_vox + margin"
+// (world.py:529-532), answered exactly through the quantised distance grid
+// ---------------------------------------------------------------------------
+template <typename T>
+__device__ __forceinline__ bool voxel_hit(const VoxGrid<T>& V, T px, T py, T pz, T R) {
+    const T fx = (px - V.org[0]) * V.inv_h;
+    const T fy = (py - V.org[1]) * V.inv_h;
+    const T fz = (pz - V.org[2]) * V.inv_h;
+    if (!(fx >= T(0) && fy >= T(0) && fz >= T(0) && fx < T(V.n[0]) && fy < T(V.n[1]) &&
+          fz < T(V.n[2])))
+        return false;  // outside the grid: farther than the list radius from every voxel
+    const int ix = static_cast<int>(fx), iy = static_cast<int>(fy), iz = static_cast<int>(fz);
+    const T gx = V.org[0] + (T(ix) + T(0.5)) * V.h;
+    const T gy = V.org[1] + (T(iy) + T(0.5)) * V.h;
+    const T gz = V.org[2] + (T(iz) + T(0.5)) * V.h;
+    const T ex = px - gx, ey = py - gy, ez_ = pz - gz;
+    const T e = tsqrt<T>(ex * ex + ey * ey + ez_ * ez_);
+    const uint32_t w =
+        __ldg(V.cells + (static_cast<int64_t>(iz) * V.n[1] + iy) * V.n[0] + ix);
+    const uint32_t qc = w >> 24;
+    const T lo = T(qc) * V.dq;
+    if (lo - e > R + V.eps) return false;                          // certainly free
+    if (qc < 255u && lo + V.dq + e <= R - V.eps) return true;      // certainly hit
+    const int4* __restrict__ L = V.lists + (w & 0x00FFFFFFu);
+    const T lim = R + e + V.eps;
+    const T R2 = R * R;
+    for (;;) {
+        const int4 E = __ldg(L);
+        ++L;
+        if (static_cast<T>(__int_as_float(E.w)) > lim) return false;
+        const T dx = px - lattice_centre(V.vorg[0], E.x, V.vside);
+        const T dy = py - lattice_centre(V.vorg[1], E.y, V.vside);
+        const T dz = pz - lattice_centre(V.vorg[2], E.z, V.vside);
+        if (dx * dx + dy * dy + dz * dz <= R2) return true;
+    }
+}
+
+template <typename T>
+__device__ __forceinline__ bool sphere_hits_obstacles(const ModelDev<T>& M,
+                                                      const SphereRec<T>& sp,
+                                                      const StaticSphereRec<T>* __restrict__ SS,
+                                                      const StaticBoxRec<T>* __restrict__ SB,
+                                                      T margin, T px, T py, T pz) {
+    for (int i = 0; i < M.n_ssph; ++i) {
+        const StaticSphereRec<T> o = SS[i];
+        const T dx = px - o.c[0], dy = py - o.c[1], dz = pz - o.c[2];
+        const T rr = (o.r + sp.r) + margin;
+        if (dx * dx + dy * dy + dz * dz <= rr * rr) return true;
+    }
+    if (M.vox.present && voxel_hit<T>(M.vox, px, py, pz, sp.rvox)) return true;
+    for (int i = 0; i < M.n_sbox; ++i) {
+        const StaticBoxRec<T>& b = SB[i];
+        const T dx = px - b.t[0], dy = py - b.t[1], dz = pz - b.t[2];
+        T d2 = T(0);
+#pragma unroll
+        for (int r = 0; r < 3; ++r) {
+            const T l = b.Rt[3 * r] * dx + b.Rt[3 * r + 1] * dy + b.Rt[3 * r + 2] * dz;
+            const T cl = fmin(fmax(l, -b.he[r]), b.he[r]);
+            d2 += (l - cl) * (l - cl);
+        }
+        if (d2 <= sp.rmar * sp.rmar) return true;
+    }
+    return false;
+}
+
+// Everything about one configuration whose sphere centres are in `cen`.
+template <typename T>
+__device__ __forceinline__ bool config_collides(const ModelDev<T>& M, const uint8_t* blob,
+                                                const T* __restrict__ cen, int stride, T margin) {
+    const SphereRec<T>* S = reinterpret_cast<const SphereRec<T>*>(blob + M.off_spheres);
+    const GroupRec* G = reinterpret_cast<const GroupRec*>(blob + M.off_groups);
+    const PairRec<T>* P = reinterpret_cast<const PairRec<T>*>(blob + M.off_pairs);
+    if (self_collides<T>(G, M.n_groups, P, cen, stride)) return true;
+    const StaticSphereRec<T>* SS = reinterpret_cast<const StaticSphereRec<T>*>(blob + M.off_ssph);
+    const StaticBoxRec<T>* SB = reinterpret_cast<const StaticBoxRec<T>*>(blob + M.off_sbox);
+    for (int s = 0; s < M.n_spheres; ++s) {
+        if (sphere_hits_obstacles<T>(M, S[s], SS, SB, margin, cen[(3 * s) * stride],
+                                     cen[(3 * s + 1) * stride], cen[(3 * s + 2) * stride]))
+            return true;
+    }
+    return false;
+}
+
+// Full check of one configuration q (dof values).  Returns true if free.
+template <typename T, typename Q>
+__device__ __forceinline__ bool config_free(const ModelDev<T>& M, const uint8_t* blob,
+                                            const Q* q, T* cen, int stride, T margin) {
+    const JointRec<T>* J = reinterpret_cast<const JointRec<T>*>(blob);
+    const SphereRec<T>* S = reinterpret_cast<const SphereRec<T>*>(blob + M.off_spheres);
+    fk_sphere_centres<T, Q>(J, M.n_joints, S, q, cen, stride);
+    return !config_collides<T>(M, blob, cen, stride, margin);
+}
+
+// Dynamic shared memory of a checking CTA: blob | sphere centres | staged rows.
+template <typename T>
+__host__ __device__ inline size_t check_smem_bytes(uint32_t blob_bytes, int n_spheres, int threads,
+                                                   int row_bytes) {
+    size_t b = blob_bytes;
+    b += static_cast<size_t>(3) * n_spheres * threads * sizeof(T);
+    b = (b + 15) & ~static_cast<size_t>(15);
+    b += static_cast<size_t>(threads) * row_bytes;
+    return (b + 15) & ~static_cast<size_t>(15);
+}
+
+}  // namespace ez

@@ -1,0 +1,709 @@
+// ez_eizo.cu — hit-and-run sampling and the device-resident EI-ZO loop.
+//
+// Reference (corridor/cpoly.py, corridor/inflation.py):
+//   hit_and_run_sample  cpoly.py:141-173 (+ _chords 127-138)      -> k_hnr
+//   inflate_edge        inflation.py:262-325                      -> ez_inflate_edge
+//     first-N_p colliding samples by index  :300-301              -> k_compact
+//     project_batch + fail-fast check + _bisection_batch :302-310 -> k_bisect
+//     _place_hyperplanes + compute_step_back :203-259             -> k_place
+// Samples, candidates and faces stay in device memory; the host reads one
+// 32-byte status record per iteration.
+#include <algorithm>
+#include <climits>
+#include <cmath>
+#include <vector>
+
+#include "ez_device.cuh"
+#include "ez_rng.cuh"
+#include "ez_world.h"
+
+namespace ez {
+
+constexpr double kMemberTol = 1e-9;   // cpoly.py:19 MEMBER_TOL
+constexpr double kChordMask = 1e-14;  // cpoly.py:134-135
+constexpr double kChordTol = 1e-12;   // cpoly.py:167
+
+// ---------------------------------------------------------------------------
+// hit-and-run walk (one thread = one walk)
+// ---------------------------------------------------------------------------
+template <int MAXD, int RNG>
+__device__ __forceinline__ int hnr_walk(double (&x)[MAXD], int d, const double* __restrict__ A,
+                                        const double* __restrict__ b, int F, int n_ms, uint64_t seed,
+                                        uint64_t walk, bool check_seed) {
+    const uint64_t key = (RNG == EZ_RNG_COUNTER) ? walk_key(seed, walk) : 0ull;
+    for (int step = 0; step < n_ms; ++step) {
+        double dir[MAXD];
+        if (RNG == EZ_RNG_COUNTER) {
+#pragma unroll
+            for (int k = 0; k < MAXD; ++k) dir[k] = (k < d) ? counter_normal(key, step, k) : 0.0;
+        } else {
+#pragma unroll
+            for (int g = 0; g < (MAXD + 3) / 4; ++g) {
+                if (4 * g < d) {
+                    const Philox4 r = philox_draw(seed, walk, static_cast<uint32_t>(step), g);
+                    float n0, n1, n2, n3;
+                    box_muller(r.x, r.y, n0, n1);
+                    box_muller(r.z, r.w, n2, n3);
+                    const float nn[4] = {n0, n1, n2, n3};
+#pragma unroll
+                    for (int k = 0; k < 4; ++k)
+                        if (4 * g + k < MAXD) dir[4 * g + k] = (4 * g + k < d) ? static_cast<double>(nn[k]) : 0.0;
+                }
+            }
+        }
+        // normalise like numpy (squares rounded, left-to-right sum, IEEE divide)
+        double ss = 0.0;
+#pragma unroll
+        for (int k = 0; k < MAXD; ++k)
+            if (k < d) ss = __dadd_rn(ss, __dmul_rn(dir[k], dir[k]));
+        const double nrm = sqrt(ss);
+#pragma unroll
+        for (int k = 0; k < MAXD; ++k)
+            if (k < d) dir[k] = dir[k] / nrm;
+        double thi = INFINITY, tlo = -INFINITY;
+        for (int f = 0; f < F; ++f) {
+            const double* a = A + static_cast<int64_t>(f) * d;
+            double g = 0.0, h = 0.0;
+#pragma unroll
+            for (int k = 0; k < MAXD; ++k) {
+                if (k < d) {
+                    const double ak = __ldg(a + k);
+                    g = fma(ak, x[k], g);
+                    h = fma(ak, dir[k], h);
+                }
+            }
+            const double sl = __ldg(b + f) - g;
+            if (check_seed && step == 0 && -sl > kMemberTol) return EZ_SEED_OUTSIDE;
+            if (h > kChordMask) thi = fmin(thi, sl / h);
+            else if (h < -kChordMask) tlo = fmax(tlo, sl / h);
+        }
+        if (thi < tlo - kChordTol) return EZ_EMPTY_CHORD;
+        tlo = fmin(tlo, 0.0);
+        thi = fmax(thi, 0.0);
+        double u;
+        if (RNG == EZ_RNG_COUNTER) {
+            u = counter_uniform(key, step, d);
+        } else {
+            const Philox4 r = philox_draw(seed, walk, static_cast<uint32_t>(step), (d + 3) / 4);
+            u = philox_u53(r.x, r.y);
+        }
+        const double tt = __dadd_rn(tlo, __dmul_rn(u, thi - tlo));
+#pragma unroll
+        for (int k = 0; k < MAXD; ++k)
+            if (k < d) x[k] = __dadd_rn(x[k], __dmul_rn(dir[k], tt));
+    }
+    return EZ_OK;
+}
+
+__device__ __forceinline__ void set_status(int32_t* status, int32_t code) {
+    if (code != EZ_OK) atomicCAS(status, 0, code);
+}
+
+// Walk i starts at seeds[i % n_seeds] (explicit seeds) or at a point of the
+// segment v1 + alpha * e drawn from the (seed, walk, SEED_STEP) stream
+// (inflation.py:288-290).  F is read from F_dev when given (EI-ZO loop).
+template <int MAXD, int RNG>
+__global__ void __launch_bounds__(128)
+k_hnr(const double* __restrict__ A, const double* __restrict__ b, const int32_t* __restrict__ F_dev, int F,
+      int d, const double* __restrict__ seeds, int64_t n_seeds, const double* __restrict__ seg,
+      const int64_t* __restrict__ n_dev, int64_t count, int n_ms, uint64_t seed, uint64_t walk_offset,
+      double* __restrict__ out, int32_t* __restrict__ status) {
+    if (F_dev) F = *F_dev;
+    if (n_dev) count = *n_dev;
+    if (*status != EZ_OK) return;
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= count) return;
+    const uint64_t walk = walk_offset + static_cast<uint64_t>(i);
+    double x[MAXD];
+    if (seeds) {
+        const double* s = seeds + (i % n_seeds) * d;
+#pragma unroll
+        for (int k = 0; k < MAXD; ++k) x[k] = (k < d) ? s[k] : 0.0;
+    } else {
+        double alpha;
+        if (RNG == EZ_RNG_COUNTER) {
+            alpha = counter_uniform(walk_key(seed, walk), kSeedStep, 0);
+        } else {
+            const Philox4 r = philox_draw(seed, walk, kPhiloxSeedStep, 0);
+            alpha = philox_u53(r.x, r.y);
+        }
+#pragma unroll
+        for (int k = 0; k < MAXD; ++k) x[k] = (k < d) ? __dadd_rn(seg[k], __dmul_rn(alpha, seg[d + k])) : 0.0;
+    }
+    const int st = hnr_walk<MAXD, RNG>(x, d, A, b, F, n_ms, seed, walk, seeds == nullptr);
+    if (st != EZ_OK) {
+        set_status(status, st);
+        return;
+    }
+    double* o = out + i * d;
+#pragma unroll
+    for (int k = 0; k < MAXD; ++k)
+        if (k < d) o[k] = x[k];
+}
+
+// reference contains_many over all explicit seeds (cpoly.py:158-159)
+__global__ void k_seed_check(const double* __restrict__ A, const double* __restrict__ b, int F, int d,
+                             const double* __restrict__ seeds, int64_t n_seeds, int32_t* __restrict__ status) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n_seeds) return;
+    double worst = -INFINITY;
+    for (int f = 0; f < F; ++f) {
+        double g = 0.0;
+        for (int k = 0; k < d; ++k) g = fma(A[f * d + k], seeds[i * d + k], g);
+        worst = fmax(worst, g - b[f]);
+    }
+    if (!(worst <= kMemberTol)) set_status(status, EZ_SEED_OUTSIDE);
+}
+
+// ---------------------------------------------------------------------------
+// EI-ZO iteration kernels
+// ---------------------------------------------------------------------------
+// status record shared with the host (one 32-byte copy per iteration)
+enum : int { kColM = 0, kNumCand = 1, kStatus = 2, kPlaced = 3, kAccept = 4, kFaces = 5 };
+
+// order-preserving compaction of the first n_p colliding sample indices and
+// the acceptance decision of the unadaptive test (inflation.py:164-172, 294-301)
+__global__ void __launch_bounds__(1024)
+k_compact(const uint8_t* __restrict__ free_flags, int64_t n, int n_p, double thr, int32_t* __restrict__ rec,
+          int32_t* __restrict__ col) {
+    __shared__ int warp_tot[32];
+    __shared__ int warp_off[32];
+    __shared__ int s_total;
+    if (rec[kStatus] != EZ_OK) return;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const bool accept = static_cast<double>(rec[kColM]) <= thr;
+    if (threadIdx.x == 0) rec[kAccept] = accept ? 1 : 0;
+    if (accept) return;
+    int run = 0;
+    for (int64_t base = 0; base < n && run < n_p; base += blockDim.x) {
+        const int64_t i = base + threadIdx.x;
+        const bool f = (i < n) && free_flags[i] == 0;
+        const unsigned m = __ballot_sync(0xffffffffu, f);
+        const int pre = __popc(m & ((1u << lane) - 1u));
+        if (lane == 0) warp_tot[wid] = __popc(m);
+        __syncthreads();
+        if (wid == 0) {
+            const int nw = blockDim.x >> 5;
+            int v = lane < nw ? warp_tot[lane] : 0;
+            int incl = v;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += y;
+            }
+            warp_off[lane] = incl - v;
+            if (lane == 31) s_total = incl;
+        }
+        __syncthreads();
+        const int pos = run + warp_off[wid] + pre;
+        if (f && pos < n_p) col[pos] = static_cast<int32_t>(i);
+        run += s_total;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) rec[kNumCand] = min(run, n_p);
+}
+
+// project_batch for one point (inflation.py:297-310)
+template <int MAXD>
+__device__ __forceinline__ double project(const double (&c)[MAXD], int d, const double* __restrict__ v1,
+                                          const double* __restrict__ e, double ee, double (&p)[MAXD]) {
+    double alpha = 0.0;
+    if (ee != 0.0) {
+        double dot = 0.0;
+#pragma unroll
+        for (int k = 0; k < MAXD; ++k)
+            if (k < d) dot = fma(c[k] - v1[k], e[k], dot);
+        alpha = fmin(fmax(dot / ee, 0.0), 1.0);
+    }
+    double ss = 0.0;
+#pragma unroll
+    for (int k = 0; k < MAXD; ++k) {
+        if (k < d) {
+            p[k] = __dadd_rn(v1[k], __dmul_rn(alpha, e[k]));
+            const double r = c[k] - p[k];
+            ss = fma(r, r, ss);
+        }
+    }
+    return sqrt(ss);
+}
+
+// One thread per candidate: project, fail-fast check of the projection, N_b
+// bisection rounds (each a full FK + collision check), t_col guard.
+template <typename T, int MAXD>
+__global__ void __launch_bounds__(128)
+k_bisect(ModelDev<T> M, T margin, const double* __restrict__ X, int d, const int32_t* __restrict__ col,
+         int32_t* __restrict__ rec, const double* __restrict__ seg, double ee, int n_b, double t_col,
+         double* __restrict__ star, double* __restrict__ pstar, double* __restrict__ dstar) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    __shared__ uint64_t bar;
+    const int C = rec[kNumCand];
+    if (rec[kStatus] != EZ_OK || rec[kAccept] || static_cast<int64_t>(blockIdx.x) * blockDim.x >= C) return;
+    tma_stage(smem, M.blob, M.blob_bytes, &bar);
+    T* cen = reinterpret_cast<T*>(smem + M.blob_bytes);
+    const size_t roff = (static_cast<size_t>(M.blob_bytes) +
+                         static_cast<size_t>(3) * M.n_spheres * blockDim.x * sizeof(T) + 15) & ~static_cast<size_t>(15);
+    double* row = reinterpret_cast<double*>(smem + roff) + threadIdx.x * d;
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= C) return;
+    const double* v1 = seg;
+    const double* e = seg + d;
+    double c[MAXD], lo[MAXD], hi[MAXD];
+    const double* xc = X + static_cast<int64_t>(col[i]) * d;
+#pragma unroll
+    for (int k = 0; k < MAXD; ++k) c[k] = (k < d) ? xc[k] : 0.0;
+    project<MAXD>(c, d, v1, e, ee, lo);
+#pragma unroll
+    for (int k = 0; k < MAXD; ++k) {
+        hi[k] = c[k];
+        if (k < d) row[k] = lo[k];
+    }
+    if (!config_free<T, double>(M, smem, row, cen + threadIdx.x, blockDim.x, margin)) {
+        set_status(rec + kStatus, EZ_SEGMENT_IN_COLLISION);  // inflation.py:303-305
+        return;
+    }
+    for (int r = 0; r < n_b; ++r) {
+        double mid[MAXD];
+#pragma unroll
+        for (int k = 0; k < MAXD; ++k) {
+            mid[k] = 0.5 * (lo[k] + hi[k]);
+            if (k < d) row[k] = mid[k];
+        }
+        const bool fr = config_free<T, double>(M, smem, row, cen + threadIdx.x, blockDim.x, margin);
+#pragma unroll
+        for (int k = 0; k < MAXD; ++k) {
+            if (fr) lo[k] = mid[k];
+            else hi[k] = mid[k];
+        }
+    }
+    double ps[MAXD];
+    const double ds = project<MAXD>(hi, d, v1, e, ee, ps);
+    if (ds <= t_col) set_status(rec + kStatus, EZ_SEGMENT_IN_COLLISION);  // inflation.py:307-310
+#pragma unroll
+    for (int k = 0; k < MAXD; ++k) {
+        if (k < d) {
+            star[static_cast<int64_t>(i) * d + k] = hi[k];
+            pstar[static_cast<int64_t>(i) * d + k] = ps[k];
+        }
+    }
+    dstar[i] = ds;
+}
+
+// Greedy hyperplane placement on one CTA (inflation.py:232-259): the closest
+// alive candidate (stable order == lexicographic (dist, index)) becomes a
+// tangent face pushed back by compute_step_back; candidates outside die.
+__global__ void __launch_bounds__(1024)
+k_place(double* __restrict__ A, double* __restrict__ b, int32_t* __restrict__ rec, int d,
+        const double* __restrict__ star, const double* __restrict__ pstar, const double* __restrict__ dstar,
+        const double* __restrict__ seg, double delta_max, int n_f) {
+    extern __shared__ uint8_t alive[];
+    __shared__ double s_bd[32];
+    __shared__ int s_bi[32];
+    __shared__ double s_a[32];
+    __shared__ double s_rhs;
+    __shared__ int s_best;
+    if (rec[kStatus] != EZ_OK || rec[kAccept]) return;
+    const int C = rec[kNumCand];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    for (int i = threadIdx.x; i < C; i += blockDim.x) alive[i] = 1;
+    int F = rec[kFaces];
+    int placed = 0;
+    const double* v1 = seg;
+    const double* e = seg + d;
+    for (int r = 0; r < n_f; ++r) {
+        __syncthreads();
+        double bd = INFINITY;
+        int bi = INT_MAX;
+        for (int i = threadIdx.x; i < C; i += blockDim.x) {
+            if (!alive[i]) continue;
+            const double di = dstar[i];
+            if (di < bd || (di == bd && i < bi)) {
+                bd = di;
+                bi = i;
+            }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const double od = __shfl_down_sync(0xffffffffu, bd, o);
+            const int oi = __shfl_down_sync(0xffffffffu, bi, o);
+            if (od < bd || (od == bd && oi < bi)) {
+                bd = od;
+                bi = oi;
+            }
+        }
+        if (lane == 0) {
+            s_bd[wid] = bd;
+            s_bi[wid] = bi;
+        }
+        __syncthreads();
+        if (wid == 0) {
+            const int nw = blockDim.x >> 5;
+            bd = lane < nw ? s_bd[lane] : INFINITY;
+            bi = lane < nw ? s_bi[lane] : INT_MAX;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                const double od = __shfl_down_sync(0xffffffffu, bd, o);
+                const int oi = __shfl_down_sync(0xffffffffu, bi, o);
+                if (od < bd || (od == bd && oi < bi)) {
+                    bd = od;
+                    bi = oi;
+                }
+            }
+            if (lane == 0) {
+                int best = (bi == INT_MAX) ? -1 : bi;
+                if (best >= 0) {
+                    const double dist = dstar[best];
+                    if (dist <= 1e-12) {
+                        set_status(rec + kStatus, EZ_GRADIENT_UNDEFINED);  // inflation.py:423-424
+                        best = -1;
+                    } else {
+                        const double* cs = star + static_cast<int64_t>(best) * d;
+                        const double* cp = pstar + static_cast<int64_t>(best) * d;
+                        double braw = 0.0, av1 = 0.0, av2 = 0.0, nn = 0.0;
+                        for (int k = 0; k < d; ++k) {
+                            const double ak = (cs[k] - cp[k]) / dist;
+                            s_a[k] = ak;
+                            braw = fma(ak, cs[k], braw);
+                            av1 = fma(ak, v1[k], av1);
+                            av2 = fma(ak, v1[k] + e[k], av2);
+                            nn = fma(ak, ak, nn);
+                        }
+                        // compute_step_back (inflation.py:203-212)
+                        const double rr = (fmax(av1, av2) - braw) + delta_max;
+                        const double delta = rr > 0.0 ? delta_max - rr : delta_max;
+                        double rhs = braw - delta;
+                        // HPolytope row normalisation (cpoly.py:32-38)
+                        const double norm = sqrt(nn);
+                        if (fabs(norm - 1.0) > 1e-12) {
+                            for (int k = 0; k < d; ++k) s_a[k] /= norm;
+                            rhs /= norm;
+                        }
+                        s_rhs = rhs;
+                        for (int k = 0; k < d; ++k) A[static_cast<int64_t>(F) * d + k] = s_a[k];
+                        b[F] = rhs;
+                    }
+                }
+                s_best = best;
+            }
+        }
+        __syncthreads();
+        if (s_best < 0) break;
+        ++F;
+        ++placed;
+        const double rhs = s_rhs;
+        for (int i = threadIdx.x; i < C; i += blockDim.x) {
+            if (!alive[i]) continue;
+            const double* t = star + static_cast<int64_t>(i) * d;
+            double dot = 0.0;
+            for (int k = 0; k < d; ++k) dot = fma(t[k], s_a[k], dot);
+            alive[i] = dot <= rhs;
+        }
+    }
+    if (threadIdx.x == 0) {
+        rec[kFaces] = F;
+        rec[kPlaced] = placed;
+    }
+}
+
+}  // namespace ez
+
+// ---------------------------------------------------------------------------
+// workspace
+// ---------------------------------------------------------------------------
+struct ez_eizo_ws {
+    int32_t d = 0;
+    int64_t n_cap = 0;      // samples
+    int32_t c_cap = 0;      // candidates (n_p)
+    int32_t f_cap = 0;      // faces
+    double* A = nullptr;
+    double* b = nullptr;
+    double* X = nullptr;
+    uint8_t* flags = nullptr;
+    int32_t* col = nullptr;
+    double* star = nullptr;
+    double* pstar = nullptr;
+    double* dstar = nullptr;
+    double* seg = nullptr;  // v1 | e | v2
+    int32_t* rec = nullptr;
+    int32_t* h_rec = nullptr;  // pinned
+    cudaStream_t stream = nullptr;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+};
+
+namespace ez {
+
+void eizo_ws_free(ez_eizo_ws* ws) {
+    if (!ws) return;
+    cudaFree(ws->A);
+    cudaFree(ws->b);
+    cudaFree(ws->X);
+    cudaFree(ws->flags);
+    cudaFree(ws->col);
+    cudaFree(ws->star);
+    cudaFree(ws->pstar);
+    cudaFree(ws->dstar);
+    cudaFree(ws->seg);
+    cudaFree(ws->rec);
+    cudaFreeHost(ws->h_rec);
+    if (ws->stream) cudaStreamDestroy(ws->stream);
+    if (ws->ev0) cudaEventDestroy(ws->ev0);
+    if (ws->ev1) cudaEventDestroy(ws->ev1);
+    delete ws;
+}
+
+template <typename Tp>
+static int32_t grow(Tp** p, int64_t old_n, int64_t new_n, bool keep) {
+    Tp* q = nullptr;
+    EZ_CUDA(cudaMalloc(&q, sizeof(Tp) * std::max<int64_t>(1, new_n)));
+    if (keep && *p && old_n > 0) EZ_CUDA(cudaMemcpy(q, *p, sizeof(Tp) * old_n, cudaMemcpyDeviceToDevice));
+    cudaFree(*p);
+    *p = q;
+    return EZ_OK;
+}
+
+static int32_t ws_reserve(ez_world* w, int d, int64_t n, int32_t c, int32_t f) {
+    if (!w->eizo) {
+        w->eizo = new ez_eizo_ws();
+        EZ_CUDA(cudaStreamCreateWithFlags(&w->eizo->stream, cudaStreamNonBlocking));
+        EZ_CUDA(cudaEventCreate(&w->eizo->ev0));
+        EZ_CUDA(cudaEventCreate(&w->eizo->ev1));
+        EZ_CUDA(cudaMalloc(&w->eizo->rec, 64));
+        EZ_CUDA(cudaMallocHost(&w->eizo->h_rec, 64));
+        EZ_CUDA(cudaMalloc(&w->eizo->seg, sizeof(double) * 3 * 64));
+    }
+    ez_eizo_ws* ws = w->eizo;
+    if (ws->d != d) {
+        ws->n_cap = ws->c_cap = ws->f_cap = 0;
+        ws->d = d;
+    }
+    if (n > ws->n_cap) {
+        EZ_TRY(grow(&ws->X, 0, n * d, false));
+        EZ_TRY(grow(&ws->flags, 0, n, false));
+        ws->n_cap = n;
+    }
+    if (c > ws->c_cap) {
+        EZ_TRY(grow(&ws->col, 0, c, false));
+        EZ_TRY(grow(&ws->star, 0, static_cast<int64_t>(c) * d, false));
+        EZ_TRY(grow(&ws->pstar, 0, static_cast<int64_t>(c) * d, false));
+        EZ_TRY(grow(&ws->dstar, 0, c, false));
+        ws->c_cap = c;
+    }
+    if (f > ws->f_cap) {
+        EZ_TRY(grow(&ws->A, static_cast<int64_t>(ws->f_cap) * d, static_cast<int64_t>(f) * d, true));
+        EZ_TRY(grow(&ws->b, ws->f_cap, f, true));
+        ws->f_cap = f;
+    }
+    return EZ_OK;
+}
+
+template <int MAXD>
+static int32_t launch_hnr(int rng, unsigned grid, cudaStream_t s, const double* A, const double* b,
+                          const int32_t* F_dev, int F, int d, const double* seeds, int64_t n_seeds,
+                          const double* seg, const int64_t* n_dev, int64_t count, int n_ms, uint64_t seed,
+                          uint64_t walk_offset, double* out, int32_t* status) {
+    if (rng == EZ_RNG_PHILOX)
+        k_hnr<MAXD, EZ_RNG_PHILOX><<<grid, 128, 0, s>>>(A, b, F_dev, F, d, seeds, n_seeds, seg, n_dev, count,
+                                                        n_ms, seed, walk_offset, out, status);
+    else
+        k_hnr<MAXD, EZ_RNG_COUNTER><<<grid, 128, 0, s>>>(A, b, F_dev, F, d, seeds, n_seeds, seg, n_dev, count,
+                                                         n_ms, seed, walk_offset, out, status);
+    EZ_CUDA(cudaGetLastError());
+    return EZ_OK;
+}
+
+static int32_t dispatch_hnr(int rng, unsigned grid, cudaStream_t s, const double* A, const double* b,
+                            const int32_t* F_dev, int F, int d, const double* seeds, int64_t n_seeds,
+                            const double* seg, const int64_t* n_dev, int64_t count, int n_ms, uint64_t seed,
+                            uint64_t walk_offset, double* out, int32_t* status) {
+    if (d <= 4) return launch_hnr<4>(rng, grid, s, A, b, F_dev, F, d, seeds, n_seeds, seg, n_dev, count, n_ms, seed, walk_offset, out, status);
+    if (d <= 8) return launch_hnr<8>(rng, grid, s, A, b, F_dev, F, d, seeds, n_seeds, seg, n_dev, count, n_ms, seed, walk_offset, out, status);
+    if (d <= 16) return launch_hnr<16>(rng, grid, s, A, b, F_dev, F, d, seeds, n_seeds, seg, n_dev, count, n_ms, seed, walk_offset, out, status);
+    if (d <= 32) return launch_hnr<32>(rng, grid, s, A, b, F_dev, F, d, seeds, n_seeds, seg, n_dev, count, n_ms, seed, walk_offset, out, status);
+    return fail(EZ_UNSUPPORTED, "hit-and-run supports dimension <= 32");
+}
+
+template <typename T, int MAXD>
+static int32_t launch_bisect_t(ez_world* w, const ModelDev<T>& M, cudaStream_t s, int n_p, int d, double ee,
+                               int n_b, double t_col) {
+    ez_eizo_ws* ws = w->eizo;
+    const size_t smem = check_smem_bytes<T>(M.blob_bytes, M.n_spheres, 128, d * static_cast<int>(sizeof(double)));
+    auto kern = k_bisect<T, MAXD>;
+    if (smem > 48 * 1024) EZ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    kern<<<static_cast<unsigned>((n_p + 127) / 128), 128, smem, s>>>(M, static_cast<T>(w->margin), ws->X, d, ws->col, ws->rec,
+                                                                  ws->seg, ee, n_b, t_col, ws->star, ws->pstar, ws->dstar);
+    EZ_CUDA(cudaGetLastError());
+    return EZ_OK;
+}
+
+template <int MAXD>
+static int32_t launch_bisect(ez_world* w, int precision, cudaStream_t s, int n_p, int d, double ee, int n_b, double t_col) {
+    if (precision == EZ_F64) return launch_bisect_t<double, MAXD>(w, w->md, s, n_p, d, ee, n_b, t_col);
+    return launch_bisect_t<float, MAXD>(w, w->mf, s, n_p, d, ee, n_b, t_col);
+}
+
+}  // namespace ez
+
+using namespace ez;
+
+extern "C" int32_t ez_hit_and_run(const double* d_A, const double* d_b, int32_t n_faces, int32_t dim,
+                                  const double* d_seeds, int64_t n_seeds, int64_t count, int32_t n_ms,
+                                  uint64_t seed, uint64_t walk_offset, int32_t rng, double* d_out, void* stream) {
+    if (count == 0) return EZ_OK;
+    if (count < 0) return fail(EZ_INVALID_ARGUMENT, "negative count");
+    if (n_ms < 1) return fail(EZ_INVALID_ARGUMENT, "need at least one mixing step");
+    if (dim < 1 || n_faces < 0 || n_seeds < 1) return fail(EZ_INVALID_ARGUMENT, "bad polytope or seed shape");
+    if (rng != EZ_RNG_COUNTER && rng != EZ_RNG_PHILOX) return fail(EZ_INVALID_ARGUMENT, "unknown rng");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    int32_t* d_status = nullptr;
+    EZ_CUDA(cudaMallocAsync(&d_status, sizeof(int32_t), s));
+    EZ_CUDA(cudaMemsetAsync(d_status, 0, sizeof(int32_t), s));
+    k_seed_check<<<static_cast<unsigned>((n_seeds + 127) / 128), 128, 0, s>>>(d_A, d_b, n_faces, dim, d_seeds, n_seeds, d_status);
+    int32_t st = dispatch_hnr(rng, static_cast<unsigned>((count + 127) / 128), s, d_A, d_b, nullptr, n_faces, dim, d_seeds,
+                              n_seeds, nullptr, nullptr, count, n_ms, seed, walk_offset, d_out, d_status);
+    int32_t h_status = 0;
+    if (st == EZ_OK) {
+        cudaError_t e = cudaMemcpyAsync(&h_status, d_status, sizeof(int32_t), cudaMemcpyDeviceToHost, s);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+        if (e != cudaSuccess) st = cuda_fail(e, "hit-and-run status", __FILE__, __LINE__);
+    }
+    cudaFreeAsync(d_status, s);
+    if (st != EZ_OK) return st;
+    if (h_status == EZ_SEED_OUTSIDE) return fail(EZ_SEED_OUTSIDE, "walk seed outside the polytope");
+    if (h_status == EZ_EMPTY_CHORD) return fail(EZ_EMPTY_CHORD, "no feasible chord; polytope numerically degenerate");
+    if (h_status != EZ_OK) return fail(h_status, "hit-and-run failed");
+    return EZ_OK;
+}
+
+// required_batch_size (inflation.py:156-161)
+static int64_t batch_size(int k, const ez_eizo_params& p) {
+    const double pi = 3.14159265358979311599796346854;  // math.pi
+    const double delta_k = 6.0 * p.delta / (pi * pi * (static_cast<double>(k) * k));
+    return static_cast<int64_t>(std::ceil(2.0 * std::log(1.0 / delta_k) / (p.eps * (p.tau * p.tau))));
+}
+
+extern "C" int32_t ez_inflate_edge(ez_world* w, const double* h_v1, const double* h_v2, int32_t dim,
+                                   const double* h_A0, const double* h_b0, int32_t n_faces0,
+                                   const ez_eizo_params* params, uint64_t seed, int32_t precision, int32_t rng,
+                                   ez_eizo_report* report, double* h_A_out, double* h_b_out, int32_t face_cap) {
+    if (!w || !params || !report) return fail(EZ_INVALID_ARGUMENT, "null argument");
+    if (dim != w->dof) return fail(EZ_DIMENSION_MISMATCH, "segment/robot dimension mismatch");
+    if (dim > 32) return fail(EZ_UNSUPPORTED, "EI-ZO supports dimension <= 32");
+    const ez_eizo_params& p = *params;
+    if (p.n_p < 1 || p.n_f < 1 || p.n_b < 1 || p.n_ms < 1) return fail(EZ_INVALID_ARGUMENT, "counts must be >= 1");
+    if (rng != EZ_RNG_COUNTER && rng != EZ_RNG_PHILOX) return fail(EZ_INVALID_ARGUMENT, "unknown rng");
+    std::lock_guard<std::mutex> lock(w->mu);
+    EZ_CUDA(cudaSetDevice(w->device));
+    const int d = dim;
+    // seed segment strictly inside the domain (inflation.py:274-277), fp64 on the host
+    for (int v = 0; v < 2; ++v) {
+        const double* x = v ? h_v2 : h_v1;
+        double worst = -INFINITY;
+        for (int f = 0; f < n_faces0; ++f) {
+            double g = 0.0;
+            for (int k = 0; k < d; ++k) g += h_A0[f * d + k] * x[k];
+            worst = std::max(worst, g - h_b0[f]);
+        }
+        if (worst >= 0.0) return fail(EZ_SEED_OUTSIDE_DOMAIN, "seed segment must be strictly inside the domain");
+    }
+    int64_t n_max = p.n_p;
+    EZ_TRY(ws_reserve(w, d, std::max<int64_t>(n_max, batch_size(1, p)), p.n_p, n_faces0 + 16 * p.n_f));
+    ez_eizo_ws* ws = w->eizo;
+    cudaStream_t s = ws->stream;
+    std::vector<double> seg(3 * d);
+    double ee = 0.0;
+    for (int k = 0; k < d; ++k) {
+        seg[k] = h_v1[k];
+        seg[d + k] = h_v2[k] - h_v1[k];
+        seg[2 * d + k] = h_v2[k];
+        ee += seg[d + k] * seg[d + k];
+    }
+    {  // ee exactly as numpy's e @ e (sequential sum of products)
+        double acc = 0.0;
+        for (int k = 0; k < d; ++k) acc = acc + seg[d + k] * seg[d + k];
+        ee = acc;
+    }
+    EZ_CUDA(cudaMemcpyAsync(ws->seg, seg.data(), sizeof(double) * 3 * d, cudaMemcpyHostToDevice, s));
+    EZ_CUDA(cudaMemcpyAsync(ws->A, h_A0, sizeof(double) * n_faces0 * d, cudaMemcpyHostToDevice, s));
+    EZ_CUDA(cudaMemcpyAsync(ws->b, h_b0, sizeof(double) * n_faces0, cudaMemcpyHostToDevice, s));
+    EZ_CUDA(cudaMemsetAsync(ws->rec, 0, 64, s));
+    {
+        int32_t f0 = n_faces0;
+        EZ_CUDA(cudaMemcpyAsync(ws->rec + kFaces, &f0, sizeof(int32_t), cudaMemcpyHostToDevice, s));
+    }
+    EZ_CUDA(cudaEventRecord(ws->ev0, s));
+    const size_t place_smem = static_cast<size_t>(p.n_p);
+    if (place_smem > 48 * 1024)
+        EZ_CUDA(cudaFuncSetAttribute(k_place, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(std::min<size_t>(place_smem, 200 * 1024))));
+    if (place_smem > 200 * 1024) return fail(EZ_UNSUPPORTED, "n_p above 204800 candidates");
+
+    int F = n_faces0;
+    uint64_t walk_offset = 0;
+    int64_t checks = 0;
+    int32_t hyper = 0;
+    int k = 1;
+    int32_t terminated = 0;
+    for (;; ++k) {
+        const int64_t m = batch_size(k, p);
+        const double thr = static_cast<double>(m) * (1.0 - p.tau) * p.eps;
+        const int64_t n_s = std::max<int64_t>(p.n_p, m);
+        if (n_s > ws->n_cap || F + p.n_f > ws->f_cap) {
+            EZ_CUDA(cudaStreamSynchronize(s));
+            EZ_TRY(ws_reserve(w, d, std::max<int64_t>(n_s, ws->n_cap), p.n_p, std::max(ws->f_cap * 2, F + 16 * p.n_f)));
+        }
+        // reset per-iteration fields (status and face count persist)
+        EZ_CUDA(cudaMemsetAsync(ws->rec + kColM, 0, 2 * sizeof(int32_t), s));
+        EZ_CUDA(cudaMemsetAsync(ws->rec + kPlaced, 0, 2 * sizeof(int32_t), s));
+        EZ_TRY(dispatch_hnr(rng, static_cast<unsigned>((n_s + 127) / 128), s, ws->A, ws->b, ws->rec + kFaces, F, d,
+                            nullptr, 1, ws->seg, nullptr, n_s, p.n_ms, seed, walk_offset, ws->X, ws->rec + kStatus));
+        EZ_TRY(launch_check(w, ws->X, EZ_F64, n_s, d, ws->flags, precision, s, m, ws->rec + kColM));
+        k_compact<<<1, 1024, 0, s>>>(ws->flags, n_s, p.n_p, thr, ws->rec, ws->col);
+        EZ_CUDA(cudaGetLastError());
+        if (d <= 4) EZ_TRY(launch_bisect<4>(w, precision, s, p.n_p, d, ee, p.n_b, p.t_col));
+        else if (d <= 8) EZ_TRY(launch_bisect<8>(w, precision, s, p.n_p, d, ee, p.n_b, p.t_col));
+        else if (d <= 16) EZ_TRY(launch_bisect<16>(w, precision, s, p.n_p, d, ee, p.n_b, p.t_col));
+        else EZ_TRY(launch_bisect<32>(w, precision, s, p.n_p, d, ee, p.n_b, p.t_col));
+        k_place<<<1, 1024, place_smem, s>>>(ws->A, ws->b, ws->rec, d, ws->star, ws->pstar, ws->dstar, ws->seg,
+                                            p.delta_max, p.n_f);
+        EZ_CUDA(cudaGetLastError());
+        EZ_CUDA(cudaMemcpyAsync(ws->h_rec, ws->rec, 32, cudaMemcpyDeviceToHost, s));
+        EZ_CUDA(cudaStreamSynchronize(s));
+        const int32_t* r = ws->h_rec;
+        if (r[kStatus] != EZ_OK) {
+            switch (r[kStatus]) {
+                case EZ_EMPTY_CHORD: return fail(EZ_EMPTY_CHORD, "no feasible chord; polytope numerically degenerate");
+                case EZ_SEED_OUTSIDE: return fail(EZ_SEED_OUTSIDE, "walk seed outside the polytope");
+                case EZ_SEGMENT_IN_COLLISION:
+                    return fail(EZ_SEGMENT_IN_COLLISION, "a projection onto the seed segment, or a bisected collision, "
+                                                         "lies in collision within t_col of the seed segment");
+                case EZ_GRADIENT_UNDEFINED: return fail(EZ_GRADIENT_UNDEFINED, "candidate collapsed onto the segment");
+                default: return fail(r[kStatus], "EI-ZO device failure");
+            }
+        }
+        walk_offset += static_cast<uint64_t>(n_s);
+        checks += n_s;
+        if (r[kAccept]) {
+            terminated = 0;
+            break;
+        }
+        checks += static_cast<int64_t>(r[kNumCand]) * (1 + p.n_b);
+        hyper += r[kPlaced];
+        F = r[kFaces];
+        if (p.n_it > 0 && k >= p.n_it) {
+            terminated = 1;
+            break;
+        }
+    }
+    EZ_CUDA(cudaEventRecord(ws->ev1, s));
+    EZ_CUDA(cudaEventSynchronize(ws->ev1));
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, ws->ev0, ws->ev1);
+    if (F > face_cap) return fail(EZ_CAPACITY, "face_cap smaller than the result polytope");
+    EZ_CUDA(cudaMemcpy(h_A_out, ws->A, sizeof(double) * F * d, cudaMemcpyDeviceToHost));
+    EZ_CUDA(cudaMemcpy(h_b_out, ws->b, sizeof(double) * F, cudaMemcpyDeviceToHost));
+    report->iterations = k;
+    report->hyperplanes_added = hyper;
+    report->collision_checks = checks;
+    report->terminated_by = terminated;
+    report->n_faces = F;
+    report->device_ms = ms;
+    return EZ_OK;
+}

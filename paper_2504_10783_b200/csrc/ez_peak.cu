@@ -1,0 +1,52 @@
+// ez_peak.cu — FP32 FMA throughput microbenchmark: the roofline denominator of
+// the checker (FP32-FMA bound); MEASURED_PEAKS.json carries
+// only HBM and bf16 tensor peaks.
+#include "ez_common.h"
+
+namespace ez {
+
+__global__ void __launch_bounds__(256) k_fma_peak(float* out, int iters, float a, float b) {
+    float x[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) x[k] = threadIdx.x * 1e-3f + k;
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int r = 0; r < 16; ++r) {
+#pragma unroll
+            for (int k = 0; k < 8; ++k) x[k] = fmaf(x[k], a, b);
+        }
+    }
+    float s = 0.f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) s += x[k];
+    if (s == 1234.5f) out[blockIdx.x] = s;  // keep the chain alive
+}
+
+}  // namespace ez
+
+extern "C" int32_t ez_fp32_peak(int32_t device, double* tflops, double* ms_out) {
+    using namespace ez;
+    EZ_CUDA(cudaSetDevice(device));
+    int sms = 0;
+    EZ_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+    float* d = nullptr;
+    EZ_CUDA(cudaMalloc(&d, 4096 * sizeof(float)));
+    cudaEvent_t e0, e1;
+    EZ_CUDA(cudaEventCreate(&e0));
+    EZ_CUDA(cudaEventCreate(&e1));
+    const int blocks = sms * 8, threads = 256, iters = 4096;
+    k_fma_peak<<<blocks, threads>>>(d, 64, 0.999f, 1e-3f);  // warm-up
+    EZ_CUDA(cudaEventRecord(e0));
+    k_fma_peak<<<blocks, threads>>>(d, iters, 0.999f, 1e-3f);
+    EZ_CUDA(cudaEventRecord(e1));
+    EZ_CUDA(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    EZ_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    const double flops = 2.0 * 8 * 16 * static_cast<double>(iters) * blocks * threads;
+    *tflops = flops / (ms * 1e-3) / 1e12;
+    if (ms_out) *ms_out = ms;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFree(d);
+    return EZ_OK;
+}

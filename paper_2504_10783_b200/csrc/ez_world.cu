@@ -1,0 +1,901 @@
+// ez_world.cu — world upload, voxel distance-grid build, fused FK + collision
+// check kernel and batched FK.  Replaces corridor/world.py:
+//   CollisionChecker.__init__   441-463 (ez_world_create)
+//   CollisionChecker.check_batch 483-495 (ez_check_batch / ez_check_batch_host)
+//   fk_batch                    195-223 (ez_fk_batch)
+#include <algorithm>
+#include <climits>
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+#include <type_traits>
+#include <vector>
+
+#include <cub/device/device_scan.cuh>
+
+#include "ez_device.cuh"
+#include "ez_world.h"
+
+namespace ez {
+
+constexpr int kCheckThreads = 128;
+
+// ---------------------------------------------------------------------------
+// host-side model folding
+// ---------------------------------------------------------------------------
+namespace {
+
+struct M3 {
+    double a[9];
+};
+
+M3 mat_eye() {
+    M3 m{};
+    m.a[0] = m.a[4] = m.a[8] = 1.0;
+    return m;
+}
+M3 mat_mul(const M3& x, const M3& y) {
+    M3 r{};
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) {
+            double s = 0.0;
+            for (int k = 0; k < 3; ++k) s += x.a[3 * i + k] * y.a[3 * k + j];
+            r.a[3 * i + j] = s;
+        }
+    return r;
+}
+M3 mat_T(const M3& x) {
+    M3 r{};
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) r.a[3 * i + j] = x.a[3 * j + i];
+    return r;
+}
+void mat_vec(const M3& m, const double* v, double* out) {
+    for (int i = 0; i < 3; ++i) out[i] = m.a[3 * i] * v[0] + m.a[3 * i + 1] * v[1] + m.a[3 * i + 2] * v[2];
+}
+// rotation/translation of a `dim`-dimensional rigid transform embedded in 3-D
+M3 embed_rot(const double* r, int dim) {
+    M3 m = mat_eye();
+    for (int i = 0; i < dim; ++i)
+        for (int j = 0; j < dim; ++j) m.a[3 * i + j] = r[dim * i + j];
+    return m;
+}
+void embed_vec(const double* v, int dim, double* out) {
+    out[0] = out[1] = out[2] = 0.0;
+    for (int i = 0; i < dim; ++i) out[i] = v[i];
+}
+// rotation P = [u v a] with P e_z = a (unit), right handed
+M3 axis_frame(const double* axis) {
+    double a[3] = {axis[0], axis[1], axis[2]};
+    const double n = std::sqrt(a[0] * a[0] + a[1] * a[1] + a[2] * a[2]);
+    for (double& x : a) x /= n;
+    double h[3] = {1.0, 0.0, 0.0};
+    if (std::fabs(a[0]) > 0.9) { h[0] = 0.0; h[1] = 1.0; }
+    const double d = h[0] * a[0] + h[1] * a[1] + h[2] * a[2];
+    double u[3] = {h[0] - d * a[0], h[1] - d * a[1], h[2] - d * a[2]};
+    const double un = std::sqrt(u[0] * u[0] + u[1] * u[1] + u[2] * u[2]);
+    for (double& x : u) x /= un;
+    const double v[3] = {a[1] * u[2] - a[2] * u[1], a[2] * u[0] - a[0] * u[2], a[0] * u[1] - a[1] * u[0]};
+    M3 P{};
+    for (int i = 0; i < 3; ++i) {
+        P.a[3 * i + 0] = u[i];
+        P.a[3 * i + 1] = v[i];
+        P.a[3 * i + 2] = a[i];
+    }
+    return P;
+}
+
+struct HJoint {
+    M3 R;
+    double t[3], ax[3];
+    int kind, parent, qidx, store_slot = -1, parent_slot = -1, sb = 0, se = 0;
+};
+struct HSphere {
+    double p[3], r, rvox, rmar;
+};
+struct HPair {
+    int b;
+    double thr2;
+};
+struct HGroup {
+    int a, begin, end;
+};
+struct HModel {
+    std::vector<HJoint> joints;
+    std::vector<M3> linkQt;
+    std::vector<HSphere> spheres;
+    std::vector<HGroup> groups;
+    std::vector<HPair> pairs;
+    std::vector<double> ssph;  // c3, r
+    std::vector<double> sbox;  // Rt9, t3, he3
+    int dof = 0, n_store = 0;
+};
+
+size_t align16(size_t x) { return (x + 15) & ~static_cast<size_t>(15); }
+
+template <typename T>
+std::vector<uint8_t> pack_blob(const HModel& hm, ModelDev<T>& md) {
+    const size_t sz_j = align16(hm.joints.size() * sizeof(JointRec<T>));
+    const size_t sz_s = align16(hm.spheres.size() * sizeof(SphereRec<T>));
+    const size_t sz_g = align16(hm.groups.size() * sizeof(GroupRec));
+    const size_t sz_p = align16(hm.pairs.size() * sizeof(PairRec<T>));
+    const size_t n_ss = hm.ssph.size() / 4, n_sb = hm.sbox.size() / 15;
+    const size_t sz_ss = align16(n_ss * sizeof(StaticSphereRec<T>));
+    const size_t sz_sb = align16(n_sb * sizeof(StaticBoxRec<T>));
+    std::vector<uint8_t> blob(std::max<size_t>(16, sz_j + sz_s + sz_g + sz_p + sz_ss + sz_sb), 0);
+    md.off_spheres = static_cast<uint32_t>(sz_j);
+    md.off_groups = static_cast<uint32_t>(sz_j + sz_s);
+    md.off_pairs = static_cast<uint32_t>(sz_j + sz_s + sz_g);
+    md.off_ssph = static_cast<uint32_t>(sz_j + sz_s + sz_g + sz_p);
+    md.off_sbox = static_cast<uint32_t>(sz_j + sz_s + sz_g + sz_p + sz_ss);
+    md.blob_bytes = static_cast<uint32_t>(blob.size());
+    auto* J = reinterpret_cast<JointRec<T>*>(blob.data());
+    for (size_t j = 0; j < hm.joints.size(); ++j) {
+        const HJoint& h = hm.joints[j];
+        JointRec<T> r{};
+        for (int k = 0; k < 9; ++k) r.R[k] = static_cast<T>(h.R.a[k]);
+        for (int k = 0; k < 3; ++k) {
+            r.t[k] = static_cast<T>(h.t[k]);
+            r.ax[k] = static_cast<T>(h.ax[k]);
+        }
+        r.kind = h.kind;
+        r.parent = h.parent;
+        r.qidx = h.qidx;
+        r.store_slot = h.store_slot;
+        r.parent_slot = h.parent_slot;
+        r.sph_begin = h.sb;
+        r.sph_end = h.se;
+        J[j] = r;
+    }
+    auto* S = reinterpret_cast<SphereRec<T>*>(blob.data() + md.off_spheres);
+    for (size_t s = 0; s < hm.spheres.size(); ++s) {
+        SphereRec<T> r{};
+        for (int k = 0; k < 3; ++k) r.p[k] = static_cast<T>(hm.spheres[s].p[k]);
+        r.r = static_cast<T>(hm.spheres[s].r);
+        r.rvox = static_cast<T>(hm.spheres[s].rvox);
+        r.rmar = static_cast<T>(hm.spheres[s].rmar);
+        S[s] = r;
+    }
+    auto* G = reinterpret_cast<GroupRec*>(blob.data() + md.off_groups);
+    for (size_t g = 0; g < hm.groups.size(); ++g) G[g] = GroupRec{hm.groups[g].a, hm.groups[g].begin, hm.groups[g].end, 0};
+    auto* P = reinterpret_cast<PairRec<T>*>(blob.data() + md.off_pairs);
+    for (size_t p = 0; p < hm.pairs.size(); ++p) {
+        PairRec<T> r{};
+        r.b = hm.pairs[p].b;
+        r.thr2 = static_cast<T>(hm.pairs[p].thr2);
+        P[p] = r;
+    }
+    auto* SS = reinterpret_cast<StaticSphereRec<T>*>(blob.data() + md.off_ssph);
+    for (size_t i = 0; i < n_ss; ++i) {
+        StaticSphereRec<T> r{};
+        for (int k = 0; k < 3; ++k) r.c[k] = static_cast<T>(hm.ssph[4 * i + k]);
+        r.r = static_cast<T>(hm.ssph[4 * i + 3]);
+        SS[i] = r;
+    }
+    auto* SB = reinterpret_cast<StaticBoxRec<T>*>(blob.data() + md.off_sbox);
+    for (size_t i = 0; i < n_sb; ++i) {
+        StaticBoxRec<T> r{};
+        for (int k = 0; k < 9; ++k) r.Rt[k] = static_cast<T>(hm.sbox[15 * i + k]);
+        for (int k = 0; k < 3; ++k) {
+            r.t[k] = static_cast<T>(hm.sbox[15 * i + 9 + k]);
+            r.he[k] = static_cast<T>(hm.sbox[15 * i + 12 + k]);
+        }
+        SB[i] = r;
+    }
+    md.n_joints = static_cast<int32_t>(hm.joints.size());
+    md.dof = hm.dof;
+    md.n_spheres = static_cast<int32_t>(hm.spheres.size());
+    md.n_groups = static_cast<int32_t>(hm.groups.size());
+    md.n_pairs = static_cast<int32_t>(hm.pairs.size());
+    md.n_ssph = static_cast<int32_t>(n_ss);
+    md.n_sbox = static_cast<int32_t>(n_sb);
+    md.n_store = hm.n_store;
+    return blob;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// voxel distance grid build (fp64, device)
+// ---------------------------------------------------------------------------
+struct GridBuild {
+    int32_t L[3];        // dense lattice dims (padded)
+    int32_t lbase[3];    // lattice index of dense cell 0
+    int32_t n[3];        // cell dims
+    int32_t sub[3];      // cells per voxel side per axis
+    double dq, e_max, r_min, r_max, eps;
+};
+
+__global__ void k_occ_scatter(const int32_t* __restrict__ idx, int64_t n, int dim, GridBuild gb,
+                              uint8_t* __restrict__ occ) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    int c[3] = {0, 0, 0};
+    for (int k = 0; k < dim; ++k) c[k] = idx[i * dim + k] - gb.lbase[k];
+    occ[(static_cast<int64_t>(c[2]) * gb.L[1] + c[1]) * gb.L[0] + c[0]] = 1;
+}
+
+// one thread per cell: nearest occupied voxel (from the distance-sorted offset
+// table of the cell's sub-position) and, where the filter can be ambiguous,
+// the candidate list length.
+template <bool kFill>
+__global__ void k_cells(GridBuild gb, const uint8_t* __restrict__ occ, const int4* __restrict__ tab,
+                        const int32_t* __restrict__ tab_off, uint32_t* __restrict__ cells,
+                        uint32_t* __restrict__ counts, int4* __restrict__ lists) {
+    const int64_t ncell = static_cast<int64_t>(gb.n[0]) * gb.n[1] * gb.n[2];
+    const int64_t ci = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (ci >= ncell) return;
+    const int cx = static_cast<int>(ci % gb.n[0]);
+    const int cy = static_cast<int>((ci / gb.n[0]) % gb.n[1]);
+    const int cz = static_cast<int>(ci / (static_cast<int64_t>(gb.n[0]) * gb.n[1]));
+    const int lx = cx / gb.sub[0], ly = cy / gb.sub[1], lz = cz / gb.sub[2];
+    const int mx = cx % gb.sub[0], my = cy % gb.sub[1], mz = cz % gb.sub[2];
+    const int tsel = (mz * gb.sub[1] + my) * gb.sub[0] + mx;
+    const int4* t = tab + tab_off[tsel];
+    const int tn = tab_off[tsel + 1] - tab_off[tsel];
+    uint32_t q = 255u;
+    bool need = false, first = true;
+    uint32_t cnt = 0;
+    uint32_t out = 0;
+    if (kFill) out = cells[ci] & 0x00FFFFFFu;  // list offset from the scan
+    for (int k = 0; k < tn; ++k) {
+        const int4 e = t[k];
+        const int X = lx + e.x, Y = ly + e.y, Z = lz + e.z;
+        if (X < 0 || Y < 0 || Z < 0 || X >= gb.L[0] || Y >= gb.L[1] || Z >= gb.L[2]) continue;
+        if (!occ[(static_cast<int64_t>(Z) * gb.L[1] + Y) * gb.L[0] + X]) continue;
+        const double d = static_cast<double>(__int_as_float(e.w));
+        if (first) {
+            first = false;
+            const double qq = floor(d / gb.dq);
+            q = qq >= 255.0 ? 255u : static_cast<uint32_t>(qq);
+            const bool always_free = double(q) * gb.dq - gb.e_max > gb.r_max + gb.eps;
+            const bool always_hit = q < 255u && (double(q) + 1.0) * gb.dq + gb.e_max <= gb.r_min - gb.eps;
+            need = !(always_free || always_hit);
+            if (!need) break;
+        }
+        if (kFill) lists[out + cnt] = make_int4(X + gb.lbase[0], Y + gb.lbase[1], Z + gb.lbase[2], e.w);
+        ++cnt;
+    }
+    if (kFill) {
+        if (need) lists[out + cnt] = make_int4(0, 0, 0, __float_as_int(INFINITY));
+    } else {
+        counts[ci] = need ? cnt + 1 : 0u;
+        cells[ci] = q << 24;
+    }
+}
+
+__global__ void k_cells_merge(int64_t ncell, const uint32_t* __restrict__ offs, uint32_t* __restrict__ cells) {
+    const int64_t ci = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (ci < ncell) cells[ci] = (cells[ci] & 0xFF000000u) | (offs[ci] & 0x00FFFFFFu);
+}
+
+static int32_t build_voxel_grid(ez_world* w, const ez_scene_desc* sc, const HModel& hm, int dim) {
+    const int64_t nv = sc->n_voxels;
+    const double s = sc->voxel_side;
+    if (!(s > 0.0)) return fail(EZ_INVALID_ARGUMENT, "voxel side must be positive");
+    if (hm.spheres.empty()) return EZ_OK;  // no sphere can meet a voxel
+    const double r_vox = 0.5 * s * std::sqrt(static_cast<double>(dim));
+    double r_min = 1e300, r_max = -1e300;
+    for (const HSphere& sp : hm.spheres) {
+        r_min = std::min(r_min, sp.rvox);
+        r_max = std::max(r_max, sp.rvox);
+    }
+    (void)r_vox;
+    int32_t lmin[3] = {0, 0, 0}, lmax[3] = {0, 0, 0};
+    for (int k = 0; k < dim; ++k) {
+        lmin[k] = INT32_MAX;
+        lmax[k] = INT32_MIN;
+    }
+    for (int64_t i = 0; i < nv; ++i)
+        for (int k = 0; k < dim; ++k) {
+            lmin[k] = std::min(lmin[k], sc->h_voxel_idx[i * dim + k]);
+            lmax[k] = std::max(lmax[k], sc->h_voxel_idx[i * dim + k]);
+        }
+    double vorg[3] = {0.0, 0.0, 0.0};
+    for (int k = 0; k < dim; ++k) vorg[k] = sc->voxel_origin[k];
+    if (dim == 2) vorg[2] = -0.5 * s;  // planar voxels sit at z = 0
+
+    // cells per voxel side: finest of 4/3/2/1 that keeps the grid under budget
+    const char* env = std::getenv("EZ_GRID_SUB");
+    int sub_pref = env ? std::max(1, std::atoi(env)) : 2;
+    double maxc = 0.0;
+    for (int k = 0; k < 3; ++k)
+        maxc = std::max({maxc, std::fabs(vorg[k] + (lmin[k] - 8.0) * s), std::fabs(vorg[k] + (lmax[k] + 8.0) * s)});
+    const double eps_build = 8.0 * std::ldexp(1.0, -23) * (1.0 + maxc);
+
+    for (int sub = sub_pref; sub >= 1; --sub) {
+        const double h = s / sub;
+        const double e_max = 0.5 * h * std::sqrt(3.0);
+        const double list_r = r_max + e_max + 2.0 * eps_build;
+        const int P = static_cast<int>(std::ceil(list_r / s)) + 1;
+        GridBuild gb{};
+        int64_t ncell = 1;
+        for (int k = 0; k < 3; ++k) {
+            const bool planar_z = (dim == 2 && k == 2);
+            gb.sub[k] = planar_z ? 1 : sub;
+            const int pad = planar_z ? 0 : P;
+            gb.lbase[k] = lmin[k] - pad;
+            gb.L[k] = lmax[k] - lmin[k] + 1 + 2 * pad;
+            gb.n[k] = gb.L[k] * gb.sub[k];
+            ncell *= gb.n[k];
+        }
+        if (ncell > (int64_t(1) << 28) && sub > 1) continue;
+        if (ncell > (int64_t(1) << 28)) return fail(EZ_CAPACITY, "voxel map extent too large for the distance grid");
+        gb.dq = list_r / 255.0;
+        gb.e_max = e_max;
+        gb.r_min = r_min;
+        gb.r_max = r_max;
+        gb.eps = eps_build;
+
+        // distance-sorted lattice offsets for each sub-position of a cell centre
+        const int K = P;
+        std::vector<int4> tab;
+        std::vector<int32_t> tab_off(1, 0);
+        for (int mz = 0; mz < gb.sub[2]; ++mz)
+            for (int my = 0; my < gb.sub[1]; ++my)
+                for (int mx = 0; mx < gb.sub[0]; ++mx) {
+                    const double dl[3] = {(mx + 0.5) / gb.sub[0] - 0.5, (my + 0.5) / gb.sub[1] - 0.5,
+                                          (mz + 0.5) / gb.sub[2] - 0.5};
+                    struct E { double d; int x, y, z; };
+                    std::vector<E> es;
+                    const int kz = (dim == 2) ? 0 : K;
+                    for (int z = -kz; z <= kz; ++z)
+                        for (int y = -K; y <= K; ++y)
+                            for (int x = -K; x <= K; ++x) {
+                                const double ddx = (x - dl[0]) * s, ddy = (y - dl[1]) * s, ddz = (z - dl[2]) * s;
+                                const double d = std::sqrt(ddx * ddx + ddy * ddy + ddz * ddz);
+                                if (d <= list_r) es.push_back({d, x, y, z});
+                            }
+                    std::sort(es.begin(), es.end(), [](const E& a, const E& b) {
+                        if (a.d != b.d) return a.d < b.d;
+                        if (a.z != b.z) return a.z < b.z;
+                        if (a.y != b.y) return a.y < b.y;
+                        return a.x < b.x;
+                    });
+                    for (const E& e : es) {
+                        // round the stored distance down: the query's break test stays exact
+                        float fd = static_cast<float>(e.d);
+                        if (static_cast<double>(fd) > e.d) fd = std::nextafter(fd, 0.0f);
+                        int4 v;
+                        v.x = e.x; v.y = e.y; v.z = e.z;
+                        std::memcpy(&v.w, &fd, 4);
+                        tab.push_back(v);
+                    }
+                    tab_off.push_back(static_cast<int32_t>(tab.size()));
+                }
+
+        const int64_t nl = static_cast<int64_t>(gb.L[0]) * gb.L[1] * gb.L[2];
+        uint8_t* d_occ = nullptr;
+        int32_t* d_idx = nullptr;
+        int4* d_tab = nullptr;
+        int32_t* d_tab_off = nullptr;
+        uint32_t* d_counts = nullptr;
+        uint32_t* d_offs = nullptr;
+        void* d_tmp = nullptr;
+        size_t tmp_bytes = 0;
+        EZ_CUDA(cudaMalloc(&d_occ, nl));
+        EZ_CUDA(cudaMemset(d_occ, 0, nl));
+        EZ_CUDA(cudaMalloc(&d_idx, sizeof(int32_t) * std::max<int64_t>(1, nv * dim)));
+        EZ_CUDA(cudaMemcpy(d_idx, sc->h_voxel_idx, sizeof(int32_t) * nv * dim, cudaMemcpyHostToDevice));
+        EZ_CUDA(cudaMalloc(&d_tab, sizeof(int4) * std::max<size_t>(1, tab.size())));
+        EZ_CUDA(cudaMemcpy(d_tab, tab.data(), sizeof(int4) * tab.size(), cudaMemcpyHostToDevice));
+        EZ_CUDA(cudaMalloc(&d_tab_off, sizeof(int32_t) * tab_off.size()));
+        EZ_CUDA(cudaMemcpy(d_tab_off, tab_off.data(), sizeof(int32_t) * tab_off.size(), cudaMemcpyHostToDevice));
+        EZ_CUDA(cudaMalloc(&w->d_cells, sizeof(uint32_t) * ncell));
+        EZ_CUDA(cudaMalloc(&d_counts, sizeof(uint32_t) * ncell));
+        EZ_CUDA(cudaMalloc(&d_offs, sizeof(uint32_t) * ncell));
+
+        k_occ_scatter<<<static_cast<unsigned>((nv + 255) / 256), 256>>>(d_idx, nv, dim, gb, d_occ);
+        const unsigned nb = static_cast<unsigned>((ncell + 255) / 256);
+        k_cells<false><<<nb, 256>>>(gb, d_occ, d_tab, d_tab_off, w->d_cells, d_counts, nullptr);
+        EZ_CUDA(cudaGetLastError());
+        EZ_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, d_counts, d_offs, static_cast<int>(ncell)));
+        EZ_CUDA(cudaMalloc(&d_tmp, tmp_bytes));
+        EZ_CUDA(cub::DeviceScan::ExclusiveSum(d_tmp, tmp_bytes, d_counts, d_offs, static_cast<int>(ncell)));
+        uint32_t last_off = 0, last_cnt = 0;
+        EZ_CUDA(cudaMemcpy(&last_off, d_offs + ncell - 1, 4, cudaMemcpyDeviceToHost));
+        EZ_CUDA(cudaMemcpy(&last_cnt, d_counts + ncell - 1, 4, cudaMemcpyDeviceToHost));
+        const int64_t total = static_cast<int64_t>(last_off) + last_cnt;
+        bool too_big = total >= (int64_t(1) << 24);
+        if (!too_big) {
+            k_cells_merge<<<nb, 256>>>(ncell, d_offs, w->d_cells);
+            EZ_CUDA(cudaMalloc(&w->d_lists, sizeof(int4) * std::max<int64_t>(1, total)));
+            k_cells<true><<<nb, 256>>>(gb, d_occ, d_tab, d_tab_off, w->d_cells, nullptr, w->d_lists);
+            EZ_CUDA(cudaGetLastError());
+            EZ_CUDA(cudaDeviceSynchronize());
+        }
+        cudaFree(d_occ);
+        cudaFree(d_idx);
+        cudaFree(d_tab);
+        cudaFree(d_tab_off);
+        cudaFree(d_counts);
+        cudaFree(d_offs);
+        cudaFree(d_tmp);
+        if (too_big) {
+            cudaFree(w->d_cells);
+            w->d_cells = nullptr;
+            if (sub > 1) continue;
+            return fail(EZ_CAPACITY, "voxel candidate lists exceed 2^24 entries");
+        }
+        w->n_list = total;
+        w->cell_h = h;
+        for (int k = 0; k < 3; ++k) w->grid_n[k] = gb.n[k];
+        w->device_bytes += ncell * 4 + total * 16;
+
+        // kernel-side views
+        const double org[3] = {vorg[0] + gb.lbase[0] * s, vorg[1] + gb.lbase[1] * s,
+                               dim == 2 ? -0.5 * h : vorg[2] + gb.lbase[2] * s};
+        auto fill = [&](auto& V, double eps) {
+            using TT = std::remove_reference_t<decltype(V.h)>;
+            V.cells = w->d_cells;
+            V.lists = w->d_lists;
+            for (int k = 0; k < 3; ++k) {
+                V.n[k] = gb.n[k];
+                V.org[k] = static_cast<TT>(org[k]);
+                V.vorg[k] = static_cast<TT>(vorg[k]);
+            }
+            V.present = 1;
+            V.h = static_cast<TT>(h);
+            V.inv_h = static_cast<TT>(1.0 / h);
+            V.dq = static_cast<TT>(gb.dq);
+            V.eps = static_cast<TT>(eps);
+            V.vside = static_cast<TT>(s);
+        };
+        fill(w->mf.vox, eps_build);
+        fill(w->md.vox, 1e-12 * (1.0 + maxc));
+        return EZ_OK;
+    }
+    return fail(EZ_CAPACITY, "could not size the voxel distance grid");
+}
+
+// ---------------------------------------------------------------------------
+// kernels: fused check, FK frames
+// ---------------------------------------------------------------------------
+template <typename T, typename Q>
+__global__ void __launch_bounds__(kCheckThreads)
+k_check(ModelDev<T> M, const Q* __restrict__ q, int64_t n, int64_t ld, uint8_t* __restrict__ out,
+        T margin, int64_t count_lim, int32_t* __restrict__ n_col) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    __shared__ uint64_t bar;
+    tma_stage(smem, M.blob, M.blob_bytes, &bar);
+    T* cen = reinterpret_cast<T*>(smem + M.blob_bytes);
+    const size_t roff = (static_cast<size_t>(M.blob_bytes) +
+                         static_cast<size_t>(3) * M.n_spheres * blockDim.x * sizeof(T) + 15) &
+                        ~static_cast<size_t>(15);
+    Q* rows = reinterpret_cast<Q*>(smem + roff);
+    const int dof = M.dof;
+    const int64_t tiles = (n + blockDim.x - 1) / blockDim.x;
+    for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+        const int64_t base = tile * blockDim.x;
+        const int nr = static_cast<int>(min(static_cast<int64_t>(blockDim.x), n - base));
+        __syncthreads();
+        // coalesced staging of this tile's configurations
+        if (ld == dof) {
+            const Q* src = q + base * dof;
+            const int tot = nr * dof;
+            for (int i = threadIdx.x; i < tot; i += blockDim.x) rows[i] = src[i];
+        } else {
+            for (int i = threadIdx.x; i < nr * dof; i += blockDim.x) {
+                const int r = i / dof, k = i - r * dof;
+                rows[i] = q[(base + r) * ld + k];
+            }
+        }
+        __syncthreads();
+        bool col = false;
+        if (threadIdx.x < nr) {
+            col = !config_free<T, Q>(M, smem, rows + threadIdx.x * dof, cen + threadIdx.x,
+                                      blockDim.x, margin);
+            out[base + threadIdx.x] = col ? 0 : 1;
+        }
+        if (n_col != nullptr) {
+            const unsigned m = __ballot_sync(0xffffffffu, col && (base + threadIdx.x) < count_lim);
+            if ((threadIdx.x & 31) == 0 && m) atomicAdd(n_col, __popc(m));
+        }
+    }
+}
+
+// link frames (true frames, fp64) for fk_batch / forward_kinematics
+__global__ void k_fk_frames(ModelDev<double> M, const double* __restrict__ Qt, const double* __restrict__ q,
+                            int64_t n, double* __restrict__ out) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const JointRec<double>* J = reinterpret_cast<const JointRec<double>*>(M.blob);
+    const int dof = M.dof, nj = M.n_joints;
+    double R[9] = {1, 0, 0, 0, 1, 0, 0, 0, 1}, t[3] = {0, 0, 0};
+    double* o = out + i * nj * 12;
+    for (int j = 0; j < nj; ++j) {
+        const JointRec<double> jr = J[j];
+        if (jr.parent != j - 1) {
+            if (jr.parent < 0) {
+                for (int k = 0; k < 9; ++k) R[k] = (k % 4 == 0) ? 1.0 : 0.0;
+                t[0] = t[1] = t[2] = 0.0;
+            } else {
+                // reload the parent's modified frame from the output (true frame * Q)
+                const double* pf = out + i * nj * 12 + jr.parent * 12;
+                const double* pq = Qt + jr.parent * 9;  // Q^T of parent
+                for (int r = 0; r < 3; ++r)
+                    for (int c = 0; c < 3; ++c)  // Rg = Rf * Q = Rf * (Q^T)^T
+                        R[3 * r + c] = pf[3 * r] * pq[3 * c] + pf[3 * r + 1] * pq[3 * c + 1] + pf[3 * r + 2] * pq[3 * c + 2];
+                for (int k = 0; k < 3; ++k) t[k] = pf[9 + k];
+            }
+        }
+        double N[9], tn[3];
+        for (int r = 0; r < 3; ++r) {
+            for (int c = 0; c < 3; ++c)
+                N[3 * r + c] = R[3 * r] * jr.R[c] + R[3 * r + 1] * jr.R[3 + c] + R[3 * r + 2] * jr.R[6 + c];
+            tn[r] = t[r] + (R[3 * r] * jr.t[0] + R[3 * r + 1] * jr.t[1] + R[3 * r + 2] * jr.t[2]);
+        }
+        if (jr.kind == EZ_JOINT_REVOLUTE) {
+            double s, c;
+            sincos(q[i * dof + jr.qidx], &s, &c);
+            for (int r = 0; r < 3; ++r) {
+                const double n0 = N[3 * r], n1 = N[3 * r + 1];
+                N[3 * r] = n0 * c + n1 * s;
+                N[3 * r + 1] = n1 * c - n0 * s;
+            }
+        } else if (jr.kind == EZ_JOINT_PRISMATIC) {
+            const double qq = q[i * dof + jr.qidx];
+            for (int r = 0; r < 3; ++r) tn[r] += (N[3 * r] * jr.ax[0] + N[3 * r + 1] * jr.ax[1] + N[3 * r + 2] * jr.ax[2]) * qq;
+        }
+        for (int k = 0; k < 9; ++k) R[k] = N[k];
+        for (int k = 0; k < 3; ++k) t[k] = tn[k];
+        const double* Qtj = Qt + j * 9;
+        double* f = o + j * 12;
+        for (int r = 0; r < 3; ++r)
+            for (int c = 0; c < 3; ++c)  // Rf = Rg * Q^T
+                f[3 * r + c] = R[3 * r] * Qtj[c] + R[3 * r + 1] * Qtj[3 + c] + R[3 * r + 2] * Qtj[6 + c];
+        for (int k = 0; k < 3; ++k) f[9 + k] = t[k];
+    }
+}
+
+template <typename T, typename Q>
+static int32_t launch_check_t(ez_world* w, const ModelDev<T>& M, const Q* d_q, int64_t n, int64_t ld,
+                              uint8_t* d_free, cudaStream_t stream, int64_t count_lim, int32_t* n_col) {
+    const size_t smem = check_smem_bytes<T>(M.blob_bytes, M.n_spheres, kCheckThreads,
+                                            static_cast<int>(M.dof * sizeof(Q)));
+    auto kern = k_check<T, Q>;
+    static thread_local size_t configured[4] = {0, 0, 0, 0};
+    const int slot = (sizeof(T) == 8 ? 2 : 0) + (sizeof(Q) == 8 ? 1 : 0);
+    if (smem > 48 * 1024 && configured[slot] < smem) {
+        EZ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+        configured[slot] = smem;
+    }
+    int occ = 0;
+    EZ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kCheckThreads, smem));
+    if (occ < 1) return fail(EZ_CAPACITY, "robot model too large for one checking CTA");
+    const int64_t tiles = (n + kCheckThreads - 1) / kCheckThreads;
+    const int64_t grid = std::min<int64_t>(tiles, static_cast<int64_t>(w->num_sms) * occ);
+    kern<<<static_cast<unsigned>(grid), kCheckThreads, smem, stream>>>(M, d_q, n, ld, d_free, static_cast<T>(w->margin),
+                                                                      count_lim, n_col);
+    EZ_CUDA(cudaGetLastError());
+    return EZ_OK;
+}
+
+int32_t launch_check(ez_world* w, const void* d_q, int32_t q_dtype, int64_t n, int64_t ld,
+                     uint8_t* d_free, int32_t precision, cudaStream_t stream, int64_t count_lim,
+                     int32_t* n_col) {
+    if (n <= 0) return EZ_OK;
+    if (precision == EZ_F64) {
+        if (q_dtype == EZ_F64)
+            return launch_check_t<double, double>(w, w->md, static_cast<const double*>(d_q), n, ld, d_free, stream, count_lim, n_col);
+        return launch_check_t<double, float>(w, w->md, static_cast<const float*>(d_q), n, ld, d_free, stream, count_lim, n_col);
+    }
+    if (q_dtype == EZ_F64)
+        return launch_check_t<float, double>(w, w->mf, static_cast<const double*>(d_q), n, ld, d_free, stream, count_lim, n_col);
+    return launch_check_t<float, float>(w, w->mf, static_cast<const float*>(d_q), n, ld, d_free, stream, count_lim, n_col);
+}
+
+}  // namespace ez
+
+// ---------------------------------------------------------------------------
+// C ABI
+// ---------------------------------------------------------------------------
+using namespace ez;
+
+static void world_free(ez_world* w) {
+    if (!w) return;
+    for (int i = 0; i < 2; ++i) {
+        cudaFree(w->d_blob[i]);
+        if (w->hstream[i]) cudaStreamDestroy(w->hstream[i]);
+        if (w->hevent[i]) cudaEventDestroy(w->hevent[i]);
+        cudaFreeHost(w->h_stage_in[i]);
+        cudaFreeHost(w->h_stage_out[i]);
+        cudaFree(w->d_stage_in[i]);
+        cudaFree(w->d_stage_out[i]);
+    }
+    cudaFree(w->d_cells);
+    cudaFree(w->d_lists);
+    cudaFree(w->d_linkQt);
+    eizo_ws_free(w->eizo);
+    delete w;
+}
+
+extern "C" int32_t ez_world_create(const ez_robot_desc* rb, const ez_scene_desc* sc, double margin,
+                                   int32_t device, ez_world** out) {
+    if (!rb || !out) return fail(EZ_INVALID_ARGUMENT, "null argument");
+    *out = nullptr;
+    const int dim = rb->dim;
+    if (dim != 2 && dim != 3) return fail(EZ_INVALID_ARGUMENT, "task-space dimension must be 2 or 3");
+    if (rb->n_joints < 1 || rb->n_joints > kMaxJoints) return fail(EZ_UNSUPPORTED, "joint count outside [1, 64]");
+    if (rb->n_geoms > kMaxSpheres) return fail(EZ_UNSUPPORTED, "more than 1024 robot geometries");
+    if (margin < 0.0) return fail(EZ_INVALID_ARGUMENT, "margin must be >= 0");
+    EZ_CUDA(cudaSetDevice(device));
+
+    HModel hm;
+    const int nj = rb->n_joints;
+    std::vector<M3> Q(nj);
+    std::vector<int> needs_store(nj, 0);
+    for (int j = 0; j < nj; ++j) {
+        const int p = rb->joint_parent[j];
+        if (p >= j || p < -1) return fail(EZ_INVALID_ARGUMENT, "joint parent must precede the joint");
+        if (p >= 0 && p != j - 1) needs_store[p] = 1;
+    }
+    int slots = 0;
+    std::vector<int> slot_of(nj, -1);
+    for (int j = 0; j < nj; ++j)
+        if (needs_store[j]) slot_of[j] = slots++;
+    if (slots > kMaxStore) return fail(EZ_UNSUPPORTED, "too many branching links");
+    hm.n_store = slots;
+    int qi = 0;
+    for (int j = 0; j < nj; ++j) {
+        HJoint h{};
+        h.kind = rb->joint_kind[j];
+        h.parent = rb->joint_parent[j];
+        const M3 Ro = embed_rot(rb->joint_rot + j * dim * dim, dim);
+        double to[3], ax[3];
+        embed_vec(rb->joint_trans + j * dim, dim, to);
+        embed_vec(rb->joint_axis + j * dim, dim, ax);
+        const M3 Qpt = h.parent >= 0 ? mat_T(Q[h.parent]) : mat_eye();
+        M3 P = mat_eye();
+        if (h.kind == EZ_JOINT_REVOLUTE && dim == 3) {
+            const double an = std::sqrt(ax[0] * ax[0] + ax[1] * ax[1] + ax[2] * ax[2]);
+            if (!(an > 0.0)) return fail(EZ_INVALID_ARGUMENT, "revolute joint needs a nonzero axis");
+            P = axis_frame(ax);
+        }
+        if (h.kind == EZ_JOINT_PRISMATIC) {
+            for (int k = 0; k < 3; ++k) h.ax[k] = ax[k];
+        } else if (h.kind != EZ_JOINT_REVOLUTE && h.kind != EZ_JOINT_FIXED) {
+            return fail(EZ_INVALID_ARGUMENT, "unknown joint kind");
+        }
+        h.R = mat_mul(mat_mul(Qpt, Ro), P);
+        mat_vec(Qpt, to, h.t);
+        h.qidx = (h.kind == EZ_JOINT_FIXED) ? -1 : qi++;
+        h.store_slot = slot_of[j];
+        h.parent_slot = (h.parent >= 0) ? slot_of[h.parent] : -1;
+        Q[j] = P;
+        hm.joints.push_back(h);
+        hm.linkQt.push_back(mat_T(P));
+    }
+    hm.dof = qi;
+
+    // robot geometry: spheres (boxes are not supported natively yet)
+    const double r_vox = (sc && sc->n_voxels > 0) ? 0.5 * sc->voxel_side * std::sqrt(static_cast<double>(dim)) : 0.0;
+    std::vector<int> sphere_of(rb->n_geoms, -1);
+    for (int g = 0; g < rb->n_geoms; ++g) {
+        if (rb->geom_kind[g] != EZ_GEOM_SPHERE)
+            return fail(EZ_UNSUPPORTED, "robot box geometries are not supported by the native checker");
+        const int link = rb->geom_link[g];
+        if (link < 0 || link >= nj) return fail(EZ_INVALID_ARGUMENT, "geometry link out of range");
+        if (g > 0 && link < rb->geom_link[g - 1]) return fail(EZ_INVALID_ARGUMENT, "geometries must be link-major");
+        HSphere s{};
+        double tl[3];
+        embed_vec(rb->geom_trans + g * dim, dim, tl);
+        mat_vec(mat_T(Q[link]), tl, s.p);
+        s.r = rb->geom_radius[g];
+        s.rvox = (s.r + r_vox) + margin;
+        s.rmar = s.r + margin;
+        sphere_of[g] = static_cast<int>(hm.spheres.size());
+        hm.spheres.push_back(s);
+    }
+    for (int j = 0; j < nj; ++j) {
+        int b = 0;
+        while (b < rb->n_geoms && rb->geom_link[b] < j) ++b;
+        int e = b;
+        while (e < rb->n_geoms && rb->geom_link[e] == j) ++e;
+        hm.joints[j].sb = b;
+        hm.joints[j].se = e;
+    }
+    // self pairs grouped by first sphere (pairs keep their order within a group)
+    {
+        std::vector<std::vector<HPair>> by_a(rb->n_geoms);
+        for (int p = 0; p < rb->n_pairs; ++p) {
+            int a = rb->pairs[2 * p], b = rb->pairs[2 * p + 1];
+            if (a < 0 || b < 0 || a >= rb->n_geoms || b >= rb->n_geoms)
+                return fail(EZ_INVALID_ARGUMENT, "self pair index out of range");
+            if (rb->geom_link[a] == rb->geom_link[b])
+                return fail(EZ_INVALID_ARGUMENT, "self-collision pair on a single link");
+            const double rr = (rb->geom_radius[a] + rb->geom_radius[b]) + margin;
+            by_a[a].push_back(HPair{b, rr * rr});
+        }
+        for (int a = 0; a < rb->n_geoms; ++a) {
+            if (by_a[a].empty()) continue;
+            HGroup g{a, static_cast<int>(hm.pairs.size()), 0};
+            for (const HPair& p : by_a[a]) hm.pairs.push_back(p);
+            g.end = static_cast<int>(hm.pairs.size());
+            hm.groups.push_back(g);
+        }
+    }
+    // static obstacles
+    for (int i = 0; sc && i < sc->n_static; ++i) {
+        double c[3];
+        embed_vec(sc->static_trans + i * dim, dim, c);
+        if (sc->static_kind[i] == EZ_GEOM_SPHERE) {
+            hm.ssph.insert(hm.ssph.end(), {c[0], c[1], c[2], sc->static_radius[i]});
+        } else {
+            const M3 Rt = mat_T(embed_rot(sc->static_rot + i * dim * dim, dim));
+            double he[3];
+            embed_vec(sc->static_half + i * dim, dim, he);
+            for (int k = 0; k < 9; ++k) hm.sbox.push_back(Rt.a[k]);
+            hm.sbox.insert(hm.sbox.end(), {c[0], c[1], c[2], he[0], he[1], he[2]});
+        }
+    }
+
+    ez_world* w = new ez_world();
+    w->device = device;
+    cudaDeviceGetAttribute(&w->num_sms, cudaDevAttrMultiProcessorCount, device);
+    w->dim = dim;
+    w->dof = hm.dof;
+    w->n_joints = nj;
+    w->n_spheres = static_cast<int32_t>(hm.spheres.size());
+    w->n_pairs = static_cast<int32_t>(hm.pairs.size());
+    w->n_groups = static_cast<int32_t>(hm.groups.size());
+    w->n_ssph = static_cast<int32_t>(hm.ssph.size() / 4);
+    w->n_sbox = static_cast<int32_t>(hm.sbox.size() / 15);
+    w->n_store = hm.n_store;
+    w->margin = margin;
+    w->n_voxels = sc ? sc->n_voxels : 0;
+
+    auto upload = [&](const std::vector<uint8_t>& blob, uint8_t** dst) -> int32_t {
+        EZ_CUDA(cudaMalloc(dst, blob.size()));
+        EZ_CUDA(cudaMemcpy(*dst, blob.data(), blob.size(), cudaMemcpyHostToDevice));
+        w->device_bytes += static_cast<int64_t>(blob.size());
+        return EZ_OK;
+    };
+    int32_t st = EZ_OK;
+    {
+        std::vector<uint8_t> bf = pack_blob<float>(hm, w->mf);
+        std::vector<uint8_t> bd = pack_blob<double>(hm, w->md);
+        st = upload(bf, &w->d_blob[0]);
+        if (st == EZ_OK) st = upload(bd, &w->d_blob[1]);
+        w->mf.blob = w->d_blob[0];
+        w->md.blob = w->d_blob[1];
+    }
+    if (st == EZ_OK) {
+        std::vector<double> qt(9 * nj);
+        for (int j = 0; j < nj; ++j)
+            for (int k = 0; k < 9; ++k) qt[9 * j + k] = hm.linkQt[j].a[k];
+        cudaError_t e = cudaMalloc(&w->d_linkQt, sizeof(double) * qt.size());
+        if (e == cudaSuccess) e = cudaMemcpy(w->d_linkQt, qt.data(), sizeof(double) * qt.size(), cudaMemcpyHostToDevice);
+        if (e != cudaSuccess) st = cuda_fail(e, "upload link frames", __FILE__, __LINE__);
+    }
+    w->mf.vox.present = 0;
+    w->md.vox.present = 0;
+    if (st == EZ_OK && sc && sc->n_voxels > 0) st = build_voxel_grid(w, sc, hm, dim);
+    if (st != EZ_OK) {
+        world_free(w);
+        return st;
+    }
+    *out = w;
+    return EZ_OK;
+}
+
+extern "C" int32_t ez_world_destroy(ez_world* w) {
+    if (!w) return EZ_OK;
+    cudaSetDevice(w->device);
+    world_free(w);
+    return EZ_OK;
+}
+
+extern "C" int32_t ez_world_get_info(const ez_world* w, ez_world_info* out) {
+    if (!w || !out) return fail(EZ_INVALID_ARGUMENT, "null argument");
+    out->dof = w->dof;
+    out->n_links = w->n_joints;
+    out->n_spheres = w->n_spheres;
+    out->n_pairs = w->n_pairs;
+    out->n_static = w->n_ssph + w->n_sbox;
+    out->n_voxels = w->n_voxels;
+    for (int k = 0; k < 3; ++k) out->grid_dims[k] = w->grid_n[k];
+    out->cell_side = w->cell_h;
+    out->list_entries = w->n_list;
+    out->device_bytes = w->device_bytes;
+    return EZ_OK;
+}
+
+extern "C" int32_t ez_check_batch(ez_world* w, const void* d_q, int32_t q_dtype, int64_t n, int64_t ld,
+                                  uint8_t* d_free, int32_t precision, void* stream) {
+    if (!w) return fail(EZ_INVALID_ARGUMENT, "null world");
+    if (n < 0 || ld < w->dof) return fail(EZ_INVALID_ARGUMENT, "bad batch shape");
+    if (n == 0) return EZ_OK;
+    if (q_dtype != EZ_F32 && q_dtype != EZ_F64) return fail(EZ_INVALID_ARGUMENT, "bad dtype");
+    EZ_CUDA(cudaSetDevice(w->device));
+    return launch_check(w, d_q, q_dtype, n, ld, d_free, precision, static_cast<cudaStream_t>(stream));
+}
+
+// Host-buffer check: the input is streamed through two pinned staging
+// buffers on two streams so the H2D copy of chunk i+1, the kernel of chunk i
+// and the D2H copy of chunk i-1 overlap.
+extern "C" int32_t ez_check_batch_host(ez_world* w, const double* h_q, int64_t n, int64_t ld,
+                                       uint8_t* h_free, int32_t precision) {
+    if (!w) return fail(EZ_INVALID_ARGUMENT, "null world");
+    if (n < 0 || ld < w->dof) return fail(EZ_INVALID_ARGUMENT, "bad batch shape");
+    if (n == 0) return EZ_OK;
+    std::lock_guard<std::mutex> lock(w->mu);
+    EZ_CUDA(cudaSetDevice(w->device));
+    const int dof = w->dof;
+    const int64_t chunk = 1 << 18;
+    if (w->stage_rows < chunk) {
+        for (int i = 0; i < 2; ++i) {
+            cudaFreeHost(w->h_stage_in[i]);
+            cudaFreeHost(w->h_stage_out[i]);
+            cudaFree(w->d_stage_in[i]);
+            cudaFree(w->d_stage_out[i]);
+            w->h_stage_in[i] = w->d_stage_in[i] = nullptr;
+            w->h_stage_out[i] = w->d_stage_out[i] = nullptr;
+            EZ_CUDA(cudaMallocHost(&w->h_stage_in[i], sizeof(double) * chunk * dof));
+            EZ_CUDA(cudaMallocHost(reinterpret_cast<void**>(&w->h_stage_out[i]), chunk));
+            EZ_CUDA(cudaMalloc(&w->d_stage_in[i], sizeof(double) * chunk * dof));
+            EZ_CUDA(cudaMalloc(reinterpret_cast<void**>(&w->d_stage_out[i]), chunk));
+            if (!w->hstream[i]) EZ_CUDA(cudaStreamCreateWithFlags(&w->hstream[i], cudaStreamNonBlocking));
+            if (!w->hevent[i]) EZ_CUDA(cudaEventCreateWithFlags(&w->hevent[i], cudaEventDisableTiming));
+        }
+        w->stage_rows = chunk;
+    }
+    cudaPointerAttributes attr{};
+    bool pinned_in = cudaPointerGetAttributes(&attr, h_q) == cudaSuccess && attr.type == cudaMemoryTypeHost;
+    cudaGetLastError();
+    bool pinned_out = cudaPointerGetAttributes(&attr, h_free) == cudaSuccess && attr.type == cudaMemoryTypeHost;
+    cudaGetLastError();
+    const int64_t nchunks = (n + chunk - 1) / chunk;
+    int64_t pending_out[2] = {-1, -1};  // chunk index whose result sits in h_stage_out[b]
+    for (int64_t c = 0; c < nchunks; ++c) {
+        const int b = static_cast<int>(c & 1);
+        cudaStream_t s = w->hstream[b];
+        const int64_t r0 = c * chunk;
+        const int64_t rows = std::min(chunk, n - r0);
+        // wait for the previous use of this buffer pair to finish
+        EZ_CUDA(cudaStreamSynchronize(s));
+        if (pending_out[b] >= 0 && !pinned_out) {
+            const int64_t pr0 = pending_out[b] * chunk;
+            std::memcpy(h_free + pr0, w->h_stage_out[b], std::min(chunk, n - pr0));
+        }
+        pending_out[b] = -1;
+        const double* src = h_q + r0 * ld;
+        if (pinned_in) {
+            EZ_CUDA(cudaMemcpy2DAsync(w->d_stage_in[b], sizeof(double) * dof, src, sizeof(double) * ld,
+                                      sizeof(double) * dof, rows, cudaMemcpyHostToDevice, s));
+        } else {
+            double* st = static_cast<double*>(w->h_stage_in[b]);
+            if (ld == dof) {
+                std::memcpy(st, src, sizeof(double) * rows * dof);
+            } else {
+                for (int64_t r = 0; r < rows; ++r) std::memcpy(st + r * dof, src + r * ld, sizeof(double) * dof);
+            }
+            EZ_CUDA(cudaMemcpyAsync(w->d_stage_in[b], st, sizeof(double) * rows * dof, cudaMemcpyHostToDevice, s));
+        }
+        EZ_TRY(launch_check(w, w->d_stage_in[b], EZ_F64, rows, dof, w->d_stage_out[b], precision, s));
+        if (pinned_out) {
+            EZ_CUDA(cudaMemcpyAsync(h_free + r0, w->d_stage_out[b], rows, cudaMemcpyDeviceToHost, s));
+        } else {
+            EZ_CUDA(cudaMemcpyAsync(w->h_stage_out[b], w->d_stage_out[b], rows, cudaMemcpyDeviceToHost, s));
+            pending_out[b] = c;
+        }
+    }
+    for (int b = 0; b < 2; ++b) {
+        EZ_CUDA(cudaStreamSynchronize(w->hstream[b]));
+        if (pending_out[b] >= 0) {
+            const int64_t pr0 = pending_out[b] * chunk;
+            std::memcpy(h_free + pr0, w->h_stage_out[b], std::min(chunk, n - pr0));
+        }
+    }
+    return EZ_OK;
+}
+
+extern "C" int32_t ez_fk_batch(ez_world* w, const double* d_q, int64_t n, double* d_frames, void* stream) {
+    if (!w) return fail(EZ_INVALID_ARGUMENT, "null world");
+    if (n <= 0) return EZ_OK;
+    EZ_CUDA(cudaSetDevice(w->device));
+    k_fk_frames<<<static_cast<unsigned>((n + 127) / 128), 128, 0, static_cast<cudaStream_t>(stream)>>>(
+        w->md, w->d_linkQt, d_q, n, d_frames);
+    EZ_CUDA(cudaGetLastError());
+    return EZ_OK;
+}

@@ -1,0 +1,59 @@
+// ez_world.h — host-side state of one device-resident world (robot + obstacles
+// for one checker margin), shared by the check, FK and EI-ZO translation units.
+#pragma once
+
+#include <mutex>
+#include <vector>
+
+#include "ez_common.h"
+
+struct ez_eizo_ws;  // EI-ZO device workspace (ez_eizo.cu)
+
+struct ez_world {
+    int32_t device = 0;
+    int32_t num_sms = 148;
+    int32_t dim = 3, dof = 0, n_joints = 0, n_spheres = 0, n_pairs = 0, n_groups = 0;
+    int32_t n_ssph = 0, n_sbox = 0, n_store = 0;
+    int64_t n_voxels = 0;
+    double margin = 0.0;
+
+    // per-link Q_j^T (fp64, row-major) to turn modified frames back into link frames
+    double* d_linkQt = nullptr;
+
+    // model blobs and views, [0] = fp32, [1] = fp64
+    uint8_t* d_blob[2] = {nullptr, nullptr};
+    ez::ModelDev<float> mf{};
+    ez::ModelDev<double> md{};
+
+    // voxel obstacle structure (shared by both precisions)
+    uint32_t* d_cells = nullptr;
+    int4* d_lists = nullptr;
+    int64_t n_list = 0;
+    int32_t grid_n[3] = {0, 0, 0};
+    double cell_h = 0.0;
+    int64_t device_bytes = 0;
+
+    // host-buffer check pipeline
+    std::mutex mu;
+    cudaStream_t hstream[2] = {nullptr, nullptr};
+    cudaEvent_t hevent[2] = {nullptr, nullptr};
+    void* h_stage_in[2] = {nullptr, nullptr};
+    uint8_t* h_stage_out[2] = {nullptr, nullptr};
+    void* d_stage_in[2] = {nullptr, nullptr};
+    uint8_t* d_stage_out[2] = {nullptr, nullptr};
+    int64_t stage_rows = 0;
+
+    ez_eizo_ws* eizo = nullptr;
+};
+
+namespace ez {
+
+// launch the fused check over n rows; q_dtype EZ_F32/EZ_F64, precision EZ_F32/EZ_F64.
+// If n_col != nullptr, atomically adds the number of colliding rows with index < count_lim.
+int32_t launch_check(ez_world* w, const void* d_q, int32_t q_dtype, int64_t n, int64_t ld,
+                     uint8_t* d_free, int32_t precision, cudaStream_t stream,
+                     int64_t count_lim = 0, int32_t* n_col = nullptr);
+
+void eizo_ws_free(ez_eizo_ws* ws);
+
+}  // namespace ez

@@ -1,0 +1,173 @@
+"""GPU parity of the fused FK + collision kernel (ez_check_batch) against the reference goldens.
+
+Bar (BASELINE.json north_star): fp32 flags bit-exact with the reference
+wherever the fp64 contact clearance exceeds 1e-5 in magnitude; fp64 mode
+bit-exact everywhere except exact ties (|clearance| < 1e-12).
+"""
+
+import numpy as np
+import pytest
+
+from conftest import golden
+from paper_2504_10783_b200 import fixtures as fx
+from paper_2504_10783_b200.checker import CollisionChecker
+from paper_2504_10783_b200.errors import DimensionMismatch
+from paper_2504_10783_b200.model import BOX, REVOLUTE, SPHERE, Geometry, Joint, Link, RigidTransform, RobotModel
+from paper_2504_10783_b200.scene import VoxelMap, World, voxelize_point_cloud
+
+pytestmark = pytest.mark.gpu
+
+BAND = 1e-5  # contact-distance band of the fp32 path (written into the north star)
+
+WORLDS = {"franka7": lambda: fx.franka7_world(), "franka7_m02": lambda: fx.franka7_world(),
+          "bimanual14": lambda: fx.bimanual14_world(), "arm3": fx.arm3_world}
+
+
+def _world(name, g):
+    if name == "forest7":
+        return fx.disc_world(fx.forest_centers(7)).with_vmap(VoxelMap(np.array([-5.0, -5.0]), 0.02, g["vox_idx"]))
+    return WORLDS[name]()
+
+
+@pytest.mark.parametrize("name", ["franka7", "franka7_m02", "bimanual14", "arm3", "forest7"])
+@pytest.mark.parametrize("precision", ["fp32", "fp64"])
+def test_flags_match_reference(name, precision):
+    g = golden(f"check_{name}.npz")
+    world = _world(name, g)
+    ck = world.checker(margin=float(g["margin"]), precision=precision)
+    Q = g["Q"].astype(np.float64)
+    free = ck.check_batch(Q)
+    assert free.dtype == bool and free.shape == (Q.shape[0],)
+    tol = BAND if precision == "fp32" else 1e-12
+    outside = np.abs(g["clearance"]) >= tol
+    mism = (free != g["free"]) & outside
+    assert not mism.any(), f"{mism.sum()} flag mismatches outside the {tol} band"
+    assert ck.calls == Q.shape[0]
+
+
+@pytest.mark.parametrize("precision", ["fp32", "fp64"])
+def test_device_path_matches_host_path(precision):
+    import torch
+
+    g = golden("check_franka7.npz")
+    ck = fx.franka7_world().checker(precision=precision)
+    host = ck.check_batch(g["Q"].astype(np.float64))
+    for dt in (torch.float32, torch.float64):
+        Qd = torch.as_tensor(g["Q"], device="cuda").to(dt)
+        dev = ck.check_batch(Qd).cpu().numpy()
+        if dt == torch.float64:
+            assert np.array_equal(dev, host)
+        else:  # fp32 inputs are the same values (the golden configs are fp32)
+            assert np.array_equal(dev, host)
+
+
+def test_strided_rows():
+    import torch
+
+    g = golden("check_arm3.npz")
+    ck = fx.arm3_world().checker()
+    Q = torch.as_tensor(g["Q"].astype(np.float64), device="cuda")
+    wide = torch.zeros((Q.shape[0], 5), dtype=torch.float64, device="cuda")
+    wide[:, :3] = Q
+    a = ck.native.check_device(wide[:, :3]).cpu().numpy()
+    b = ck.native.check_device(Q).cpu().numpy()
+    assert np.array_equal(a, b)
+
+
+def test_large_batch_matches_chunks():
+    rng = np.random.default_rng(3)
+    w = fx.franka7_world()
+    Q = rng.uniform(w.lower, w.upper, size=(600_000, 7))
+    ck = w.checker()
+    full = ck.check_batch(Q)
+    parts = np.concatenate([ck.check_batch(Q[i:i + 70_001]) for i in range(0, Q.shape[0], 70_001)])
+    assert np.array_equal(full, parts)
+    assert ck.calls == 2 * Q.shape[0]
+
+
+# --- semantics of world.py / test_world.py ---------------------------------------
+
+def test_empty_batch_and_dimension_mismatch():
+    ck = World(fx.point_robot_model()).checker()
+    assert ck.check_batch(np.zeros((0, 2))).shape == (0,)
+    with pytest.raises(DimensionMismatch):
+        ck.check_batch(np.zeros((3, 3)))
+    assert ck.check([0.0, 0.0])
+
+
+@pytest.mark.parametrize("precision", ["fp32", "fp64"])
+def test_boundary_contact_counts_as_collision(precision):
+    gap = 1e-6 if precision == "fp32" else 1e-9
+    w = fx.disc_world([[0.0, 0.0]], radius=1.0)
+    assert not w.checker(precision=precision).check([1.0, 0.0])
+    assert w.checker(precision=precision).check([1.0 + gap, 0.0])
+    assert not fx.disc_world([[0.0, 3.0]], radius=1.0).checker(precision=precision).check([0.0, 3.0])
+
+
+@pytest.mark.parametrize("precision", ["fp32", "fp64"])
+def test_box_boundary_contact(precision):
+    box = Geometry(BOX, RigidTransform.planar(2.0, 0.0), half_extents=np.array([1.0, 1.0]))
+    ck = World(fx.point_robot_model(), static=(box,)).checker(precision=precision)
+    assert not ck.check([1.0, 0.0])
+    assert ck.check([1.0 - (1e-6 if precision == "fp32" else 1e-9), 0.0])
+
+
+def test_self_collision_pair():
+    joints = (Joint(REVOLUTE, -1, RigidTransform.identity(2)), Joint(REVOLUTE, 0, RigidTransform.planar(1.0, 0.0)))
+    links = (Link((Geometry(SPHERE, RigidTransform.planar(0.25, 0.0), radius=0.1),)),
+             Link((Geometry(SPHERE, RigidTransform.planar(0.75, 0.0), radius=0.1),)))
+    model = RobotModel(2, joints, links, [-np.pi] * 2, [np.pi] * 2, self_pairs=((0, 1),))
+    ck = World(model).checker()
+    assert ck.check([0.0, 0.0])
+    assert not ck.check([0.0, np.pi])
+
+
+def test_margin_inflates_tests():
+    w = fx.disc_world([[0.0, 0.0]], radius=1.0)
+    assert w.checker().check([1.2, 0.0])
+    assert not w.checker(margin=0.3).check([1.2, 0.0])
+
+
+def test_voxel_map_obstacle():
+    vm = voxelize_point_cloud(np.array([[1.0, 1.0]]), 0.5, np.zeros(2))
+    ck = World(fx.point_robot_model(), vmap=vm).checker()
+    assert not ck.check([1.25, 1.25])
+    assert ck.check([4.0, 4.0])
+    r = vm.sphere_radius
+    assert not ck.check([1.25 + r - 1e-5, 1.25])    # inside the voxel sphere
+    assert ck.check([1.25 + r + 1e-5, 1.25])
+
+
+def test_check_segment():
+    w = fx.disc_world([[0.0, 2.0]], radius=0.5)
+    ck = w.checker()
+    assert ck.check_segment([1.0, 0.0], [1.0, 0.0], 0.1)
+    assert not ck.check_segment([-2.0, 2.0], [2.0, 2.0], 0.01)
+
+
+def test_fk_matches_reference():
+    from paper_2504_10783_b200.model import fk_batch
+
+    z = golden("fk.npz")
+    for name, world in (("franka7", fx.franka7_world(False)), ("bimanual14", fx.bimanual14_world(False)),
+                        ("arm3", fx.arm3_world())):
+        rots, trans = fk_batch(world.model, z[f"{name}_Q"])
+        assert np.allclose(np.stack(rots, axis=1), z[f"{name}_rot"], atol=1e-12)
+        assert np.allclose(np.stack(trans, axis=1), z[f"{name}_trans"], atol=1e-12)
+
+
+def test_world_info_reports_grid():
+    ck = fx.franka7_world().checker()
+    info = ck.native.info()
+    assert info["n_spheres"] == 33 and info["n_pairs"] == 232 and info["n_voxels"] == 10_000
+    assert info["list_entries"] > 0 and all(n > 0 for n in info["grid_dims"])
+
+
+def test_robot_boxes_rejected_loudly():
+    from paper_2504_10783_b200.errors import CorridorError
+
+    joints = (Joint(REVOLUTE, -1, RigidTransform.identity(2)),)
+    links = (Link((Geometry(BOX, RigidTransform.identity(2), half_extents=np.array([0.1, 0.1])),)),)
+    model = RobotModel(2, joints, links, [-1.0], [1.0])
+    with pytest.raises((NotImplementedError, CorridorError)):
+        World(model).checker().check([0.0])

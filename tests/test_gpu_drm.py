@@ -1,0 +1,73 @@
+"""GPU voxelisation (ez_voxelize) and DRM prune (ez_collision_set) vs the reference: exact set equality."""
+
+import numpy as np
+import pytest
+
+from conftest import golden
+from paper_2504_10783_b200.errors import GridMismatch
+from paper_2504_10783_b200.roadmap import CollisionSet, Drm, Grid, collision_set
+from paper_2504_10783_b200.scene import VoxelMap, voxelize_point_cloud
+
+pytestmark = pytest.mark.gpu
+
+
+def test_voxelize_matches_reference():
+    z = golden("voxelize.npz")
+    vm3 = voxelize_point_cloud(z["p3"], 0.02, z["o3"])
+    assert np.array_equal(vm3.index_array(), z["idx3"])
+    vm2 = voxelize_point_cloud(z["p2"], 0.5, z["o2"])
+    assert np.array_equal(vm2.index_array(), z["idx2"])
+    assert vm2.occupied == frozenset(map(tuple, z["idx2"].tolist()))
+
+
+def test_voxelize_conventions():
+    assert voxelize_point_cloud(np.zeros((0, 2)), 0.5, np.zeros(2)).n_occupied == 0
+    vm = voxelize_point_cloud(np.array([[0.25, 0.25], [0.26, 0.24]]), 0.5, np.zeros(2))
+    assert vm.occupied == frozenset({(0, 0)})
+    assert voxelize_point_cloud(np.array([[1.0, 0.2]]), 0.5, np.zeros(2)).occupied == frozenset({(2, 0)})
+    neg = voxelize_point_cloud(np.array([[-0.1, -3.0, 0.0]]), 0.5, np.zeros(3))
+    assert neg.occupied == frozenset({(-1, -6, 0)})
+    with pytest.raises(ValueError):
+        voxelize_point_cloud(np.zeros((1, 2)), 0.0, np.zeros(2))
+
+
+def _drm(off, ids, grid):
+    n_nodes = int(ids.max()) + 1 if ids.size else 1
+    z = np.zeros((n_nodes, 2))
+    return Drm(z, np.zeros(n_nodes + 1, np.int64), np.zeros(0, np.int32), off, ids, z, grid)
+
+
+def test_collision_set_forest_matches_reference():
+    z = golden("drm.npz")
+    grid = Grid(np.array([-5.0, -5.0]), 0.25, (40, 40))
+    drm = Drm(np.zeros((200, 2)), np.zeros(201, np.int64), np.zeros(0, np.int32), z["f_off"], z["f_ids"],
+              np.zeros((200, 3)), grid)
+    for i in range(int(z["f_nmaps"])):
+        vm = VoxelMap(z[f"f{i}_org"], float(z[f"f{i}_side"]), z[f"f{i}_idx"])
+        got = collision_set(drm, vm)
+        assert np.array_equal(got.ids, z[f"f{i}_blocked"])
+        assert got.blocked == frozenset(z[f"f{i}_blocked"].tolist())
+
+
+def test_collision_set_franka_matches_reference():
+    z = golden("drm.npz")
+    grid = Grid(np.array([-0.75, -1.02, -0.36]), 0.06, (25, 34, 26))
+    n = z["g_nodes"].shape[0]
+    drm = Drm(z["g_nodes"], np.zeros(n + 1, np.int64), np.zeros(0, np.int32), z["g_off"], z["g_ids"],
+              np.zeros((n, 7)), grid)
+    for tag in ("same", "fine"):
+        vm = VoxelMap(z[f"g_{tag}_org"], float(z[f"g_{tag}_side"]), z[f"g_{tag}_idx"])
+        assert np.array_equal(collision_set(drm, vm).ids, z[f"g_{tag}_blocked"])
+
+
+def test_collision_set_empty_all_and_mismatch():
+    z = golden("drm.npz")
+    grid = Grid(np.array([-5.0, -5.0]), 0.25, (40, 40))
+    drm = Drm(np.zeros((200, 2)), np.zeros(201, np.int64), np.zeros(0, np.int32), z["f_off"], z["f_ids"],
+              np.zeros((200, 3)), grid)
+    assert collision_set(drm, VoxelMap(grid.origin, grid.side, ())).blocked == frozenset()
+    allv = VoxelMap(grid.origin, grid.side, [(i, j) for i in range(40) for j in range(40)])
+    union = np.unique(z["f_ids"]).astype(np.int64)
+    assert np.array_equal(collision_set(drm, allv).ids, union)
+    with pytest.raises(GridMismatch):
+        collision_set(drm, VoxelMap(np.zeros(3), 0.25, [(0, 0, 0)]))

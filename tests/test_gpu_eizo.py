@@ -1,0 +1,110 @@
+"""GPU EI-ZO (ez_inflate_edge) against the reference's own inflations and test_inflation.py contracts."""
+
+import numpy as np
+import pytest
+
+from conftest import golden, inflate_index
+from paper_2504_10783_b200 import fixtures as fx
+from paper_2504_10783_b200.eizo import InflationParams, Segment, inflate_edge
+from paper_2504_10783_b200.errors import SeedOutsideDomain, SegmentInCollision
+from paper_2504_10783_b200.polytope import HPolytope
+from paper_2504_10783_b200.scene import World
+
+pytestmark = pytest.mark.gpu
+
+
+def _world(scene):
+    if scene == "arm3":
+        return fx.arm3_world()
+    return {"disc_0_3": fx.disc_world([[0.0, 3.0]], 1.0), "disc_0_2": fx.disc_world([[0.0, 2.0]], 0.6),
+            "disc_two": fx.disc_world([[0.0, 2.0], [0.0, -2.0]], 0.7),
+            "disc_nit": fx.disc_world([[0.0, 1.2], [0.0, -1.2], [2.0, 1.2]], 0.5)}[scene]
+
+
+def _run(rec, z, precision):
+    world = _world(rec["scene"])
+    v = z[f"{rec['key']}_v"]
+    dom = HPolytope.from_bounds(world.lower, world.upper)
+    ck = world.checker(precision=precision)
+    rep = inflate_edge(Segment(v[0], v[1]), dom, InflationParams(**rec["params"]), ck, seed=rec["seed"])
+    return rep, ck, dom, v
+
+
+def test_fp64_reproduces_reference_polytopes():
+    # same RNG stream + fp64 checks: the reference's polytope, iteration and check counts
+    z, index = inflate_index()
+    for rec in index:
+        rep, ck, dom, v = _run(rec, z, "fp64")
+        assert rep.iterations == rec["iterations"], rec["key"]
+        assert rep.hyperplanes_added == rec["hyperplanes_added"], rec["key"]
+        assert rep.collision_checks == rec["collision_checks"], rec["key"]
+        assert rep.terminated_by == rec["terminated_by"], rec["key"]
+        assert ck.calls == rec["collision_checks"]
+        assert np.allclose(rep.polytope.A, z[f"{rec['key']}_A"], atol=1e-9), rec["key"]
+        assert np.allclose(rep.polytope.b, z[f"{rec['key']}_b"], atol=1e-9), rec["key"]
+
+
+def test_fp32_matches_reference_outside_contact_band():
+    z, index = inflate_index()
+    same = 0
+    for rec in index:
+        rep, ck, dom, v = _run(rec, z, "fp32")
+        P = rep.polytope
+        assert P.contains(v[0], 1e-9) and P.contains(v[1], 1e-9)
+        if (rep.hyperplanes_added == rec["hyperplanes_added"] and P.n_faces == z[f"{rec['key']}_A"].shape[0]
+                and np.allclose(P.A, z[f"{rec['key']}_A"], atol=1e-6)):
+            same += 1
+    assert same >= len(index) - 1
+
+
+def test_empty_world_returns_domain():
+    dom = HPolytope.from_bounds([-5, -5], [5, 5])
+    ck = World(fx.point_robot_model()).checker()
+    rep = inflate_edge(Segment(np.array([-1.0, 0.0]), np.array([1.0, 0.0])), dom, InflationParams(), ck, seed=3)
+    assert rep.terminated_by == "test_accepted" and rep.iterations == 1 and rep.hyperplanes_added == 0
+    assert np.array_equal(rep.polytope.A, dom.A) and np.array_equal(rep.polytope.b, dom.b)
+
+
+def test_seed_outside_domain_and_segment_in_collision():
+    dom = HPolytope.from_bounds([-1, -1], [1, 1])
+    ck = World(fx.point_robot_model()).checker()
+    with pytest.raises(SeedOutsideDomain):
+        inflate_edge(Segment(np.array([0.0, 0.0]), np.array([2.0, 0.0])), dom, InflationParams(), ck)
+    w = fx.disc_world([[1.0, 0.0]], radius=1.0)
+    with pytest.raises(SegmentInCollision):
+        inflate_edge(Segment(np.array([1.0, 0.0]), np.array([3.0, 0.0])), HPolytope.from_bounds([-5, -5], [5, 5]),
+                     InflationParams(), w.checker(), seed=1)
+
+
+@pytest.mark.parametrize("rng", ["counter", "philox"])
+def test_structure_determinism_and_eps_audit(rng):
+    dom = HPolytope.from_bounds([-5, -5], [5, 5])
+    seg = Segment(np.array([-1.0, 0.0]), np.array([1.0, 0.0]))
+    world = fx.disc_world([[0.0, 3.0]], radius=1.0)
+    passes = 0
+    for run in range(10):
+        rep = inflate_edge(seg, dom, InflationParams(), world.checker(), seed=run, rng=rng)
+        P = rep.polytope
+        assert P.contains(seg.v1, 1e-9) and P.contains(seg.v2, 1e-9)
+        assert rep.terminated_by == "test_accepted"
+        assert np.array_equal(P.A[:dom.n_faces], dom.A) and P.n_faces == dom.n_faces + rep.hyperplanes_added
+        mc = np.random.default_rng(10_000 + run)
+        pts = mc.uniform(-5, 5, size=(200_000, 2))
+        inside = pts[P.contains_many(pts)][:20_000]
+        passes += np.mean(~world.checker().check_batch(inside)) <= 0.01
+    assert passes >= 8
+    r1 = inflate_edge(seg, dom, InflationParams(), world.checker(), seed=11, rng=rng)
+    r2 = inflate_edge(seg, dom, InflationParams(), world.checker(), seed=11, rng=rng)
+    assert np.array_equal(r1.polytope.A, r2.polytope.A) and r1.collision_checks == r2.collision_checks
+
+
+def test_franka7_region_contains_segment():
+    world = fx.franka7_world()
+    v1, v2 = fx.random_free_segment(world, seed=3)
+    dom = HPolytope.from_bounds(world.lower, world.upper)
+    rep = inflate_edge(Segment(v1, v2), dom, InflationParams(**fx.FRANKA_PARAMS), world.checker(), seed=7)
+    P = rep.polytope
+    assert rep.terminated_by == "test_accepted"
+    assert P.contains(v1, 1e-9) and P.contains(v2, 1e-9)
+    assert rep.iterations >= 2 and rep.hyperplanes_added >= 10
+    assert np.allclose(np.linalg.norm(P.A, axis=1), 1.0, atol=1e-12)
