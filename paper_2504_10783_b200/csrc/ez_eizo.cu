@@ -525,10 +525,12 @@ template <typename T, int MAXD>
 static int32_t launch_bisect_t(ez_world* w, const ModelDev<T>& M, cudaStream_t s, int n_p, int d, double ee,
                                int n_b, double t_col) {
     ez_eizo_ws* ws = w->eizo;
-    const size_t smem = check_smem_bytes<T>(M.blob_bytes, M.n_spheres, 128, d * static_cast<int>(sizeof(double)));
+    size_t smem = 0;
+    const int threads = check_block_threads<T>(w, M.blob_bytes, M.n_spheres, d * static_cast<int>(sizeof(double)), &smem);
+    if (threads == 0) return fail(EZ_CAPACITY, "robot model too large for one bisection CTA");
     auto kern = k_bisect<T, MAXD>;
     if (smem > 48 * 1024) EZ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    kern<<<static_cast<unsigned>((n_p + 127) / 128), 128, smem, s>>>(M, static_cast<T>(w->margin), ws->X, d, ws->col, ws->rec,
+    kern<<<static_cast<unsigned>((n_p + threads - 1) / threads), threads, smem, s>>>(M, static_cast<T>(w->margin), ws->X, d, ws->col, ws->rec,
                                                                   ws->seg, ee, n_b, t_col, ws->star, ws->pstar, ws->dstar);
     EZ_CUDA(cudaGetLastError());
     return EZ_OK;

@@ -551,22 +551,18 @@ __global__ void k_fk_frames(ModelDev<double> M, const double* __restrict__ Qt, c
 template <typename T, typename Q>
 static int32_t launch_check_t(ez_world* w, const ModelDev<T>& M, const Q* d_q, int64_t n, int64_t ld,
                               uint8_t* d_free, cudaStream_t stream, int64_t count_lim, int32_t* n_col) {
-    const size_t smem = check_smem_bytes<T>(M.blob_bytes, M.n_spheres, kCheckThreads,
-                                            static_cast<int>(M.dof * sizeof(Q)));
+    size_t smem = 0;
+    const int threads = check_block_threads<T>(w, M.blob_bytes, M.n_spheres, static_cast<int>(M.dof * sizeof(Q)), &smem);
+    if (threads == 0) return fail(EZ_CAPACITY, "robot model too large for one checking CTA");
     auto kern = k_check<T, Q>;
-    static thread_local size_t configured[4] = {0, 0, 0, 0};
-    const int slot = (sizeof(T) == 8 ? 2 : 0) + (sizeof(Q) == 8 ? 1 : 0);
-    if (smem > 48 * 1024 && configured[slot] < smem) {
-        EZ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-        configured[slot] = smem;
-    }
+    if (smem > 48 * 1024) EZ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     int occ = 0;
-    EZ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kCheckThreads, smem));
+    EZ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem));
     if (occ < 1) return fail(EZ_CAPACITY, "robot model too large for one checking CTA");
-    const int64_t tiles = (n + kCheckThreads - 1) / kCheckThreads;
+    const int64_t tiles = (n + threads - 1) / threads;
     const int64_t grid = std::min<int64_t>(tiles, static_cast<int64_t>(w->num_sms) * occ);
-    kern<<<static_cast<unsigned>(grid), kCheckThreads, smem, stream>>>(M, d_q, n, ld, d_free, static_cast<T>(w->margin),
-                                                                      count_lim, n_col);
+    kern<<<static_cast<unsigned>(grid), threads, smem, stream>>>(M, d_q, n, ld, d_free, static_cast<T>(w->margin),
+                                                                 count_lim, n_col);
     EZ_CUDA(cudaGetLastError());
     return EZ_OK;
 }
@@ -733,6 +729,7 @@ extern "C" int32_t ez_world_create(const ez_robot_desc* rb, const ez_scene_desc*
     ez_world* w = new ez_world();
     w->device = device;
     cudaDeviceGetAttribute(&w->num_sms, cudaDevAttrMultiProcessorCount, device);
+    cudaDeviceGetAttribute(&w->smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
     w->dim = dim;
     w->dof = hm.dof;
     w->n_joints = nj;
@@ -860,7 +857,9 @@ extern "C" int32_t ez_check_batch_host(ez_world* w, const double* h_q, int64_t n
         }
         pending_out[b] = -1;
         const double* src = h_q + r0 * ld;
-        if (pinned_in) {
+        if (pinned_in && ld == dof) {
+            EZ_CUDA(cudaMemcpyAsync(w->d_stage_in[b], src, sizeof(double) * rows * dof, cudaMemcpyHostToDevice, s));
+        } else if (pinned_in) {
             EZ_CUDA(cudaMemcpy2DAsync(w->d_stage_in[b], sizeof(double) * dof, src, sizeof(double) * ld,
                                       sizeof(double) * dof, rows, cudaMemcpyHostToDevice, s));
         } else {
