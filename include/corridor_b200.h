@@ -72,6 +72,8 @@ typedef struct ez_robot_desc {
     const double* geom_half;      /* [n_geoms][dim] box half extents         */
     int32_t n_pairs;
     const int32_t* pairs;         /* [n_pairs][2] global geometry indices    */
+    const double* joint_lower;    /* [dof] joint limits (optional: used to   */
+    const double* joint_upper;    /* order the tests by hit frequency)       */
 } ez_robot_desc;
 
 /* Obstacles: static geometry posed in the world plus one voxel map
@@ -92,7 +94,7 @@ typedef struct ez_scene_desc {
 
 /* Summary of the device obstacle structure (for tests and benchmarks). */
 typedef struct ez_world_info {
-    int32_t dof, n_links, n_spheres, n_pairs, n_static;
+    int32_t dof, n_links, n_spheres, n_pairs, n_static, n_hot_pairs;
     int64_t n_voxels;
     int32_t grid_dims[3];         /* cells of the voxel distance grid        */
     double cell_side;             /* h = voxel side / subdivision            */

@@ -27,7 +27,7 @@ class RobotDesc(C.Structure):
                 ("joint_trans", P_dbl), ("joint_axis", P_dbl),
                 ("n_geoms", c_i32), ("geom_link", P_i32), ("geom_kind", P_i32), ("geom_rot", P_dbl),
                 ("geom_trans", P_dbl), ("geom_radius", P_dbl), ("geom_half", P_dbl),
-                ("n_pairs", c_i32), ("pairs", P_i32)]
+                ("n_pairs", c_i32), ("pairs", P_i32), ("joint_lower", P_dbl), ("joint_upper", P_dbl)]
 
 
 class SceneDesc(C.Structure):
@@ -39,7 +39,7 @@ class SceneDesc(C.Structure):
 
 class WorldInfo(C.Structure):
     _fields_ = [("dof", c_i32), ("n_links", c_i32), ("n_spheres", c_i32), ("n_pairs", c_i32),
-                ("n_static", c_i32), ("n_voxels", c_i64), ("grid_dims", c_i32 * 3),
+                ("n_static", c_i32), ("n_hot_pairs", c_i32), ("n_voxels", c_i64), ("grid_dims", c_i32 * 3),
                 ("cell_side", c_dbl), ("list_entries", c_i64), ("device_bytes", c_i64)]
 
 

@@ -67,6 +67,16 @@ struct alignas(16) SphereRec {
     T pad_[2];
 };
 
+// The self pairs most likely to collide (calibrated on uniform samples at
+// world creation) are tested first, flat, so most colliding configurations
+// leave after one or two pairs; the rest are grouped by first sphere.
+template <typename T>
+struct alignas(16) HotRec {
+    int32_t a, b;
+    T thr2;
+    T pad_;
+};
+
 struct alignas(16) GroupRec {   // self pairs grouped by first sphere
     int32_t a, begin, end, pad_;
 };
@@ -114,10 +124,10 @@ struct VoxGrid {
 
 template <typename T>
 struct ModelDev {
-    const uint8_t* blob;      // device: joints | spheres | groups | pairs | ssph | sbox
+    const uint8_t* blob;      // device: joints | spheres | hot | groups | pairs | order | ssph | sbox
     uint32_t blob_bytes;      // multiple of 16
-    int32_t n_joints, dof, n_spheres, n_groups, n_pairs, n_ssph, n_sbox, n_store;
-    uint32_t off_spheres, off_groups, off_pairs, off_ssph, off_sbox;
+    int32_t n_joints, dof, n_spheres, n_hot, n_groups, n_pairs, n_ssph, n_sbox, n_store;
+    uint32_t off_spheres, off_hot, off_groups, off_pairs, off_order, off_ssph, off_sbox;
     VoxGrid<T> vox;
 };
 

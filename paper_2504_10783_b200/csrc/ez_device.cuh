@@ -244,22 +244,46 @@ __device__ __forceinline__ bool sphere_hits_obstacles(const ModelDev<T>& M,
     return false;
 }
 
-// Everything about one configuration whose sphere centres are in `cen`.
+// Phase A: the calibrated hot self pairs (flat list, most frequent first).
 template <typename T>
-__device__ __forceinline__ bool config_collides(const ModelDev<T>& M, const uint8_t* blob,
-                                                const T* __restrict__ cen, int stride, T margin) {
+__device__ __forceinline__ bool hot_pairs_collide(const ModelDev<T>& M, const uint8_t* blob,
+                                                  const T* __restrict__ cen, int stride) {
+    const HotRec<T>* H = reinterpret_cast<const HotRec<T>*>(blob + M.off_hot);
+    for (int p = 0; p < M.n_hot; ++p) {
+        const HotRec<T> h = H[p];
+        const T dx = cen[(3 * h.a) * stride] - cen[(3 * h.b) * stride];
+        const T dy = cen[(3 * h.a + 1) * stride] - cen[(3 * h.b + 1) * stride];
+        const T dz = cen[(3 * h.a + 2) * stride] - cen[(3 * h.b + 2) * stride];
+        if (dx * dx + dy * dy + dz * dz <= h.thr2) return true;
+    }
+    return false;
+}
+
+// Phase B: obstacles (spheres in calibrated hit-frequency order), then the
+// remaining self pairs grouped by first sphere.
+template <typename T>
+__device__ __forceinline__ bool rest_collides(const ModelDev<T>& M, const uint8_t* blob,
+                                              const T* __restrict__ cen, int stride, T margin) {
     const SphereRec<T>* S = reinterpret_cast<const SphereRec<T>*>(blob + M.off_spheres);
-    const GroupRec* G = reinterpret_cast<const GroupRec*>(blob + M.off_groups);
-    const PairRec<T>* P = reinterpret_cast<const PairRec<T>*>(blob + M.off_pairs);
-    if (self_collides<T>(G, M.n_groups, P, cen, stride)) return true;
+    const int32_t* order = reinterpret_cast<const int32_t*>(blob + M.off_order);
     const StaticSphereRec<T>* SS = reinterpret_cast<const StaticSphereRec<T>*>(blob + M.off_ssph);
     const StaticBoxRec<T>* SB = reinterpret_cast<const StaticBoxRec<T>*>(blob + M.off_sbox);
-    for (int s = 0; s < M.n_spheres; ++s) {
+    for (int k = 0; k < M.n_spheres; ++k) {
+        const int s = order[k];
         if (sphere_hits_obstacles<T>(M, S[s], SS, SB, margin, cen[(3 * s) * stride],
                                      cen[(3 * s + 1) * stride], cen[(3 * s + 2) * stride]))
             return true;
     }
-    return false;
+    const GroupRec* G = reinterpret_cast<const GroupRec*>(blob + M.off_groups);
+    const PairRec<T>* P = reinterpret_cast<const PairRec<T>*>(blob + M.off_pairs);
+    return self_collides<T>(G, M.n_groups, P, cen, stride);
+}
+
+// Everything about one configuration whose sphere centres are in `cen`.
+template <typename T>
+__device__ __forceinline__ bool config_collides(const ModelDev<T>& M, const uint8_t* blob,
+                                                const T* __restrict__ cen, int stride, T margin) {
+    return hot_pairs_collide<T>(M, blob, cen, stride) || rest_collides<T>(M, blob, cen, stride, margin);
 }
 
 // Full check of one configuration q (dof values).  Returns true if free.

@@ -11,6 +11,7 @@
 #include <algorithm>
 #include <climits>
 #include <cmath>
+#include <mutex>
 #include <vector>
 
 #include "ez_device.cuh"
@@ -460,17 +461,26 @@ static int32_t grow(Tp** p, int64_t old_n, int64_t new_n, bool keep) {
     return EZ_OK;
 }
 
+// One EI-ZO workspace per device, shared by every world on it (inflations on
+// a device are serialised by g_ws_mu), so repeated inflations with fresh
+// checkers never allocate inside the loop.
+static std::mutex g_ws_mu;
+static ez_eizo_ws* g_ws[64] = {};
+
+static ez_eizo_ws*& device_ws(int device) { return g_ws[device & 63]; }
+
 static int32_t ws_reserve(ez_world* w, int d, int64_t n, int32_t c, int32_t f) {
-    if (!w->eizo) {
-        w->eizo = new ez_eizo_ws();
-        EZ_CUDA(cudaStreamCreateWithFlags(&w->eizo->stream, cudaStreamNonBlocking));
-        EZ_CUDA(cudaEventCreate(&w->eizo->ev0));
-        EZ_CUDA(cudaEventCreate(&w->eizo->ev1));
-        EZ_CUDA(cudaMalloc(&w->eizo->rec, 64));
-        EZ_CUDA(cudaMallocHost(&w->eizo->h_rec, 64));
-        EZ_CUDA(cudaMalloc(&w->eizo->seg, sizeof(double) * 3 * 64));
+    ez_eizo_ws*& slot = device_ws(w->device);
+    if (!slot) {
+        slot = new ez_eizo_ws();
+        EZ_CUDA(cudaStreamCreateWithFlags(&slot->stream, cudaStreamNonBlocking));
+        EZ_CUDA(cudaEventCreate(&slot->ev0));
+        EZ_CUDA(cudaEventCreate(&slot->ev1));
+        EZ_CUDA(cudaMalloc(&slot->rec, 64));
+        EZ_CUDA(cudaMallocHost(&slot->h_rec, 64));
+        EZ_CUDA(cudaMalloc(&slot->seg, sizeof(double) * 3 * 64));
     }
-    ez_eizo_ws* ws = w->eizo;
+    ez_eizo_ws* ws = slot;
     if (ws->d != d) {
         ws->n_cap = ws->c_cap = ws->f_cap = 0;
         ws->d = d;
@@ -524,7 +534,7 @@ static int32_t dispatch_hnr(int rng, unsigned grid, cudaStream_t s, const double
 template <typename T, int MAXD>
 static int32_t launch_bisect_t(ez_world* w, const ModelDev<T>& M, cudaStream_t s, int n_p, int d, double ee,
                                int n_b, double t_col) {
-    ez_eizo_ws* ws = w->eizo;
+    ez_eizo_ws* ws = device_ws(w->device);
     size_t smem = 0;
     const int threads = check_block_threads<T>(w, M.blob_bytes, M.n_spheres, d * static_cast<int>(sizeof(double)), &smem);
     if (threads == 0) return fail(EZ_CAPACITY, "robot model too large for one bisection CTA");
@@ -592,7 +602,7 @@ extern "C" int32_t ez_inflate_edge(ez_world* w, const double* h_v1, const double
     const ez_eizo_params& p = *params;
     if (p.n_p < 1 || p.n_f < 1 || p.n_b < 1 || p.n_ms < 1) return fail(EZ_INVALID_ARGUMENT, "counts must be >= 1");
     if (rng != EZ_RNG_COUNTER && rng != EZ_RNG_PHILOX) return fail(EZ_INVALID_ARGUMENT, "unknown rng");
-    std::lock_guard<std::mutex> lock(w->mu);
+    std::lock_guard<std::mutex> lock(g_ws_mu);
     EZ_CUDA(cudaSetDevice(w->device));
     const int d = dim;
     // seed segment strictly inside the domain (inflation.py:274-277), fp64 on the host
@@ -606,9 +616,9 @@ extern "C" int32_t ez_inflate_edge(ez_world* w, const double* h_v1, const double
         }
         if (worst >= 0.0) return fail(EZ_SEED_OUTSIDE_DOMAIN, "seed segment must be strictly inside the domain");
     }
-    int64_t n_max = p.n_p;
-    EZ_TRY(ws_reserve(w, d, std::max<int64_t>(n_max, batch_size(1, p)), p.n_p, n_faces0 + 16 * p.n_f));
-    ez_eizo_ws* ws = w->eizo;
+    // capacity for 64 iterations up front: no allocation inside the loop
+    EZ_TRY(ws_reserve(w, d, std::max<int64_t>(p.n_p, batch_size(64, p)), p.n_p, n_faces0 + 64 * p.n_f));
+    ez_eizo_ws* ws = device_ws(w->device);
     cudaStream_t s = ws->stream;
     std::vector<double> seg(3 * d);
     double ee = 0.0;

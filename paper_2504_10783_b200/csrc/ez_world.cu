@@ -14,11 +14,12 @@
 #include <cub/device/device_scan.cuh>
 
 #include "ez_device.cuh"
+#include "ez_rng.cuh"
 #include "ez_world.h"
 
 namespace ez {
 
-constexpr int kCheckThreads = 128;
+constexpr int kCheckThreads = 256;
 
 // ---------------------------------------------------------------------------
 // host-side model folding
@@ -100,16 +101,68 @@ struct HPair {
 struct HGroup {
     int a, begin, end;
 };
+struct HSelfPair {   // input order
+    int a, b;
+    double thr2;
+};
 struct HModel {
     std::vector<HJoint> joints;
     std::vector<M3> linkQt;
     std::vector<HSphere> spheres;
+    std::vector<HSelfPair> all_pairs;
+    std::vector<HSelfPair> hot;
     std::vector<HGroup> groups;
     std::vector<HPair> pairs;
+    std::vector<int> pair_src;  // flat grouped position -> index in all_pairs
+    std::vector<int32_t> order; // obstacle-test order of the spheres
     std::vector<double> ssph;  // c3, r
     std::vector<double> sbox;  // Rt9, t3, he3
     int dof = 0, n_store = 0;
 };
+
+constexpr int kHotPairs = 16;
+
+// Pair/sphere layout.  Without statistics: no hot list, link order.  With
+// per-pair and per-sphere hit counts: the kHotPairs most frequent self pairs
+// first (flat), the rest grouped by first sphere, spheres tested against
+// obstacles in decreasing hit frequency.
+void layout_pairs(HModel& hm, const std::vector<uint32_t>* pair_hits, const std::vector<uint32_t>* sph_hits) {
+    const int np = static_cast<int>(hm.all_pairs.size());
+    std::vector<int> rank(np);
+    for (int i = 0; i < np; ++i) rank[i] = i;
+    std::vector<char> is_hot(np, 0);
+    hm.hot.clear();
+    if (pair_hits) {
+        std::stable_sort(rank.begin(), rank.end(), [&](int x, int y) { return (*pair_hits)[x] > (*pair_hits)[y]; });
+        for (int k = 0; k < std::min(kHotPairs, np); ++k) {
+            if ((*pair_hits)[rank[k]] == 0) break;
+            is_hot[rank[k]] = 1;
+            hm.hot.push_back(hm.all_pairs[rank[k]]);
+        }
+    }
+    const int ns = static_cast<int>(hm.spheres.size());
+    std::vector<std::vector<int>> by_a(ns);
+    for (int i = 0; i < np; ++i)
+        if (!is_hot[i]) by_a[hm.all_pairs[i].a].push_back(i);
+    hm.groups.clear();
+    hm.pairs.clear();
+    hm.pair_src.clear();
+    for (int a = 0; a < ns; ++a) {
+        if (by_a[a].empty()) continue;
+        HGroup g{a, static_cast<int>(hm.pairs.size()), 0};
+        for (int i : by_a[a]) {
+            hm.pairs.push_back(HPair{hm.all_pairs[i].b, hm.all_pairs[i].thr2});
+            hm.pair_src.push_back(i);
+        }
+        g.end = static_cast<int>(hm.pairs.size());
+        hm.groups.push_back(g);
+    }
+    hm.order.resize(ns);
+    for (int i = 0; i < ns; ++i) hm.order[i] = i;
+    if (sph_hits)
+        std::stable_sort(hm.order.begin(), hm.order.end(),
+                         [&](int x, int y) { return (*sph_hits)[x] > (*sph_hits)[y]; });
+}
 
 size_t align16(size_t x) { return (x + 15) & ~static_cast<size_t>(15); }
 
@@ -117,18 +170,33 @@ template <typename T>
 std::vector<uint8_t> pack_blob(const HModel& hm, ModelDev<T>& md) {
     const size_t sz_j = align16(hm.joints.size() * sizeof(JointRec<T>));
     const size_t sz_s = align16(hm.spheres.size() * sizeof(SphereRec<T>));
+    const size_t sz_h = align16(hm.hot.size() * sizeof(HotRec<T>));
     const size_t sz_g = align16(hm.groups.size() * sizeof(GroupRec));
     const size_t sz_p = align16(hm.pairs.size() * sizeof(PairRec<T>));
+    const size_t sz_o = align16(hm.order.size() * sizeof(int32_t));
     const size_t n_ss = hm.ssph.size() / 4, n_sb = hm.sbox.size() / 15;
     const size_t sz_ss = align16(n_ss * sizeof(StaticSphereRec<T>));
     const size_t sz_sb = align16(n_sb * sizeof(StaticBoxRec<T>));
-    std::vector<uint8_t> blob(std::max<size_t>(16, sz_j + sz_s + sz_g + sz_p + sz_ss + sz_sb), 0);
-    md.off_spheres = static_cast<uint32_t>(sz_j);
-    md.off_groups = static_cast<uint32_t>(sz_j + sz_s);
-    md.off_pairs = static_cast<uint32_t>(sz_j + sz_s + sz_g);
-    md.off_ssph = static_cast<uint32_t>(sz_j + sz_s + sz_g + sz_p);
-    md.off_sbox = static_cast<uint32_t>(sz_j + sz_s + sz_g + sz_p + sz_ss);
+    size_t off = sz_j;
+    md.off_spheres = static_cast<uint32_t>(off); off += sz_s;
+    md.off_hot = static_cast<uint32_t>(off); off += sz_h;
+    md.off_groups = static_cast<uint32_t>(off); off += sz_g;
+    md.off_pairs = static_cast<uint32_t>(off); off += sz_p;
+    md.off_order = static_cast<uint32_t>(off); off += sz_o;
+    md.off_ssph = static_cast<uint32_t>(off); off += sz_ss;
+    md.off_sbox = static_cast<uint32_t>(off); off += sz_sb;
+    std::vector<uint8_t> blob(std::max<size_t>(16, off), 0);
     md.blob_bytes = static_cast<uint32_t>(blob.size());
+    auto* HR = reinterpret_cast<HotRec<T>*>(blob.data() + md.off_hot);
+    for (size_t i = 0; i < hm.hot.size(); ++i) {
+        HotRec<T> r{};
+        r.a = hm.hot[i].a;
+        r.b = hm.hot[i].b;
+        r.thr2 = static_cast<T>(hm.hot[i].thr2);
+        HR[i] = r;
+    }
+    auto* OR = reinterpret_cast<int32_t*>(blob.data() + md.off_order);
+    for (size_t i = 0; i < hm.order.size(); ++i) OR[i] = hm.order[i];
     auto* J = reinterpret_cast<JointRec<T>*>(blob.data());
     for (size_t j = 0; j < hm.joints.size(); ++j) {
         const HJoint& h = hm.joints[j];
@@ -185,6 +253,7 @@ std::vector<uint8_t> pack_blob(const HModel& hm, ModelDev<T>& md) {
     md.n_joints = static_cast<int32_t>(hm.joints.size());
     md.dof = hm.dof;
     md.n_spheres = static_cast<int32_t>(hm.spheres.size());
+    md.n_hot = static_cast<int32_t>(hm.hot.size());
     md.n_groups = static_cast<int32_t>(hm.groups.size());
     md.n_pairs = static_cast<int32_t>(hm.pairs.size());
     md.n_ssph = static_cast<int32_t>(n_ss);
@@ -451,12 +520,42 @@ static int32_t build_voxel_grid(ez_world* w, const ez_scene_desc* sc, const HMod
 // ---------------------------------------------------------------------------
 // kernels: fused check, FK frames
 // ---------------------------------------------------------------------------
+// Fused FK + collision check in two phases:
+//   A) per tile, every thread: FK -> sphere centres (smem) -> calibrated hot
+//      self pairs.  Most colliding configurations are decided here.
+//   B) survivors are appended (in order) to a CTA queue; whenever a full
+//      CTA's worth is queued, every thread takes one, reloads its row,
+//      recomputes FK and runs the obstacle tests and remaining pairs.  Phase B
+//      therefore always runs on full warps and no warp idles at a barrier
+//      while a few lanes finish the expensive tail.
+template <typename T, typename Q>
+__device__ __forceinline__ void check_phase_b(const ModelDev<T>& M, const uint8_t* smem, const Q* __restrict__ q,
+                                              int64_t ld, int64_t idx, Q* row, T* cen, int stride, T margin,
+                                              uint8_t* __restrict__ out, int64_t count_lim, int32_t* n_col) {
+    const int dof = M.dof;
+    Q v[32];
+#pragma unroll
+    for (int k = 0; k < 32; ++k)
+        if (k < dof) v[k] = q[idx * ld + k];
+#pragma unroll
+    for (int k = 0; k < 32; ++k)
+        if (k < dof) row[k] = v[k];
+    const JointRec<T>* J = reinterpret_cast<const JointRec<T>*>(smem);
+    const SphereRec<T>* S = reinterpret_cast<const SphereRec<T>*>(smem + M.off_spheres);
+    fk_sphere_centres<T, Q>(J, M.n_joints, S, row, cen, stride);
+    const bool c2 = rest_collides<T>(M, smem, cen, stride, margin);
+    out[idx] = c2 ? 0 : 1;
+    if (n_col != nullptr && c2 && idx < count_lim) atomicAdd(n_col, 1);
+}
+
 template <typename T, typename Q>
 __global__ void __launch_bounds__(kCheckThreads)
 k_check(ModelDev<T> M, const Q* __restrict__ q, int64_t n, int64_t ld, uint8_t* __restrict__ out,
         T margin, int64_t count_lim, int32_t* __restrict__ n_col) {
     extern __shared__ __align__(16) uint8_t smem[];
     __shared__ uint64_t bar;
+    __shared__ int32_t s_queue[2 * kCheckThreads];
+    __shared__ int s_warp[kCheckThreads / 32];
     tma_stage(smem, M.blob, M.blob_bytes, &bar);
     T* cen = reinterpret_cast<T*>(smem + M.blob_bytes);
     const size_t roff = (static_cast<size_t>(M.blob_bytes) +
@@ -464,34 +563,68 @@ k_check(ModelDev<T> M, const Q* __restrict__ q, int64_t n, int64_t ld, uint8_t* 
                         ~static_cast<size_t>(15);
     Q* rows = reinterpret_cast<Q*>(smem + roff);
     const int dof = M.dof;
-    const int64_t tiles = (n + blockDim.x - 1) / blockDim.x;
+    const int T_ = blockDim.x, qcap = 2 * blockDim.x;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+    const JointRec<T>* J = reinterpret_cast<const JointRec<T>*>(smem);
+    const SphereRec<T>* S = reinterpret_cast<const SphereRec<T>*>(smem + M.off_spheres);
+    T* my_cen = cen + threadIdx.x;
+    Q* my_row = rows + threadIdx.x * dof;
+    int qhead = 0, qn = 0;  // ring buffer state (uniform across the CTA)
+    const int64_t tiles = (n + T_ - 1) / T_;
     for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
-        const int64_t base = tile * blockDim.x;
-        const int nr = static_cast<int>(min(static_cast<int64_t>(blockDim.x), n - base));
+        const int64_t base = tile * T_;
+        const int nr = static_cast<int>(min(static_cast<int64_t>(T_), n - base));
         __syncthreads();
-        // coalesced staging of this tile's configurations
         if (ld == dof) {
             const Q* src = q + base * dof;
             const int tot = nr * dof;
-            for (int i = threadIdx.x; i < tot; i += blockDim.x) rows[i] = src[i];
+            for (int i = threadIdx.x; i < tot; i += T_) rows[i] = src[i];
         } else {
-            for (int i = threadIdx.x; i < nr * dof; i += blockDim.x) {
+            for (int i = threadIdx.x; i < nr * dof; i += T_) {
                 const int r = i / dof, k = i - r * dof;
                 rows[i] = q[(base + r) * ld + k];
             }
         }
         __syncthreads();
+        // phase A
+        const bool valid = threadIdx.x < nr;
         bool col = false;
-        if (threadIdx.x < nr) {
-            col = !config_free<T, Q>(M, smem, rows + threadIdx.x * dof, cen + threadIdx.x,
-                                      blockDim.x, margin);
-            out[base + threadIdx.x] = col ? 0 : 1;
+        if (valid) {
+            fk_sphere_centres<T, Q>(J, M.n_joints, S, my_row, my_cen, T_);
+            col = hot_pairs_collide<T>(M, smem, my_cen, T_);
+            if (col) out[base + threadIdx.x] = 0;
         }
         if (n_col != nullptr) {
             const unsigned m = __ballot_sync(0xffffffffu, col && (base + threadIdx.x) < count_lim);
-            if ((threadIdx.x & 31) == 0 && m) atomicAdd(n_col, __popc(m));
+            if (lane == 0 && m) atomicAdd(n_col, __popc(m));
+        }
+        // append the survivors to the queue, in index order
+        const bool surv = valid && !col;
+        const unsigned sm = __ballot_sync(0xffffffffu, surv);
+        if (lane == 0) s_warp[wid] = __popc(sm);
+        __syncthreads();
+        int off = 0, add = 0;
+        for (int w = 0; w < nwarps; ++w) {
+            const int c = s_warp[w];
+            off += (w < wid) ? c : 0;
+            add += c;
+        }
+        if (surv) s_queue[(qhead + qn + off + __popc(sm & ((1u << lane) - 1u))) % qcap] = static_cast<int32_t>(base + threadIdx.x);
+        qn += add;
+        __syncthreads();
+        // phase B on full CTAs
+        while (qn >= T_) {
+            check_phase_b<T, Q>(M, smem, q, ld, s_queue[(qhead + threadIdx.x) % qcap], my_row, my_cen, T_, margin,
+                                out, count_lim, n_col);
+            qhead = (qhead + T_) % qcap;
+            qn -= T_;
+            __syncthreads();
         }
     }
+    // drain
+    if (threadIdx.x < qn)
+        check_phase_b<T, Q>(M, smem, q, ld, s_queue[(qhead + threadIdx.x) % qcap], my_row, my_cen, T_, margin, out,
+                            count_lim, n_col);
 }
 
 // link frames (true frames, fp64) for fk_batch / forward_kinematics
@@ -548,22 +681,155 @@ __global__ void k_fk_frames(ModelDev<double> M, const double* __restrict__ Qt, c
     }
 }
 
+// Hit statistics of every self pair and every sphere-vs-obstacle test over
+// uniform samples of the joint box; used only to order the tests.
+__global__ void __launch_bounds__(128)
+k_calibrate(ModelDev<float> M, const float* __restrict__ lo, const float* __restrict__ hi, int n, uint64_t seed,
+            float margin, uint32_t* __restrict__ pair_hits, uint32_t* __restrict__ sph_hits) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    __shared__ uint64_t bar;
+    tma_stage(smem, M.blob, M.blob_bytes, &bar);
+    float* cen = reinterpret_cast<float*>(smem + M.blob_bytes);
+    const size_t roff = (static_cast<size_t>(M.blob_bytes) + static_cast<size_t>(3) * M.n_spheres * blockDim.x * 4 + 15) &
+                        ~static_cast<size_t>(15);
+    float* q = reinterpret_cast<float*>(smem + roff) + threadIdx.x * M.dof;
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    for (int k = 0; k < M.dof; ++k) {
+        const Philox4 r = philox_draw(seed, static_cast<uint64_t>(i), static_cast<uint32_t>(k), 0u);
+        const float u = (static_cast<float>(r.x >> 8) + 0.5f) * 0x1p-24f;
+        q[k] = lo[k] + (hi[k] - lo[k]) * u;
+    }
+    const JointRec<float>* J = reinterpret_cast<const JointRec<float>*>(smem);
+    const SphereRec<float>* S = reinterpret_cast<const SphereRec<float>*>(smem + M.off_spheres);
+    float* c = cen + threadIdx.x;
+    const int st = blockDim.x;
+    fk_sphere_centres<float, float>(J, M.n_joints, S, q, c, st);
+    const GroupRec* G = reinterpret_cast<const GroupRec*>(smem + M.off_groups);
+    const PairRec<float>* P = reinterpret_cast<const PairRec<float>*>(smem + M.off_pairs);
+    for (int g = 0; g < M.n_groups; ++g) {
+        const GroupRec gr = G[g];
+        for (int p = gr.begin; p < gr.end; ++p) {
+            const int b = P[p].b;
+            const float dx = c[3 * gr.a * st] - c[3 * b * st], dy = c[(3 * gr.a + 1) * st] - c[(3 * b + 1) * st],
+                        dz = c[(3 * gr.a + 2) * st] - c[(3 * b + 2) * st];
+            if (dx * dx + dy * dy + dz * dz <= P[p].thr2) atomicAdd(pair_hits + p, 1u);
+        }
+    }
+    const StaticSphereRec<float>* SS = reinterpret_cast<const StaticSphereRec<float>*>(smem + M.off_ssph);
+    const StaticBoxRec<float>* SB = reinterpret_cast<const StaticBoxRec<float>*>(smem + M.off_sbox);
+    for (int s = 0; s < M.n_spheres; ++s)
+        if (sphere_hits_obstacles<float>(M, S[s], SS, SB, margin, c[3 * s * st], c[(3 * s + 1) * st], c[(3 * s + 2) * st]))
+            atomicAdd(sph_hits + s, 1u);
+}
+
+static int32_t calibrate_layout(ez_world* w, HModel& hm, const double* lower, const double* upper) {
+    const int n = 1 << 15;
+    const int dof = hm.dof;
+    std::vector<float> lh(2 * dof);
+    for (int k = 0; k < dof; ++k) {
+        lh[k] = static_cast<float>(lower[k]);
+        lh[dof + k] = static_cast<float>(upper[k]);
+    }
+    const size_t np = std::max<size_t>(1, hm.pairs.size()), ns = std::max<size_t>(1, hm.spheres.size());
+    float* d_lh = nullptr;
+    uint32_t* d_cnt = nullptr;
+    EZ_CUDA(cudaMalloc(&d_lh, sizeof(float) * 2 * dof));
+    EZ_CUDA(cudaMemcpy(d_lh, lh.data(), sizeof(float) * 2 * dof, cudaMemcpyHostToDevice));
+    EZ_CUDA(cudaMalloc(&d_cnt, sizeof(uint32_t) * (np + ns)));
+    EZ_CUDA(cudaMemset(d_cnt, 0, sizeof(uint32_t) * (np + ns)));
+    size_t smem = 0;
+    const int threads = check_block_threads<float>(w, w->mf.blob_bytes, w->mf.n_spheres, dof * 4, &smem);
+    if (threads == 0) return fail(EZ_CAPACITY, "robot model too large for one checking CTA");
+    if (smem > 48 * 1024)
+        EZ_CUDA(cudaFuncSetAttribute(k_calibrate, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    k_calibrate<<<(n + threads - 1) / threads, threads, smem>>>(w->mf, d_lh, d_lh + dof, n, 0x5EEDC0DEull,
+                                                                static_cast<float>(w->margin), d_cnt, d_cnt + np);
+    EZ_CUDA(cudaGetLastError());
+    std::vector<uint32_t> cnt(np + ns);
+    EZ_CUDA(cudaMemcpy(cnt.data(), d_cnt, sizeof(uint32_t) * (np + ns), cudaMemcpyDeviceToHost));
+    cudaFree(d_lh);
+    cudaFree(d_cnt);
+    std::vector<uint32_t> pair_hits(hm.all_pairs.size(), 0), sph_hits(hm.spheres.size(), 0);
+    for (size_t p = 0; p < hm.pair_src.size(); ++p) pair_hits[hm.pair_src[p]] = cnt[p];
+    for (size_t s = 0; s < hm.spheres.size(); ++s) sph_hits[s] = cnt[np + s];
+    layout_pairs(hm, &pair_hits, &sph_hits);
+    for (int i = 0; i < 2; ++i) {
+        std::vector<uint8_t> blob = (i == 0) ? pack_blob<float>(hm, w->mf) : pack_blob<double>(hm, w->md);
+        uint8_t* d = nullptr;
+        EZ_CUDA(cudaMalloc(&d, blob.size()));
+        EZ_CUDA(cudaMemcpy(d, blob.data(), blob.size(), cudaMemcpyHostToDevice));
+        cudaFree(w->d_blob[i]);
+        w->d_blob[i] = d;
+    }
+    w->mf.blob = w->d_blob[0];
+    w->md.blob = w->d_blob[1];
+    w->n_groups = static_cast<int32_t>(hm.groups.size());
+    w->n_hot = static_cast<int32_t>(hm.hot.size());
+    return EZ_OK;
+}
+
+// CTA size with the most resident warps per SM: the per-thread sphere-centre
+// store makes shared memory the occupancy limiter, and 256-thread CTAs can
+// strand a large fraction of it (e.g. 160 x 3 CTAs beats 256 x 1 for the
+// 33-sphere arm).  Cached per kernel instantiation and model size.
+template <typename K>
+static int32_t pick_threads(const ez_world* w, K kern, uint32_t blob_bytes, int n_spheres, int tsize, int row_bytes,
+                            int max_threads, int* threads, size_t* smem) {
+    cudaFuncAttributes fa{};
+    EZ_CUDA(cudaFuncGetAttributes(&fa, kern));
+    const size_t max_dyn = static_cast<size_t>(w->smem_optin) - fa.sharedSizeBytes;
+    EZ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(max_dyn)));
+    int best_t = 0, best_warps = -1;
+    size_t best_s = 0;
+    for (int t = 32; t <= max_threads; t += 32) {
+        size_t b = blob_bytes + static_cast<size_t>(3) * n_spheres * t * tsize;
+        b = (b + 15) & ~static_cast<size_t>(15);
+        b += static_cast<size_t>(t) * row_bytes;
+        b = (b + 15) & ~static_cast<size_t>(15);
+        if (b > max_dyn) break;
+        int occ = 0;
+        EZ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, t, b));
+        const int warps = occ * t / 32;
+        if (warps >= best_warps && occ > 0) {
+            best_warps = warps;
+            best_t = t;
+            best_s = b;
+        }
+    }
+    if (best_t == 0) return fail(EZ_CAPACITY, "robot model too large for one checking CTA");
+    *threads = best_t;
+    *smem = best_s;
+    return EZ_OK;
+}
+
 template <typename T, typename Q>
 static int32_t launch_check_t(ez_world* w, const ModelDev<T>& M, const Q* d_q, int64_t n, int64_t ld,
                               uint8_t* d_free, cudaStream_t stream, int64_t count_lim, int32_t* n_col) {
-    size_t smem = 0;
-    const int threads = check_block_threads<T>(w, M.blob_bytes, M.n_spheres, static_cast<int>(M.dof * sizeof(Q)), &smem);
-    if (threads == 0) return fail(EZ_CAPACITY, "robot model too large for one checking CTA");
     auto kern = k_check<T, Q>;
-    if (smem > 48 * 1024) EZ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    int occ = 0;
-    EZ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem));
-    if (occ < 1) return fail(EZ_CAPACITY, "robot model too large for one checking CTA");
-    const int64_t tiles = (n + threads - 1) / threads;
-    const int64_t grid = std::min<int64_t>(tiles, static_cast<int64_t>(w->num_sms) * occ);
-    kern<<<static_cast<unsigned>(grid), threads, smem, stream>>>(M, d_q, n, ld, d_free, static_cast<T>(w->margin),
-                                                                 count_lim, n_col);
-    EZ_CUDA(cudaGetLastError());
+    const int slot = (sizeof(T) == 8 ? 2 : 0) + (sizeof(Q) == 8 ? 1 : 0);
+    if (w->launch_threads[slot] == 0) {
+        int t = 0;
+        size_t sm = 0;
+        EZ_TRY(pick_threads(w, kern, M.blob_bytes, M.n_spheres, static_cast<int>(sizeof(T)),
+                            static_cast<int>(M.dof * sizeof(Q)), kCheckThreads, &t, &sm));
+        int occ = 0;
+        EZ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, t, sm));
+        w->launch_threads[slot] = t;
+        w->launch_smem[slot] = sm;
+        w->launch_occ[slot] = occ;
+    }
+    const int threads = w->launch_threads[slot];
+    const size_t smem = w->launch_smem[slot];
+    const int64_t chunk = int64_t(1) << 30;  // queue entries are int32 row indices
+    for (int64_t r0 = 0; r0 < n; r0 += chunk) {
+        const int64_t rows = std::min(chunk, n - r0);
+        const int64_t tiles = (rows + threads - 1) / threads;
+        const int64_t grid = std::min<int64_t>(tiles, static_cast<int64_t>(w->num_sms) * w->launch_occ[slot]);
+        kern<<<static_cast<unsigned>(grid), threads, smem, stream>>>(
+            M, d_q + r0 * ld, rows, ld, d_free + r0, static_cast<T>(w->margin), count_lim - r0, n_col);
+        EZ_CUDA(cudaGetLastError());
+    }
     return EZ_OK;
 }
 
@@ -663,6 +929,7 @@ extern "C" int32_t ez_world_create(const ez_robot_desc* rb, const ez_scene_desc*
         hm.linkQt.push_back(mat_T(P));
     }
     hm.dof = qi;
+    if (hm.dof > 32) return fail(EZ_UNSUPPORTED, "more than 32 degrees of freedom");
 
     // robot geometry: spheres (boxes are not supported natively yet)
     const double r_vox = (sc && sc->n_voxels > 0) ? 0.5 * sc->voxel_side * std::sqrt(static_cast<double>(dim)) : 0.0;
@@ -691,26 +958,18 @@ extern "C" int32_t ez_world_create(const ez_robot_desc* rb, const ez_scene_desc*
         hm.joints[j].sb = b;
         hm.joints[j].se = e;
     }
-    // self pairs grouped by first sphere (pairs keep their order within a group)
-    {
-        std::vector<std::vector<HPair>> by_a(rb->n_geoms);
-        for (int p = 0; p < rb->n_pairs; ++p) {
-            int a = rb->pairs[2 * p], b = rb->pairs[2 * p + 1];
-            if (a < 0 || b < 0 || a >= rb->n_geoms || b >= rb->n_geoms)
-                return fail(EZ_INVALID_ARGUMENT, "self pair index out of range");
-            if (rb->geom_link[a] == rb->geom_link[b])
-                return fail(EZ_INVALID_ARGUMENT, "self-collision pair on a single link");
-            const double rr = (rb->geom_radius[a] + rb->geom_radius[b]) + margin;
-            by_a[a].push_back(HPair{b, rr * rr});
-        }
-        for (int a = 0; a < rb->n_geoms; ++a) {
-            if (by_a[a].empty()) continue;
-            HGroup g{a, static_cast<int>(hm.pairs.size()), 0};
-            for (const HPair& p : by_a[a]) hm.pairs.push_back(p);
-            g.end = static_cast<int>(hm.pairs.size());
-            hm.groups.push_back(g);
-        }
+    // self pairs (input order); layout_pairs groups them (and, after
+    // calibration, moves the most frequently colliding ones to the hot list)
+    for (int p = 0; p < rb->n_pairs; ++p) {
+        const int a = rb->pairs[2 * p], b = rb->pairs[2 * p + 1];
+        if (a < 0 || b < 0 || a >= rb->n_geoms || b >= rb->n_geoms)
+            return fail(EZ_INVALID_ARGUMENT, "self pair index out of range");
+        if (rb->geom_link[a] == rb->geom_link[b])
+            return fail(EZ_INVALID_ARGUMENT, "self-collision pair on a single link");
+        const double rr = (rb->geom_radius[a] + rb->geom_radius[b]) + margin;
+        hm.all_pairs.push_back(HSelfPair{a, b, rr * rr});
     }
+    layout_pairs(hm, nullptr, nullptr);
     // static obstacles
     for (int i = 0; sc && i < sc->n_static; ++i) {
         double c[3];
@@ -734,7 +993,7 @@ extern "C" int32_t ez_world_create(const ez_robot_desc* rb, const ez_scene_desc*
     w->dof = hm.dof;
     w->n_joints = nj;
     w->n_spheres = static_cast<int32_t>(hm.spheres.size());
-    w->n_pairs = static_cast<int32_t>(hm.pairs.size());
+    w->n_pairs = static_cast<int32_t>(hm.all_pairs.size());
     w->n_groups = static_cast<int32_t>(hm.groups.size());
     w->n_ssph = static_cast<int32_t>(hm.ssph.size() / 4);
     w->n_sbox = static_cast<int32_t>(hm.sbox.size() / 15);
@@ -768,6 +1027,8 @@ extern "C" int32_t ez_world_create(const ez_robot_desc* rb, const ez_scene_desc*
     w->mf.vox.present = 0;
     w->md.vox.present = 0;
     if (st == EZ_OK && sc && sc->n_voxels > 0) st = build_voxel_grid(w, sc, hm, dim);
+    if (st == EZ_OK && rb->joint_lower && rb->joint_upper && hm.dof > 0 && !hm.spheres.empty())
+        st = calibrate_layout(w, hm, rb->joint_lower, rb->joint_upper);
     if (st != EZ_OK) {
         world_free(w);
         return st;
@@ -790,6 +1051,7 @@ extern "C" int32_t ez_world_get_info(const ez_world* w, ez_world_info* out) {
     out->n_spheres = w->n_spheres;
     out->n_pairs = w->n_pairs;
     out->n_static = w->n_ssph + w->n_sbox;
+    out->n_hot_pairs = w->n_hot;
     out->n_voxels = w->n_voxels;
     for (int k = 0; k < 3; ++k) out->grid_dims[k] = w->grid_n[k];
     out->cell_side = w->cell_h;

@@ -14,7 +14,7 @@ struct ez_world {
     int32_t num_sms = 148;
     int32_t smem_optin = 232448;  // max dynamic shared memory per CTA
     int32_t dim = 3, dof = 0, n_joints = 0, n_spheres = 0, n_pairs = 0, n_groups = 0;
-    int32_t n_ssph = 0, n_sbox = 0, n_store = 0;
+    int32_t n_ssph = 0, n_sbox = 0, n_store = 0, n_hot = 0;
     int64_t n_voxels = 0;
     double margin = 0.0;
 
@@ -45,6 +45,11 @@ struct ez_world {
     int64_t stage_rows = 0;
 
     ez_eizo_ws* eizo = nullptr;
+
+    // cached launch shapes of k_check, [T fp64][Q fp64]
+    int32_t launch_threads[4] = {0, 0, 0, 0};
+    size_t launch_smem[4] = {0, 0, 0, 0};
+    int32_t launch_occ[4] = {0, 0, 0, 0};
 };
 
 namespace ez {
@@ -57,11 +62,13 @@ int32_t launch_check(ez_world* w, const void* d_q, int32_t q_dtype, int64_t n, i
 
 void eizo_ws_free(ez_eizo_ws* ws);
 
-// CTA size (128, 64 or 32 threads) whose per-thread sphere-centre store fits
-// in shared memory; writes the dynamic smem bytes.  0 if even 32 do not fit.
+// CTA size (max_threads, halved down to 32) whose per-thread sphere-centre
+// store fits in shared memory; writes the dynamic smem bytes.  0 if even 32
+// threads do not fit.
 template <typename T>
-inline int check_block_threads(const ez_world* w, uint32_t blob_bytes, int n_spheres, int row_bytes, size_t* smem) {
-    for (int t = 128; t >= 32; t /= 2) {
+inline int check_block_threads(const ez_world* w, uint32_t blob_bytes, int n_spheres, int row_bytes, size_t* smem,
+                               int max_threads = 128) {
+    for (int t = max_threads; t >= 32; t /= 2) {
         size_t b = blob_bytes + static_cast<size_t>(3) * n_spheres * t * sizeof(T);
         b = (b + 15) & ~static_cast<size_t>(15);
         b += static_cast<size_t>(t) * row_bytes;

@@ -60,12 +60,15 @@ def _robot_arrays(model):
     arrs = dict(kind=kind, parent=parent, rot=np.ascontiguousarray(rot), trans=np.ascontiguousarray(trans),
                 axis=np.ascontiguousarray(axis), glink=glink, gkind=gkind,
                 grot=np.ascontiguousarray(grot, dtype=np.float64), gtr=np.ascontiguousarray(gtr, dtype=np.float64),
-                grad=grad, ghalf=np.ascontiguousarray(ghalf), pairs=np.ascontiguousarray(pairs))
+                grad=grad, ghalf=np.ascontiguousarray(ghalf), pairs=np.ascontiguousarray(pairs),
+                lower=np.ascontiguousarray(model.lower, dtype=np.float64),
+                upper=np.ascontiguousarray(model.upper, dtype=np.float64))
     desc = N.RobotDesc(
         d, nj, N.ptr(arrs["kind"], C.c_int32), N.ptr(arrs["parent"], C.c_int32), N.ptr(arrs["rot"]),
         N.ptr(arrs["trans"]), N.ptr(arrs["axis"]), ng, N.ptr(arrs["glink"], C.c_int32),
         N.ptr(arrs["gkind"], C.c_int32), N.ptr(arrs["grot"]), N.ptr(arrs["gtr"]), N.ptr(arrs["grad"]),
-        N.ptr(arrs["ghalf"]), pairs.shape[0], N.ptr(arrs["pairs"], C.c_int32))
+        N.ptr(arrs["ghalf"]), pairs.shape[0], N.ptr(arrs["pairs"], C.c_int32), N.ptr(arrs["lower"]),
+        N.ptr(arrs["upper"]))
     return desc, arrs
 
 
@@ -134,6 +137,7 @@ class NativeWorld:
         wi = N.WorldInfo()
         N.check(N.lib().ez_world_get_info(self._h, C.byref(wi)))
         return {"dof": wi.dof, "n_links": wi.n_links, "n_spheres": wi.n_spheres, "n_pairs": wi.n_pairs,
+                "n_hot_pairs": wi.n_hot_pairs,
                 "n_static": wi.n_static, "n_voxels": wi.n_voxels, "grid_dims": tuple(wi.grid_dims),
                 "cell_side": wi.cell_side, "list_entries": wi.list_entries, "device_bytes": wi.device_bytes}
 
