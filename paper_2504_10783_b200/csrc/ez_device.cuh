@@ -167,7 +167,21 @@ __device__ __forceinline__ bool self_collides(const GroupRec* __restrict__ G, in
         const GroupRec gr = G[g];
         const T ax = cen[(3 * gr.a) * stride], ay = cen[(3 * gr.a + 1) * stride],
                 az = cen[(3 * gr.a + 2) * stride];
-        for (int p = gr.begin; p < gr.end; ++p) {
+        int p = gr.begin;
+        // four independent pair tests per branch: loads and math overlap
+        for (; p + 4 <= gr.end; p += 4) {
+            bool hit = false;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const PairRec<T> pr = P[p + u];
+                const T dx = ax - cen[(3 * pr.b) * stride];
+                const T dy = ay - cen[(3 * pr.b + 1) * stride];
+                const T dz = az - cen[(3 * pr.b + 2) * stride];
+                hit |= dx * dx + dy * dy + dz * dz <= pr.thr2;
+            }
+            if (hit) return true;
+        }
+        for (; p < gr.end; ++p) {
             const PairRec<T> pr = P[p];
             const T dx = ax - cen[(3 * pr.b) * stride];
             const T dy = ay - cen[(3 * pr.b + 1) * stride];
@@ -182,22 +196,29 @@ __device__ __forceinline__ bool self_collides(const GroupRec* __restrict__ G, in
 // voxel spheres: "nearest voxel centre within r + r_vox + margin"
 // (world.py:529-532), answered exactly through the quantised distance grid
 // ---------------------------------------------------------------------------
+// Cell of the distance grid holding p (-1 outside the grid: farther than the
+// list radius from every voxel) and the distance e from p to the cell centre.
 template <typename T>
-__device__ __forceinline__ bool voxel_hit(const VoxGrid<T>& V, T px, T py, T pz, T R) {
+__device__ __forceinline__ int64_t voxel_cell(const VoxGrid<T>& V, T px, T py, T pz, T& e) {
     const T fx = (px - V.org[0]) * V.inv_h;
     const T fy = (py - V.org[1]) * V.inv_h;
     const T fz = (pz - V.org[2]) * V.inv_h;
-    if (!(fx >= T(0) && fy >= T(0) && fz >= T(0) && fx < T(V.n[0]) && fy < T(V.n[1]) &&
-          fz < T(V.n[2])))
-        return false;  // outside the grid: farther than the list radius from every voxel
+    e = T(0);
+    if (!(fx >= T(0) && fy >= T(0) && fz >= T(0) && fx < T(V.n[0]) && fy < T(V.n[1]) && fz < T(V.n[2])))
+        return -1;
     const int ix = static_cast<int>(fx), iy = static_cast<int>(fy), iz = static_cast<int>(fz);
-    const T gx = V.org[0] + (T(ix) + T(0.5)) * V.h;
-    const T gy = V.org[1] + (T(iy) + T(0.5)) * V.h;
-    const T gz = V.org[2] + (T(iz) + T(0.5)) * V.h;
-    const T ex = px - gx, ey = py - gy, ez_ = pz - gz;
-    const T e = tsqrt<T>(ex * ex + ey * ey + ez_ * ez_);
-    const uint32_t w =
-        __ldg(V.cells + (static_cast<int64_t>(iz) * V.n[1] + iy) * V.n[0] + ix);
+    const T ex = px - (V.org[0] + (T(ix) + T(0.5)) * V.h);
+    const T ey = py - (V.org[1] + (T(iy) + T(0.5)) * V.h);
+    const T ez_ = pz - (V.org[2] + (T(iz) + T(0.5)) * V.h);
+    e = tsqrt<T>(ex * ex + ey * ey + ez_ * ez_);
+    return (static_cast<int64_t>(iz) * V.n[1] + iy) * V.n[0] + ix;
+}
+
+constexpr uint32_t kFarCell = 0xFF000000u;  // q = 255: no voxel within the list radius
+
+// Decide "some voxel centre within R of p" from the cell word w.
+template <typename T>
+__device__ __forceinline__ bool voxel_decide(const VoxGrid<T>& V, uint32_t w, T e, T px, T py, T pz, T R) {
     const uint32_t qc = w >> 24;
     const T lo = T(qc) * V.dq;
     if (lo - e > R + V.eps) return false;                          // certainly free
@@ -217,18 +238,23 @@ __device__ __forceinline__ bool voxel_hit(const VoxGrid<T>& V, T px, T py, T pz,
 }
 
 template <typename T>
-__device__ __forceinline__ bool sphere_hits_obstacles(const ModelDev<T>& M,
-                                                      const SphereRec<T>& sp,
-                                                      const StaticSphereRec<T>* __restrict__ SS,
-                                                      const StaticBoxRec<T>* __restrict__ SB,
-                                                      T margin, T px, T py, T pz) {
+__device__ __forceinline__ bool voxel_hit(const VoxGrid<T>& V, T px, T py, T pz, T R) {
+    T e;
+    const int64_t c = voxel_cell<T>(V, px, py, pz, e);
+    if (c < 0) return false;
+    return voxel_decide<T>(V, __ldg(V.cells + c), e, px, py, pz, R);
+}
+
+template <typename T>
+__device__ __forceinline__ bool static_hits(const ModelDev<T>& M, const SphereRec<T>& sp,
+                                            const StaticSphereRec<T>* __restrict__ SS,
+                                            const StaticBoxRec<T>* __restrict__ SB, T margin, T px, T py, T pz) {
     for (int i = 0; i < M.n_ssph; ++i) {
         const StaticSphereRec<T> o = SS[i];
         const T dx = px - o.c[0], dy = py - o.c[1], dz = pz - o.c[2];
         const T rr = (o.r + sp.r) + margin;
         if (dx * dx + dy * dy + dz * dz <= rr * rr) return true;
     }
-    if (M.vox.present && voxel_hit<T>(M.vox, px, py, pz, sp.rvox)) return true;
     for (int i = 0; i < M.n_sbox; ++i) {
         const StaticBoxRec<T>& b = SB[i];
         const T dx = px - b.t[0], dy = py - b.t[1], dz = pz - b.t[2];
@@ -242,6 +268,16 @@ __device__ __forceinline__ bool sphere_hits_obstacles(const ModelDev<T>& M,
         if (d2 <= sp.rmar * sp.rmar) return true;
     }
     return false;
+}
+
+template <typename T>
+__device__ __forceinline__ bool sphere_hits_obstacles(const ModelDev<T>& M,
+                                                      const SphereRec<T>& sp,
+                                                      const StaticSphereRec<T>* __restrict__ SS,
+                                                      const StaticBoxRec<T>* __restrict__ SB,
+                                                      T margin, T px, T py, T pz) {
+    if (static_hits<T>(M, sp, SS, SB, margin, px, py, pz)) return true;
+    return M.vox.present && voxel_hit<T>(M.vox, px, py, pz, sp.rvox);
 }
 
 // Phase A: the calibrated hot self pairs (flat list, most frequent first).
@@ -259,8 +295,11 @@ __device__ __forceinline__ bool hot_pairs_collide(const ModelDev<T>& M, const ui
     return false;
 }
 
-// Phase B: obstacles (spheres in calibrated hit-frequency order), then the
-// remaining self pairs grouped by first sphere.
+// Phase B: obstacles (spheres in calibrated hit-frequency order, distance-
+// grid cells fetched kVoxBatch at a time so their L2 latencies overlap), then
+// the remaining self pairs grouped by first sphere.
+constexpr int kVoxBatch = 4;
+
 template <typename T>
 __device__ __forceinline__ bool rest_collides(const ModelDev<T>& M, const uint8_t* blob,
                                               const T* __restrict__ cen, int stride, T margin) {
@@ -268,11 +307,34 @@ __device__ __forceinline__ bool rest_collides(const ModelDev<T>& M, const uint8_
     const int32_t* order = reinterpret_cast<const int32_t*>(blob + M.off_order);
     const StaticSphereRec<T>* SS = reinterpret_cast<const StaticSphereRec<T>*>(blob + M.off_ssph);
     const StaticBoxRec<T>* SB = reinterpret_cast<const StaticBoxRec<T>*>(blob + M.off_sbox);
-    for (int k = 0; k < M.n_spheres; ++k) {
-        const int s = order[k];
-        if (sphere_hits_obstacles<T>(M, S[s], SS, SB, margin, cen[(3 * s) * stride],
-                                     cen[(3 * s + 1) * stride], cen[(3 * s + 2) * stride]))
-            return true;
+    const bool vox = M.vox.present;
+    for (int k0 = 0; k0 < M.n_spheres; k0 += kVoxBatch) {
+        T px[kVoxBatch], py[kVoxBatch], pz[kVoxBatch], e[kVoxBatch];
+        uint32_t w[kVoxBatch];
+        int sid[kVoxBatch];
+#pragma unroll
+        for (int j = 0; j < kVoxBatch; ++j) {
+            const int k = min(k0 + j, M.n_spheres - 1);
+            const int s = order[k];
+            sid[j] = s;
+            px[j] = cen[(3 * s) * stride];
+            py[j] = cen[(3 * s + 1) * stride];
+            pz[j] = cen[(3 * s + 2) * stride];
+            w[j] = kFarCell;
+            e[j] = T(0);
+            if (vox) {
+                const int64_t c = voxel_cell<T>(M.vox, px[j], py[j], pz[j], e[j]);
+                if (c >= 0) w[j] = __ldg(M.vox.cells + c);
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < kVoxBatch; ++j) {
+            if (k0 + j >= M.n_spheres) break;
+            const SphereRec<T>& sp = S[sid[j]];
+            if (static_hits<T>(M, sp, SS, SB, margin, px[j], py[j], pz[j])) return true;
+            if (vox && w[j] != kFarCell && voxel_decide<T>(M.vox, w[j], e[j], px[j], py[j], pz[j], sp.rvox))
+                return true;
+        }
     }
     const GroupRec* G = reinterpret_cast<const GroupRec*>(blob + M.off_groups);
     const PairRec<T>* P = reinterpret_cast<const PairRec<T>*>(blob + M.off_pairs);

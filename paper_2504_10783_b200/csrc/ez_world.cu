@@ -19,7 +19,6 @@
 
 namespace ez {
 
-constexpr int kCheckThreads = 256;
 
 // ---------------------------------------------------------------------------
 // host-side model folding
@@ -548,50 +547,69 @@ __device__ __forceinline__ void check_phase_b(const ModelDev<T>& M, const uint8_
     if (n_col != nullptr && c2 && idx < count_lim) atomicAdd(n_col, 1);
 }
 
-template <typename T, typename Q>
-__global__ void __launch_bounds__(kCheckThreads)
+constexpr int kPrefetch = 8;  // registers per thread for the next tile's rows (dof*BT/BT <= 8)
+
+template <typename T, typename Q, int BT>
+__global__ void __launch_bounds__(BT)
 k_check(ModelDev<T> M, const Q* __restrict__ q, int64_t n, int64_t ld, uint8_t* __restrict__ out,
         T margin, int64_t count_lim, int32_t* __restrict__ n_col) {
     extern __shared__ __align__(16) uint8_t smem[];
     __shared__ uint64_t bar;
-    __shared__ int32_t s_queue[2 * kCheckThreads];
-    __shared__ int s_warp[kCheckThreads / 32];
+    __shared__ int32_t s_queue[2 * BT];
+    __shared__ int s_warp[BT / 32];
     tma_stage(smem, M.blob, M.blob_bytes, &bar);
     T* cen = reinterpret_cast<T*>(smem + M.blob_bytes);
-    const size_t roff = (static_cast<size_t>(M.blob_bytes) +
-                         static_cast<size_t>(3) * M.n_spheres * blockDim.x * sizeof(T) + 15) &
+    const size_t roff = (static_cast<size_t>(M.blob_bytes) + static_cast<size_t>(3) * M.n_spheres * BT * sizeof(T) + 15) &
                         ~static_cast<size_t>(15);
     Q* rows = reinterpret_cast<Q*>(smem + roff);
     const int dof = M.dof;
-    const int T_ = blockDim.x, qcap = 2 * blockDim.x;
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+    constexpr int qcap = 2 * BT;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const JointRec<T>* J = reinterpret_cast<const JointRec<T>*>(smem);
     const SphereRec<T>* S = reinterpret_cast<const SphereRec<T>*>(smem + M.off_spheres);
     T* my_cen = cen + threadIdx.x;
     Q* my_row = rows + threadIdx.x * dof;
+    const bool contiguous = (ld == dof) && (dof <= kPrefetch);
     int qhead = 0, qn = 0;  // ring buffer state (uniform across the CTA)
-    const int64_t tiles = (n + T_ - 1) / T_;
+    const int64_t tiles = (n + BT - 1) / BT;
+    Q pf[kPrefetch];
+    auto prefetch = [&](int64_t tile) {
+        if (tile >= tiles) return;
+        const int64_t base = tile * BT;
+        const int tot = static_cast<int>(min(static_cast<int64_t>(BT), n - base)) * dof;
+        const Q* src = q + base * dof;
+#pragma unroll
+        for (int j = 0; j < kPrefetch; ++j) {
+            const int i = threadIdx.x + j * BT;
+            if (i < tot) pf[j] = src[i];
+        }
+    };
+    if (contiguous) prefetch(blockIdx.x);
     for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
-        const int64_t base = tile * T_;
-        const int nr = static_cast<int>(min(static_cast<int64_t>(T_), n - base));
+        const int64_t base = tile * BT;
+        const int nr = static_cast<int>(min(static_cast<int64_t>(BT), n - base));
         __syncthreads();
-        if (ld == dof) {
-            const Q* src = q + base * dof;
+        if (contiguous) {
             const int tot = nr * dof;
-            for (int i = threadIdx.x; i < tot; i += T_) rows[i] = src[i];
+#pragma unroll
+            for (int j = 0; j < kPrefetch; ++j) {
+                const int i = threadIdx.x + j * BT;
+                if (i < tot) rows[i] = pf[j];
+            }
         } else {
-            for (int i = threadIdx.x; i < nr * dof; i += T_) {
+            for (int i = threadIdx.x; i < nr * dof; i += BT) {
                 const int r = i / dof, k = i - r * dof;
                 rows[i] = q[(base + r) * ld + k];
             }
         }
         __syncthreads();
+        if (contiguous) prefetch(tile + gridDim.x);  // lands while this tile is checked
         // phase A
         const bool valid = threadIdx.x < nr;
         bool col = false;
         if (valid) {
-            fk_sphere_centres<T, Q>(J, M.n_joints, S, my_row, my_cen, T_);
-            col = hot_pairs_collide<T>(M, smem, my_cen, T_);
+            fk_sphere_centres<T, Q>(J, M.n_joints, S, my_row, my_cen, BT);
+            col = hot_pairs_collide<T>(M, smem, my_cen, BT);
             if (col) out[base + threadIdx.x] = 0;
         }
         if (n_col != nullptr) {
@@ -604,7 +622,8 @@ k_check(ModelDev<T> M, const Q* __restrict__ q, int64_t n, int64_t ld, uint8_t* 
         if (lane == 0) s_warp[wid] = __popc(sm);
         __syncthreads();
         int off = 0, add = 0;
-        for (int w = 0; w < nwarps; ++w) {
+#pragma unroll
+        for (int w = 0; w < BT / 32; ++w) {
             const int c = s_warp[w];
             off += (w < wid) ? c : 0;
             add += c;
@@ -613,17 +632,17 @@ k_check(ModelDev<T> M, const Q* __restrict__ q, int64_t n, int64_t ld, uint8_t* 
         qn += add;
         __syncthreads();
         // phase B on full CTAs
-        while (qn >= T_) {
-            check_phase_b<T, Q>(M, smem, q, ld, s_queue[(qhead + threadIdx.x) % qcap], my_row, my_cen, T_, margin,
+        while (qn >= BT) {
+            check_phase_b<T, Q>(M, smem, q, ld, s_queue[(qhead + threadIdx.x) % qcap], my_row, my_cen, BT, margin,
                                 out, count_lim, n_col);
-            qhead = (qhead + T_) % qcap;
-            qn -= T_;
+            qhead = (qhead + BT) % qcap;
+            qn -= BT;
             __syncthreads();
         }
     }
     // drain
     if (threadIdx.x < qn)
-        check_phase_b<T, Q>(M, smem, q, ld, s_queue[(qhead + threadIdx.x) % qcap], my_row, my_cen, T_, margin, out,
+        check_phase_b<T, Q>(M, smem, q, ld, s_queue[(qhead + threadIdx.x) % qcap], my_row, my_cen, BT, margin, out,
                             count_lim, n_col);
 }
 
@@ -769,65 +788,80 @@ static int32_t calibrate_layout(ez_world* w, HModel& hm, const double* lower, co
     return EZ_OK;
 }
 
-// CTA size with the most resident warps per SM: the per-thread sphere-centre
-// store makes shared memory the occupancy limiter, and 256-thread CTAs can
-// strand a large fraction of it (e.g. 160 x 3 CTAs beats 256 x 1 for the
-// 33-sphere arm).  Cached per kernel instantiation and model size.
-template <typename K>
-static int32_t pick_threads(const ez_world* w, K kern, uint32_t blob_bytes, int n_spheres, int tsize, int row_bytes,
-                            int max_threads, int* threads, size_t* smem) {
+// CTA size with the most resident warps per SM.  The per-thread sphere-centre
+// store makes shared memory the occupancy limiter and a 256-thread CTA can
+// strand a large part of it (160 x 3 CTAs beats 256 x 1 for the 33-sphere
+// arm), so every candidate size is an instantiation (constant smem strides)
+// and the best is picked once per world from the occupancy calculator.
+template <typename T, typename Q, int BT>
+static int32_t eval_bt(const ez_world* w, const ModelDev<T>& M, int* best_warps, int* best_t, size_t* best_s,
+                       int* best_occ) {
+    auto kern = k_check<T, Q, BT>;
     cudaFuncAttributes fa{};
     EZ_CUDA(cudaFuncGetAttributes(&fa, kern));
     const size_t max_dyn = static_cast<size_t>(w->smem_optin) - fa.sharedSizeBytes;
+    size_t b = M.blob_bytes + static_cast<size_t>(3) * M.n_spheres * BT * sizeof(T);
+    b = (b + 15) & ~static_cast<size_t>(15);
+    b += static_cast<size_t>(BT) * M.dof * sizeof(Q);
+    b = (b + 15) & ~static_cast<size_t>(15);
+    if (b > max_dyn) return EZ_OK;
     EZ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(max_dyn)));
-    int best_t = 0, best_warps = -1;
-    size_t best_s = 0;
-    for (int t = 32; t <= max_threads; t += 32) {
-        size_t b = blob_bytes + static_cast<size_t>(3) * n_spheres * t * tsize;
-        b = (b + 15) & ~static_cast<size_t>(15);
-        b += static_cast<size_t>(t) * row_bytes;
-        b = (b + 15) & ~static_cast<size_t>(15);
-        if (b > max_dyn) break;
-        int occ = 0;
-        EZ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, t, b));
-        const int warps = occ * t / 32;
-        if (warps >= best_warps && occ > 0) {
-            best_warps = warps;
-            best_t = t;
-            best_s = b;
-        }
+    int occ = 0;
+    EZ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, BT, b));
+    const int warps = occ * BT / 32;
+    if (occ > 0 && warps >= *best_warps) {
+        *best_warps = warps;
+        *best_t = BT;
+        *best_s = b;
+        *best_occ = occ;
     }
-    if (best_t == 0) return fail(EZ_CAPACITY, "robot model too large for one checking CTA");
-    *threads = best_t;
-    *smem = best_s;
     return EZ_OK;
+}
+
+template <typename T, typename Q, int BT>
+static void launch_bt(const ModelDev<T>& M, unsigned grid, size_t smem, cudaStream_t stream, const Q* d_q, int64_t n,
+                      int64_t ld, uint8_t* d_free, T margin, int64_t count_lim, int32_t* n_col) {
+    k_check<T, Q, BT><<<grid, BT, smem, stream>>>(M, d_q, n, ld, d_free, margin, count_lim, n_col);
 }
 
 template <typename T, typename Q>
 static int32_t launch_check_t(ez_world* w, const ModelDev<T>& M, const Q* d_q, int64_t n, int64_t ld,
                               uint8_t* d_free, cudaStream_t stream, int64_t count_lim, int32_t* n_col) {
-    auto kern = k_check<T, Q>;
     const int slot = (sizeof(T) == 8 ? 2 : 0) + (sizeof(Q) == 8 ? 1 : 0);
     if (w->launch_threads[slot] == 0) {
-        int t = 0;
-        size_t sm = 0;
-        EZ_TRY(pick_threads(w, kern, M.blob_bytes, M.n_spheres, static_cast<int>(sizeof(T)),
-                            static_cast<int>(M.dof * sizeof(Q)), kCheckThreads, &t, &sm));
-        int occ = 0;
-        EZ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, t, sm));
-        w->launch_threads[slot] = t;
-        w->launch_smem[slot] = sm;
-        w->launch_occ[slot] = occ;
+        int bw = -1, bt = 0, bo = 0;
+        size_t bs = 0;
+        EZ_TRY((eval_bt<T, Q, 64>(w, M, &bw, &bt, &bs, &bo)));
+        EZ_TRY((eval_bt<T, Q, 96>(w, M, &bw, &bt, &bs, &bo)));
+        EZ_TRY((eval_bt<T, Q, 128>(w, M, &bw, &bt, &bs, &bo)));
+        EZ_TRY((eval_bt<T, Q, 160>(w, M, &bw, &bt, &bs, &bo)));
+        EZ_TRY((eval_bt<T, Q, 192>(w, M, &bw, &bt, &bs, &bo)));
+        EZ_TRY((eval_bt<T, Q, 256>(w, M, &bw, &bt, &bs, &bo)));
+        if (bt == 0) return fail(EZ_CAPACITY, "robot model too large for one checking CTA");
+        w->launch_threads[slot] = bt;
+        w->launch_smem[slot] = bs;
+        w->launch_occ[slot] = bo;
     }
     const int threads = w->launch_threads[slot];
     const size_t smem = w->launch_smem[slot];
+    const T margin = static_cast<T>(w->margin);
     const int64_t chunk = int64_t(1) << 30;  // queue entries are int32 row indices
     for (int64_t r0 = 0; r0 < n; r0 += chunk) {
         const int64_t rows = std::min(chunk, n - r0);
         const int64_t tiles = (rows + threads - 1) / threads;
-        const int64_t grid = std::min<int64_t>(tiles, static_cast<int64_t>(w->num_sms) * w->launch_occ[slot]);
-        kern<<<static_cast<unsigned>(grid), threads, smem, stream>>>(
-            M, d_q + r0 * ld, rows, ld, d_free + r0, static_cast<T>(w->margin), count_lim - r0, n_col);
+        const unsigned grid =
+            static_cast<unsigned>(std::min<int64_t>(tiles, static_cast<int64_t>(w->num_sms) * w->launch_occ[slot]));
+        const Q* qp = d_q + r0 * ld;
+        uint8_t* op = d_free + r0;
+        const int64_t cl = count_lim - r0;
+        switch (threads) {
+            case 64: launch_bt<T, Q, 64>(M, grid, smem, stream, qp, rows, ld, op, margin, cl, n_col); break;
+            case 96: launch_bt<T, Q, 96>(M, grid, smem, stream, qp, rows, ld, op, margin, cl, n_col); break;
+            case 128: launch_bt<T, Q, 128>(M, grid, smem, stream, qp, rows, ld, op, margin, cl, n_col); break;
+            case 160: launch_bt<T, Q, 160>(M, grid, smem, stream, qp, rows, ld, op, margin, cl, n_col); break;
+            case 192: launch_bt<T, Q, 192>(M, grid, smem, stream, qp, rows, ld, op, margin, cl, n_col); break;
+            default: launch_bt<T, Q, 256>(M, grid, smem, stream, qp, rows, ld, op, margin, cl, n_col); break;
+        }
         EZ_CUDA(cudaGetLastError());
     }
     return EZ_OK;
@@ -1081,7 +1115,7 @@ extern "C" int32_t ez_check_batch_host(ez_world* w, const double* h_q, int64_t n
     std::lock_guard<std::mutex> lock(w->mu);
     EZ_CUDA(cudaSetDevice(w->device));
     const int dof = w->dof;
-    const int64_t chunk = 1 << 18;
+    const int64_t chunk = 1 << 16;
     if (w->stage_rows < chunk) {
         for (int i = 0; i < 2; ++i) {
             cudaFreeHost(w->h_stage_in[i]);
@@ -1111,8 +1145,9 @@ extern "C" int32_t ez_check_batch_host(ez_world* w, const double* h_q, int64_t n
         cudaStream_t s = w->hstream[b];
         const int64_t r0 = c * chunk;
         const int64_t rows = std::min(chunk, n - r0);
-        // wait for the previous use of this buffer pair to finish
-        EZ_CUDA(cudaStreamSynchronize(s));
+        // host staging buffers are reused: wait for their previous chunk (all
+        // device work stays ordered on the stream, so pinned I/O never waits)
+        if (!(pinned_in && pinned_out)) EZ_CUDA(cudaStreamSynchronize(s));
         if (pending_out[b] >= 0 && !pinned_out) {
             const int64_t pr0 = pending_out[b] * chunk;
             std::memcpy(h_free + pr0, w->h_stage_out[b], std::min(chunk, n - pr0));
