@@ -358,6 +358,135 @@ __device__ __forceinline__ bool config_free(const ModelDev<T>& M, const uint8_t*
     return !config_collides<T>(M, blob, cen, stride, margin);
 }
 
+// ---------------------------------------------------------------------------
+// cooperative check: G lanes of a warp evaluate one configuration.  Used on
+// latency-bound paths (bisection rounds) where there are only ~1e4
+// configurations in flight.  Every lane runs the (cheap, serial) joint chain;
+// sphere centres, pair tests and obstacle tests are split across the lanes
+// and joined with a group ballot.  All loop trip counts are group-uniform.
+// Centres live in a per-configuration store cen[3 s + k].
+// ---------------------------------------------------------------------------
+template <int G>
+__device__ __forceinline__ unsigned coop_mask() {
+    if (G == 32) return 0xffffffffu;
+    return ((1u << G) - 1u) << ((threadIdx.x & 31) & ~(G - 1));
+}
+
+template <typename T, typename Q, int G>
+__device__ __forceinline__ void fk_centres_coop(const JointRec<T>* __restrict__ J, int nj,
+                                                const SphereRec<T>* __restrict__ S, const Q* __restrict__ q,
+                                                T* __restrict__ cen, int lane) {
+    T R[9] = {T(1), T(0), T(0), T(0), T(1), T(0), T(0), T(0), T(1)};
+    T t[3] = {T(0), T(0), T(0)};
+    T store[kMaxStore][12];
+    for (int j = 0; j < nj; ++j) {
+        const JointRec<T>& jr = J[j];
+        if (jr.parent != j - 1) {
+            if (jr.parent < 0) {
+#pragma unroll
+                for (int k = 0; k < 9; ++k) R[k] = (k % 4 == 0) ? T(1) : T(0);
+                t[0] = t[1] = t[2] = T(0);
+            } else {
+#pragma unroll
+                for (int k = 0; k < 9; ++k) R[k] = store[jr.parent_slot][k];
+#pragma unroll
+                for (int k = 0; k < 3; ++k) t[k] = store[jr.parent_slot][9 + k];
+            }
+        }
+        T N[9], tn[3];
+#pragma unroll
+        for (int r = 0; r < 3; ++r) {
+#pragma unroll
+            for (int c = 0; c < 3; ++c)
+                N[3 * r + c] = R[3 * r] * jr.R[c] + R[3 * r + 1] * jr.R[3 + c] + R[3 * r + 2] * jr.R[6 + c];
+            tn[r] = t[r] + (R[3 * r] * jr.t[0] + R[3 * r + 1] * jr.t[1] + R[3 * r + 2] * jr.t[2]);
+        }
+        if (jr.kind == EZ_JOINT_REVOLUTE) {
+            T sn, cs;
+            Angle<T, Q>::sc(q[jr.qidx], sn, cs);
+#pragma unroll
+            for (int r = 0; r < 3; ++r) {
+                const T n0 = N[3 * r], n1 = N[3 * r + 1];
+                N[3 * r] = n0 * cs + n1 * sn;
+                N[3 * r + 1] = n1 * cs - n0 * sn;
+            }
+        } else if (jr.kind == EZ_JOINT_PRISMATIC) {
+            const T qq = static_cast<T>(q[jr.qidx]);
+#pragma unroll
+            for (int r = 0; r < 3; ++r)
+                tn[r] += (N[3 * r] * jr.ax[0] + N[3 * r + 1] * jr.ax[1] + N[3 * r + 2] * jr.ax[2]) * qq;
+        }
+#pragma unroll
+        for (int k = 0; k < 9; ++k) R[k] = N[k];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) t[k] = tn[k];
+        if (jr.store_slot >= 0) {
+#pragma unroll
+            for (int k = 0; k < 9; ++k) store[jr.store_slot][k] = R[k];
+#pragma unroll
+            for (int k = 0; k < 3; ++k) store[jr.store_slot][9 + k] = t[k];
+        }
+        for (int s = jr.sph_begin + lane; s < jr.sph_end; s += G) {
+            const SphereRec<T>& sp = S[s];
+#pragma unroll
+            for (int r = 0; r < 3; ++r)
+                cen[3 * s + r] = t[r] + (R[3 * r] * sp.p[0] + R[3 * r + 1] * sp.p[1] + R[3 * r + 2] * sp.p[2]);
+        }
+    }
+}
+
+template <typename T, typename Q, int G>
+__device__ __forceinline__ bool config_free_coop(const ModelDev<T>& M, const uint8_t* blob, const Q* q,
+                                                 T* __restrict__ cen, T margin) {
+    const unsigned gm = coop_mask<G>();
+    const int lane = threadIdx.x & (G - 1);
+    const JointRec<T>* J = reinterpret_cast<const JointRec<T>*>(blob);
+    const SphereRec<T>* S = reinterpret_cast<const SphereRec<T>*>(blob + M.off_spheres);
+    fk_centres_coop<T, Q, G>(J, M.n_joints, S, q, cen, lane);
+    __syncwarp(gm);
+    const HotRec<T>* H = reinterpret_cast<const HotRec<T>*>(blob + M.off_hot);
+    for (int p0 = 0; p0 < M.n_hot; p0 += G) {
+        const int p = p0 + lane;
+        bool hit = false;
+        if (p < M.n_hot) {
+            const HotRec<T> h = H[p];
+            const T dx = cen[3 * h.a] - cen[3 * h.b], dy = cen[3 * h.a + 1] - cen[3 * h.b + 1],
+                    dz = cen[3 * h.a + 2] - cen[3 * h.b + 2];
+            hit = dx * dx + dy * dy + dz * dz <= h.thr2;
+        }
+        if (__ballot_sync(gm, hit)) return false;
+    }
+    const int32_t* order = reinterpret_cast<const int32_t*>(blob + M.off_order);
+    const StaticSphereRec<T>* SS = reinterpret_cast<const StaticSphereRec<T>*>(blob + M.off_ssph);
+    const StaticBoxRec<T>* SB = reinterpret_cast<const StaticBoxRec<T>*>(blob + M.off_sbox);
+    for (int k0 = 0; k0 < M.n_spheres; k0 += G) {
+        const int k = k0 + lane;
+        bool hit = false;
+        if (k < M.n_spheres) {
+            const int s = order[k];
+            hit = sphere_hits_obstacles<T>(M, S[s], SS, SB, margin, cen[3 * s], cen[3 * s + 1], cen[3 * s + 2]);
+        }
+        if (__ballot_sync(gm, hit)) return false;
+    }
+    const GroupRec* Gr = reinterpret_cast<const GroupRec*>(blob + M.off_groups);
+    const PairRec<T>* P = reinterpret_cast<const PairRec<T>*>(blob + M.off_pairs);
+    for (int g = 0; g < M.n_groups; ++g) {
+        const GroupRec gr = Gr[g];
+        const T ax = cen[3 * gr.a], ay = cen[3 * gr.a + 1], az = cen[3 * gr.a + 2];
+        for (int p0 = gr.begin; p0 < gr.end; p0 += G) {
+            const int p = p0 + lane;
+            bool hit = false;
+            if (p < gr.end) {
+                const PairRec<T> pr = P[p];
+                const T dx = ax - cen[3 * pr.b], dy = ay - cen[3 * pr.b + 1], dz = az - cen[3 * pr.b + 2];
+                hit = dx * dx + dy * dy + dz * dz <= pr.thr2;
+            }
+            if (__ballot_sync(gm, hit)) return false;
+        }
+    }
+    return true;
+}
+
 // Dynamic shared memory of a checking CTA: blob | sphere centres | staged rows.
 template <typename T>
 __host__ __device__ inline size_t check_smem_bytes(uint32_t blob_bytes, int n_spheres, int threads,

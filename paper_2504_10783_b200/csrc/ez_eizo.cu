@@ -25,31 +25,62 @@ constexpr double kChordMask = 1e-14;  // cpoly.py:134-135
 constexpr double kChordTol = 1e-12;   // cpoly.py:167
 
 // ---------------------------------------------------------------------------
-// hit-and-run walk (one thread = one walk)
+// hit-and-run: one group of LPW lanes per walk.  Lane l draws the normals
+// k = l, l + LPW, ... and owns the faces f = l, l + LPW, ...; directions are
+// exchanged and the chord end points reduced with shuffles inside the group,
+// so every lane holds the same walk state and the result is bitwise identical
+// to a one-thread walk (the min/max over faces is order independent).
 // ---------------------------------------------------------------------------
-template <int MAXD, int RNG>
+__device__ __forceinline__ void set_status(int32_t* status, int32_t code) {
+    if (code != EZ_OK) atomicCAS(status, 0, code);
+}
+
+template <int LPW>
+__device__ __forceinline__ unsigned group_mask() {
+    if (LPW == 32) return 0xffffffffu;
+    return ((1u << LPW) - 1u) << ((threadIdx.x & 31) & ~(LPW - 1));
+}
+
+template <int MAXD, int RNG, int LPW>
 __device__ __forceinline__ int hnr_walk(double (&x)[MAXD], int d, const double* __restrict__ A,
                                         const double* __restrict__ b, int F, int n_ms, uint64_t seed,
                                         uint64_t walk, bool check_seed) {
+    constexpr int PER = (MAXD + LPW - 1) / LPW;  // normals drawn per lane
+    const unsigned gm = group_mask<LPW>();
+    const int lane = threadIdx.x & (LPW - 1);
     const uint64_t key = (RNG == EZ_RNG_COUNTER) ? walk_key(seed, walk) : 0ull;
     for (int step = 0; step < n_ms; ++step) {
         double dir[MAXD];
         if (RNG == EZ_RNG_COUNTER) {
+            double mine[PER];
 #pragma unroll
-            for (int k = 0; k < MAXD; ++k) dir[k] = (k < d) ? counter_normal(key, step, k) : 0.0;
+            for (int j = 0; j < PER; ++j) {
+                const int k = lane + j * LPW;
+                mine[j] = (k < d) ? counter_normal(key, static_cast<uint64_t>(step), k) : 0.0;
+            }
+#pragma unroll
+            for (int k = 0; k < MAXD; ++k) dir[k] = __shfl_sync(gm, mine[k / LPW], k % LPW, LPW);
         } else {
+            // Philox: lane l produces normals 4g..4g+3 of the groups g = l, l + LPW, ...
+            constexpr int NG = (MAXD + 3) / 4;
+            constexpr int PERG = (NG + LPW - 1) / LPW;
+            float mine[PERG][4];
 #pragma unroll
-            for (int g = 0; g < (MAXD + 3) / 4; ++g) {
+            for (int j = 0; j < PERG; ++j) {
+                const int g = lane + j * LPW;
                 if (4 * g < d) {
-                    const Philox4 r = philox_draw(seed, walk, static_cast<uint32_t>(step), g);
-                    float n0, n1, n2, n3;
-                    box_muller(r.x, r.y, n0, n1);
-                    box_muller(r.z, r.w, n2, n3);
-                    const float nn[4] = {n0, n1, n2, n3};
-#pragma unroll
-                    for (int k = 0; k < 4; ++k)
-                        if (4 * g + k < MAXD) dir[4 * g + k] = (4 * g + k < d) ? static_cast<double>(nn[k]) : 0.0;
+                    const Philox4 r = philox_draw(seed, walk, static_cast<uint32_t>(step), static_cast<uint32_t>(g));
+                    box_muller(r.x, r.y, mine[j][0], mine[j][1]);
+                    box_muller(r.z, r.w, mine[j][2], mine[j][3]);
+                } else {
+                    mine[j][0] = mine[j][1] = mine[j][2] = mine[j][3] = 0.f;
                 }
+            }
+#pragma unroll
+            for (int k = 0; k < MAXD; ++k) {
+                const int g = k / 4;
+                const float v = __shfl_sync(gm, mine[g / LPW][k % 4], g % LPW, LPW);
+                dir[k] = (k < d) ? static_cast<double>(v) : 0.0;
             }
         }
         // normalise like numpy (squares rounded, left-to-right sum, IEEE divide)
@@ -58,34 +89,70 @@ __device__ __forceinline__ int hnr_walk(double (&x)[MAXD], int d, const double* 
         for (int k = 0; k < MAXD; ++k)
             if (k < d) ss = __dadd_rn(ss, __dmul_rn(dir[k], dir[k]));
         const double nrm = sqrt(ss);
+        // lane l divides components l, l + LPW, ... (IEEE division, as numpy);
+        // the quotients are broadcast back to the group
+        double qv[PER];
 #pragma unroll
-        for (int k = 0; k < MAXD; ++k)
-            if (k < d) dir[k] = dir[k] / nrm;
-        double thi = INFINITY, tlo = -INFINITY;
-        for (int f = 0; f < F; ++f) {
+        for (int j = 0; j < PER; ++j) {
+            const int k = lane + j * LPW;
+            double v = 0.0;
+#pragma unroll
+            for (int kk = 0; kk < MAXD; ++kk)
+                if (kk == k) v = dir[kk];
+            qv[j] = (k < d) ? v / nrm : 0.0;
+        }
+#pragma unroll
+        for (int k = 0; k < MAXD; ++k) dir[k] = __shfl_sync(gm, qv[k / LPW], k % LPW, LPW);
+        // chord end points: t_hi = min over h > 0 of sl / h, t_lo = max over h < 0.
+        // The arg-min/max is tracked as the fraction (sl, h), compared by
+        // cross-multiplication, and divided once at the end.
+        // fractions carry their sign in the denominator: hi = (s, h > 0),
+        // lo = (s, h < 0); the empty chord ends are +inf/1 and +inf/-1.
+        double hi_s = INFINITY, hi_h = 1.0, lo_s = INFINITY, lo_h = -1.0;
+        int outside = 0;
+#pragma unroll 2
+        for (int f = lane; f < F; f += LPW) {
             const double* a = A + static_cast<int64_t>(f) * d;
-            double g = 0.0, h = 0.0;
+            double g0 = 0.0, g1 = 0.0, h0 = 0.0, h1 = 0.0;
 #pragma unroll
-            for (int k = 0; k < MAXD; ++k) {
+            for (int k = 0; k < MAXD; k += 2) {
                 if (k < d) {
-                    const double ak = __ldg(a + k);
-                    g = fma(ak, x[k], g);
-                    h = fma(ak, dir[k], h);
+                    g0 = fma(a[k], x[k], g0);
+                    h0 = fma(a[k], dir[k], h0);
+                }
+                if (k + 1 < d) {
+                    g1 = fma(a[k + 1], x[k + 1], g1);
+                    h1 = fma(a[k + 1], dir[k + 1], h1);
                 }
             }
-            const double sl = __ldg(b + f) - g;
-            if (check_seed && step == 0 && -sl > kMemberTol) return EZ_SEED_OUTSIDE;
-            if (h > kChordMask) thi = fmin(thi, sl / h);
-            else if (h < -kChordMask) tlo = fmax(tlo, sl / h);
+            const double sl = b[f] - (g0 + g1);
+            const double h = h0 + h1;
+            outside |= (check_seed && step == 0 && -sl > kMemberTol);
+            if (h > kChordMask) {
+                if (sl * hi_h < hi_s * h) { hi_s = sl; hi_h = h; }       // sl/h < hi_s/hi_h
+            } else if (h < -kChordMask) {
+                if (sl * lo_h > lo_s * h) { lo_s = sl; lo_h = h; }       // sl/h > lo_s/lo_h (h, lo_h < 0)
+            }
         }
+#pragma unroll
+        for (int o = LPW / 2; o > 0; o >>= 1) {
+            const double os = __shfl_xor_sync(gm, hi_s, o, LPW), oh = __shfl_xor_sync(gm, hi_h, o, LPW);
+            if (os * hi_h < hi_s * oh) { hi_s = os; hi_h = oh; }
+            const double ls = __shfl_xor_sync(gm, lo_s, o, LPW), lh = __shfl_xor_sync(gm, lo_h, o, LPW);
+            if (ls * lo_h > lo_s * lh) { lo_s = ls; lo_h = lh; }
+            outside |= __shfl_xor_sync(gm, outside, o, LPW);
+        }
+        double thi = hi_s / hi_h;
+        double tlo = lo_s / lo_h;
+        if (outside) return EZ_SEED_OUTSIDE;
         if (thi < tlo - kChordTol) return EZ_EMPTY_CHORD;
         tlo = fmin(tlo, 0.0);
         thi = fmax(thi, 0.0);
         double u;
         if (RNG == EZ_RNG_COUNTER) {
-            u = counter_uniform(key, step, d);
+            u = counter_uniform(key, static_cast<uint64_t>(step), d);
         } else {
-            const Philox4 r = philox_draw(seed, walk, static_cast<uint32_t>(step), (d + 3) / 4);
+            const Philox4 r = philox_draw(seed, walk, static_cast<uint32_t>(step), static_cast<uint32_t>((d + 3) / 4));
             u = philox_u53(r.x, r.y);
         }
         const double tt = __dadd_rn(tlo, __dmul_rn(u, thi - tlo));
@@ -96,24 +163,30 @@ __device__ __forceinline__ int hnr_walk(double (&x)[MAXD], int d, const double* 
     return EZ_OK;
 }
 
-__device__ __forceinline__ void set_status(int32_t* status, int32_t code) {
-    if (code != EZ_OK) atomicCAS(status, 0, code);
-}
-
 // Walk i starts at seeds[i % n_seeds] (explicit seeds) or at a point of the
 // segment v1 + alpha * e drawn from the (seed, walk, SEED_STEP) stream
-// (inflation.py:288-290).  F is read from F_dev when given (EI-ZO loop).
-template <int MAXD, int RNG>
+// (inflation.py:288-290).  F is read from F_dev when given (EI-ZO loop);
+// faces are staged in shared memory when F <= smem_faces.
+template <int MAXD, int RNG, int LPW>
 __global__ void __launch_bounds__(128)
 k_hnr(const double* __restrict__ A, const double* __restrict__ b, const int32_t* __restrict__ F_dev, int F,
-      int d, const double* __restrict__ seeds, int64_t n_seeds, const double* __restrict__ seg,
-      const int64_t* __restrict__ n_dev, int64_t count, int n_ms, uint64_t seed, uint64_t walk_offset,
-      double* __restrict__ out, int32_t* __restrict__ status) {
+      int d, const double* __restrict__ seeds, int64_t n_seeds, const double* __restrict__ seg, int64_t count,
+      int n_ms, uint64_t seed, uint64_t walk_offset, double* __restrict__ out, int32_t* __restrict__ status,
+      int smem_faces) {
+    extern __shared__ double s_faces[];
     if (F_dev) F = *F_dev;
-    if (n_dev) count = *n_dev;
-    if (*status != EZ_OK) return;
-    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (i >= count) return;
+    if (status[0] != EZ_OK || status[1] != 0) return;  // (status, stop)
+    const bool staged = F <= smem_faces;
+    if (staged) {
+        for (int i = threadIdx.x; i < F * d; i += blockDim.x) s_faces[i] = A[i];
+        for (int i = threadIdx.x; i < F; i += blockDim.x) s_faces[F * d + i] = b[i];
+    }
+    __syncthreads();
+    const double* AA = staged ? s_faces : A;
+    const double* bb = staged ? s_faces + F * d : b;
+    const int64_t i = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) / LPW;
+    if (i >= count) return;  // whole groups leave together
+    const int lane = threadIdx.x & (LPW - 1);
     const uint64_t walk = walk_offset + static_cast<uint64_t>(i);
     double x[MAXD];
     if (seeds) {
@@ -131,15 +204,15 @@ k_hnr(const double* __restrict__ A, const double* __restrict__ b, const int32_t*
 #pragma unroll
         for (int k = 0; k < MAXD; ++k) x[k] = (k < d) ? __dadd_rn(seg[k], __dmul_rn(alpha, seg[d + k])) : 0.0;
     }
-    const int st = hnr_walk<MAXD, RNG>(x, d, A, b, F, n_ms, seed, walk, seeds == nullptr);
+    const int st = hnr_walk<MAXD, RNG, LPW>(x, d, AA, bb, F, n_ms, seed, walk, seeds == nullptr);
     if (st != EZ_OK) {
-        set_status(status, st);
+        if (lane == 0) set_status(status, st);
         return;
     }
     double* o = out + i * d;
 #pragma unroll
     for (int k = 0; k < MAXD; ++k)
-        if (k < d) o[k] = x[k];
+        if (k < d && (k % LPW) == lane) o[k] = x[k];
 }
 
 // reference contains_many over all explicit seeds (cpoly.py:158-159)
@@ -159,21 +232,30 @@ __global__ void k_seed_check(const double* __restrict__ A, const double* __restr
 // ---------------------------------------------------------------------------
 // EI-ZO iteration kernels
 // ---------------------------------------------------------------------------
-// status record shared with the host (one 32-byte copy per iteration)
-enum : int { kColM = 0, kNumCand = 1, kStatus = 2, kPlaced = 3, kAccept = 4, kFaces = 5 };
+// Device record shared with the host.  Global part (rec): status (first
+// error wins), stop (set when an iteration accepts; every later kernel
+// returns at once) and the face count.  Per-iteration part (it, double
+// buffered so the host can enqueue iteration k+1 before reading k).
+enum : int { kStatus = 0, kStop = 1, kFaces = 2 };
+enum : int { kColM = 0, kNumCand = 1, kPlaced = 2, kAccept = 3 };
+constexpr int kRecInts = 32;               // rec[0..7] global, slots at 8 and 16
+__host__ __device__ constexpr int slot_offset(int k) { return 8 + 8 * (k & 1); }
 
 // order-preserving compaction of the first n_p colliding sample indices and
 // the acceptance decision of the unadaptive test (inflation.py:164-172, 294-301)
 __global__ void __launch_bounds__(1024)
 k_compact(const uint8_t* __restrict__ free_flags, int64_t n, int n_p, double thr, int32_t* __restrict__ rec,
-          int32_t* __restrict__ col) {
+          int32_t* __restrict__ it, int32_t* __restrict__ col) {
     __shared__ int warp_tot[32];
     __shared__ int warp_off[32];
     __shared__ int s_total;
-    if (rec[kStatus] != EZ_OK) return;
+    if (rec[kStatus] != EZ_OK || rec[kStop]) return;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const bool accept = static_cast<double>(rec[kColM]) <= thr;
-    if (threadIdx.x == 0) rec[kAccept] = accept ? 1 : 0;
+    const bool accept = static_cast<double>(it[kColM]) <= thr;
+    if (threadIdx.x == 0) {
+        it[kAccept] = accept ? 1 : 0;
+        if (accept) rec[kStop] = 1;
+    }
     if (accept) return;
     int run = 0;
     for (int64_t base = 0; base < n && run < n_p; base += blockDim.x) {
@@ -201,7 +283,7 @@ k_compact(const uint8_t* __restrict__ free_flags, int64_t n, int n_p, double thr
         run += s_total;
         __syncthreads();
     }
-    if (threadIdx.x == 0) rec[kNumCand] = min(run, n_p);
+    if (threadIdx.x == 0) it[kNumCand] = min(run, n_p);
 }
 
 // project_batch for one point (inflation.py:297-310)
@@ -228,24 +310,31 @@ __device__ __forceinline__ double project(const double (&c)[MAXD], int d, const 
     return sqrt(ss);
 }
 
-// One thread per candidate: project, fail-fast check of the projection, N_b
-// bisection rounds (each a full FK + collision check), t_col guard.
-template <typename T, int MAXD>
+// One group of G lanes per candidate: project, fail-fast check of the
+// projection, N_b bisection rounds (each a cooperative FK + collision check),
+// t_col guard.  The group shares the candidate's row and centre store.
+constexpr int kBisectLanes = 8;
+
+template <typename T, int MAXD, int G>
 __global__ void __launch_bounds__(128)
 k_bisect(ModelDev<T> M, T margin, const double* __restrict__ X, int d, const int32_t* __restrict__ col,
-         int32_t* __restrict__ rec, const double* __restrict__ seg, double ee, int n_b, double t_col,
+         int32_t* __restrict__ rec, const int32_t* __restrict__ it, const double* __restrict__ seg, double ee,
+         int n_b, double t_col,
          double* __restrict__ star, double* __restrict__ pstar, double* __restrict__ dstar) {
     extern __shared__ __align__(16) uint8_t smem[];
     __shared__ uint64_t bar;
-    const int C = rec[kNumCand];
-    if (rec[kStatus] != EZ_OK || rec[kAccept] || static_cast<int64_t>(blockIdx.x) * blockDim.x >= C) return;
+    constexpr int CPB = 128 / G;  // candidates per CTA
+    const int C = it[kNumCand];
+    if (rec[kStatus] != EZ_OK || rec[kStop] || static_cast<int64_t>(blockIdx.x) * CPB >= C) return;
     tma_stage(smem, M.blob, M.blob_bytes, &bar);
-    T* cen = reinterpret_cast<T*>(smem + M.blob_bytes);
-    const size_t roff = (static_cast<size_t>(M.blob_bytes) +
-                         static_cast<size_t>(3) * M.n_spheres * blockDim.x * sizeof(T) + 15) & ~static_cast<size_t>(15);
-    double* row = reinterpret_cast<double*>(smem + roff) + threadIdx.x * d;
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= C) return;
+    const int slot = threadIdx.x / G, lane = threadIdx.x & (G - 1);
+    T* cen = reinterpret_cast<T*>(smem + M.blob_bytes) + static_cast<size_t>(slot) * 3 * M.n_spheres;
+    const size_t roff = (static_cast<size_t>(M.blob_bytes) + static_cast<size_t>(3) * M.n_spheres * CPB * sizeof(T) + 15) &
+                        ~static_cast<size_t>(15);
+    double* row = reinterpret_cast<double*>(smem + roff) + slot * d;
+    const int i = blockIdx.x * CPB + slot;
+    if (i >= C) return;  // whole groups leave together
+    const unsigned gm = coop_mask<G>();
     const double* v1 = seg;
     const double* e = seg + d;
     double c[MAXD], lo[MAXD], hi[MAXD];
@@ -256,20 +345,23 @@ k_bisect(ModelDev<T> M, T margin, const double* __restrict__ X, int d, const int
 #pragma unroll
     for (int k = 0; k < MAXD; ++k) {
         hi[k] = c[k];
-        if (k < d) row[k] = lo[k];
+        if (k < d && (k % G) == lane) row[k] = lo[k];
     }
-    if (!config_free<T, double>(M, smem, row, cen + threadIdx.x, blockDim.x, margin)) {
-        set_status(rec + kStatus, EZ_SEGMENT_IN_COLLISION);  // inflation.py:303-305
+    __syncwarp(gm);
+    if (!config_free_coop<T, double, G>(M, smem, row, cen, margin)) {
+        if (lane == 0) set_status(rec + kStatus, EZ_SEGMENT_IN_COLLISION);  // inflation.py:303-305
         return;
     }
     for (int r = 0; r < n_b; ++r) {
         double mid[MAXD];
+        __syncwarp(gm);
 #pragma unroll
         for (int k = 0; k < MAXD; ++k) {
             mid[k] = 0.5 * (lo[k] + hi[k]);
-            if (k < d) row[k] = mid[k];
+            if (k < d && (k % G) == lane) row[k] = mid[k];
         }
-        const bool fr = config_free<T, double>(M, smem, row, cen + threadIdx.x, blockDim.x, margin);
+        __syncwarp(gm);
+        const bool fr = config_free_coop<T, double, G>(M, smem, row, cen, margin);
 #pragma unroll
         for (int k = 0; k < MAXD; ++k) {
             if (fr) lo[k] = mid[k];
@@ -278,22 +370,22 @@ k_bisect(ModelDev<T> M, T margin, const double* __restrict__ X, int d, const int
     }
     double ps[MAXD];
     const double ds = project<MAXD>(hi, d, v1, e, ee, ps);
-    if (ds <= t_col) set_status(rec + kStatus, EZ_SEGMENT_IN_COLLISION);  // inflation.py:307-310
+    if (ds <= t_col && lane == 0) set_status(rec + kStatus, EZ_SEGMENT_IN_COLLISION);  // inflation.py:307-310
 #pragma unroll
     for (int k = 0; k < MAXD; ++k) {
-        if (k < d) {
+        if (k < d && (k % G) == lane) {
             star[static_cast<int64_t>(i) * d + k] = hi[k];
             pstar[static_cast<int64_t>(i) * d + k] = ps[k];
         }
     }
-    dstar[i] = ds;
+    if (lane == 0) dstar[i] = ds;
 }
 
 // Greedy hyperplane placement on one CTA (inflation.py:232-259): the closest
 // alive candidate (stable order == lexicographic (dist, index)) becomes a
 // tangent face pushed back by compute_step_back; candidates outside die.
 __global__ void __launch_bounds__(1024)
-k_place(double* __restrict__ A, double* __restrict__ b, int32_t* __restrict__ rec, int d,
+k_place(double* __restrict__ A, double* __restrict__ b, int32_t* __restrict__ rec, int32_t* __restrict__ it, int d,
         const double* __restrict__ star, const double* __restrict__ pstar, const double* __restrict__ dstar,
         const double* __restrict__ seg, double delta_max, int n_f) {
     extern __shared__ uint8_t alive[];
@@ -302,8 +394,8 @@ k_place(double* __restrict__ A, double* __restrict__ b, int32_t* __restrict__ re
     __shared__ double s_a[32];
     __shared__ double s_rhs;
     __shared__ int s_best;
-    if (rec[kStatus] != EZ_OK || rec[kAccept]) return;
-    const int C = rec[kNumCand];
+    if (rec[kStatus] != EZ_OK || rec[kStop]) return;
+    const int C = it[kNumCand];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     for (int i = threadIdx.x; i < C; i += blockDim.x) alive[i] = 1;
     int F = rec[kFaces];
@@ -401,7 +493,7 @@ k_place(double* __restrict__ A, double* __restrict__ b, int32_t* __restrict__ re
     }
     if (threadIdx.x == 0) {
         rec[kFaces] = F;
-        rec[kPlaced] = placed;
+        it[kPlaced] = placed;
     }
 }
 
@@ -428,6 +520,7 @@ struct ez_eizo_ws {
     int32_t* h_rec = nullptr;  // pinned
     cudaStream_t stream = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    cudaEvent_t ev_it[2] = {nullptr, nullptr};
 };
 
 namespace ez {
@@ -448,6 +541,8 @@ void eizo_ws_free(ez_eizo_ws* ws) {
     if (ws->stream) cudaStreamDestroy(ws->stream);
     if (ws->ev0) cudaEventDestroy(ws->ev0);
     if (ws->ev1) cudaEventDestroy(ws->ev1);
+    for (cudaEvent_t e : ws->ev_it)
+        if (e) cudaEventDestroy(e);
     delete ws;
 }
 
@@ -476,8 +571,10 @@ static int32_t ws_reserve(ez_world* w, int d, int64_t n, int32_t c, int32_t f) {
         EZ_CUDA(cudaStreamCreateWithFlags(&slot->stream, cudaStreamNonBlocking));
         EZ_CUDA(cudaEventCreate(&slot->ev0));
         EZ_CUDA(cudaEventCreate(&slot->ev1));
-        EZ_CUDA(cudaMalloc(&slot->rec, 64));
-        EZ_CUDA(cudaMallocHost(&slot->h_rec, 64));
+        EZ_CUDA(cudaEventCreateWithFlags(&slot->ev_it[0], cudaEventDisableTiming));
+        EZ_CUDA(cudaEventCreateWithFlags(&slot->ev_it[1], cudaEventDisableTiming));
+        EZ_CUDA(cudaMalloc(&slot->rec, kRecInts * sizeof(int32_t)));
+        EZ_CUDA(cudaMallocHost(&slot->h_rec, 2 * kRecInts * sizeof(int32_t)));
         EZ_CUDA(cudaMalloc(&slot->seg, sizeof(double) * 3 * 64));
     }
     ez_eizo_ws* ws = slot;
@@ -506,50 +603,67 @@ static int32_t ws_reserve(ez_world* w, int d, int64_t n, int32_t c, int32_t f) {
 }
 
 template <int MAXD>
-static int32_t launch_hnr(int rng, unsigned grid, cudaStream_t s, const double* A, const double* b,
-                          const int32_t* F_dev, int F, int d, const double* seeds, int64_t n_seeds,
-                          const double* seg, const int64_t* n_dev, int64_t count, int n_ms, uint64_t seed,
-                          uint64_t walk_offset, double* out, int32_t* status) {
-    if (rng == EZ_RNG_PHILOX)
-        k_hnr<MAXD, EZ_RNG_PHILOX><<<grid, 128, 0, s>>>(A, b, F_dev, F, d, seeds, n_seeds, seg, n_dev, count,
-                                                        n_ms, seed, walk_offset, out, status);
-    else
-        k_hnr<MAXD, EZ_RNG_COUNTER><<<grid, 128, 0, s>>>(A, b, F_dev, F, d, seeds, n_seeds, seg, n_dev, count,
-                                                         n_ms, seed, walk_offset, out, status);
+static int32_t launch_hnr(int rng, cudaStream_t s, const double* A, const double* b, const int32_t* F_dev, int F,
+                          int f_bound, int d, const double* seeds, int64_t n_seeds, const double* seg, int64_t count,
+                          int n_ms, uint64_t seed, uint64_t walk_offset, double* out, int32_t* status) {
+    constexpr int LPW = MAXD;  // lanes per walk
+    const int64_t threads = count * LPW;
+    const unsigned grid = static_cast<unsigned>((threads + 127) / 128);
+    const size_t per_face = static_cast<size_t>(d + 1) * sizeof(double);
+    int smem_faces = std::max(F, f_bound);
+    if (static_cast<size_t>(smem_faces) * per_face > 96 * 1024) smem_faces = 0;  // large polytopes: read from L1/L2
+    const size_t smem = static_cast<size_t>(smem_faces) * per_face;
+    if (rng == EZ_RNG_PHILOX) {
+        auto k = k_hnr<MAXD, EZ_RNG_PHILOX, LPW>;
+        if (smem > 48 * 1024) EZ_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
+        k<<<grid, 128, smem, s>>>(A, b, F_dev, F, d, seeds, n_seeds, seg, count, n_ms, seed, walk_offset, out, status,
+                                  smem_faces);
+    } else {
+        auto k = k_hnr<MAXD, EZ_RNG_COUNTER, LPW>;
+        if (smem > 48 * 1024) EZ_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
+        k<<<grid, 128, smem, s>>>(A, b, F_dev, F, d, seeds, n_seeds, seg, count, n_ms, seed, walk_offset, out, status,
+                                  smem_faces);
+    }
     EZ_CUDA(cudaGetLastError());
     return EZ_OK;
 }
 
-static int32_t dispatch_hnr(int rng, unsigned grid, cudaStream_t s, const double* A, const double* b,
-                            const int32_t* F_dev, int F, int d, const double* seeds, int64_t n_seeds,
-                            const double* seg, const int64_t* n_dev, int64_t count, int n_ms, uint64_t seed,
-                            uint64_t walk_offset, double* out, int32_t* status) {
-    if (d <= 4) return launch_hnr<4>(rng, grid, s, A, b, F_dev, F, d, seeds, n_seeds, seg, n_dev, count, n_ms, seed, walk_offset, out, status);
-    if (d <= 8) return launch_hnr<8>(rng, grid, s, A, b, F_dev, F, d, seeds, n_seeds, seg, n_dev, count, n_ms, seed, walk_offset, out, status);
-    if (d <= 16) return launch_hnr<16>(rng, grid, s, A, b, F_dev, F, d, seeds, n_seeds, seg, n_dev, count, n_ms, seed, walk_offset, out, status);
-    if (d <= 32) return launch_hnr<32>(rng, grid, s, A, b, F_dev, F, d, seeds, n_seeds, seg, n_dev, count, n_ms, seed, walk_offset, out, status);
+// f_bound: largest face count the walk may see (faces live on the device in the EI-ZO loop)
+static int32_t dispatch_hnr(int rng, cudaStream_t s, const double* A, const double* b, const int32_t* F_dev, int F,
+                            int f_bound, int d, const double* seeds, int64_t n_seeds, const double* seg,
+                            int64_t count, int n_ms, uint64_t seed, uint64_t walk_offset, double* out,
+                            int32_t* status) {
+    if (d <= 4) return launch_hnr<4>(rng, s, A, b, F_dev, F, f_bound, d, seeds, n_seeds, seg, count, n_ms, seed, walk_offset, out, status);
+    if (d <= 8) return launch_hnr<8>(rng, s, A, b, F_dev, F, f_bound, d, seeds, n_seeds, seg, count, n_ms, seed, walk_offset, out, status);
+    if (d <= 16) return launch_hnr<16>(rng, s, A, b, F_dev, F, f_bound, d, seeds, n_seeds, seg, count, n_ms, seed, walk_offset, out, status);
+    if (d <= 32) return launch_hnr<32>(rng, s, A, b, F_dev, F, f_bound, d, seeds, n_seeds, seg, count, n_ms, seed, walk_offset, out, status);
     return fail(EZ_UNSUPPORTED, "hit-and-run supports dimension <= 32");
 }
 
 template <typename T, int MAXD>
-static int32_t launch_bisect_t(ez_world* w, const ModelDev<T>& M, cudaStream_t s, int n_p, int d, double ee,
-                               int n_b, double t_col) {
+static int32_t launch_bisect_t(ez_world* w, const ModelDev<T>& M, cudaStream_t s, const int32_t* it, int n_p, int d,
+                               double ee, int n_b, double t_col) {
     ez_eizo_ws* ws = device_ws(w->device);
-    size_t smem = 0;
-    const int threads = check_block_threads<T>(w, M.blob_bytes, M.n_spheres, d * static_cast<int>(sizeof(double)), &smem);
-    if (threads == 0) return fail(EZ_CAPACITY, "robot model too large for one bisection CTA");
-    auto kern = k_bisect<T, MAXD>;
+    constexpr int G = kBisectLanes, CPB = 128 / G;
+    size_t smem = M.blob_bytes + static_cast<size_t>(3) * M.n_spheres * CPB * sizeof(T);
+    smem = (smem + 15) & ~static_cast<size_t>(15);
+    smem += static_cast<size_t>(CPB) * d * sizeof(double);
+    smem = (smem + 15) & ~static_cast<size_t>(15);
+    auto kern = k_bisect<T, MAXD, G>;
+    if (smem > static_cast<size_t>(w->smem_optin) - 1024) return fail(EZ_CAPACITY, "robot model too large for one bisection CTA");
     if (smem > 48 * 1024) EZ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    kern<<<static_cast<unsigned>((n_p + threads - 1) / threads), threads, smem, s>>>(M, static_cast<T>(w->margin), ws->X, d, ws->col, ws->rec,
-                                                                  ws->seg, ee, n_b, t_col, ws->star, ws->pstar, ws->dstar);
+    kern<<<static_cast<unsigned>((n_p + CPB - 1) / CPB), 128, smem, s>>>(M, static_cast<T>(w->margin), ws->X, d, ws->col,
+                                                                     ws->rec, it, ws->seg, ee, n_b, t_col, ws->star,
+                                                                     ws->pstar, ws->dstar);
     EZ_CUDA(cudaGetLastError());
     return EZ_OK;
 }
 
 template <int MAXD>
-static int32_t launch_bisect(ez_world* w, int precision, cudaStream_t s, int n_p, int d, double ee, int n_b, double t_col) {
-    if (precision == EZ_F64) return launch_bisect_t<double, MAXD>(w, w->md, s, n_p, d, ee, n_b, t_col);
-    return launch_bisect_t<float, MAXD>(w, w->mf, s, n_p, d, ee, n_b, t_col);
+static int32_t launch_bisect(ez_world* w, int precision, cudaStream_t s, const int32_t* it, int n_p, int d, double ee,
+                             int n_b, double t_col) {
+    if (precision == EZ_F64) return launch_bisect_t<double, MAXD>(w, w->md, s, it, n_p, d, ee, n_b, t_col);
+    return launch_bisect_t<float, MAXD>(w, w->mf, s, it, n_p, d, ee, n_b, t_col);
 }
 
 }  // namespace ez
@@ -566,11 +680,11 @@ extern "C" int32_t ez_hit_and_run(const double* d_A, const double* d_b, int32_t 
     if (rng != EZ_RNG_COUNTER && rng != EZ_RNG_PHILOX) return fail(EZ_INVALID_ARGUMENT, "unknown rng");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     int32_t* d_status = nullptr;
-    EZ_CUDA(cudaMallocAsync(&d_status, sizeof(int32_t), s));
-    EZ_CUDA(cudaMemsetAsync(d_status, 0, sizeof(int32_t), s));
+    EZ_CUDA(cudaMallocAsync(&d_status, 2 * sizeof(int32_t), s));  // (status, stop)
+    EZ_CUDA(cudaMemsetAsync(d_status, 0, 2 * sizeof(int32_t), s));
     k_seed_check<<<static_cast<unsigned>((n_seeds + 127) / 128), 128, 0, s>>>(d_A, d_b, n_faces, dim, d_seeds, n_seeds, d_status);
-    int32_t st = dispatch_hnr(rng, static_cast<unsigned>((count + 127) / 128), s, d_A, d_b, nullptr, n_faces, dim, d_seeds,
-                              n_seeds, nullptr, nullptr, count, n_ms, seed, walk_offset, d_out, d_status);
+    int32_t st = dispatch_hnr(rng, s, d_A, d_b, nullptr, n_faces, n_faces, dim, d_seeds, n_seeds, nullptr, count, n_ms,
+                              seed, walk_offset, d_out, d_status);
     int32_t h_status = 0;
     if (st == EZ_OK) {
         cudaError_t e = cudaMemcpyAsync(&h_status, d_status, sizeof(int32_t), cudaMemcpyDeviceToHost, s);
@@ -636,7 +750,7 @@ extern "C" int32_t ez_inflate_edge(ez_world* w, const double* h_v1, const double
     EZ_CUDA(cudaMemcpyAsync(ws->seg, seg.data(), sizeof(double) * 3 * d, cudaMemcpyHostToDevice, s));
     EZ_CUDA(cudaMemcpyAsync(ws->A, h_A0, sizeof(double) * n_faces0 * d, cudaMemcpyHostToDevice, s));
     EZ_CUDA(cudaMemcpyAsync(ws->b, h_b0, sizeof(double) * n_faces0, cudaMemcpyHostToDevice, s));
-    EZ_CUDA(cudaMemsetAsync(ws->rec, 0, 64, s));
+    EZ_CUDA(cudaMemsetAsync(ws->rec, 0, kRecInts * sizeof(int32_t), s));
     {
         int32_t f0 = n_faces0;
         EZ_CUDA(cudaMemcpyAsync(ws->rec + kFaces, &f0, sizeof(int32_t), cudaMemcpyHostToDevice, s));
@@ -647,70 +761,97 @@ extern "C" int32_t ez_inflate_edge(ez_world* w, const double* h_v1, const double
         EZ_CUDA(cudaFuncSetAttribute(k_place, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(std::min<size_t>(place_smem, 200 * 1024))));
     if (place_smem > 200 * 1024) return fail(EZ_UNSUPPORTED, "n_p above 204800 candidates");
 
+    // One iteration = hit-and-run, check (+ first-M count), compaction/test,
+    // bisection, placement, and a 128-byte record copy.  Iteration k+1 is
+    // enqueued before the host waits for k's record (its walk offset and
+    // batch size are host-known); if k accepted, k+1's kernels see `stop`
+    // and return at once.
+    std::vector<int64_t> n_s_of(2), m_of(2);
+    auto enqueue = [&](int k, uint64_t woff, int f_known) -> int32_t {
+        const int64_t m = batch_size(k, p);
+        const double thr = static_cast<double>(m) * (1.0 - p.tau) * p.eps;
+        const int64_t n_s = std::max<int64_t>(p.n_p, m);
+        int32_t* it = ws->rec + slot_offset(k);
+        EZ_CUDA(cudaMemsetAsync(it, 0, 8 * sizeof(int32_t), s));
+        EZ_TRY(dispatch_hnr(rng, s, ws->A, ws->b, ws->rec + kFaces, f_known, f_known + 2 * p.n_f, d, nullptr, 1,
+                            ws->seg, n_s, p.n_ms, seed, woff, ws->X, ws->rec + kStatus));
+        EZ_TRY(launch_check(w, ws->X, EZ_F64, n_s, d, ws->flags, precision, s, m, it + kColM));
+        k_compact<<<1, 1024, 0, s>>>(ws->flags, n_s, p.n_p, thr, ws->rec, it, ws->col);
+        EZ_CUDA(cudaGetLastError());
+        if (d <= 4) EZ_TRY(launch_bisect<4>(w, precision, s, it, p.n_p, d, ee, p.n_b, p.t_col));
+        else if (d <= 8) EZ_TRY(launch_bisect<8>(w, precision, s, it, p.n_p, d, ee, p.n_b, p.t_col));
+        else if (d <= 16) EZ_TRY(launch_bisect<16>(w, precision, s, it, p.n_p, d, ee, p.n_b, p.t_col));
+        else EZ_TRY(launch_bisect<32>(w, precision, s, it, p.n_p, d, ee, p.n_b, p.t_col));
+        k_place<<<1, 1024, place_smem, s>>>(ws->A, ws->b, ws->rec, it, d, ws->star, ws->pstar, ws->dstar, ws->seg,
+                                            p.delta_max, p.n_f);
+        EZ_CUDA(cudaGetLastError());
+        EZ_CUDA(cudaMemcpyAsync(ws->h_rec + kRecInts * (k & 1), ws->rec, kRecInts * sizeof(int32_t),
+                                cudaMemcpyDeviceToHost, s));
+        EZ_CUDA(cudaEventRecord(ws->ev_it[k & 1], s));
+        n_s_of[k & 1] = n_s;
+        m_of[k & 1] = m;
+        return EZ_OK;
+    };
+    auto drain_and_fail = [&](int32_t st, const char* msg) -> int32_t {
+        cudaStreamSynchronize(s);
+        return fail(st, msg);
+    };
+
     int F = n_faces0;
     uint64_t walk_offset = 0;
     int64_t checks = 0;
     int32_t hyper = 0;
     int k = 1;
     int32_t terminated = 0;
+    EZ_TRY(enqueue(1, 0, F));
     for (;; ++k) {
-        const int64_t m = batch_size(k, p);
-        const double thr = static_cast<double>(m) * (1.0 - p.tau) * p.eps;
-        const int64_t n_s = std::max<int64_t>(p.n_p, m);
-        if (n_s > ws->n_cap || F + p.n_f > ws->f_cap) {
-            EZ_CUDA(cudaStreamSynchronize(s));
-            EZ_TRY(ws_reserve(w, d, std::max<int64_t>(n_s, ws->n_cap), p.n_p, std::max(ws->f_cap * 2, F + 16 * p.n_f)));
-        }
-        // reset per-iteration fields (status and face count persist)
-        EZ_CUDA(cudaMemsetAsync(ws->rec + kColM, 0, 2 * sizeof(int32_t), s));
-        EZ_CUDA(cudaMemsetAsync(ws->rec + kPlaced, 0, 2 * sizeof(int32_t), s));
-        EZ_TRY(dispatch_hnr(rng, static_cast<unsigned>((n_s + 127) / 128), s, ws->A, ws->b, ws->rec + kFaces, F, d,
-                            nullptr, 1, ws->seg, nullptr, n_s, p.n_ms, seed, walk_offset, ws->X, ws->rec + kStatus));
-        EZ_TRY(launch_check(w, ws->X, EZ_F64, n_s, d, ws->flags, precision, s, m, ws->rec + kColM));
-        k_compact<<<1, 1024, 0, s>>>(ws->flags, n_s, p.n_p, thr, ws->rec, ws->col);
-        EZ_CUDA(cudaGetLastError());
-        if (d <= 4) EZ_TRY(launch_bisect<4>(w, precision, s, p.n_p, d, ee, p.n_b, p.t_col));
-        else if (d <= 8) EZ_TRY(launch_bisect<8>(w, precision, s, p.n_p, d, ee, p.n_b, p.t_col));
-        else if (d <= 16) EZ_TRY(launch_bisect<16>(w, precision, s, p.n_p, d, ee, p.n_b, p.t_col));
-        else EZ_TRY(launch_bisect<32>(w, precision, s, p.n_p, d, ee, p.n_b, p.t_col));
-        k_place<<<1, 1024, place_smem, s>>>(ws->A, ws->b, ws->rec, d, ws->star, ws->pstar, ws->dstar, ws->seg,
-                                            p.delta_max, p.n_f);
-        EZ_CUDA(cudaGetLastError());
-        EZ_CUDA(cudaMemcpyAsync(ws->h_rec, ws->rec, 32, cudaMemcpyDeviceToHost, s));
-        EZ_CUDA(cudaStreamSynchronize(s));
-        const int32_t* r = ws->h_rec;
-        if (r[kStatus] != EZ_OK) {
-            switch (r[kStatus]) {
-                case EZ_EMPTY_CHORD: return fail(EZ_EMPTY_CHORD, "no feasible chord; polytope numerically degenerate");
-                case EZ_SEED_OUTSIDE: return fail(EZ_SEED_OUTSIDE, "walk seed outside the polytope");
+        const uint64_t next_offset = walk_offset + static_cast<uint64_t>(n_s_of[k & 1]);
+        const bool may_continue = !(p.n_it > 0 && k >= p.n_it);
+        const bool fits = (k + 1 <= 64) && (F + 2 * p.n_f <= ws->f_cap);
+        if (may_continue && fits) EZ_TRY(enqueue(k + 1, next_offset, F + p.n_f));
+        EZ_CUDA(cudaEventSynchronize(ws->ev_it[k & 1]));
+        const int32_t* g = ws->h_rec + kRecInts * (k & 1);
+        const int32_t* r = g + slot_offset(k);
+        if (g[kStatus] != EZ_OK) {
+            switch (g[kStatus]) {
+                case EZ_EMPTY_CHORD: return drain_and_fail(EZ_EMPTY_CHORD, "no feasible chord; polytope numerically degenerate");
+                case EZ_SEED_OUTSIDE: return drain_and_fail(EZ_SEED_OUTSIDE, "walk seed outside the polytope");
                 case EZ_SEGMENT_IN_COLLISION:
-                    return fail(EZ_SEGMENT_IN_COLLISION, "a projection onto the seed segment, or a bisected collision, "
-                                                         "lies in collision within t_col of the seed segment");
-                case EZ_GRADIENT_UNDEFINED: return fail(EZ_GRADIENT_UNDEFINED, "candidate collapsed onto the segment");
-                default: return fail(r[kStatus], "EI-ZO device failure");
+                    return drain_and_fail(EZ_SEGMENT_IN_COLLISION,
+                                          "a projection onto the seed segment, or a bisected collision, "
+                                          "lies in collision within t_col of the seed segment");
+                case EZ_GRADIENT_UNDEFINED: return drain_and_fail(EZ_GRADIENT_UNDEFINED, "candidate collapsed onto the segment");
+                default: return drain_and_fail(g[kStatus], "EI-ZO device failure");
             }
         }
-        walk_offset += static_cast<uint64_t>(n_s);
-        checks += n_s;
+        checks += n_s_of[k & 1];
+        walk_offset = next_offset;
         if (r[kAccept]) {
             terminated = 0;
             break;
         }
         checks += static_cast<int64_t>(r[kNumCand]) * (1 + p.n_b);
         hyper += r[kPlaced];
-        F = r[kFaces];
-        if (p.n_it > 0 && k >= p.n_it) {
+        F = g[kFaces];
+        if (!may_continue) {
             terminated = 1;
             break;
         }
+        if (!fits) {  // grow the workspace, then continue without lookahead for this step
+            EZ_CUDA(cudaStreamSynchronize(s));
+            EZ_TRY(ws_reserve(w, d, std::max<int64_t>(ws->n_cap, std::max<int64_t>(p.n_p, batch_size(k + 64, p))),
+                              p.n_p, std::max(ws->f_cap * 2, F + 64 * p.n_f)));
+            EZ_TRY(enqueue(k + 1, walk_offset, F));
+        }
     }
     EZ_CUDA(cudaEventRecord(ws->ev1, s));
-    EZ_CUDA(cudaEventSynchronize(ws->ev1));
+    EZ_CUDA(cudaEventSynchronize(ws->ev1));  // also drains the void look-ahead iteration
     float ms = 0.f;
     cudaEventElapsedTime(&ms, ws->ev0, ws->ev1);
     if (F > face_cap) return fail(EZ_CAPACITY, "face_cap smaller than the result polytope");
-    EZ_CUDA(cudaMemcpy(h_A_out, ws->A, sizeof(double) * F * d, cudaMemcpyDeviceToHost));
-    EZ_CUDA(cudaMemcpy(h_b_out, ws->b, sizeof(double) * F, cudaMemcpyDeviceToHost));
+    EZ_CUDA(cudaMemcpyAsync(h_A_out, ws->A, sizeof(double) * F * d, cudaMemcpyDeviceToHost, s));
+    EZ_CUDA(cudaMemcpyAsync(h_b_out, ws->b, sizeof(double) * F, cudaMemcpyDeviceToHost, s));
+    EZ_CUDA(cudaStreamSynchronize(s));
     report->iterations = k;
     report->hyperplanes_added = hyper;
     report->collision_checks = checks;
