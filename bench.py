@@ -123,6 +123,102 @@ def cpu_oracle_rate(world, n: int, workers: int) -> dict:
             "sample": f"{n} uniform 7-DOF configs, oracle/ref.py (numpy+cKDTree restatement of world.py:483-565)"}
 
 
+def clustered_cloud(n_points: int, n_blobs: int, seed: int = 0) -> np.ndarray:
+    """Synthetic perception: Gaussian blobs in front of the arm."""
+    rng = np.random.default_rng(seed)
+    per = n_points // n_blobs
+    pts = []
+    for _ in range(n_blobs):
+        c = rng.uniform([0.3, -0.6, 0.0], [0.9, 0.6, 1.0])
+        r = rng.uniform(0.03, 0.10)
+        pts.append(c + rng.normal(size=(per, 3)) * r / 2)
+    return np.concatenate(pts)
+
+
+def bench_config4(checks_n: int = 1 << 20) -> dict:
+    """Config 4: 14-DOF bimanual (66 spheres, 1,248 pairs): checks/s and one EI-ZO region."""
+    import torch
+
+    from paper_2504_10783_b200 import fixtures as fx
+    from paper_2504_10783_b200.eizo import InflationParams, Segment, inflate_edge
+    from paper_2504_10783_b200.polytope import HPolytope
+
+    world = fx.bimanual14_world()
+    ck = world.checker()
+    lo = torch.as_tensor(world.lower, dtype=torch.float32, device="cuda")
+    hi = torch.as_tensor(world.upper, dtype=torch.float32, device="cuda")
+    Q = lo + (hi - lo) * torch.rand((checks_n, 14), device="cuda")
+    nat = ck.native
+    for _ in range(3):
+        nat.check_device(Q)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(5):
+        nat.check_device(Q)
+    e1.record()
+    torch.cuda.synchronize()
+    rate = 5 * checks_n / (e0.elapsed_time(e1) * 1e-3)
+    v1, v2 = fx.random_free_segment(world, seed=3)
+    dom = HPolytope.from_bounds(world.lower, world.upper)
+    params = InflationParams(**fx.FRANKA_PARAMS)
+    rep = inflate_edge(Segment(v1, v2), dom, params, ck, seed=7)
+    t0 = time.perf_counter()
+    rep = inflate_edge(Segment(v1, v2), dom, params, ck, seed=7)
+    wall = (time.perf_counter() - t0) * 1e3
+    return {"checks_per_s": rate, "flop_per_check": 13104,
+            "eizo_ms_wall": wall, "eizo_device_ms": rep.device_ms, "iterations": rep.iterations,
+            "faces": rep.hyperplanes_added, "collision_checks": rep.collision_checks,
+            "terminated_by": rep.terminated_by,
+            "workload": "14-DOF bimanual sphere model vs 10k voxels; EI-ZO single segment, Franka (eps, delta)"}
+
+
+def bench_drm(n_nodes: int = 100_000, reps: int = 10, cpu: bool = True) -> dict:
+    """Config 5: point cloud -> active voxels -> blocked nodes on a 25x34x26 grid, 100k-node roadmap."""
+    import torch
+
+    from paper_2504_10783_b200 import fixtures as fx
+    from paper_2504_10783_b200.roadmap import DeviceRoadmap, Drm, Grid, collision_set, sample_free_nodes
+    from paper_2504_10783_b200.scene import voxelize_point_cloud
+
+    grid = Grid(np.array([-0.75, -1.02, -0.36]), 0.06, (25, 34, 26))
+    base = fx.franka7_world(False)
+    t0 = time.perf_counter()
+    nodes = sample_free_nodes(base, n_nodes, seed=0)
+    t_nodes = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    rm = DeviceRoadmap.build(base, nodes, grid)
+    torch.cuda.synchronize()
+    t_map = time.perf_counter() - t0
+    off, ids = rm.export()
+    drm = Drm(nodes, np.zeros(n_nodes + 1, np.int64), np.zeros(0, np.int32), off, ids, np.zeros((n_nodes, 7)), grid)
+    out = {"grid": "25x34x26 side 0.06", "n_nodes": n_nodes, "cmap_nnz": int(ids.shape[0]),
+           "node_sampling_s": t_nodes, "cmap_build_s": t_map, "clouds": []}
+    for blobs in (3, 8):
+        pts = clustered_cloud(100_000, blobs, seed=blobs)
+        vm = voxelize_point_cloud(pts, grid.side, grid.origin)
+        cs = collision_set(drm, vm)
+        times = []
+        for _ in range(reps):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            vm = voxelize_point_cloud(pts, grid.side, grid.origin)
+            cs = collision_set(drm, vm)
+            times.append((time.perf_counter() - t0) * 1e3)
+        rec = {"points": pts.shape[0], "blobs": blobs, "active_voxels": vm.n_occupied, "blocked": len(cs),
+               "voxelize_plus_prune_ms": float(np.median(times))}
+        if cpu:
+            from oracle import ref
+
+            t0 = time.perf_counter()
+            idx = ref.voxelize(pts, grid.side, grid.origin)
+            blocked = ref.collision_set(off, ids, grid.origin, grid.side, grid.extents, idx, grid.origin, grid.side)
+            rec["cpu_port_ms"] = (time.perf_counter() - t0) * 1e3
+            rec["cpu_matches"] = bool(np.array_equal(blocked, cs.ids))
+        out["clouds"].append(rec)
+    return out
+
+
 def run_reference(args):
     rank, world_size, _ = _rank()
     if rank != 0:
@@ -274,6 +370,10 @@ def run_ours(args):
     if world_size == 1 and not args.skip_cpu:
         cpu = cpu_oracle_rate(world, args.cpu_sample, 1)
     peaks = _measured_peaks()
+    extra = {}
+    if world_size == 1 and not args.skip_extra:
+        extra["config4"] = bench_config4()
+        extra["drm"] = bench_drm(cpu=not args.skip_cpu)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world_size, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": max_ms / args.steps, "higher_is_better": True, "scaling": "weak",
@@ -294,6 +394,7 @@ def run_ours(args):
         "clocks": clk.summary(),
         "cpu_baseline": cpu,
         "eizo": eizo,
+        **extra,
     }
     print(json.dumps(line), flush=True)
     if world_size > 1:
@@ -308,6 +409,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--skip-eizo", action="store_true")
     ap.add_argument("--skip-cpu", action="store_true")
+    ap.add_argument("--skip-extra", action="store_true", help="skip the config-4 and config-5 (DRM) sections")
     ap.add_argument("--cpu-sample", type=int, default=30_000)
     args = ap.parse_args()
     if args.impl == "reference":

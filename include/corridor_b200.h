@@ -186,6 +186,15 @@ int32_t ez_roadmap_create(const int64_t* h_cmap_offsets, const int32_t* h_cmap_i
                           const double* h_origin, double side, const int32_t* h_extents,
                           int32_t device, ez_roadmap** out);
 int32_t ez_roadmap_destroy(ez_roadmap* roadmap);
+/* Offline collision map on the GPU (replaces drm.py:170-204 _node_voxel_pairs
+ * + the CSR assembly of build_drm, drm.py:250-251): voxel v lists every node
+ * whose robot spheres touch v's circumscribing sphere, (r + r_vox)^2 test in
+ * fp64, node ids ascending.  d_nodes: [n_nodes][dof] fp64 device rows. */
+int32_t ez_roadmap_build(ez_world* world, const double* d_nodes, int64_t n_nodes, int32_t dim,
+                         const double* h_origin, double side, const int32_t* h_extents, void* stream,
+                         ez_roadmap** out);
+int32_t ez_roadmap_info(const ez_roadmap* roadmap, int64_t* n_voxels, int64_t* n_nodes, int64_t* nnz);
+int32_t ez_roadmap_export(const ez_roadmap* roadmap, int64_t* h_offsets, int32_t* h_ids);
 int32_t ez_collision_set(ez_roadmap* roadmap, const int32_t* d_vox_idx, int64_t n_vox,
                          const double* h_vmap_origin, double vmap_side, int32_t same_grid,
                          uint32_t* d_blocked_bits, int64_t* n_blocked, void* stream);

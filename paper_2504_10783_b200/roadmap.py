@@ -143,6 +143,45 @@ class Drm:
 class DeviceRoadmap:
     """``ez_roadmap`` handle: the CSR collision map resident on one device."""
 
+    @classmethod
+    def build(cls, world_or_model, nodes, grid: Grid) -> "DeviceRoadmap":
+        """Collision map of ``nodes`` on ``grid`` computed on the GPU (ez_roadmap_build).
+
+        Replaces the node x voxel sweep of ``build_drm`` (drm.py:170-204,
+        250-251): voxel v lists every node whose spheres touch v's
+        circumscribing sphere (fp64, no margin), ids ascending.
+        """
+        import torch
+
+        from .native_world import NativeWorld
+        from .scene import World
+
+        model = getattr(world_or_model, "model", world_or_model)
+        nw = NativeWorld(model, (), None, 0.0)
+        dev = torch_device()
+        q = torch.as_tensor(np.ascontiguousarray(nodes, dtype=np.float64), device=dev)
+        if q.dim() != 2 or q.shape[1] != model.dof:
+            raise DimensionMismatch("node rows must have one value per degree of freedom")
+        org = np.ascontiguousarray(grid.origin, dtype=np.float64)
+        ext = np.ascontiguousarray(grid.extents, dtype=np.int32)
+        h = C.c_void_p()
+        N.check(N.lib().ez_roadmap_build(nw.handle, q.data_ptr(), q.shape[0], grid.dim, N.ptr(org), float(grid.side),
+                                         N.ptr(ext, C.c_int32), stream_handle(), C.byref(h)))
+        self = cls.__new__(cls)
+        self._h = h
+        self.n_nodes = int(q.shape[0])
+        self.grid = grid
+        return self
+
+    def export(self):
+        """(cmap_offsets int64 [n_voxels+1], cmap_ids int32 [nnz]) on the host."""
+        nv, nn, nnz = C.c_int64(), C.c_int64(), C.c_int64()
+        N.check(N.lib().ez_roadmap_info(self._h, C.byref(nv), C.byref(nn), C.byref(nnz)))
+        off = np.empty(nv.value + 1, dtype=np.int64)
+        ids = np.empty(nnz.value, dtype=np.int32)
+        N.check(N.lib().ez_roadmap_export(self._h, N.ptr(off, C.c_int64), N.ptr(ids, C.c_int32)))
+        return off, ids
+
     def __init__(self, drm: Drm, device: int):
         require_cuda()
         g = drm.grid
@@ -178,6 +217,41 @@ class DeviceRoadmap:
         N.check(N.lib().ez_collision_set(self._h, idx.data_ptr(), vmap.n_occupied, N.ptr(vorg), float(vmap.side),
                                          1 if same else 0, bits.data_ptr(), C.byref(n_blocked), stream_handle()))
         return bits, n_blocked.value
+
+
+def build_collision_map(world_or_model, nodes, grid: Grid):
+    """(cmap_offsets, cmap_ids) of ``nodes`` on ``grid``, computed on the GPU."""
+    return DeviceRoadmap.build(world_or_model, nodes, grid).export()
+
+
+def sample_free_nodes(world, n: int, seed: int = 0, batch: int = 1 << 20) -> np.ndarray:
+    """Uniform collision-free configurations of ``world`` (rejection sampling, GPU checks).
+
+    Same distribution as ``sample_free_configurations`` (drm.py:147-167);
+    the stream is torch's Philox, not numpy's.
+    """
+    import torch
+
+    dev = torch_device()
+    ck = world.checker()
+    lo = torch.as_tensor(world.lower, dtype=torch.float64, device=dev)
+    hi = torch.as_tensor(world.upper, dtype=torch.float64, device=dev)
+    g = torch.Generator(device=dev)
+    g.manual_seed(int(seed))
+    out, have = [], 0
+    for _ in range(1000):
+        Q = lo + (hi - lo) * torch.rand((batch, lo.shape[0]), generator=g, device=dev, dtype=torch.float64)
+        free = ck.check_batch(Q)
+        good = Q[free]
+        out.append(good)
+        have += int(good.shape[0])
+        if have >= n:
+            break
+    else:
+        from .errors import SamplingExhausted
+
+        raise SamplingExhausted(f"only {have}/{n} free configurations found")
+    return torch.cat(out)[:n].cpu().numpy()
 
 
 def collision_set(drm: Drm, vmap: VoxelMap) -> CollisionSet:
