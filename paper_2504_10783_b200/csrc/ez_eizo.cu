@@ -807,7 +807,7 @@ extern "C" int32_t ez_inflate_edge(ez_world* w, const double* h_v1, const double
     for (;; ++k) {
         const uint64_t next_offset = walk_offset + static_cast<uint64_t>(n_s_of[k & 1]);
         const bool may_continue = !(p.n_it > 0 && k >= p.n_it);
-        const bool fits = (k + 1 <= 64) && (F + 2 * p.n_f <= ws->f_cap);
+        const bool fits = (std::max<int64_t>(p.n_p, batch_size(k + 1, p)) <= ws->n_cap) && (F + 2 * p.n_f <= ws->f_cap);
         if (may_continue && fits) EZ_TRY(enqueue(k + 1, next_offset, F + p.n_f));
         EZ_CUDA(cudaEventSynchronize(ws->ev_it[k & 1]));
         const int32_t* g = ws->h_rec + kRecInts * (k & 1);
@@ -840,7 +840,7 @@ extern "C" int32_t ez_inflate_edge(ez_world* w, const double* h_v1, const double
         if (!fits) {  // grow the workspace, then continue without lookahead for this step
             EZ_CUDA(cudaStreamSynchronize(s));
             EZ_TRY(ws_reserve(w, d, std::max<int64_t>(ws->n_cap, std::max<int64_t>(p.n_p, batch_size(k + 64, p))),
-                              p.n_p, std::max(ws->f_cap * 2, F + 64 * p.n_f)));
+                              p.n_p, std::max(ws->f_cap, F + 64 * p.n_f)));
             EZ_TRY(enqueue(k + 1, walk_offset, F));
         }
     }
