@@ -171,6 +171,17 @@ int32_t ez_inflate_edge(ez_world* world, const double* h_v1, const double* h_v2,
                         int32_t rng, ez_eizo_report* report, double* h_A_out, double* h_b_out,
                         int32_t face_cap);
 
+/* Set repair, the device part of refine_sets (planner.py:159-224): project
+ * n_cols host collisions onto the seed segment, fail-fast check, N_b
+ * bisection rounds, then uncapped step-back faces discarding candidates whose
+ * ORIGINAL collision leaves the set (planner.py:191-192).  Appends faces to
+ * (h_A, h_b) and writes the result to h_A_out/h_b_out (capacity face_cap). */
+int32_t ez_refine_set(ez_world* world, const double* h_v1, const double* h_v2, int32_t dim,
+                      const double* h_A, const double* h_b, int32_t n_faces, const double* h_cols,
+                      int32_t n_cols, double delta_max, double t_col, int32_t n_b, int32_t precision,
+                      double* h_A_out, double* h_b_out, int32_t face_cap, int32_t* n_faces_out,
+                      int64_t* collision_checks);
+
 /* ---------------- DRM online phase ----------------
  * ez_voxelize        replaces voxelize_point_cloud (world.py:315-328): unique
  *                    occupied bins floor((p - origin)/side), lexicographically

@@ -228,13 +228,57 @@ def gen_drm(C):
     np.savez_compressed(GOLDEN / "drm.npz", **out)
 
 
+def gen_corridor(C):
+    """inflate_path + refine_sets (planner.py:103-224) on a Forest disc world."""
+    import corridor.planner as PL
+    from paper_2504_10783_b200 import fixtures as fx
+
+    centers = fx.forest_centers(7003)
+    world = fx.disc_world(centers)
+    rw = _to_ref_world(world, C)
+    ck = rw.checker(margin=0.05)
+    rng = np.random.default_rng(12)
+    knots = [np.array([1.2, 0.6])]
+    while len(knots) < 5:  # chained free segments (margin 0.05, step 0.01), length 1.0..1.5
+        d = rng.normal(size=2)
+        d /= np.linalg.norm(d)
+        nxt = knots[-1] + d * rng.uniform(1.0, 1.5)
+        if np.all(np.abs(nxt) < 4.6) and ck.check_segment(knots[-1], nxt, 0.01):
+            knots.append(nxt)
+    path = C.drm.PwlPath(np.array(knots))
+    dom = C.cpoly.HPolytope.from_bounds([-5, -5], [5, 5])
+    # a capped inflation (n_it=1, n_f=3) leaves collisions inside the sets for the repair
+    params = C.inflation.InflationParams(n_it=1, n_f=2)
+    scs = PL.inflate_path(path, dom, params, rw.checker(), seed=21)
+    pts = np.random.default_rng(5).uniform(-5, 5, size=(400_000, 2))
+    cols = []
+    for j, P in enumerate(scs.sets):
+        inside = pts[P.contains_many(pts)]
+        for c in inside[~rw.checker().check_batch(inside)][:4]:
+            cols.append((j, c))
+    col = [c for _, c in cols]
+    assert cols, "no collisions inside the capped sets"
+    ref = PL.refine_sets(scs, cols, path, params, rw.checker(), seed=9)
+    out = {"knots": path.knots, "centers": centers, "n_cols": len(cols), "cols": np.array(col),
+           "col_sets": np.array([j for j, _ in cols]),
+           "n_sets": len(scs.sets), "coverage": np.array(scs.coverage),
+           "r_n_sets": len(ref.sets), "r_coverage": np.array(ref.coverage)}
+    for i, Pi in enumerate(scs.sets):
+        out[f"set{i}_A"], out[f"set{i}_b"] = Pi.A, Pi.b
+    for i, Pi in enumerate(ref.sets):
+        out[f"rset{i}_A"], out[f"rset{i}_b"] = Pi.A, Pi.b
+    np.savez_compressed(GOLDEN / "corridor.npz", **out)
+    print(f"corridor: {len(scs.sets)} sets (coverage {scs.coverage}), {len(cols)} collisions -> "
+          f"{len(ref.sets)} sets after repair")
+
+
 def main(which=None):
     GOLDEN.mkdir(parents=True, exist_ok=True)
     C = _import_reference()
     import corridor.bench, corridor.cpoly, corridor.drm, corridor.inflation, corridor.world  # noqa: E401,F401
 
     steps = {"checks": gen_checks, "fk": gen_fk, "hnr": gen_hnr, "inflate": gen_inflate,
-             "voxelize": gen_voxelize, "drm": gen_drm}
+             "voxelize": gen_voxelize, "drm": gen_drm, "corridor": gen_corridor}
     for name, fn in steps.items():
         if which and name not in which:
             continue

@@ -69,6 +69,8 @@ SIGNATURES = {
                                c_vp, c_vp]),
     "ez_inflate_edge": (c_i32, [c_vp, P_dbl, P_dbl, c_i32, P_dbl, P_dbl, c_i32, C.POINTER(EizoParams),
                                 c_u64, c_i32, c_i32, C.POINTER(EizoReport), P_dbl, P_dbl, c_i32]),
+    "ez_refine_set": (c_i32, [c_vp, P_dbl, P_dbl, c_i32, P_dbl, P_dbl, c_i32, P_dbl, c_i32, c_dbl, c_dbl, c_i32,
+                              c_i32, P_dbl, P_dbl, c_i32, P_i32, P_i64]),
     "ez_voxelize": (c_i32, [c_vp, c_i64, c_i32, P_dbl, c_dbl, c_vp, P_i64, c_vp]),
     "ez_roadmap_create": (c_i32, [P_i64, P_i32, c_i64, c_i64, c_i32, P_dbl, c_dbl, P_i32, c_i32,
                                   C.POINTER(c_vp)]),

@@ -387,7 +387,7 @@ k_bisect(ModelDev<T> M, T margin, const double* __restrict__ X, int d, const int
 __global__ void __launch_bounds__(1024)
 k_place(double* __restrict__ A, double* __restrict__ b, int32_t* __restrict__ rec, int32_t* __restrict__ it, int d,
         const double* __restrict__ star, const double* __restrict__ pstar, const double* __restrict__ dstar,
-        const double* __restrict__ seg, double delta_max, int n_f) {
+        const double* __restrict__ seg, double delta_max, int n_f, const double* __restrict__ targets) {
     extern __shared__ uint8_t alive[];
     __shared__ double s_bd[32];
     __shared__ int s_bi[32];
@@ -485,7 +485,9 @@ k_place(double* __restrict__ A, double* __restrict__ b, int32_t* __restrict__ re
         const double rhs = s_rhs;
         for (int i = threadIdx.x; i < C; i += blockDim.x) {
             if (!alive[i]) continue;
-            const double* t = star + static_cast<int64_t>(i) * d;
+            // discard test on the anchors (inflation) or on the original collisions (repair,
+            // planner.py:191-192)
+            const double* t = (targets ? targets : star) + static_cast<int64_t>(i) * d;
             double dot = 0.0;
             for (int k = 0; k < d; ++k) dot = fma(t[k], s_a[k], dot);
             alive[i] = dot <= rhs;
@@ -783,7 +785,7 @@ extern "C" int32_t ez_inflate_edge(ez_world* w, const double* h_v1, const double
         else if (d <= 16) EZ_TRY(launch_bisect<16>(w, precision, s, it, p.n_p, d, ee, p.n_b, p.t_col));
         else EZ_TRY(launch_bisect<32>(w, precision, s, it, p.n_p, d, ee, p.n_b, p.t_col));
         k_place<<<1, 1024, place_smem, s>>>(ws->A, ws->b, ws->rec, it, d, ws->star, ws->pstar, ws->dstar, ws->seg,
-                                            p.delta_max, p.n_f);
+                                            p.delta_max, p.n_f, nullptr);
         EZ_CUDA(cudaGetLastError());
         EZ_CUDA(cudaMemcpyAsync(ws->h_rec + kRecInts * (k & 1), ws->rec, kRecInts * sizeof(int32_t),
                                 cudaMemcpyDeviceToHost, s));
@@ -858,5 +860,73 @@ extern "C" int32_t ez_inflate_edge(ez_world* w, const double* h_v1, const double
     report->terminated_by = terminated;
     report->n_faces = F;
     report->device_ms = ms;
+    return EZ_OK;
+}
+
+// Set repair (planner.py:159-224 inner loop): project the reported collisions
+// onto the set's seed segment, fail-fast check, N_b bisection rounds, then
+// place uncapped step-back faces, discarding candidates whose ORIGINAL
+// collision leaves the set.  Appends faces to (A_in, b_in).
+extern "C" int32_t ez_refine_set(ez_world* w, const double* h_v1, const double* h_v2, int32_t dim,
+                                 const double* h_A, const double* h_b, int32_t n_faces, const double* h_cols,
+                                 int32_t n_cols, double delta_max, double t_col, int32_t n_b, int32_t precision,
+                                 double* h_A_out, double* h_b_out, int32_t face_cap, int32_t* n_faces_out,
+                                 int64_t* collision_checks) {
+    if (!w || !h_cols || !n_faces_out) return fail(EZ_INVALID_ARGUMENT, "null argument");
+    if (dim != w->dof) return fail(EZ_DIMENSION_MISMATCH, "segment/robot dimension mismatch");
+    if (n_cols < 1) return fail(EZ_INVALID_ARGUMENT, "refine_sets needs at least one collision");
+    if (n_b < 1) return fail(EZ_INVALID_ARGUMENT, "n_b must be >= 1");
+    if (dim > 32) return fail(EZ_UNSUPPORTED, "dimension <= 32");
+    std::lock_guard<std::mutex> lock(g_ws_mu);
+    EZ_CUDA(cudaSetDevice(w->device));
+    const int d = dim;
+    EZ_TRY(ws_reserve(w, d, n_cols, n_cols, n_faces + n_cols + 1));
+    ez_eizo_ws* ws = device_ws(w->device);
+    cudaStream_t s = ws->stream;
+    std::vector<double> seg(3 * d);
+    double ee = 0.0;
+    for (int k = 0; k < d; ++k) {
+        seg[k] = h_v1[k];
+        seg[d + k] = h_v2[k] - h_v1[k];
+        seg[2 * d + k] = h_v2[k];
+        ee = ee + seg[d + k] * seg[d + k];
+    }
+    std::vector<int32_t> iota(n_cols);
+    for (int i = 0; i < n_cols; ++i) iota[i] = i;
+    int32_t rec0[kRecInts] = {0};
+    rec0[kFaces] = n_faces;
+    rec0[slot_offset(0) + kNumCand] = n_cols;
+    EZ_CUDA(cudaMemcpyAsync(ws->seg, seg.data(), sizeof(double) * 3 * d, cudaMemcpyHostToDevice, s));
+    EZ_CUDA(cudaMemcpyAsync(ws->A, h_A, sizeof(double) * n_faces * d, cudaMemcpyHostToDevice, s));
+    EZ_CUDA(cudaMemcpyAsync(ws->b, h_b, sizeof(double) * n_faces, cudaMemcpyHostToDevice, s));
+    EZ_CUDA(cudaMemcpyAsync(ws->X, h_cols, sizeof(double) * n_cols * d, cudaMemcpyHostToDevice, s));
+    EZ_CUDA(cudaMemcpyAsync(ws->col, iota.data(), sizeof(int32_t) * n_cols, cudaMemcpyHostToDevice, s));
+    EZ_CUDA(cudaMemcpyAsync(ws->rec, rec0, sizeof(rec0), cudaMemcpyHostToDevice, s));
+    const int32_t* it = ws->rec + slot_offset(0);
+    if (d <= 4) EZ_TRY(launch_bisect<4>(w, precision, s, it, n_cols, d, ee, n_b, t_col));
+    else if (d <= 8) EZ_TRY(launch_bisect<8>(w, precision, s, it, n_cols, d, ee, n_b, t_col));
+    else if (d <= 16) EZ_TRY(launch_bisect<16>(w, precision, s, it, n_cols, d, ee, n_b, t_col));
+    else EZ_TRY(launch_bisect<32>(w, precision, s, it, n_cols, d, ee, n_b, t_col));
+    const size_t place_smem = static_cast<size_t>(n_cols);
+    if (place_smem > 200 * 1024) return fail(EZ_UNSUPPORTED, "more than 204800 collisions in one repair");
+    if (place_smem > 48 * 1024)
+        EZ_CUDA(cudaFuncSetAttribute(k_place, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(place_smem)));
+    k_place<<<1, 1024, place_smem, s>>>(ws->A, ws->b, ws->rec, ws->rec + slot_offset(0), d, ws->star, ws->pstar,
+                                        ws->dstar, ws->seg, delta_max, n_cols, ws->X);
+    EZ_CUDA(cudaGetLastError());
+    EZ_CUDA(cudaMemcpyAsync(ws->h_rec, ws->rec, kRecInts * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    EZ_CUDA(cudaStreamSynchronize(s));
+    const int32_t* g = ws->h_rec;
+    if (g[kStatus] == EZ_SEGMENT_IN_COLLISION)
+        return fail(EZ_SEGMENT_IN_COLLISION, "seed segment projection in collision, or a collision within t_col, during repair");
+    if (g[kStatus] == EZ_GRADIENT_UNDEFINED) return fail(EZ_GRADIENT_UNDEFINED, "candidate collapsed onto the segment");
+    if (g[kStatus] != EZ_OK) return fail(g[kStatus], "repair device failure");
+    const int F = g[kFaces];
+    if (F > face_cap) return fail(EZ_CAPACITY, "face_cap smaller than the repaired polytope");
+    EZ_CUDA(cudaMemcpyAsync(h_A_out, ws->A, sizeof(double) * F * d, cudaMemcpyDeviceToHost, s));
+    EZ_CUDA(cudaMemcpyAsync(h_b_out, ws->b, sizeof(double) * F, cudaMemcpyDeviceToHost, s));
+    EZ_CUDA(cudaStreamSynchronize(s));
+    *n_faces_out = F;
+    if (collision_checks) *collision_checks = static_cast<int64_t>(n_cols) * (1 + n_b);
     return EZ_OK;
 }
