@@ -51,6 +51,7 @@ enum { EZ_RNG_COUNTER = 0, EZ_RNG_PHILOX = 1 };
 
 typedef struct ez_world ez_world;          /* opaque, device-resident */
 typedef struct ez_roadmap ez_roadmap;      /* opaque, device-resident */
+typedef struct ez_eizo_session ez_eizo_session;  /* opaque: one rank's share of a sharded EI-ZO */
 
 /* Robot description (host arrays, read during ez_world_create).
  * Mirrors world.RobotModel (world.py:122-167): joints in chain order with
@@ -170,6 +171,28 @@ int32_t ez_inflate_edge(ez_world* world, const double* h_v1, const double* h_v2,
                         const ez_eizo_params* params, uint64_t seed, int32_t precision,
                         int32_t rng, ez_eizo_report* report, double* h_A_out, double* h_b_out,
                         int32_t face_cap);
+
+/* In-segment batch sharding: EI-ZO as resumable steps.  Each
+ * rank runs a session over the same segment/domain/seed; per iteration k the
+ * caller (torch.distributed over NCCL) all-reduces the first-m collision
+ * counts returned by _sample, all-gathers the candidate counts, bisects its
+ * share of the global first n_p (_bisect, rows copied to caller device
+ * buffers), all-gathers (star, pstar, dstar) and places the same faces on every rank
+ * (_place).  Samples are keyed by global walk index, so the result equals
+ * ez_inflate_edge for any number of ranks. */
+int32_t ez_eizo_session_begin(ez_world* world, const double* h_v1, const double* h_v2, int32_t dim,
+                              const double* h_A0, const double* h_b0, int32_t n_faces0,
+                              const ez_eizo_params* params, uint64_t seed, int32_t precision, int32_t rng,
+                              ez_eizo_session** out);
+int32_t ez_eizo_session_end(ez_eizo_session* session);
+int32_t ez_eizo_session_sample(ez_eizo_session* session, int32_t k, uint64_t walk_begin, int64_t count,
+                               int64_t m_local, int32_t* n_col_m, int32_t* n_cand);
+int32_t ez_eizo_session_bisect(ez_eizo_session* session, int32_t k, int32_t n_take, double* d_star,
+                               double* d_pstar, double* d_dstar);
+int32_t ez_eizo_session_place(ez_eizo_session* session, int32_t k, const double* d_star, const double* d_pstar,
+                              const double* d_dstar, int32_t n_total, int32_t* placed, int32_t* n_faces);
+int32_t ez_eizo_session_result(ez_eizo_session* session, double* h_A_out, double* h_b_out, int32_t face_cap,
+                               int32_t* n_faces);
 
 /* Set repair, the device part of refine_sets (planner.py:159-224): project
  * n_cols host collisions onto the seed segment, fail-fast check, N_b

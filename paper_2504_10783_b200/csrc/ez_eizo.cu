@@ -12,6 +12,7 @@
 #include <climits>
 #include <cmath>
 #include <mutex>
+#include <type_traits>
 #include <vector>
 
 #include "ez_device.cuh"
@@ -930,3 +931,5 @@ extern "C" int32_t ez_refine_set(ez_world* w, const double* h_v1, const double* 
     if (collision_checks) *collision_checks = static_cast<int64_t>(n_cols) * (1 + n_b);
     return EZ_OK;
 }
+
+#include "ez_eizo_session.inc"
