@@ -137,3 +137,23 @@ def random_free_segment(world, seed: int = 3, length: float = 0.6, margin: float
         if np.all(v2 > lo) and np.all(v2 < hi) and ck.check_segment(v1, v2, step):
             return v1, v2
     raise RuntimeError("no free segment found")
+
+
+def random_free_path(world, n_segments: int = 10, seed: int = 3, length: float = 0.6, margin: float = 0.02,
+                     step: float = 0.01, max_tries: int = 100_000) -> np.ndarray:
+    """Knots of a chain of ``n_segments`` segments, each free with ``margin`` at spacing ``step`` (config 3)."""
+    v1, v2 = random_free_segment(world, seed=seed, length=length, margin=margin, step=step)
+    knots = [v1, v2]
+    ck = world.checker(margin=margin)
+    rng = np.random.default_rng(seed + 1)
+    lo, hi = world.lower, world.upper
+    tries = 0
+    while len(knots) < n_segments + 1:
+        tries += 1
+        if tries > max_tries:
+            raise RuntimeError("could not extend the path")
+        d = rng.normal(size=lo.shape[0])
+        nxt = knots[-1] + d / np.linalg.norm(d) * length
+        if np.all(nxt > lo) and np.all(nxt < hi) and ck.check_segment(knots[-1], nxt, step):
+            knots.append(nxt)
+    return np.array(knots)
