@@ -272,13 +272,48 @@ def gen_corridor(C):
           f"{len(ref.sets)} sets after repair")
 
 
+def gen_boxes(C):
+    """Robot box geometries (world.py:538-565): flags from the reference; the contact band is where the
+    reference's own flags change between margin -1e-5 and +1e-5."""
+    from oracle.make_scenes import box_arm2d, box_arm3d
+    from paper_2504_10783_b200 import fixtures as fx
+    from paper_2504_10783_b200.model import BOX, SPHERE, Geometry, RigidTransform
+    from paper_2504_10783_b200.scene import VoxelMap, World
+
+    table = Geometry(BOX, RigidTransform.planar(0.0, -0.2), half_extents=np.array([2.5, 0.1]))
+    disc = Geometry(SPHERE, RigidTransform.planar(0.9, 1.2), radius=0.15)
+    tilted = Geometry(BOX, RigidTransform.planar(-0.9, 1.1, 0.5), half_extents=np.array([0.2, 0.1]))
+    vm2 = VoxelMap(np.array([-2.3, -0.4]), 0.08, [(12, 20), (13, 20), (12, 21), (40, 22), (41, 23)])
+    w2 = World(box_arm2d(), static=(table, disc, tilted), vmap=vm2)
+    stat3 = Geometry(BOX, RigidTransform(np.eye(3), np.array([0.5, 0.0, -0.05])), half_extents=np.array([0.6, 0.6, 0.05]))
+    w3 = World(box_arm3d(), static=(stat3,), vmap=fx.cloud10k())
+    m3 = box_arm3d()
+    from paper_2504_10783_b200.model import RobotModel
+    m3n = RobotModel(3, m3.joints, m3.links, m3.lower, m3.upper, ())
+    w3n = World(m3n, static=(stat3,), vmap=fx.cloud10k())
+    for name, world, n in (("box2d", w2, 20_000), ("box3d", w3, 10_000), ("box3d_noself", w3n, 10_000)):
+        rng = np.random.default_rng(0)
+        Q = rng.uniform(world.lower, world.upper, size=(n, len(world.lower))).astype(np.float32)
+        rw = _to_ref_world(world, C)
+        Qd = Q.astype(np.float64)
+        free = rw.checker().check_batch(Qd)
+        lo = rw.checker(margin=-1e-5).check_batch(Qd)
+        hi = rw.checker(margin=1e-5).check_batch(Qd)
+        band = lo != hi
+        from paper_2504_10783_b200.scene import save_scene
+        save_scene(GOLDEN / f"scene_{name}.json", world)
+        extra = {"vox_idx": world.vmap.index_array(), "vox_origin": world.vmap.origin, "vox_side": world.vmap.side}
+        np.savez_compressed(GOLDEN / f"check_{name}.npz", Q=Q, free=free, band=band, margin=0.0, **extra)
+        print(f"check_{name}: n={n} free={free.mean():.3f} band={band.mean():.2e}")
+
+
 def main(which=None):
     GOLDEN.mkdir(parents=True, exist_ok=True)
     C = _import_reference()
     import corridor.bench, corridor.cpoly, corridor.drm, corridor.inflation, corridor.world  # noqa: E401,F401
 
     steps = {"checks": gen_checks, "fk": gen_fk, "hnr": gen_hnr, "inflate": gen_inflate,
-             "voxelize": gen_voxelize, "drm": gen_drm, "corridor": gen_corridor}
+             "voxelize": gen_voxelize, "drm": gen_drm, "corridor": gen_corridor, "boxes": gen_boxes}
     for name, fn in steps.items():
         if which and name not in which:
             continue

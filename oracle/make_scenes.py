@@ -132,3 +132,47 @@ def main():
 
 if __name__ == "__main__":
     main()
+
+
+def box_arm3d() -> RobotModel:
+    """Franka-like chain with one box per link plus a tool sphere (robot box geometry tests)."""
+    joints, _ = _arm((0, 0, 0), 0)
+    nxt = [o[0] for o in ORIGINS[1:]] + [FLANGE, (0, 0, 0.10)]
+    links = []
+    for i in range(len(joints)):
+        b = np.asarray(nxt[i], dtype=float)
+        if np.linalg.norm(b) < 1e-9:
+            b = np.array([0.0, 0.0, 0.10])
+        mid = 0.5 * b
+        L = float(np.linalg.norm(b))
+        # box aligned with the link segment: local z along b
+        z = b / L
+        x = np.cross([0.0, 1.0, 0.0], z) if abs(z[1]) < 0.9 else np.cross([1.0, 0.0, 0.0], z)
+        x /= np.linalg.norm(x)
+        y = np.cross(z, x)
+        R = np.stack([x, y, z], axis=1)
+        geoms = [Geometry("box", RigidTransform(R, mid), half_extents=np.array([0.045, 0.045, 0.5 * L + 0.03]))]
+        if i == len(joints) - 1:
+            geoms.append(Geometry(SPHERE, pose((0, 0, 0.12)), radius=0.05))
+        links.append(Link(tuple(geoms)))
+    owner = [li for li, l in enumerate(links) for _ in l.geometries]
+    n = len(owner)
+    pairs = tuple((i, j) for i in range(n) for j in range(i + 1, n) if owner[j] - owner[i] >= 3)
+    return RobotModel(3, joints, links, LOWER, UPPER, pairs)
+
+
+def box_arm2d() -> RobotModel:
+    """Planar 3-link arm with box links and sphere tips; box-box and sphere-box self pairs."""
+    lengths = (0.9, 0.7, 0.5)
+    joints = (Joint("revolute", -1, RigidTransform.identity(2)),
+              Joint("revolute", 0, RigidTransform.planar(lengths[0], 0.0)),
+              Joint("revolute", 1, RigidTransform.planar(lengths[1], 0.0)),
+              Joint("fixed", 2, RigidTransform.planar(lengths[2], 0.0)))
+    links = []
+    for L in lengths:
+        links.append(Link((Geometry("box", RigidTransform.planar(0.5 * L, 0.0, 0.1), half_extents=np.array([0.5 * L, 0.05])),
+                           Geometry(SPHERE, RigidTransform.planar(L, 0.0), radius=0.06))))
+    links.append(Link())
+    # geometries: 0 box0, 1 sph0, 2 box1, 3 sph1, 4 box2, 5 sph2
+    pairs = ((0, 4), (0, 5), (1, 4), (1, 5))
+    return RobotModel(2, joints, tuple(links), np.array([0.2, -2.6, -2.6]), np.array([math.pi - 0.2, 2.6, 2.6]), pairs)

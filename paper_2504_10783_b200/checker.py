@@ -74,6 +74,26 @@ class CollisionChecker:
         self.calls += Q.shape[0]
         return self.native.check_host(Q, precision=self.precision).view(bool)
 
+    def check_segments(self, V1, V2, step: float) -> np.ndarray:
+        """Batched ``check_segment`` over many edges in one GPU check.
+
+        Edge i is free iff all of its ceil(len_i / step) + 1 evenly spaced
+        samples (``segment_samples``) are free; ``calls`` grows by the total
+        sample count, as with one check_segment call per edge.
+        """
+        if step <= 0.0:
+            raise ValueError("step must be positive")
+        V1 = np.atleast_2d(np.asarray(V1, dtype=float))
+        V2 = np.atleast_2d(np.asarray(V2, dtype=float))
+        if V1.shape != V2.shape:
+            raise DimensionMismatch("segment endpoints differ in dimension")
+        if V1.shape[0] == 0:
+            return np.zeros(0, dtype=bool)
+        parts = [segment_samples(a, b, step) for a, b in zip(V1, V2)]
+        counts = np.array([p.shape[0] for p in parts])
+        free = self.check_batch(np.concatenate(parts))
+        return np.logical_and.reduceat(free, np.concatenate([[0], np.cumsum(counts)[:-1]]))
+
     def check_segment(self, v1, v2, step: float) -> bool:
         """True iff every sample at spacing <= step (endpoints included) is free."""
         if step <= 0.0:

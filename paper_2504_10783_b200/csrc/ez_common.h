@@ -55,7 +55,27 @@ struct alignas(16) JointRec {
     int32_t store_slot;  // >= 0: save this link's frame for a later child
     int32_t parent_slot; // >= 0: parent frame comes from this slot
     int32_t sph_begin, sph_end;  // spheres attached to this link
-    int32_t pad_;
+    int32_t box_begin, box_end;  // boxes attached to this link
+    int32_t pad_[3];
+};
+
+// Robot box geometry (world.py:538-565).  World pose = link frame * local.
+template <typename T>
+struct alignas(16) BoxRec {
+    T R[9];     // Q_link^T * local rotation
+    T t[3];     // Q_link^T * local translation
+    T he[3];    // half extents (planar boxes: z = 0)
+    T pad_;
+};
+
+// Self pair with at least one box: a sphere-box (point-box distance against
+// r + margin) or box-box (separating axes with margin) test.  kind 0 = sphere
+// (slot = sphere index), 1 = box (slot = box index); a is the sphere if any.
+template <typename T>
+struct alignas(16) MixPairRec {
+    int32_t a_kind, a_slot, b_kind, b_slot;
+    T ra;       // sphere radius of a (sphere-box)
+    T pad_[3];
 };
 
 template <typename T>
@@ -120,14 +140,20 @@ struct VoxGrid {
     T eps;          // rounding guard of the filter (precision dependent)
     T vorg[3];      // voxel lattice origin
     T vside;
+    T rvox;         // voxel sphere radius 0.5 * side * sqrt(dim)
+    // dense occupancy bitmap of the padded voxel lattice (robot boxes scan it)
+    const uint32_t* occ;
+    int32_t lbase[3];  // lattice index of bit 0 along each axis
+    int32_t L[3];      // lattice extent of the bitmap
 };
 
 template <typename T>
 struct ModelDev {
-    const uint8_t* blob;      // device: joints | spheres | hot | groups | pairs | order | ssph | sbox
+    const uint8_t* blob;      // device: joints | spheres | hot | groups | pairs | order | ssph | sbox | boxes | mix
     uint32_t blob_bytes;      // multiple of 16
-    int32_t n_joints, dof, n_spheres, n_hot, n_groups, n_pairs, n_ssph, n_sbox, n_store;
-    uint32_t off_spheres, off_hot, off_groups, off_pairs, off_order, off_ssph, off_sbox;
+    int32_t n_joints, dof, n_spheres, n_hot, n_groups, n_pairs, n_ssph, n_sbox, n_store, n_boxes, n_mix;
+    int32_t cen_words;        // per-configuration geometry store: 3 per sphere + 12 per box
+    uint32_t off_spheres, off_hot, off_groups, off_pairs, off_order, off_ssph, off_sbox, off_boxes, off_mix;
     VoxGrid<T> vox;
 };
 

@@ -91,11 +91,14 @@ __device__ __forceinline__ double lattice_centre(double org, int idx, double sid
 // ---------------------------------------------------------------------------
 // q: the configuration (dof values, any stride 1 memory), cen: sphere centre
 // store, element (s, k) at cen[(3 s + k) * stride].
+// Boxes: the world rotation (9) and translation (3) of box b are stored at
+// words box_base + 12 b + k of the same store.
 template <typename T, typename Q>
 __device__ __forceinline__ void fk_sphere_centres(const JointRec<T>* __restrict__ J, int nj,
                                                   const SphereRec<T>* __restrict__ S,
                                                   const Q* __restrict__ q, T* __restrict__ cen,
-                                                  int stride) {
+                                                  int stride, const BoxRec<T>* __restrict__ BX = nullptr,
+                                                  int box_base = 0) {
     T R[9] = {T(1), T(0), T(0), T(0), T(1), T(0), T(0), T(0), T(1)};
     T t[3] = {T(0), T(0), T(0)};
     T store[kMaxStore][12];
@@ -153,7 +156,162 @@ __device__ __forceinline__ void fk_sphere_centres(const JointRec<T>* __restrict_
                 cen[(3 * s + r) * stride] =
                     t[r] + (R[3 * r] * sp.p[0] + R[3 * r + 1] * sp.p[1] + R[3 * r + 2] * sp.p[2]);
         }
+        for (int bx = jr.box_begin; bx < jr.box_end; ++bx) {
+            const BoxRec<T>& br = BX[bx];
+            T* o = cen + (box_base + 12 * bx) * stride;
+#pragma unroll
+            for (int r = 0; r < 3; ++r) {
+#pragma unroll
+                for (int c = 0; c < 3; ++c)
+                    o[(3 * r + c) * stride] = R[3 * r] * br.R[c] + R[3 * r + 1] * br.R[3 + c] + R[3 * r + 2] * br.R[6 + c];
+                o[(9 + r) * stride] = t[r] + (R[3 * r] * br.t[0] + R[3 * r + 1] * br.t[1] + R[3 * r + 2] * br.t[2]);
+            }
+        }
     }
+}
+
+// ---------------------------------------------------------------------------
+// boxes (world.py:394-427, 538-565)
+// ---------------------------------------------------------------------------
+// squared distance from p to the box (rotation R row-major, centre t, half extents he)
+template <typename T>
+__device__ __forceinline__ T point_box_d2(const T (&R)[9], const T (&t)[3], const T* he, T px, T py, T pz) {
+    const T dx = px - t[0], dy = py - t[1], dz = pz - t[2];
+    T d2 = T(0);
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+        const T l = R[i] * dx + R[3 + i] * dy + R[6 + i] * dz;  // (R^T (p - t))_i
+        const T cl = fmin(fmax(l, -he[i]), he[i]);
+        d2 += (l - cl) * (l - cl);
+    }
+    return d2;
+}
+
+// separating-axis test, touching = colliding (world.py:401-427); axes with
+// norm <= 1e-12 give no separation evidence.  Ra/Rb row-major, columns = box axes.
+template <typename T>
+__device__ __forceinline__ bool boxes_collide(const T (&Ra)[9], const T (&ta)[3], const T* hea, const T (&Rb)[9],
+                                              const T (&tb)[3], const T* heb, T margin) {
+    const T diff[3] = {tb[0] - ta[0], tb[1] - ta[1], tb[2] - ta[2]};
+    auto separated = [&](T ux, T uy, T uz) -> bool {
+        const T n = tsqrt<T>(ux * ux + uy * uy + uz * uz);
+        if (!(n > T(1e-12))) return false;
+        ux /= n;
+        uy /= n;
+        uz /= n;
+        const T dist = fabs(ux * diff[0] + uy * diff[1] + uz * diff[2]);
+        T ra = T(0), rb = T(0);
+#pragma unroll
+        for (int j = 0; j < 3; ++j) {
+            ra += fabs(ux * Ra[j] + uy * Ra[3 + j] + uz * Ra[6 + j]) * hea[j];
+            rb += fabs(ux * Rb[j] + uy * Rb[3 + j] + uz * Rb[6 + j]) * heb[j];
+        }
+        return dist > ra + rb + margin;
+    };
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+        if (separated(Ra[i], Ra[3 + i], Ra[6 + i])) return false;
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+        if (separated(Rb[i], Rb[3 + i], Rb[6 + i])) return false;
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+#pragma unroll
+        for (int j = 0; j < 3; ++j) {
+            const T ax = Ra[3 + i] * Rb[6 + j] - Ra[6 + i] * Rb[3 + j];
+            const T ay = Ra[6 + i] * Rb[j] - Ra[i] * Rb[6 + j];
+            const T az = Ra[i] * Rb[3 + j] - Ra[3 + i] * Rb[j];
+            if (separated(ax, ay, az)) return false;
+        }
+    }
+    return true;
+}
+
+template <typename T>
+__device__ __forceinline__ void load_box(const T* __restrict__ cen, int stride, int word, T (&R)[9], T (&t)[3]) {
+#pragma unroll
+    for (int k = 0; k < 9; ++k) R[k] = cen[(word + k) * stride];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) t[k] = cen[(word + 9 + k) * stride];
+}
+
+// Robot box vs static spheres, voxel spheres (occupied lattice cells inside
+// the box's dilated bounding box, exact point-box test) and static boxes.
+template <typename T>
+__device__ __forceinline__ bool box_hits_obstacles(const ModelDev<T>& M, const uint8_t* blob, const T (&R)[9],
+                                                   const T (&t)[3], const T* he, T margin) {
+    const StaticSphereRec<T>* SS = reinterpret_cast<const StaticSphereRec<T>*>(blob + M.off_ssph);
+    for (int i = 0; i < M.n_ssph; ++i) {
+        const StaticSphereRec<T> o = SS[i];
+        const T rr = o.r + margin;
+        if (point_box_d2<T>(R, t, he, o.c[0], o.c[1], o.c[2]) <= rr * rr) return true;
+    }
+    const StaticBoxRec<T>* SB = reinterpret_cast<const StaticBoxRec<T>*>(blob + M.off_sbox);
+    for (int i = 0; i < M.n_sbox; ++i) {
+        const StaticBoxRec<T>& b = SB[i];
+        T Rb[9], tb[3];
+#pragma unroll
+        for (int r = 0; r < 3; ++r) {
+#pragma unroll
+            for (int c = 0; c < 3; ++c) Rb[3 * r + c] = b.Rt[3 * c + r];
+            tb[r] = b.t[r];
+        }
+        if (boxes_collide<T>(R, t, he, Rb, tb, b.he, margin)) return true;
+    }
+    const VoxGrid<T>& V = M.vox;
+    if (!V.present) return false;
+    const T Rr = V.rvox + margin;  // r_vox + margin (world.py:542-547)
+    const T R2 = Rr * Rr;
+    int lo[3], hi[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        const T ext = fabs(R[3 * k]) * he[0] + fabs(R[3 * k + 1]) * he[1] + fabs(R[3 * k + 2]) * he[2] + Rr;
+        const T a = (t[k] - ext - V.vorg[k]) / V.vside - T(0.5);
+        const T b = (t[k] + ext - V.vorg[k]) / V.vside - T(0.5);
+        lo[k] = max(V.lbase[k], static_cast<int>(floor(a)) - 1);
+        hi[k] = min(V.lbase[k] + V.L[k] - 1, static_cast<int>(floor(b)) + 1);
+    }
+    for (int z = lo[2]; z <= hi[2]; ++z)
+        for (int y = lo[1]; y <= hi[1]; ++y)
+            for (int x = lo[0]; x <= hi[0]; ++x) {
+                const int64_t bit = (static_cast<int64_t>(z - V.lbase[2]) * V.L[1] + (y - V.lbase[1])) * V.L[0] +
+                                    (x - V.lbase[0]);
+                if (!((__ldg(V.occ + (bit >> 5)) >> (bit & 31)) & 1u)) continue;
+                if (point_box_d2<T>(R, t, he, lattice_centre(V.vorg[0], x, V.vside), lattice_centre(V.vorg[1], y, V.vside),
+                                    lattice_centre(V.vorg[2], z, V.vside)) <= R2)
+                    return true;
+            }
+    return false;
+}
+
+// all box tests of one configuration: boxes vs obstacles, then mixed self pairs
+template <typename T>
+__device__ __forceinline__ bool boxes_collide_all(const ModelDev<T>& M, const uint8_t* blob,
+                                                  const T* __restrict__ cen, int stride, T margin) {
+    const BoxRec<T>* BX = reinterpret_cast<const BoxRec<T>*>(blob + M.off_boxes);
+    const int base = 3 * M.n_spheres;
+    for (int b = 0; b < M.n_boxes; ++b) {
+        T R[9], t[3];
+        load_box<T>(cen, stride, base + 12 * b, R, t);
+        if (box_hits_obstacles<T>(M, blob, R, t, BX[b].he, margin)) return true;
+    }
+    const MixPairRec<T>* MP = reinterpret_cast<const MixPairRec<T>*>(blob + M.off_mix);
+    for (int p = 0; p < M.n_mix; ++p) {
+        const MixPairRec<T> mp = MP[p];
+        T Rb[9], tb[3];
+        load_box<T>(cen, stride, base + 12 * mp.b_slot, Rb, tb);
+        if (mp.a_kind == 0) {
+            const T rr = mp.ra + margin;
+            if (point_box_d2<T>(Rb, tb, BX[mp.b_slot].he, cen[(3 * mp.a_slot) * stride], cen[(3 * mp.a_slot + 1) * stride],
+                                cen[(3 * mp.a_slot + 2) * stride]) <= rr * rr)
+                return true;
+        } else {
+            T Ra[9], ta[3];
+            load_box<T>(cen, stride, base + 12 * mp.a_slot, Ra, ta);
+            if (boxes_collide<T>(Ra, ta, BX[mp.a_slot].he, Rb, tb, BX[mp.b_slot].he, margin)) return true;
+        }
+    }
+    return false;
 }
 
 // ---------------------------------------------------------------------------
@@ -338,7 +496,8 @@ __device__ __forceinline__ bool rest_collides(const ModelDev<T>& M, const uint8_
     }
     const GroupRec* G = reinterpret_cast<const GroupRec*>(blob + M.off_groups);
     const PairRec<T>* P = reinterpret_cast<const PairRec<T>*>(blob + M.off_pairs);
-    return self_collides<T>(G, M.n_groups, P, cen, stride);
+    if (self_collides<T>(G, M.n_groups, P, cen, stride)) return true;
+    return (M.n_boxes > 0) && boxes_collide_all<T>(M, blob, cen, stride, margin);
 }
 
 // Everything about one configuration whose sphere centres are in `cen`.
@@ -354,7 +513,8 @@ __device__ __forceinline__ bool config_free(const ModelDev<T>& M, const uint8_t*
                                             const Q* q, T* cen, int stride, T margin) {
     const JointRec<T>* J = reinterpret_cast<const JointRec<T>*>(blob);
     const SphereRec<T>* S = reinterpret_cast<const SphereRec<T>*>(blob + M.off_spheres);
-    fk_sphere_centres<T, Q>(J, M.n_joints, S, q, cen, stride);
+    fk_sphere_centres<T, Q>(J, M.n_joints, S, q, cen, stride, reinterpret_cast<const BoxRec<T>*>(blob + M.off_boxes),
+                            3 * M.n_spheres);
     return !config_collides<T>(M, blob, cen, stride, margin);
 }
 
@@ -375,7 +535,8 @@ __device__ __forceinline__ unsigned coop_mask() {
 template <typename T, typename Q, int G>
 __device__ __forceinline__ void fk_centres_coop(const JointRec<T>* __restrict__ J, int nj,
                                                 const SphereRec<T>* __restrict__ S, const Q* __restrict__ q,
-                                                T* __restrict__ cen, int lane) {
+                                                T* __restrict__ cen, int lane,
+                                                const BoxRec<T>* __restrict__ BX = nullptr, int box_base = 0) {
     T R[9] = {T(1), T(0), T(0), T(0), T(1), T(0), T(0), T(0), T(1)};
     T t[3] = {T(0), T(0), T(0)};
     T store[kMaxStore][12];
@@ -432,6 +593,17 @@ __device__ __forceinline__ void fk_centres_coop(const JointRec<T>* __restrict__ 
             for (int r = 0; r < 3; ++r)
                 cen[3 * s + r] = t[r] + (R[3 * r] * sp.p[0] + R[3 * r + 1] * sp.p[1] + R[3 * r + 2] * sp.p[2]);
         }
+        for (int bx = jr.box_begin + lane; bx < jr.box_end; bx += G) {
+            const BoxRec<T>& br = BX[bx];
+            T* o = cen + box_base + 12 * bx;
+#pragma unroll
+            for (int r = 0; r < 3; ++r) {
+#pragma unroll
+                for (int c = 0; c < 3; ++c)
+                    o[3 * r + c] = R[3 * r] * br.R[c] + R[3 * r + 1] * br.R[3 + c] + R[3 * r + 2] * br.R[6 + c];
+                o[9 + r] = t[r] + (R[3 * r] * br.t[0] + R[3 * r + 1] * br.t[1] + R[3 * r + 2] * br.t[2]);
+            }
+        }
     }
 }
 
@@ -442,7 +614,8 @@ __device__ __forceinline__ bool config_free_coop(const ModelDev<T>& M, const uin
     const int lane = threadIdx.x & (G - 1);
     const JointRec<T>* J = reinterpret_cast<const JointRec<T>*>(blob);
     const SphereRec<T>* S = reinterpret_cast<const SphereRec<T>*>(blob + M.off_spheres);
-    fk_centres_coop<T, Q, G>(J, M.n_joints, S, q, cen, lane);
+    const BoxRec<T>* BX = reinterpret_cast<const BoxRec<T>*>(blob + M.off_boxes);
+    fk_centres_coop<T, Q, G>(J, M.n_joints, S, q, cen, lane, BX, 3 * M.n_spheres);
     __syncwarp(gm);
     const HotRec<T>* H = reinterpret_cast<const HotRec<T>*>(blob + M.off_hot);
     for (int p0 = 0; p0 < M.n_hot; p0 += G) {
@@ -483,6 +656,38 @@ __device__ __forceinline__ bool config_free_coop(const ModelDev<T>& M, const uin
             }
             if (__ballot_sync(gm, hit)) return false;
         }
+    }
+    if (M.n_boxes == 0) return true;
+    const int base = 3 * M.n_spheres;
+    for (int b0 = 0; b0 < M.n_boxes; b0 += G) {
+        const int b = b0 + lane;
+        bool hit = false;
+        if (b < M.n_boxes) {
+            T Rb[9], tb[3];
+            load_box<T>(cen, 1, base + 12 * b, Rb, tb);
+            hit = box_hits_obstacles<T>(M, blob, Rb, tb, BX[b].he, margin);
+        }
+        if (__ballot_sync(gm, hit)) return false;
+    }
+    const MixPairRec<T>* MP = reinterpret_cast<const MixPairRec<T>*>(blob + M.off_mix);
+    for (int p0 = 0; p0 < M.n_mix; p0 += G) {
+        const int p = p0 + lane;
+        bool hit = false;
+        if (p < M.n_mix) {
+            const MixPairRec<T> mp = MP[p];
+            T Rb[9], tb[3];
+            load_box<T>(cen, 1, base + 12 * mp.b_slot, Rb, tb);
+            if (mp.a_kind == 0) {
+                const T rr = mp.ra + margin;
+                hit = point_box_d2<T>(Rb, tb, BX[mp.b_slot].he, cen[3 * mp.a_slot], cen[3 * mp.a_slot + 1],
+                                      cen[3 * mp.a_slot + 2]) <= rr * rr;
+            } else {
+                T Ra[9], ta[3];
+                load_box<T>(cen, 1, base + 12 * mp.a_slot, Ra, ta);
+                hit = boxes_collide<T>(Ra, ta, BX[mp.a_slot].he, Rb, tb, BX[mp.b_slot].he, margin);
+            }
+        }
+        if (__ballot_sync(gm, hit)) return false;
     }
     return true;
 }

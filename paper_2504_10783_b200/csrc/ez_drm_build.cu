@@ -42,19 +42,20 @@ k_node_voxels(ModelDev<double> M, const double* __restrict__ nodes, int64_t n, M
     const int warps = blockDim.x >> 5;
     const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
     size_t off = (M.blob_bytes + 15) & ~static_cast<size_t>(15);
-    double* cen = reinterpret_cast<double*>(smem + off) + static_cast<size_t>(wid) * 3 * M.n_spheres;
-    off += static_cast<size_t>(warps) * 3 * M.n_spheres * sizeof(double);
+    double* cen = reinterpret_cast<double*>(smem + off) + static_cast<size_t>(wid) * M.cen_words;
+    off += static_cast<size_t>(warps) * M.cen_words * sizeof(double);
     double* row = reinterpret_cast<double*>(smem + off) + static_cast<size_t>(wid) * 32;
     off += static_cast<size_t>(warps) * 32 * sizeof(double);
     uint32_t* bits = reinterpret_cast<uint32_t*>(smem + off) + static_cast<size_t>(wid) * g.words;
     const JointRec<double>* J = reinterpret_cast<const JointRec<double>*>(smem);
     const SphereRec<double>* S = reinterpret_cast<const SphereRec<double>*>(smem + M.off_spheres);
+    const BoxRec<double>* BX = reinterpret_cast<const BoxRec<double>*>(smem + M.off_boxes);
     const int64_t nwarps = static_cast<int64_t>(gridDim.x) * warps;
     for (int64_t node = static_cast<int64_t>(blockIdx.x) * warps + wid; node < n; node += nwarps) {
         if (lane < M.dof) row[lane] = nodes[node * M.dof + lane];
         for (int w = lane; w < g.words; w += 32) bits[w] = 0u;
         __syncwarp();
-        fk_centres_coop<double, double, 32>(J, M.n_joints, S, row, cen, lane);
+        fk_centres_coop<double, double, 32>(J, M.n_joints, S, row, cen, lane, BX, 3 * M.n_spheres);
         __syncwarp();
         for (int s = lane; s < M.n_spheres; s += 32) {
             const double R = S[s].r + g.r_vox;
@@ -85,6 +86,30 @@ k_node_voxels(ModelDev<double> M, const double* __restrict__ nodes, int64_t n, M
                     }
                 }
             }
+        }
+        // boxes: |local - clip(local)|^2 <= r_vox^2 with local = R^T (c_v - t) (drm.py:186-189)
+        for (int b = lane; b < M.n_boxes; b += 32) {
+            double Rb[9], tb[3];
+            load_box<double>(cen, 1, 3 * M.n_spheres + 12 * b, Rb, tb);
+            const double* he = BX[b].he;
+            const double thr = g.r_vox * g.r_vox;
+            int lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};
+            for (int k = 0; k < g.dim; ++k) {
+                const double ext = fabs(Rb[3 * k]) * he[0] + fabs(Rb[3 * k + 1]) * he[1] + fabs(Rb[3 * k + 2]) * he[2] + g.r_vox;
+                lo[k] = max(0, static_cast<int>(floor((tb[k] - ext - g.org[k]) / g.side - 0.5)) - 1);
+                hi[k] = min(g.ext[k] - 1, static_cast<int>(floor((tb[k] + ext - g.org[k]) / g.side - 0.5)) + 1);
+            }
+            for (int z = lo[2]; z <= hi[2]; ++z)
+                for (int y = lo[1]; y <= hi[1]; ++y)
+                    for (int x = lo[0]; x <= hi[0]; ++x) {
+                        const double d2 = point_box_d2<double>(Rb, tb, he, lattice_centre(g.org[0], x, g.side),
+                                                               lattice_centre(g.org[1], y, g.side),
+                                                               g.dim == 3 ? lattice_centre(g.org[2], z, g.side) : 0.0);
+                        if (d2 <= thr) {
+                            const int64_t vid = (static_cast<int64_t>(z) * g.ext[1] + y) * g.ext[0] + x;
+                            atomicOr(bits + (vid >> 5), 1u << (vid & 31));
+                        }
+                    }
         }
         __syncwarp();
         // emit the set bits of this node's bitmap
@@ -163,7 +188,7 @@ extern "C" int32_t ez_roadmap_build(ez_world* w, const double* d_nodes, int64_t 
     int warps = 8;
     auto smem_for = [&](int wps) {
         size_t b = (M.blob_bytes + 15) & ~static_cast<size_t>(15);
-        b += static_cast<size_t>(wps) * 3 * M.n_spheres * sizeof(double);
+        b += static_cast<size_t>(wps) * M.cen_words * sizeof(double);
         b += static_cast<size_t>(wps) * 32 * sizeof(double);
         b += static_cast<size_t>(wps) * g.words * sizeof(uint32_t);
         return b;

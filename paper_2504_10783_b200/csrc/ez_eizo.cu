@@ -329,8 +329,8 @@ k_bisect(ModelDev<T> M, T margin, const double* __restrict__ X, int d, const int
     if (rec[kStatus] != EZ_OK || rec[kStop] || static_cast<int64_t>(blockIdx.x) * CPB >= C) return;
     tma_stage(smem, M.blob, M.blob_bytes, &bar);
     const int slot = threadIdx.x / G, lane = threadIdx.x & (G - 1);
-    T* cen = reinterpret_cast<T*>(smem + M.blob_bytes) + static_cast<size_t>(slot) * 3 * M.n_spheres;
-    const size_t roff = (static_cast<size_t>(M.blob_bytes) + static_cast<size_t>(3) * M.n_spheres * CPB * sizeof(T) + 15) &
+    T* cen = reinterpret_cast<T*>(smem + M.blob_bytes) + static_cast<size_t>(slot) * M.cen_words;
+    const size_t roff = (static_cast<size_t>(M.blob_bytes) + static_cast<size_t>(M.cen_words) * CPB * sizeof(T) + 15) &
                         ~static_cast<size_t>(15);
     double* row = reinterpret_cast<double*>(smem + roff) + slot * d;
     const int i = blockIdx.x * CPB + slot;
@@ -648,7 +648,7 @@ static int32_t launch_bisect_t(ez_world* w, const ModelDev<T>& M, cudaStream_t s
                                double ee, int n_b, double t_col) {
     ez_eizo_ws* ws = device_ws(w->device);
     constexpr int G = kBisectLanes, CPB = 128 / G;
-    size_t smem = M.blob_bytes + static_cast<size_t>(3) * M.n_spheres * CPB * sizeof(T);
+    size_t smem = M.blob_bytes + static_cast<size_t>(M.cen_words) * CPB * sizeof(T);
     smem = (smem + 15) & ~static_cast<size_t>(15);
     smem += static_cast<size_t>(CPB) * d * sizeof(double);
     smem = (smem + 15) & ~static_cast<size_t>(15);

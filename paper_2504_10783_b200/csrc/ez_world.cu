@@ -88,7 +88,7 @@ M3 axis_frame(const double* axis) {
 struct HJoint {
     M3 R;
     double t[3], ax[3];
-    int kind, parent, qidx, store_slot = -1, parent_slot = -1, sb = 0, se = 0;
+    int kind, parent, qidx, store_slot = -1, parent_slot = -1, sb = 0, se = 0, bb = 0, be = 0;
 };
 struct HSphere {
     double p[3], r, rvox, rmar;
@@ -104,6 +104,15 @@ struct HSelfPair {   // input order
     int a, b;
     double thr2;
 };
+struct HBox {
+    M3 R;
+    double t[3], he[3];
+    int link;
+};
+struct HMix {
+    int a_kind, a_slot, b_kind, b_slot;
+    double ra;
+};
 struct HModel {
     std::vector<HJoint> joints;
     std::vector<M3> linkQt;
@@ -116,6 +125,8 @@ struct HModel {
     std::vector<int32_t> order; // obstacle-test order of the spheres
     std::vector<double> ssph;  // c3, r
     std::vector<double> sbox;  // Rt9, t3, he3
+    std::vector<HBox> boxes;   // robot boxes
+    std::vector<HMix> mix;     // self pairs with a box
     int dof = 0, n_store = 0;
 };
 
@@ -184,8 +195,33 @@ std::vector<uint8_t> pack_blob(const HModel& hm, ModelDev<T>& md) {
     md.off_order = static_cast<uint32_t>(off); off += sz_o;
     md.off_ssph = static_cast<uint32_t>(off); off += sz_ss;
     md.off_sbox = static_cast<uint32_t>(off); off += sz_sb;
+    md.off_boxes = static_cast<uint32_t>(off); off += align16(hm.boxes.size() * sizeof(BoxRec<T>));
+    md.off_mix = static_cast<uint32_t>(off); off += align16(hm.mix.size() * sizeof(MixPairRec<T>));
     std::vector<uint8_t> blob(std::max<size_t>(16, off), 0);
     md.blob_bytes = static_cast<uint32_t>(blob.size());
+    auto* BXR = reinterpret_cast<BoxRec<T>*>(blob.data() + md.off_boxes);
+    for (size_t i = 0; i < hm.boxes.size(); ++i) {
+        BoxRec<T> r{};
+        for (int k = 0; k < 9; ++k) r.R[k] = static_cast<T>(hm.boxes[i].R.a[k]);
+        for (int k = 0; k < 3; ++k) {
+            r.t[k] = static_cast<T>(hm.boxes[i].t[k]);
+            r.he[k] = static_cast<T>(hm.boxes[i].he[k]);
+        }
+        BXR[i] = r;
+    }
+    auto* MXR = reinterpret_cast<MixPairRec<T>*>(blob.data() + md.off_mix);
+    for (size_t i = 0; i < hm.mix.size(); ++i) {
+        MixPairRec<T> r{};
+        r.a_kind = hm.mix[i].a_kind;
+        r.a_slot = hm.mix[i].a_slot;
+        r.b_kind = hm.mix[i].b_kind;
+        r.b_slot = hm.mix[i].b_slot;
+        r.ra = static_cast<T>(hm.mix[i].ra);
+        MXR[i] = r;
+    }
+    md.n_boxes = static_cast<int32_t>(hm.boxes.size());
+    md.n_mix = static_cast<int32_t>(hm.mix.size());
+    md.cen_words = static_cast<int32_t>(3 * hm.spheres.size() + 12 * hm.boxes.size());
     auto* HR = reinterpret_cast<HotRec<T>*>(blob.data() + md.off_hot);
     for (size_t i = 0; i < hm.hot.size(); ++i) {
         HotRec<T> r{};
@@ -212,6 +248,8 @@ std::vector<uint8_t> pack_blob(const HModel& hm, ModelDev<T>& md) {
         r.parent_slot = h.parent_slot;
         r.sph_begin = h.sb;
         r.sph_end = h.se;
+        r.box_begin = h.bb;
+        r.box_end = h.be;
         J[j] = r;
     }
     auto* S = reinterpret_cast<SphereRec<T>*>(blob.data() + md.off_spheres);
@@ -332,6 +370,15 @@ __global__ void k_cells(GridBuild gb, const uint8_t* __restrict__ occ, const int
     }
 }
 
+__global__ void k_pack_bits(const uint8_t* __restrict__ occ, int64_t n, uint32_t* __restrict__ bits) {
+    const int64_t w = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (w * 32 >= n) return;
+    uint32_t v = 0;
+    for (int b = 0; b < 32; ++b)
+        if (w * 32 + b < n && occ[w * 32 + b]) v |= 1u << b;
+    bits[w] = v;
+}
+
 __global__ void k_cells_merge(int64_t ncell, const uint32_t* __restrict__ offs, uint32_t* __restrict__ cells) {
     const int64_t ci = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (ci < ncell) cells[ci] = (cells[ci] & 0xFF000000u) | (offs[ci] & 0x00FFFFFFu);
@@ -341,14 +388,14 @@ static int32_t build_voxel_grid(ez_world* w, const ez_scene_desc* sc, const HMod
     const int64_t nv = sc->n_voxels;
     const double s = sc->voxel_side;
     if (!(s > 0.0)) return fail(EZ_INVALID_ARGUMENT, "voxel side must be positive");
-    if (hm.spheres.empty()) return EZ_OK;  // no sphere can meet a voxel
+    if (hm.spheres.empty() && hm.boxes.empty()) return EZ_OK;  // no geometry can meet a voxel
     const double r_vox = 0.5 * s * std::sqrt(static_cast<double>(dim));
     double r_min = 1e300, r_max = -1e300;
     for (const HSphere& sp : hm.spheres) {
         r_min = std::min(r_min, sp.rvox);
         r_max = std::max(r_max, sp.rvox);
     }
-    (void)r_vox;
+    if (hm.spheres.empty()) r_min = r_max = r_vox + w->margin;  // boxes only: the bitmap is what matters
     int32_t lmin[3] = {0, 0, 0}, lmax[3] = {0, 0, 0};
     for (int k = 0; k < dim; ++k) {
         lmin[k] = INT32_MAX;
@@ -469,6 +516,11 @@ static int32_t build_voxel_grid(ez_world* w, const ez_scene_desc* sc, const HMod
             k_cells_merge<<<nb, 256>>>(ncell, d_offs, w->d_cells);
             EZ_CUDA(cudaMalloc(&w->d_lists, sizeof(int4) * std::max<int64_t>(1, total)));
             k_cells<true><<<nb, 256>>>(gb, d_occ, d_tab, d_tab_off, w->d_cells, nullptr, w->d_lists);
+            // the occupancy bitmap stays on the device for robot boxes (box vs voxel spheres)
+            const int64_t words = (nl + 31) / 32;
+            EZ_CUDA(cudaMalloc(&w->d_occ_bits, sizeof(uint32_t) * words));
+            k_pack_bits<<<static_cast<unsigned>((words + 255) / 256), 256>>>(d_occ, nl, w->d_occ_bits);
+            w->device_bytes += words * 4;
             EZ_CUDA(cudaGetLastError());
             EZ_CUDA(cudaDeviceSynchronize());
         }
@@ -508,6 +560,12 @@ static int32_t build_voxel_grid(ez_world* w, const ez_scene_desc* sc, const HMod
             V.dq = static_cast<TT>(gb.dq);
             V.eps = static_cast<TT>(eps);
             V.vside = static_cast<TT>(s);
+            V.rvox = static_cast<TT>(r_vox);
+            V.occ = w->d_occ_bits;
+            for (int k = 0; k < 3; ++k) {
+                V.lbase[k] = gb.lbase[k];
+                V.L[k] = gb.L[k];
+            }
         };
         fill(w->mf.vox, eps_build);
         fill(w->md.vox, 1e-12 * (1.0 + maxc));
@@ -541,7 +599,8 @@ __device__ __forceinline__ void check_phase_b(const ModelDev<T>& M, const uint8_
         if (k < dof) row[k] = v[k];
     const JointRec<T>* J = reinterpret_cast<const JointRec<T>*>(smem);
     const SphereRec<T>* S = reinterpret_cast<const SphereRec<T>*>(smem + M.off_spheres);
-    fk_sphere_centres<T, Q>(J, M.n_joints, S, row, cen, stride);
+    fk_sphere_centres<T, Q>(J, M.n_joints, S, row, cen, stride, reinterpret_cast<const BoxRec<T>*>(smem + M.off_boxes),
+                            3 * M.n_spheres);
     const bool c2 = rest_collides<T>(M, smem, cen, stride, margin);
     out[idx] = c2 ? 0 : 1;
     if (n_col != nullptr && c2 && idx < count_lim) atomicAdd(n_col, 1);
@@ -559,7 +618,7 @@ k_check(ModelDev<T> M, const Q* __restrict__ q, int64_t n, int64_t ld, uint8_t* 
     __shared__ int s_warp[BT / 32];
     tma_stage(smem, M.blob, M.blob_bytes, &bar);
     T* cen = reinterpret_cast<T*>(smem + M.blob_bytes);
-    const size_t roff = (static_cast<size_t>(M.blob_bytes) + static_cast<size_t>(3) * M.n_spheres * BT * sizeof(T) + 15) &
+    const size_t roff = (static_cast<size_t>(M.blob_bytes) + static_cast<size_t>(M.cen_words) * BT * sizeof(T) + 15) &
                         ~static_cast<size_t>(15);
     Q* rows = reinterpret_cast<Q*>(smem + roff);
     const int dof = M.dof;
@@ -608,7 +667,8 @@ k_check(ModelDev<T> M, const Q* __restrict__ q, int64_t n, int64_t ld, uint8_t* 
         const bool valid = threadIdx.x < nr;
         bool col = false;
         if (valid) {
-            fk_sphere_centres<T, Q>(J, M.n_joints, S, my_row, my_cen, BT);
+            fk_sphere_centres<T, Q>(J, M.n_joints, S, my_row, my_cen, BT,
+                                    reinterpret_cast<const BoxRec<T>*>(smem + M.off_boxes), 3 * M.n_spheres);
             col = hot_pairs_collide<T>(M, smem, my_cen, BT);
             if (col) out[base + threadIdx.x] = 0;
         }
@@ -709,7 +769,7 @@ k_calibrate(ModelDev<float> M, const float* __restrict__ lo, const float* __rest
     __shared__ uint64_t bar;
     tma_stage(smem, M.blob, M.blob_bytes, &bar);
     float* cen = reinterpret_cast<float*>(smem + M.blob_bytes);
-    const size_t roff = (static_cast<size_t>(M.blob_bytes) + static_cast<size_t>(3) * M.n_spheres * blockDim.x * 4 + 15) &
+    const size_t roff = (static_cast<size_t>(M.blob_bytes) + static_cast<size_t>(M.cen_words) * blockDim.x * 4 + 15) &
                         ~static_cast<size_t>(15);
     float* q = reinterpret_cast<float*>(smem + roff) + threadIdx.x * M.dof;
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -723,7 +783,8 @@ k_calibrate(ModelDev<float> M, const float* __restrict__ lo, const float* __rest
     const SphereRec<float>* S = reinterpret_cast<const SphereRec<float>*>(smem + M.off_spheres);
     float* c = cen + threadIdx.x;
     const int st = blockDim.x;
-    fk_sphere_centres<float, float>(J, M.n_joints, S, q, c, st);
+    fk_sphere_centres<float, float>(J, M.n_joints, S, q, c, st,
+                                    reinterpret_cast<const BoxRec<float>*>(smem + M.off_boxes), 3 * M.n_spheres);
     const GroupRec* G = reinterpret_cast<const GroupRec*>(smem + M.off_groups);
     const PairRec<float>* P = reinterpret_cast<const PairRec<float>*>(smem + M.off_pairs);
     for (int g = 0; g < M.n_groups; ++g) {
@@ -758,7 +819,7 @@ static int32_t calibrate_layout(ez_world* w, HModel& hm, const double* lower, co
     EZ_CUDA(cudaMalloc(&d_cnt, sizeof(uint32_t) * (np + ns)));
     EZ_CUDA(cudaMemset(d_cnt, 0, sizeof(uint32_t) * (np + ns)));
     size_t smem = 0;
-    const int threads = check_block_threads<float>(w, w->mf.blob_bytes, w->mf.n_spheres, dof * 4, &smem);
+    const int threads = check_block_threads<float>(w, w->mf.blob_bytes, w->mf.cen_words, dof * 4, &smem);
     if (threads == 0) return fail(EZ_CAPACITY, "robot model too large for one checking CTA");
     if (smem > 48 * 1024)
         EZ_CUDA(cudaFuncSetAttribute(k_calibrate, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
@@ -800,7 +861,7 @@ static int32_t eval_bt(const ez_world* w, const ModelDev<T>& M, int* best_warps,
     cudaFuncAttributes fa{};
     EZ_CUDA(cudaFuncGetAttributes(&fa, kern));
     const size_t max_dyn = static_cast<size_t>(w->smem_optin) - fa.sharedSizeBytes;
-    size_t b = M.blob_bytes + static_cast<size_t>(3) * M.n_spheres * BT * sizeof(T);
+    size_t b = M.blob_bytes + static_cast<size_t>(M.cen_words) * BT * sizeof(T);
     b = (b + 15) & ~static_cast<size_t>(15);
     b += static_cast<size_t>(BT) * M.dof * sizeof(Q);
     b = (b + 15) & ~static_cast<size_t>(15);
@@ -901,6 +962,7 @@ static void world_free(ez_world* w) {
     }
     cudaFree(w->d_cells);
     cudaFree(w->d_lists);
+    cudaFree(w->d_occ_bits);
     cudaFree(w->d_linkQt);
     eizo_ws_free(w->eizo);
     delete w;
@@ -965,43 +1027,73 @@ extern "C" int32_t ez_world_create(const ez_robot_desc* rb, const ez_scene_desc*
     hm.dof = qi;
     if (hm.dof > 32) return fail(EZ_UNSUPPORTED, "more than 32 degrees of freedom");
 
-    // robot geometry: spheres (boxes are not supported natively yet)
+    // robot geometry: spheres and boxes, each in link-major order
     const double r_vox = (sc && sc->n_voxels > 0) ? 0.5 * sc->voxel_side * std::sqrt(static_cast<double>(dim)) : 0.0;
-    std::vector<int> sphere_of(rb->n_geoms, -1);
+    std::vector<int> sphere_of(rb->n_geoms, -1), box_of(rb->n_geoms, -1), geom_link(rb->n_geoms);
     for (int g = 0; g < rb->n_geoms; ++g) {
-        if (rb->geom_kind[g] != EZ_GEOM_SPHERE)
-            return fail(EZ_UNSUPPORTED, "robot box geometries are not supported by the native checker");
         const int link = rb->geom_link[g];
         if (link < 0 || link >= nj) return fail(EZ_INVALID_ARGUMENT, "geometry link out of range");
         if (g > 0 && link < rb->geom_link[g - 1]) return fail(EZ_INVALID_ARGUMENT, "geometries must be link-major");
-        HSphere s{};
+        geom_link[g] = link;
         double tl[3];
         embed_vec(rb->geom_trans + g * dim, dim, tl);
-        mat_vec(mat_T(Q[link]), tl, s.p);
-        s.r = rb->geom_radius[g];
-        s.rvox = (s.r + r_vox) + margin;
-        s.rmar = s.r + margin;
-        sphere_of[g] = static_cast<int>(hm.spheres.size());
-        hm.spheres.push_back(s);
+        const M3 Qt = mat_T(Q[link]);
+        if (rb->geom_kind[g] == EZ_GEOM_SPHERE) {
+            HSphere s{};
+            mat_vec(Qt, tl, s.p);
+            s.r = rb->geom_radius[g];
+            s.rvox = (s.r + r_vox) + margin;
+            s.rmar = s.r + margin;
+            sphere_of[g] = static_cast<int>(hm.spheres.size());
+            hm.spheres.push_back(s);
+        } else if (rb->geom_kind[g] == EZ_GEOM_BOX) {
+            HBox bx{};
+            bx.R = mat_mul(Qt, embed_rot(rb->geom_rot + g * dim * dim, dim));
+            mat_vec(Qt, tl, bx.t);
+            embed_vec(rb->geom_half + g * dim, dim, bx.he);
+            bx.link = link;
+            box_of[g] = static_cast<int>(hm.boxes.size());
+            hm.boxes.push_back(bx);
+        } else {
+            return fail(EZ_INVALID_ARGUMENT, "unknown geometry kind");
+        }
     }
     for (int j = 0; j < nj; ++j) {
-        int b = 0;
-        while (b < rb->n_geoms && rb->geom_link[b] < j) ++b;
-        int e = b;
-        while (e < rb->n_geoms && rb->geom_link[e] == j) ++e;
-        hm.joints[j].sb = b;
-        hm.joints[j].se = e;
+        int sb = 0, bb = 0;
+        for (int g = 0; g < rb->n_geoms; ++g) {
+            if (geom_link[g] >= j) break;
+            sb += sphere_of[g] >= 0;
+            bb += box_of[g] >= 0;
+        }
+        int se = sb, be = bb;
+        for (int g = 0; g < rb->n_geoms; ++g) {
+            if (geom_link[g] != j) continue;
+            se += sphere_of[g] >= 0;
+            be += box_of[g] >= 0;
+        }
+        hm.joints[j].sb = sb;
+        hm.joints[j].se = se;
+        hm.joints[j].bb = bb;
+        hm.joints[j].be = be;
     }
-    // self pairs (input order); layout_pairs groups them (and, after
-    // calibration, moves the most frequently colliding ones to the hot list)
+    // self pairs (input order); sphere-sphere pairs go through layout_pairs
+    // (grouping, and after calibration the hot list), pairs with a box are
+    // tested by the box stage (sphere first for sphere-box)
     for (int p = 0; p < rb->n_pairs; ++p) {
         const int a = rb->pairs[2 * p], b = rb->pairs[2 * p + 1];
         if (a < 0 || b < 0 || a >= rb->n_geoms || b >= rb->n_geoms)
             return fail(EZ_INVALID_ARGUMENT, "self pair index out of range");
         if (rb->geom_link[a] == rb->geom_link[b])
             return fail(EZ_INVALID_ARGUMENT, "self-collision pair on a single link");
-        const double rr = (rb->geom_radius[a] + rb->geom_radius[b]) + margin;
-        hm.all_pairs.push_back(HSelfPair{a, b, rr * rr});
+        if (sphere_of[a] >= 0 && sphere_of[b] >= 0) {
+            const double rr = (rb->geom_radius[a] + rb->geom_radius[b]) + margin;
+            hm.all_pairs.push_back(HSelfPair{sphere_of[a], sphere_of[b], rr * rr});
+        } else if (sphere_of[a] >= 0 || sphere_of[b] >= 0) {
+            const int s = sphere_of[a] >= 0 ? a : b, x = sphere_of[a] >= 0 ? b : a;
+            hm.mix.push_back(HMix{0, sphere_of[s], 1, box_of[x], rb->geom_radius[s]});
+        } else {
+            hm.mix.push_back(HMix{1, box_of[a], 1, box_of[b], 0.0});
+        }
     }
     layout_pairs(hm, nullptr, nullptr);
     // static obstacles

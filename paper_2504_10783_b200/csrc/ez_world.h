@@ -29,6 +29,7 @@ struct ez_world {
     // voxel obstacle structure (shared by both precisions)
     uint32_t* d_cells = nullptr;
     int4* d_lists = nullptr;
+    uint32_t* d_occ_bits = nullptr;  // dense occupancy bitmap of the padded voxel lattice
     int64_t n_list = 0;
     int32_t grid_n[3] = {0, 0, 0};
     double cell_h = 0.0;
@@ -66,10 +67,10 @@ void eizo_ws_free(ez_eizo_ws* ws);
 // store fits in shared memory; writes the dynamic smem bytes.  0 if even 32
 // threads do not fit.
 template <typename T>
-inline int check_block_threads(const ez_world* w, uint32_t blob_bytes, int n_spheres, int row_bytes, size_t* smem,
+inline int check_block_threads(const ez_world* w, uint32_t blob_bytes, int cen_words, int row_bytes, size_t* smem,
                                int max_threads = 128) {
     for (int t = max_threads; t >= 32; t /= 2) {
-        size_t b = blob_bytes + static_cast<size_t>(3) * n_spheres * t * sizeof(T);
+        size_t b = blob_bytes + static_cast<size_t>(cen_words) * t * sizeof(T);
         b = (b + 15) & ~static_cast<size_t>(15);
         b += static_cast<size_t>(t) * row_bytes;
         b = (b + 15) & ~static_cast<size_t>(15);

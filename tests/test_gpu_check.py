@@ -163,7 +163,7 @@ def test_world_info_reports_grid():
     assert info["list_entries"] > 0 and all(n > 0 for n in info["grid_dims"])
 
 
-def test_robot_boxes_rejected_loudly():
+def _unused_robot_boxes_rejected_loudly():
     from paper_2504_10783_b200.errors import CorridorError
 
     joints = (Joint(REVOLUTE, -1, RigidTransform.identity(2)),)
@@ -171,3 +171,29 @@ def test_robot_boxes_rejected_loudly():
     model = RobotModel(2, joints, links, [-1.0], [1.0])
     with pytest.raises((NotImplementedError, CorridorError)):
         World(model).checker().check([0.0])
+
+
+def test_check_segments_batched_equals_loop():
+    w = fx.disc_world(fx.forest_centers(5))
+    rng = np.random.default_rng(8)
+    V1 = rng.uniform(-4.5, 4.5, size=(200, 2))
+    V2 = V1 + rng.normal(size=(200, 2))
+    ck = w.checker()
+    batched = ck.check_segments(V1, V2, 0.01)
+    loop = np.array([w.checker().check_segment(a, b, 0.01) for a, b in zip(V1, V2)])
+    assert np.array_equal(batched, loop) and batched.any() and (~batched).any()
+
+
+@pytest.mark.parametrize("name", ["box2d", "box3d", "box3d_noself"])
+@pytest.mark.parametrize("precision", ["fp32", "fp64"])
+def test_robot_box_geometries_match_reference(name, precision):
+    # world.py:538-565: box vs static spheres / voxel spheres / static boxes (SAT), sphere-box and box-box pairs
+    from conftest import GOLDEN
+    from paper_2504_10783_b200.scene import load_scene
+
+    g = golden(f"check_{name}.npz")
+    world = load_scene(GOLDEN / f"scene_{name}.json").with_vmap(
+        VoxelMap(g["vox_origin"], float(g["vox_side"]), g["vox_idx"]))
+    free = world.checker(precision=precision).check_batch(g["Q"].astype(np.float64))
+    mism = (free != g["free"]) & ~g["band"]
+    assert not mism.any(), f"{mism.sum()} mismatches outside the contact band"
