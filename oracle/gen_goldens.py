@@ -291,7 +291,12 @@ def gen_boxes(C):
     from paper_2504_10783_b200.model import RobotModel
     m3n = RobotModel(3, m3.joints, m3.links, m3.lower, m3.upper, ())
     w3n = World(m3n, static=(stat3,), vmap=fx.cloud10k())
-    for name, world, n in (("box2d", w2, 20_000), ("box3d", w3, 10_000), ("box3d_noself", w3n, 10_000)):
+    import os
+
+    only = os.environ.get("EZ_GOLDEN_ONLY")
+    for name, world, n in (("box2d", w2, 20_000), ("box3d", w3, 10_000), ("box3d_noself", w3n, 2_000)):
+        if only and name not in only.split(","):
+            continue
         rng = np.random.default_rng(0)
         Q = rng.uniform(world.lower, world.upper, size=(n, len(world.lower))).astype(np.float32)
         rw = _to_ref_world(world, C)
