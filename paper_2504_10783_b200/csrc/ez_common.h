@@ -59,6 +59,20 @@ struct alignas(16) JointRec {
     int32_t pad_[3];
 };
 
+// Self pairs outside the hot list are tested in blocks, one per pair of
+// links: each link is bounded by a ball around one of its spheres (the
+// anchor) enclosing all the link's spheres; if the anchors are farther apart
+// than R_a + R_b + margin, no pair of the block can touch and the block is
+// skipped.  thr2 carries a small upward
+// slack, so the skip is conservative in fp32.
+template <typename T>
+struct alignas(16) BlockRec {
+    int32_t ba, bb;       // anchor sphere indices
+    int32_t begin, end;   // range in the rest-pair list (HotRec layout)
+    T thr2;               // (R_a + R_b + margin)^2 (+ slack)
+    T pad_[3];
+};
+
 // Robot box geometry (world.py:538-565).  World pose = link frame * local.
 template <typename T>
 struct alignas(16) BoxRec {
@@ -89,23 +103,12 @@ struct alignas(16) SphereRec {
 
 // The self pairs most likely to collide (calibrated on uniform samples at
 // world creation) are tested first, flat, so most colliding configurations
-// leave after one or two pairs; the rest are grouped by first sphere.
+// leave after one or two pairs; the rest are tested in link-pair blocks.
 template <typename T>
 struct alignas(16) HotRec {
     int32_t a, b;
     T thr2;
     T pad_;
-};
-
-struct alignas(16) GroupRec {   // self pairs grouped by first sphere
-    int32_t a, begin, end, pad_;
-};
-
-template <typename T>
-struct alignas(8) PairRec {     // second sphere + (ra + rb + margin)^2  (world.py:557)
-    int32_t b;
-    int32_t pad_;
-    T thr2;
 };
 
 template <typename T>
@@ -149,11 +152,12 @@ struct VoxGrid {
 
 template <typename T>
 struct ModelDev {
-    const uint8_t* blob;      // device: joints | spheres | hot | groups | pairs | order | ssph | sbox | boxes | mix
+    const uint8_t* blob;      // device: joints | spheres | hot | blocks | rest | order | ssph | sbox | boxes | mix
     uint32_t blob_bytes;      // multiple of 16
-    int32_t n_joints, dof, n_spheres, n_hot, n_groups, n_pairs, n_ssph, n_sbox, n_store, n_boxes, n_mix;
-    int32_t cen_words;        // per-configuration geometry store: 3 per sphere + 12 per box
-    uint32_t off_spheres, off_hot, off_groups, off_pairs, off_order, off_ssph, off_sbox, off_boxes, off_mix;
+    int32_t n_joints, dof, n_spheres, n_hot, n_blocks, n_rest, n_ssph, n_sbox, n_store, n_boxes, n_mix;
+    int32_t cen_words;        // per-configuration store: 3 per sphere + 12 per box
+    int32_t box_base;         // first word of the box frames: 3 * n_spheres
+    uint32_t off_spheres, off_hot, off_blocks, off_rest, off_order, off_ssph, off_sbox, off_boxes, off_mix;
     VoxGrid<T> vox;
 };
 

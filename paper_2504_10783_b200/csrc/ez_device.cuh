@@ -289,7 +289,7 @@ template <typename T>
 __device__ __forceinline__ bool boxes_collide_all(const ModelDev<T>& M, const uint8_t* blob,
                                                   const T* __restrict__ cen, int stride, T margin) {
     const BoxRec<T>* BX = reinterpret_cast<const BoxRec<T>*>(blob + M.off_boxes);
-    const int base = 3 * M.n_spheres;
+    const int base = M.box_base;
     for (int b = 0; b < M.n_boxes; ++b) {
         T R[9], t[3];
         load_box<T>(cen, stride, base + 12 * b, R, t);
@@ -318,34 +318,36 @@ __device__ __forceinline__ bool boxes_collide_all(const ModelDev<T>& M, const ui
 // self pairs (world.py:514-516, 554-557)
 // ---------------------------------------------------------------------------
 template <typename T>
-__device__ __forceinline__ bool self_collides(const GroupRec* __restrict__ G, int ng,
-                                              const PairRec<T>* __restrict__ P,
-                                              const T* __restrict__ cen, int stride) {
-    for (int g = 0; g < ng; ++g) {
-        const GroupRec gr = G[g];
-        const T ax = cen[(3 * gr.a) * stride], ay = cen[(3 * gr.a + 1) * stride],
-                az = cen[(3 * gr.a + 2) * stride];
-        int p = gr.begin;
-        // four independent pair tests per branch: loads and math overlap
-        for (; p + 4 <= gr.end; p += 4) {
+__device__ __forceinline__ bool pair_hits(const HotRec<T>& h, const T* __restrict__ cen, int stride) {
+    const T dx = cen[(3 * h.a) * stride] - cen[(3 * h.b) * stride];
+    const T dy = cen[(3 * h.a + 1) * stride] - cen[(3 * h.b + 1) * stride];
+    const T dz = cen[(3 * h.a + 2) * stride] - cen[(3 * h.b + 2) * stride];
+    return dx * dx + dy * dy + dz * dz <= h.thr2;
+}
+
+// Non-hot self pairs, block by link pair: the bounding-sphere test skips
+// whole blocks (see BlockRec); inside a block four independent pair tests run
+// per branch so their loads and math overlap.
+template <typename T>
+__device__ __forceinline__ bool blocks_collide(const ModelDev<T>& M, const uint8_t* blob,
+                                               const T* __restrict__ cen, int stride) {
+    const BlockRec<T>* B = reinterpret_cast<const BlockRec<T>*>(blob + M.off_blocks);
+    const HotRec<T>* P = reinterpret_cast<const HotRec<T>*>(blob + M.off_rest);
+    for (int k = 0; k < M.n_blocks; ++k) {
+        const BlockRec<T> bk = B[k];
+        const T bx = cen[(3 * bk.ba) * stride] - cen[(3 * bk.bb) * stride];
+        const T by = cen[(3 * bk.ba + 1) * stride] - cen[(3 * bk.bb + 1) * stride];
+        const T bz = cen[(3 * bk.ba + 2) * stride] - cen[(3 * bk.bb + 2) * stride];
+        if (bx * bx + by * by + bz * bz > bk.thr2) continue;
+        int p = bk.begin;
+        for (; p + 4 <= bk.end; p += 4) {
             bool hit = false;
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const PairRec<T> pr = P[p + u];
-                const T dx = ax - cen[(3 * pr.b) * stride];
-                const T dy = ay - cen[(3 * pr.b + 1) * stride];
-                const T dz = az - cen[(3 * pr.b + 2) * stride];
-                hit |= dx * dx + dy * dy + dz * dz <= pr.thr2;
-            }
+            for (int u = 0; u < 4; ++u) hit |= pair_hits<T>(P[p + u], cen, stride);
             if (hit) return true;
         }
-        for (; p < gr.end; ++p) {
-            const PairRec<T> pr = P[p];
-            const T dx = ax - cen[(3 * pr.b) * stride];
-            const T dy = ay - cen[(3 * pr.b + 1) * stride];
-            const T dz = az - cen[(3 * pr.b + 2) * stride];
-            if (dx * dx + dy * dy + dz * dz <= pr.thr2) return true;
-        }
+        for (; p < bk.end; ++p)
+            if (pair_hits<T>(P[p], cen, stride)) return true;
     }
     return false;
 }
@@ -494,9 +496,7 @@ __device__ __forceinline__ bool rest_collides(const ModelDev<T>& M, const uint8_
                 return true;
         }
     }
-    const GroupRec* G = reinterpret_cast<const GroupRec*>(blob + M.off_groups);
-    const PairRec<T>* P = reinterpret_cast<const PairRec<T>*>(blob + M.off_pairs);
-    if (self_collides<T>(G, M.n_groups, P, cen, stride)) return true;
+    if (blocks_collide<T>(M, blob, cen, stride)) return true;
     return (M.n_boxes > 0) && boxes_collide_all<T>(M, blob, cen, stride, margin);
 }
 
@@ -514,7 +514,7 @@ __device__ __forceinline__ bool config_free(const ModelDev<T>& M, const uint8_t*
     const JointRec<T>* J = reinterpret_cast<const JointRec<T>*>(blob);
     const SphereRec<T>* S = reinterpret_cast<const SphereRec<T>*>(blob + M.off_spheres);
     fk_sphere_centres<T, Q>(J, M.n_joints, S, q, cen, stride, reinterpret_cast<const BoxRec<T>*>(blob + M.off_boxes),
-                            3 * M.n_spheres);
+                            M.box_base);
     return !config_collides<T>(M, blob, cen, stride, margin);
 }
 
@@ -615,7 +615,7 @@ __device__ __forceinline__ bool config_free_coop(const ModelDev<T>& M, const uin
     const JointRec<T>* J = reinterpret_cast<const JointRec<T>*>(blob);
     const SphereRec<T>* S = reinterpret_cast<const SphereRec<T>*>(blob + M.off_spheres);
     const BoxRec<T>* BX = reinterpret_cast<const BoxRec<T>*>(blob + M.off_boxes);
-    fk_centres_coop<T, Q, G>(J, M.n_joints, S, q, cen, lane, BX, 3 * M.n_spheres);
+    fk_centres_coop<T, Q, G>(J, M.n_joints, S, q, cen, lane, BX, M.box_base);
     __syncwarp(gm);
     const HotRec<T>* H = reinterpret_cast<const HotRec<T>*>(blob + M.off_hot);
     for (int p0 = 0; p0 < M.n_hot; p0 += G) {
@@ -641,24 +641,21 @@ __device__ __forceinline__ bool config_free_coop(const ModelDev<T>& M, const uin
         }
         if (__ballot_sync(gm, hit)) return false;
     }
-    const GroupRec* Gr = reinterpret_cast<const GroupRec*>(blob + M.off_groups);
-    const PairRec<T>* P = reinterpret_cast<const PairRec<T>*>(blob + M.off_pairs);
-    for (int g = 0; g < M.n_groups; ++g) {
-        const GroupRec gr = Gr[g];
-        const T ax = cen[3 * gr.a], ay = cen[3 * gr.a + 1], az = cen[3 * gr.a + 2];
-        for (int p0 = gr.begin; p0 < gr.end; p0 += G) {
+    const BlockRec<T>* Bk = reinterpret_cast<const BlockRec<T>*>(blob + M.off_blocks);
+    const HotRec<T>* P = reinterpret_cast<const HotRec<T>*>(blob + M.off_rest);
+    for (int k = 0; k < M.n_blocks; ++k) {
+        const BlockRec<T> bk = Bk[k];
+        const T bx = cen[3 * bk.ba] - cen[3 * bk.bb], by = cen[3 * bk.ba + 1] - cen[3 * bk.bb + 1],
+                bz = cen[3 * bk.ba + 2] - cen[3 * bk.bb + 2];
+        if (bx * bx + by * by + bz * bz > bk.thr2) continue;  // group-uniform
+        for (int p0 = bk.begin; p0 < bk.end; p0 += G) {
             const int p = p0 + lane;
-            bool hit = false;
-            if (p < gr.end) {
-                const PairRec<T> pr = P[p];
-                const T dx = ax - cen[3 * pr.b], dy = ay - cen[3 * pr.b + 1], dz = az - cen[3 * pr.b + 2];
-                hit = dx * dx + dy * dy + dz * dz <= pr.thr2;
-            }
+            const bool hit = p < bk.end && pair_hits<T>(P[p], cen, 1);
             if (__ballot_sync(gm, hit)) return false;
         }
     }
     if (M.n_boxes == 0) return true;
-    const int base = 3 * M.n_spheres;
+    const int base = M.box_base;
     for (int b0 = 0; b0 < M.n_boxes; b0 += G) {
         const int b = b0 + lane;
         bool hit = false;

@@ -55,7 +55,7 @@ k_node_voxels(ModelDev<double> M, const double* __restrict__ nodes, int64_t n, M
         if (lane < M.dof) row[lane] = nodes[node * M.dof + lane];
         for (int w = lane; w < g.words; w += 32) bits[w] = 0u;
         __syncwarp();
-        fk_centres_coop<double, double, 32>(J, M.n_joints, S, row, cen, lane, BX, 3 * M.n_spheres);
+        fk_centres_coop<double, double, 32>(J, M.n_joints, S, row, cen, lane, BX, M.box_base);
         __syncwarp();
         for (int s = lane; s < M.n_spheres; s += 32) {
             const double R = S[s].r + g.r_vox;
@@ -90,7 +90,7 @@ k_node_voxels(ModelDev<double> M, const double* __restrict__ nodes, int64_t n, M
         // boxes: |local - clip(local)|^2 <= r_vox^2 with local = R^T (c_v - t) (drm.py:186-189)
         for (int b = lane; b < M.n_boxes; b += 32) {
             double Rb[9], tb[3];
-            load_box<double>(cen, 1, 3 * M.n_spheres + 12 * b, Rb, tb);
+            load_box<double>(cen, 1, M.box_base + 12 * b, Rb, tb);
             const double* he = BX[b].he;
             const double thr = g.r_vox * g.r_vox;
             int lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};

@@ -93,15 +93,12 @@ struct HJoint {
 struct HSphere {
     double p[3], r, rvox, rmar;
 };
-struct HPair {
-    int b;
+struct HSelfPair {
+    int a, b;
     double thr2;
 };
-struct HGroup {
-    int a, begin, end;
-};
-struct HSelfPair {   // input order
-    int a, b;
+struct HBlock {     // self pairs between two links
+    int ba, bb, begin, end;
     double thr2;
 };
 struct HBox {
@@ -119,53 +116,107 @@ struct HModel {
     std::vector<HSphere> spheres;
     std::vector<HSelfPair> all_pairs;
     std::vector<HSelfPair> hot;
-    std::vector<HGroup> groups;
-    std::vector<HPair> pairs;
-    std::vector<int> pair_src;  // flat grouped position -> index in all_pairs
-    std::vector<int32_t> order; // obstacle-test order of the spheres
+    std::vector<HBlock> blocks;
+    std::vector<HSelfPair> rest;    // non-hot pairs, block-major
+    std::vector<int> pair_src;      // rest position -> index in all_pairs
+    std::vector<int32_t> order;     // obstacle-test order of the spheres
     std::vector<double> ssph;  // c3, r
     std::vector<double> sbox;  // Rt9, t3, he3
     std::vector<HBox> boxes;   // robot boxes
     std::vector<HMix> mix;     // self pairs with a box
+    double margin = 0.0;
     int dof = 0, n_store = 0;
 };
 
 constexpr int kHotPairs = 16;
+constexpr int kMinBlock = 3;   // smaller link-pair blocks are tested without the bounding-sphere skip
 
-// Pair/sphere layout.  Without statistics: no hot list, link order.  With
-// per-pair and per-sphere hit counts: the kHotPairs most frequent self pairs
-// first (flat), the rest grouped by first sphere, spheres tested against
-// obstacles in decreasing hit frequency.
+// Pair/sphere layout.  Without statistics: no hot list, blocks in link order.
+// With per-pair and per-sphere hit counts: the kHotPairs most frequent self
+// pairs first (flat), the rest in link-pair blocks ordered by hits, spheres
+// tested against obstacles in decreasing hit frequency.
 void layout_pairs(HModel& hm, const std::vector<uint32_t>* pair_hits, const std::vector<uint32_t>* sph_hits) {
     const int np = static_cast<int>(hm.all_pairs.size());
+    auto hits = [&](int i) -> uint64_t { return pair_hits ? (*pair_hits)[i] : 0; };
     std::vector<int> rank(np);
     for (int i = 0; i < np; ++i) rank[i] = i;
     std::vector<char> is_hot(np, 0);
     hm.hot.clear();
     if (pair_hits) {
-        std::stable_sort(rank.begin(), rank.end(), [&](int x, int y) { return (*pair_hits)[x] > (*pair_hits)[y]; });
+        std::stable_sort(rank.begin(), rank.end(), [&](int x, int y) { return hits(x) > hits(y); });
         for (int k = 0; k < std::min(kHotPairs, np); ++k) {
-            if ((*pair_hits)[rank[k]] == 0) break;
+            if (hits(rank[k]) == 0) break;
             is_hot[rank[k]] = 1;
             hm.hot.push_back(hm.all_pairs[rank[k]]);
         }
     }
     const int ns = static_cast<int>(hm.spheres.size());
-    std::vector<std::vector<int>> by_a(ns);
-    for (int i = 0; i < np; ++i)
-        if (!is_hot[i]) by_a[hm.all_pairs[i].a].push_back(i);
-    hm.groups.clear();
-    hm.pairs.clear();
+    const int nl = static_cast<int>(hm.joints.size());
+    std::vector<int> link_of(ns, 0);
+    for (int l = 0; l < nl; ++l) {
+        for (int s = hm.joints[l].sb; s < hm.joints[l].se; ++s) link_of[s] = l;
+    }
+    // non-hot pairs by unordered link pair
+    std::vector<std::vector<int>> by_key(static_cast<size_t>(nl) * nl);
+    for (int i = 0; i < np; ++i) {
+        if (is_hot[i]) continue;
+        const int la = link_of[hm.all_pairs[i].a], lb = link_of[hm.all_pairs[i].b];
+        by_key[static_cast<size_t>(std::min(la, lb)) * nl + std::max(la, lb)].push_back(i);
+    }
+    std::vector<int> keys;
+    std::vector<uint64_t> key_hits(by_key.size(), 0);
+    for (size_t k = 0; k < by_key.size(); ++k) {
+        if (by_key[k].empty()) continue;
+        keys.push_back(static_cast<int>(k));
+        for (int i : by_key[k]) key_hits[k] += hits(i);
+        std::stable_sort(by_key[k].begin(), by_key[k].end(), [&](int x, int y) { return hits(x) > hits(y); });
+    }
+    std::stable_sort(keys.begin(), keys.end(), [&](int x, int y) { return key_hits[x] > key_hits[y]; });
+    // A link's bound is one of its own spheres (the anchor, chosen to minimise
+    // the radius enclosing every sphere of the link around it): no extra FK
+    // work or centre storage, at a slightly looser radius than a free centre.
+    std::vector<int> anchor(nl, -1);
+    std::vector<double> bound_r(nl, 0.0);
+    auto bound_of = [&](int l) -> int {
+        if (anchor[l] >= 0) return anchor[l];
+        const HJoint& j = hm.joints[l];
+        auto dist = [&](int s, const double* x) {
+            const double dx = hm.spheres[s].p[0] - x[0], dy = hm.spheres[s].p[1] - x[1], dz = hm.spheres[s].p[2] - x[2];
+            return std::sqrt(dx * dx + dy * dy + dz * dz);
+        };
+        double best = 1e300;
+        for (int a = j.sb; a < j.se; ++a) {
+            double R = 0.0;
+            for (int s = j.sb; s < j.se; ++s) R = std::max(R, dist(s, hm.spheres[a].p) + hm.spheres[s].r);
+            if (R < best) {
+                best = R;
+                anchor[l] = a;
+            }
+        }
+        bound_r[l] = best;
+        return anchor[l];
+    };
+    hm.blocks.clear();
+    hm.rest.clear();
     hm.pair_src.clear();
-    for (int a = 0; a < ns; ++a) {
-        if (by_a[a].empty()) continue;
-        HGroup g{a, static_cast<int>(hm.pairs.size()), 0};
-        for (int i : by_a[a]) {
-            hm.pairs.push_back(HPair{hm.all_pairs[i].b, hm.all_pairs[i].thr2});
+    for (int k : keys) {
+        const std::vector<int>& ps = by_key[k];
+        HBlock b{0, 0, static_cast<int>(hm.rest.size()), 0, 1e30};  // small block: always tested
+        if (static_cast<int>(ps.size()) >= kMinBlock) {
+            const int la = k / nl, lb = k % nl;
+            b.ba = bound_of(la);
+            b.bb = bound_of(lb);
+            const double Ra = bound_r[la], Rb = bound_r[lb];
+            // conservative: fp32 FK error is far below the 1e-4 relative slack
+            const double thr = (Ra + Rb + hm.margin) * (1.0 + 1e-4) + 1e-5;
+            b.thr2 = thr * thr;
+        }
+        for (int i : ps) {
+            hm.rest.push_back(hm.all_pairs[i]);
             hm.pair_src.push_back(i);
         }
-        g.end = static_cast<int>(hm.pairs.size());
-        hm.groups.push_back(g);
+        b.end = static_cast<int>(hm.rest.size());
+        hm.blocks.push_back(b);
     }
     hm.order.resize(ns);
     for (int i = 0; i < ns; ++i) hm.order[i] = i;
@@ -179,10 +230,11 @@ size_t align16(size_t x) { return (x + 15) & ~static_cast<size_t>(15); }
 template <typename T>
 std::vector<uint8_t> pack_blob(const HModel& hm, ModelDev<T>& md) {
     const size_t sz_j = align16(hm.joints.size() * sizeof(JointRec<T>));
-    const size_t sz_s = align16(hm.spheres.size() * sizeof(SphereRec<T>));
+    const size_t n_sph = hm.spheres.size();
+    const size_t sz_s = align16(n_sph * sizeof(SphereRec<T>));
     const size_t sz_h = align16(hm.hot.size() * sizeof(HotRec<T>));
-    const size_t sz_g = align16(hm.groups.size() * sizeof(GroupRec));
-    const size_t sz_p = align16(hm.pairs.size() * sizeof(PairRec<T>));
+    const size_t sz_g = align16(hm.blocks.size() * sizeof(BlockRec<T>));
+    const size_t sz_p = align16(hm.rest.size() * sizeof(HotRec<T>));
     const size_t sz_o = align16(hm.order.size() * sizeof(int32_t));
     const size_t n_ss = hm.ssph.size() / 4, n_sb = hm.sbox.size() / 15;
     const size_t sz_ss = align16(n_ss * sizeof(StaticSphereRec<T>));
@@ -190,8 +242,8 @@ std::vector<uint8_t> pack_blob(const HModel& hm, ModelDev<T>& md) {
     size_t off = sz_j;
     md.off_spheres = static_cast<uint32_t>(off); off += sz_s;
     md.off_hot = static_cast<uint32_t>(off); off += sz_h;
-    md.off_groups = static_cast<uint32_t>(off); off += sz_g;
-    md.off_pairs = static_cast<uint32_t>(off); off += sz_p;
+    md.off_blocks = static_cast<uint32_t>(off); off += sz_g;
+    md.off_rest = static_cast<uint32_t>(off); off += sz_p;
     md.off_order = static_cast<uint32_t>(off); off += sz_o;
     md.off_ssph = static_cast<uint32_t>(off); off += sz_ss;
     md.off_sbox = static_cast<uint32_t>(off); off += sz_sb;
@@ -221,14 +273,29 @@ std::vector<uint8_t> pack_blob(const HModel& hm, ModelDev<T>& md) {
     }
     md.n_boxes = static_cast<int32_t>(hm.boxes.size());
     md.n_mix = static_cast<int32_t>(hm.mix.size());
-    md.cen_words = static_cast<int32_t>(3 * hm.spheres.size() + 12 * hm.boxes.size());
-    auto* HR = reinterpret_cast<HotRec<T>*>(blob.data() + md.off_hot);
-    for (size_t i = 0; i < hm.hot.size(); ++i) {
-        HotRec<T> r{};
-        r.a = hm.hot[i].a;
-        r.b = hm.hot[i].b;
-        r.thr2 = static_cast<T>(hm.hot[i].thr2);
-        HR[i] = r;
+    md.box_base = static_cast<int32_t>(3 * n_sph);
+    md.cen_words = static_cast<int32_t>(3 * n_sph + 12 * hm.boxes.size());
+    auto put_pairs = [&](const std::vector<HSelfPair>& src, uint32_t off_) {
+        auto* HR = reinterpret_cast<HotRec<T>*>(blob.data() + off_);
+        for (size_t i = 0; i < src.size(); ++i) {
+            HotRec<T> r{};
+            r.a = src[i].a;
+            r.b = src[i].b;
+            r.thr2 = static_cast<T>(src[i].thr2);
+            HR[i] = r;
+        }
+    };
+    put_pairs(hm.hot, md.off_hot);
+    put_pairs(hm.rest, md.off_rest);
+    auto* BK = reinterpret_cast<BlockRec<T>*>(blob.data() + md.off_blocks);
+    for (size_t i = 0; i < hm.blocks.size(); ++i) {
+        BlockRec<T> r{};
+        r.ba = hm.blocks[i].ba;
+        r.bb = hm.blocks[i].bb;
+        r.begin = hm.blocks[i].begin;
+        r.end = hm.blocks[i].end;
+        r.thr2 = static_cast<T>(hm.blocks[i].thr2);
+        BK[i] = r;
     }
     auto* OR = reinterpret_cast<int32_t*>(blob.data() + md.off_order);
     for (size_t i = 0; i < hm.order.size(); ++i) OR[i] = hm.order[i];
@@ -253,22 +320,14 @@ std::vector<uint8_t> pack_blob(const HModel& hm, ModelDev<T>& md) {
         J[j] = r;
     }
     auto* S = reinterpret_cast<SphereRec<T>*>(blob.data() + md.off_spheres);
-    for (size_t s = 0; s < hm.spheres.size(); ++s) {
+    for (size_t s = 0; s < n_sph; ++s) {
+        const HSphere& h = hm.spheres[s];
         SphereRec<T> r{};
-        for (int k = 0; k < 3; ++k) r.p[k] = static_cast<T>(hm.spheres[s].p[k]);
-        r.r = static_cast<T>(hm.spheres[s].r);
-        r.rvox = static_cast<T>(hm.spheres[s].rvox);
-        r.rmar = static_cast<T>(hm.spheres[s].rmar);
+        for (int k = 0; k < 3; ++k) r.p[k] = static_cast<T>(h.p[k]);
+        r.r = static_cast<T>(h.r);
+        r.rvox = static_cast<T>(h.rvox);
+        r.rmar = static_cast<T>(h.rmar);
         S[s] = r;
-    }
-    auto* G = reinterpret_cast<GroupRec*>(blob.data() + md.off_groups);
-    for (size_t g = 0; g < hm.groups.size(); ++g) G[g] = GroupRec{hm.groups[g].a, hm.groups[g].begin, hm.groups[g].end, 0};
-    auto* P = reinterpret_cast<PairRec<T>*>(blob.data() + md.off_pairs);
-    for (size_t p = 0; p < hm.pairs.size(); ++p) {
-        PairRec<T> r{};
-        r.b = hm.pairs[p].b;
-        r.thr2 = static_cast<T>(hm.pairs[p].thr2);
-        P[p] = r;
     }
     auto* SS = reinterpret_cast<StaticSphereRec<T>*>(blob.data() + md.off_ssph);
     for (size_t i = 0; i < n_ss; ++i) {
@@ -291,8 +350,8 @@ std::vector<uint8_t> pack_blob(const HModel& hm, ModelDev<T>& md) {
     md.dof = hm.dof;
     md.n_spheres = static_cast<int32_t>(hm.spheres.size());
     md.n_hot = static_cast<int32_t>(hm.hot.size());
-    md.n_groups = static_cast<int32_t>(hm.groups.size());
-    md.n_pairs = static_cast<int32_t>(hm.pairs.size());
+    md.n_blocks = static_cast<int32_t>(hm.blocks.size());
+    md.n_rest = static_cast<int32_t>(hm.rest.size());
     md.n_ssph = static_cast<int32_t>(n_ss);
     md.n_sbox = static_cast<int32_t>(n_sb);
     md.n_store = hm.n_store;
@@ -600,7 +659,7 @@ __device__ __forceinline__ void check_phase_b(const ModelDev<T>& M, const uint8_
     const JointRec<T>* J = reinterpret_cast<const JointRec<T>*>(smem);
     const SphereRec<T>* S = reinterpret_cast<const SphereRec<T>*>(smem + M.off_spheres);
     fk_sphere_centres<T, Q>(J, M.n_joints, S, row, cen, stride, reinterpret_cast<const BoxRec<T>*>(smem + M.off_boxes),
-                            3 * M.n_spheres);
+                            M.box_base);
     const bool c2 = rest_collides<T>(M, smem, cen, stride, margin);
     out[idx] = c2 ? 0 : 1;
     if (n_col != nullptr && c2 && idx < count_lim) atomicAdd(n_col, 1);
@@ -668,7 +727,7 @@ k_check(ModelDev<T> M, const Q* __restrict__ q, int64_t n, int64_t ld, uint8_t* 
         bool col = false;
         if (valid) {
             fk_sphere_centres<T, Q>(J, M.n_joints, S, my_row, my_cen, BT,
-                                    reinterpret_cast<const BoxRec<T>*>(smem + M.off_boxes), 3 * M.n_spheres);
+                                    reinterpret_cast<const BoxRec<T>*>(smem + M.off_boxes), M.box_base);
             col = hot_pairs_collide<T>(M, smem, my_cen, BT);
             if (col) out[base + threadIdx.x] = 0;
         }
@@ -764,7 +823,7 @@ __global__ void k_fk_frames(ModelDev<double> M, const double* __restrict__ Qt, c
 // uniform samples of the joint box; used only to order the tests.
 __global__ void __launch_bounds__(128)
 k_calibrate(ModelDev<float> M, const float* __restrict__ lo, const float* __restrict__ hi, int n, uint64_t seed,
-            float margin, uint32_t* __restrict__ pair_hits, uint32_t* __restrict__ sph_hits) {
+            float margin, uint32_t* __restrict__ pcount, uint32_t* __restrict__ sph_hits) {
     extern __shared__ __align__(16) uint8_t smem[];
     __shared__ uint64_t bar;
     tma_stage(smem, M.blob, M.blob_bytes, &bar);
@@ -784,18 +843,10 @@ k_calibrate(ModelDev<float> M, const float* __restrict__ lo, const float* __rest
     float* c = cen + threadIdx.x;
     const int st = blockDim.x;
     fk_sphere_centres<float, float>(J, M.n_joints, S, q, c, st,
-                                    reinterpret_cast<const BoxRec<float>*>(smem + M.off_boxes), 3 * M.n_spheres);
-    const GroupRec* G = reinterpret_cast<const GroupRec*>(smem + M.off_groups);
-    const PairRec<float>* P = reinterpret_cast<const PairRec<float>*>(smem + M.off_pairs);
-    for (int g = 0; g < M.n_groups; ++g) {
-        const GroupRec gr = G[g];
-        for (int p = gr.begin; p < gr.end; ++p) {
-            const int b = P[p].b;
-            const float dx = c[3 * gr.a * st] - c[3 * b * st], dy = c[(3 * gr.a + 1) * st] - c[(3 * b + 1) * st],
-                        dz = c[(3 * gr.a + 2) * st] - c[(3 * b + 2) * st];
-            if (dx * dx + dy * dy + dz * dz <= P[p].thr2) atomicAdd(pair_hits + p, 1u);
-        }
-    }
+                                    reinterpret_cast<const BoxRec<float>*>(smem + M.off_boxes), M.box_base);
+    const HotRec<float>* P = reinterpret_cast<const HotRec<float>*>(smem + M.off_rest);
+    for (int p = 0; p < M.n_rest; ++p)
+        if (pair_hits<float>(P[p], c, st)) atomicAdd(pcount + p, 1u);
     const StaticSphereRec<float>* SS = reinterpret_cast<const StaticSphereRec<float>*>(smem + M.off_ssph);
     const StaticBoxRec<float>* SB = reinterpret_cast<const StaticBoxRec<float>*>(smem + M.off_sbox);
     for (int s = 0; s < M.n_spheres; ++s)
@@ -811,7 +862,7 @@ static int32_t calibrate_layout(ez_world* w, HModel& hm, const double* lower, co
         lh[k] = static_cast<float>(lower[k]);
         lh[dof + k] = static_cast<float>(upper[k]);
     }
-    const size_t np = std::max<size_t>(1, hm.pairs.size()), ns = std::max<size_t>(1, hm.spheres.size());
+    const size_t np = std::max<size_t>(1, hm.rest.size()), ns = std::max<size_t>(1, hm.spheres.size());
     float* d_lh = nullptr;
     uint32_t* d_cnt = nullptr;
     EZ_CUDA(cudaMalloc(&d_lh, sizeof(float) * 2 * dof));
@@ -844,7 +895,7 @@ static int32_t calibrate_layout(ez_world* w, HModel& hm, const double* lower, co
     }
     w->mf.blob = w->d_blob[0];
     w->md.blob = w->d_blob[1];
-    w->n_groups = static_cast<int32_t>(hm.groups.size());
+    w->n_blocks = static_cast<int32_t>(hm.blocks.size());
     w->n_hot = static_cast<int32_t>(hm.hot.size());
     return EZ_OK;
 }
@@ -1095,6 +1146,7 @@ extern "C" int32_t ez_world_create(const ez_robot_desc* rb, const ez_scene_desc*
             hm.mix.push_back(HMix{1, box_of[a], 1, box_of[b], 0.0});
         }
     }
+    hm.margin = margin;
     layout_pairs(hm, nullptr, nullptr);
     // static obstacles
     for (int i = 0; sc && i < sc->n_static; ++i) {
@@ -1120,7 +1172,7 @@ extern "C" int32_t ez_world_create(const ez_robot_desc* rb, const ez_scene_desc*
     w->n_joints = nj;
     w->n_spheres = static_cast<int32_t>(hm.spheres.size());
     w->n_pairs = static_cast<int32_t>(hm.all_pairs.size());
-    w->n_groups = static_cast<int32_t>(hm.groups.size());
+    w->n_blocks = static_cast<int32_t>(hm.blocks.size());
     w->n_ssph = static_cast<int32_t>(hm.ssph.size() / 4);
     w->n_sbox = static_cast<int32_t>(hm.sbox.size() / 15);
     w->n_store = hm.n_store;

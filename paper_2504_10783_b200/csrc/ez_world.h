@@ -13,7 +13,7 @@ struct ez_world {
     int32_t device = 0;
     int32_t num_sms = 148;
     int32_t smem_optin = 232448;  // max dynamic shared memory per CTA
-    int32_t dim = 3, dof = 0, n_joints = 0, n_spheres = 0, n_pairs = 0, n_groups = 0;
+    int32_t dim = 3, dof = 0, n_joints = 0, n_spheres = 0, n_pairs = 0, n_blocks = 0;
     int32_t n_ssph = 0, n_sbox = 0, n_store = 0, n_hot = 0;
     int64_t n_voxels = 0;
     double margin = 0.0;
