@@ -17,6 +17,7 @@ namespace ez {
 void set_error(const std::string& msg);
 int32_t fail(int32_t status, const std::string& msg);
 int32_t cuda_fail(cudaError_t err, const char* what, const char* file, int line);
+int32_t retain_async_pool();  // keep the current device's default mem pool cached
 
 #define EZ_CUDA(call)                                                        \
     do {                                                                     \

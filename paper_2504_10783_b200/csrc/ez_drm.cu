@@ -172,6 +172,7 @@ extern "C" int32_t ez_voxelize(const double* d_points, int64_t n, int32_t dim, c
     vp.dim = dim;
     int32_t* d_tmp = nullptr;   // bbox[6] + overflow
     int32_t* d_idx = nullptr;
+    EZ_TRY(retain_async_pool());
     EZ_CUDA(cudaMallocAsync(&d_tmp, sizeof(int32_t) * 8, s));
     EZ_CUDA(cudaMallocAsync(&d_idx, sizeof(int32_t) * n * dim, s));
     int32_t init[8] = {INT_MAX, INT_MIN, INT_MAX, INT_MIN, INT_MAX, INT_MIN, 0, 0};

@@ -42,8 +42,10 @@ __device__ __forceinline__ unsigned group_mask() {
     return ((1u << LPW) - 1u) << ((threadIdx.x & 31) & ~(LPW - 1));
 }
 
-template <int MAXD, int RNG, int LPW>
-__device__ __forceinline__ int hnr_walk(double (&x)[MAXD], int d, const double* __restrict__ A,
+// A: faces, row f at A + f * lda.  VEC: rows are 16-byte aligned with lda
+// even (shared-memory staging), so a row is read as double2 pairs.
+template <int MAXD, int RNG, int LPW, bool VEC>
+__device__ __forceinline__ int hnr_walk(double (&x)[MAXD], int d, const double* __restrict__ A, int lda,
                                         const double* __restrict__ b, int F, int n_ms, uint64_t seed,
                                         uint64_t walk, bool check_seed) {
     constexpr int PER = (MAXD + LPW - 1) / LPW;  // normals drawn per lane
@@ -113,17 +115,26 @@ __device__ __forceinline__ int hnr_walk(double (&x)[MAXD], int d, const double* 
         int outside = 0;
 #pragma unroll 2
         for (int f = lane; f < F; f += LPW) {
-            const double* a = A + static_cast<int64_t>(f) * d;
+            const double* a = A + static_cast<int64_t>(f) * lda;
             double g0 = 0.0, g1 = 0.0, h0 = 0.0, h1 = 0.0;
 #pragma unroll
             for (int k = 0; k < MAXD; k += 2) {
                 if (k < d) {
-                    g0 = fma(a[k], x[k], g0);
-                    h0 = fma(a[k], dir[k], h0);
-                }
-                if (k + 1 < d) {
-                    g1 = fma(a[k + 1], x[k + 1], g1);
-                    h1 = fma(a[k + 1], dir[k + 1], h1);
+                    double a0, a1;
+                    if (VEC) {
+                        const double2 v = *reinterpret_cast<const double2*>(a + k);
+                        a0 = v.x;
+                        a1 = v.y;
+                    } else {
+                        a0 = a[k];
+                        a1 = (k + 1 < d) ? a[k + 1] : 0.0;
+                    }
+                    g0 = fma(a0, x[k], g0);
+                    h0 = fma(a0, dir[k], h0);
+                    if (k + 1 < d) {
+                        g1 = fma(a1, x[k + 1], g1);
+                        h1 = fma(a1, dir[k + 1], h1);
+                    }
                 }
             }
             const double sl = b[f] - (g0 + g1);
@@ -166,26 +177,30 @@ __device__ __forceinline__ int hnr_walk(double (&x)[MAXD], int d, const double* 
 
 // Walk i starts at seeds[i % n_seeds] (explicit seeds) or at a point of the
 // segment v1 + alpha * e drawn from the (seed, walk, SEED_STEP) stream
-// (inflation.py:288-290).  F is read from F_dev when given (EI-ZO loop);
-// faces are staged in shared memory when F <= smem_faces.
-template <int MAXD, int RNG, int LPW>
-__global__ void __launch_bounds__(128)
+// (inflation.py:288-290).  F is read from F_dev when given (EI-ZO loop).
+// Faces are staged in shared memory when F <= smem_faces, with the padded
+// row stride lda (even, lda / 2 odd: the LPW lanes' double2 reads of
+// distinct rows fall in distinct bank groups); otherwise they are read from
+// L1/L2 with stride d.
+template <int MAXD, int RNG, int LPW, int BT>
+__global__ void __launch_bounds__(BT)
 k_hnr(const double* __restrict__ A, const double* __restrict__ b, const int32_t* __restrict__ F_dev, int F,
       int d, const double* __restrict__ seeds, int64_t n_seeds, const double* __restrict__ seg, int64_t count,
       int n_ms, uint64_t seed, uint64_t walk_offset, double* __restrict__ out, int32_t* __restrict__ status,
-      int smem_faces) {
-    extern __shared__ double s_faces[];
+      int smem_faces, int lda) {
+    extern __shared__ __align__(16) double s_faces[];
     if (F_dev) F = *F_dev;
     if (status[0] != EZ_OK || status[1] != 0) return;  // (status, stop)
     const bool staged = F <= smem_faces;
     if (staged) {
-        for (int i = threadIdx.x; i < F * d; i += blockDim.x) s_faces[i] = A[i];
-        for (int i = threadIdx.x; i < F; i += blockDim.x) s_faces[F * d + i] = b[i];
+        for (int i = threadIdx.x; i < F * lda; i += BT) {
+            const int f = i / lda, k = i - f * lda;
+            s_faces[i] = (k < d) ? A[static_cast<int64_t>(f) * d + k] : 0.0;
+        }
+        for (int i = threadIdx.x; i < F; i += BT) s_faces[F * lda + i] = b[i];
     }
     __syncthreads();
-    const double* AA = staged ? s_faces : A;
-    const double* bb = staged ? s_faces + F * d : b;
-    const int64_t i = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) / LPW;
+    const int64_t i = (static_cast<int64_t>(blockIdx.x) * BT + threadIdx.x) / LPW;
     if (i >= count) return;  // whole groups leave together
     const int lane = threadIdx.x & (LPW - 1);
     const uint64_t walk = walk_offset + static_cast<uint64_t>(i);
@@ -205,7 +220,9 @@ k_hnr(const double* __restrict__ A, const double* __restrict__ b, const int32_t*
 #pragma unroll
         for (int k = 0; k < MAXD; ++k) x[k] = (k < d) ? __dadd_rn(seg[k], __dmul_rn(alpha, seg[d + k])) : 0.0;
     }
-    const int st = hnr_walk<MAXD, RNG, LPW>(x, d, AA, bb, F, n_ms, seed, walk, seeds == nullptr);
+    const int st = staged ? hnr_walk<MAXD, RNG, LPW, true>(x, d, s_faces, lda, s_faces + F * lda, F, n_ms, seed, walk,
+                                                           seeds == nullptr)
+                          : hnr_walk<MAXD, RNG, LPW, false>(x, d, A, d, b, F, n_ms, seed, walk, seeds == nullptr);
     if (st != EZ_OK) {
         if (lane == 0) set_status(status, st);
         return;
@@ -214,6 +231,192 @@ k_hnr(const double* __restrict__ A, const double* __restrict__ b, const int32_t*
 #pragma unroll
     for (int k = 0; k < MAXD; ++k)
         if (k < d && (k % LPW) == lane) o[k] = x[k];
+}
+
+// ---------------------------------------------------------------------------
+// hit-and-run for large polytopes on the FP64 tensor cores.  Per mixing step
+// the chord data of a warp's 8 walks against all faces is one small GEMM:
+//     G'[f][w] = sum_k Ap[f][k] * xt_w[k],   H[f][w] = sum_k Ap[f][k] * dir_w[k]
+// with Ap = [A | -b | 0] (KP = 4 KC columns) and xt_w = [x_w | 1 | 0], so the
+// slack is b_f - a_f.x_w = -G'.  Each mma.sync.m8n8k4.f64 takes one A value
+// per lane (8 faces x 4 columns) and the walk fragments stay in registers, so
+// a face row is read once per 8 walks instead of once per walk (the
+// lane-per-face kernel above is shared-memory bound for large F).
+//
+// Fragment ownership (PTX m8n8k4 .row.col): lane = 4 wl + c holds x and dir
+// components k = 4 j + c of walk wl (the B fragments), and the C entries of
+// face wl of each 8-face tile for walks 2c and 2c + 1.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void dmma_8x8x4(double& c0, double& c1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                 : "+d"(c0), "+d"(c1) : "d"(a), "d"(b));
+}
+
+// Ap rows 0 .. ceil8(F) - 1 from (A, b); rows >= F are zero (inert faces:
+// h = 0 is masked out and the slack 0 is not "outside").
+__global__ void k_pack_faces(const double* __restrict__ A, const double* __restrict__ b,
+                             const int32_t* __restrict__ F_dev, int F, int d, int kp, double* __restrict__ Ap) {
+    if (F_dev) F = *F_dev;
+    const int rows = (F + 7) & ~7;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < rows * kp; i += gridDim.x * blockDim.x) {
+        const int f = i / kp, k = i - f * kp;
+        double v = 0.0;
+        if (f < F) v = (k < d) ? A[static_cast<int64_t>(f) * d + k] : (k == d ? -b[f] : 0.0);
+        Ap[i] = v;
+    }
+}
+
+__device__ __forceinline__ void chord_update(double sl, double h, double& hs, double& hh, double& ls, double& lh) {
+    if (h > kChordMask) {
+        if (sl * hh < hs * h) { hs = sl; hh = h; }
+    } else if (h < -kChordMask) {
+        if (sl * lh > ls * h) { ls = sl; lh = h; }
+    }
+}
+
+template <int KC>
+__global__ void __launch_bounds__(128)
+k_hnr_mma(const double* __restrict__ Ap, const int32_t* __restrict__ F_dev, int F, int d,
+          const double* __restrict__ seeds, int64_t n_seeds, const double* __restrict__ seg, int64_t count,
+          int n_ms, uint64_t seed, uint64_t walk_offset, double* __restrict__ out, int32_t* __restrict__ status) {
+    constexpr int KP = 4 * KC;
+    if (F_dev) F = *F_dev;
+    if (status[0] != EZ_OK || status[1] != 0) return;
+    const int lane = threadIdx.x & 31;
+    const int64_t wbase = ((static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5) * 8;
+    if (wbase >= count) return;  // warp-uniform
+    const int wl = lane >> 2, c = lane & 3;
+    const int64_t wi = min(wbase + wl, count - 1);  // idle slots shadow the last walk
+    const uint64_t key = walk_key(seed, walk_offset + static_cast<uint64_t>(wi));
+    // the walks whose C entries this lane owns
+    uint64_t skey[2];
+#pragma unroll
+    for (int s2 = 0; s2 < 2; ++s2)
+        skey[s2] = walk_key(seed, walk_offset + static_cast<uint64_t>(min(wbase + 2 * c + s2, count - 1)));
+    double x[KC], dr[KC];
+    if (seeds) {
+        const double* sp = seeds + (wi % n_seeds) * d;
+#pragma unroll
+        for (int j = 0; j < KC; ++j) {
+            const int k = 4 * j + c;
+            x[j] = (k < d) ? sp[k] : (k == d ? 1.0 : 0.0);
+        }
+    } else {
+        const double alpha = counter_uniform(key, kSeedStep, 0);
+#pragma unroll
+        for (int j = 0; j < KC; ++j) {
+            const int k = 4 * j + c;
+            x[j] = (k < d) ? __dadd_rn(seg[k], __dmul_rn(alpha, seg[d + k])) : (k == d ? 1.0 : 0.0);
+        }
+    }
+    const bool check_seed = seeds == nullptr;
+    const int tiles = (F + 7) >> 3;
+    const double* arow = Ap + static_cast<int64_t>(wl) * KP + c;
+    for (int step = 0; step < n_ms; ++step) {
+#pragma unroll
+        for (int j = 0; j < KC; ++j) {
+            const int k = 4 * j + c;
+            dr[j] = (k < d) ? counter_normal(key, static_cast<uint64_t>(step), k) : 0.0;
+        }
+        // numpy-order norm: squares summed left to right over k
+        double ss = 0.0;
+#pragma unroll
+        for (int k = 0; k < KP; ++k) {
+            const double v = __shfl_sync(0xffffffffu, dr[k >> 2], (lane & ~3) | (k & 3));
+            if (k < d) ss = __dadd_rn(ss, __dmul_rn(v, v));
+        }
+        const double nrm = sqrt(ss);
+#pragma unroll
+        for (int j = 0; j < KC; ++j)
+            if (4 * j + c < d) dr[j] = dr[j] / nrm;
+        double hs[2] = {INFINITY, INFINITY}, hh[2] = {1.0, 1.0}, ls[2] = {INFINITY, INFINITY}, lh[2] = {-1.0, -1.0};
+        bool outside = false;
+        int t = 0;
+        for (; t + 1 < tiles; t += 2) {
+            double g[2][2] = {{0.0, 0.0}, {0.0, 0.0}}, h[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+            const double* a0 = arow + static_cast<int64_t>(t) * 8 * KP;
+            const double* a1 = a0 + 8 * KP;
+#pragma unroll
+            for (int j = 0; j < KC; ++j) {
+                const double v0 = __ldg(a0 + 4 * j), v1 = __ldg(a1 + 4 * j);
+                dmma_8x8x4(g[0][0], g[0][1], v0, x[j]);
+                dmma_8x8x4(h[0][0], h[0][1], v0, dr[j]);
+                dmma_8x8x4(g[1][0], g[1][1], v1, x[j]);
+                dmma_8x8x4(h[1][0], h[1][1], v1, dr[j]);
+            }
+#pragma unroll
+            for (int u = 0; u < 2; ++u)
+#pragma unroll
+                for (int s2 = 0; s2 < 2; ++s2) {
+                    outside |= check_seed && step == 0 && g[u][s2] > kMemberTol;
+                    chord_update(-g[u][s2], h[u][s2], hs[s2], hh[s2], ls[s2], lh[s2]);
+                }
+        }
+        if (t < tiles) {
+            double g0 = 0.0, g1 = 0.0, h0 = 0.0, h1 = 0.0;
+            const double* a0 = arow + static_cast<int64_t>(t) * 8 * KP;
+#pragma unroll
+            for (int j = 0; j < KC; ++j) {
+                const double v0 = __ldg(a0 + 4 * j);
+                dmma_8x8x4(g0, g1, v0, x[j]);
+                dmma_8x8x4(h0, h1, v0, dr[j]);
+            }
+            outside |= check_seed && step == 0 && (g0 > kMemberTol || g1 > kMemberTol);
+            chord_update(-g0, h0, hs[0], hh[0], ls[0], lh[0]);
+            chord_update(-g1, h1, hs[1], hh[1], ls[1], lh[1]);
+        }
+        // reduce over the 8 face rows (lanes with the same c)
+#pragma unroll
+        for (int o = 4; o < 32; o <<= 1) {
+#pragma unroll
+            for (int s2 = 0; s2 < 2; ++s2) {
+                const double os = __shfl_xor_sync(0xffffffffu, hs[s2], o), oh = __shfl_xor_sync(0xffffffffu, hh[s2], o);
+                if (os * hh[s2] < hs[s2] * oh) { hs[s2] = os; hh[s2] = oh; }
+                const double qs = __shfl_xor_sync(0xffffffffu, ls[s2], o), qh = __shfl_xor_sync(0xffffffffu, lh[s2], o);
+                if (qs * lh[s2] > ls[s2] * qh) { ls[s2] = qs; lh[s2] = qh; }
+            }
+        }
+        const bool any_out = __any_sync(0xffffffffu, outside);
+        double tt[2];
+        int err = EZ_OK;
+#pragma unroll
+        for (int s2 = 0; s2 < 2; ++s2) {
+            double thi = hs[s2] / hh[s2];
+            double tlo = ls[s2] / lh[s2];
+            if (thi < tlo - kChordTol) err = EZ_EMPTY_CHORD;
+            tlo = fmin(tlo, 0.0);
+            thi = fmax(thi, 0.0);
+            const double u = counter_uniform(skey[s2], static_cast<uint64_t>(step), d);
+            tt[s2] = __dadd_rn(tlo, __dmul_rn(u, thi - tlo));
+        }
+        if (any_out) {
+            if (lane == 0) set_status(status, EZ_SEED_OUTSIDE);
+            return;
+        }
+        if (__any_sync(0xffffffffu, err != EZ_OK)) {
+            if (err != EZ_OK) set_status(status, err);
+            return;
+        }
+        // walk wl's step length lives in lanes with c == wl / 2, slot wl & 1
+        const double t0 = __shfl_sync(0xffffffffu, tt[0], wl >> 1), t1 = __shfl_sync(0xffffffffu, tt[1], wl >> 1);
+        const double mine = (wl & 1) ? t1 : t0;
+#pragma unroll
+        for (int j = 0; j < KC; ++j)
+            if (4 * j + c < d) x[j] = __dadd_rn(x[j], __dmul_rn(dr[j], mine));
+    }
+    if (wbase + wl < count) {
+        double* o = out + (wbase + wl) * d;
+#pragma unroll
+        for (int j = 0; j < KC; ++j)
+            if (4 * j + c < d) o[4 * j + c] = x[j];
+    }
+}
+
+// Ap geometry: KP columns (d + 1 rounded up to a multiple of 4 k-chunks),
+// rows padded to a multiple of 8
+static int hnr_mma_kp(int d) { return d < 8 ? 8 : (d < 16 ? 16 : 32); }
+static int64_t hnr_ap_words(int f_bound, int d) {
+    return static_cast<int64_t>((f_bound + 7) & ~7) * hnr_mma_kp(d);
 }
 
 // reference contains_many over all explicit seeds (cpoly.py:158-159)
@@ -512,6 +715,8 @@ struct ez_eizo_ws {
     int32_t f_cap = 0;      // faces
     double* A = nullptr;
     double* b = nullptr;
+    double* Ap = nullptr;   // padded faces for the tensor-core walk
+    int64_t ap_cap = 0;
     double* X = nullptr;
     uint8_t* flags = nullptr;
     int32_t* col = nullptr;
@@ -532,6 +737,7 @@ void eizo_ws_free(ez_eizo_ws* ws) {
     if (!ws) return;
     cudaFree(ws->A);
     cudaFree(ws->b);
+    cudaFree(ws->Ap);
     cudaFree(ws->X);
     cudaFree(ws->flags);
     cudaFree(ws->col);
@@ -602,44 +808,150 @@ static int32_t ws_reserve(ez_world* w, int d, int64_t n, int32_t c, int32_t f) {
         EZ_TRY(grow(&ws->b, ws->f_cap, f, true));
         ws->f_cap = f;
     }
+    if (hnr_ap_words(f, d) > ws->ap_cap) {
+        EZ_TRY(grow(&ws->Ap, 0, hnr_ap_words(f, d), false));
+        ws->ap_cap = hnr_ap_words(f, d);
+    }
     return EZ_OK;
 }
 
-template <int MAXD>
-static int32_t launch_hnr(int rng, cudaStream_t s, const double* A, const double* b, const int32_t* F_dev, int F,
-                          int f_bound, int d, const double* seeds, int64_t n_seeds, const double* seg, int64_t count,
-                          int n_ms, uint64_t seed, uint64_t walk_offset, double* out, int32_t* status) {
-    constexpr int LPW = MAXD;  // lanes per walk
+// padded shared-memory row stride: even, with an odd number of 16-byte units
+static int hnr_lda(int d) {
+    int l = d + (d & 1);
+    if ((l / 2) % 2 == 0) l += 2;
+    return l;
+}
+
+template <int MAXD, int RNG, int LPW, int BT>
+static int32_t launch_hnr_t(cudaStream_t s, const double* A, const double* b, const int32_t* F_dev,
+                            int F, int smem_faces, int d, const double* seeds, int64_t n_seeds, const double* seg,
+                            int64_t count, int n_ms, uint64_t seed, uint64_t walk_offset, double* out,
+                            int32_t* status) {
+    auto k = k_hnr<MAXD, RNG, LPW, BT>;
+    const int lda = hnr_lda(d);
+    const size_t smem = static_cast<size_t>(smem_faces) * (lda + 1) * sizeof(double);
+    if (smem > 48 * 1024) EZ_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     const int64_t threads = count * LPW;
-    const unsigned grid = static_cast<unsigned>((threads + 127) / 128);
-    const size_t per_face = static_cast<size_t>(d + 1) * sizeof(double);
-    int smem_faces = std::max(F, f_bound);
-    if (static_cast<size_t>(smem_faces) * per_face > 96 * 1024) smem_faces = 0;  // large polytopes: read from L1/L2
-    const size_t smem = static_cast<size_t>(smem_faces) * per_face;
-    if (rng == EZ_RNG_PHILOX) {
-        auto k = k_hnr<MAXD, EZ_RNG_PHILOX, LPW>;
-        if (smem > 48 * 1024) EZ_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
-        k<<<grid, 128, smem, s>>>(A, b, F_dev, F, d, seeds, n_seeds, seg, count, n_ms, seed, walk_offset, out, status,
-                                  smem_faces);
-    } else {
-        auto k = k_hnr<MAXD, EZ_RNG_COUNTER, LPW>;
-        if (smem > 48 * 1024) EZ_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
-        k<<<grid, 128, smem, s>>>(A, b, F_dev, F, d, seeds, n_seeds, seg, count, n_ms, seed, walk_offset, out, status,
-                                  smem_faces);
-    }
+    const unsigned grid = static_cast<unsigned>((threads + BT - 1) / BT);
+    k<<<grid, BT, smem, s>>>(A, b, F_dev, F, d, seeds, n_seeds, seg, count, n_ms, seed, walk_offset, out, status,
+                             smem_faces, lda);
     EZ_CUDA(cudaGetLastError());
     return EZ_OK;
 }
 
-// f_bound: largest face count the walk may see (faces live on the device in the EI-ZO loop)
-static int32_t dispatch_hnr(int rng, cudaStream_t s, const double* A, const double* b, const int32_t* F_dev, int F,
-                            int f_bound, int d, const double* seeds, int64_t n_seeds, const double* seg,
-                            int64_t count, int n_ms, uint64_t seed, uint64_t walk_offset, double* out,
-                            int32_t* status) {
-    if (d <= 4) return launch_hnr<4>(rng, s, A, b, F_dev, F, f_bound, d, seeds, n_seeds, seg, count, n_ms, seed, walk_offset, out, status);
-    if (d <= 8) return launch_hnr<8>(rng, s, A, b, F_dev, F, f_bound, d, seeds, n_seeds, seg, count, n_ms, seed, walk_offset, out, status);
-    if (d <= 16) return launch_hnr<16>(rng, s, A, b, F_dev, F, f_bound, d, seeds, n_seeds, seg, count, n_ms, seed, walk_offset, out, status);
-    if (d <= 32) return launch_hnr<32>(rng, s, A, b, F_dev, F, f_bound, d, seeds, n_seeds, seg, count, n_ms, seed, walk_offset, out, status);
+// Launch shape: lanes per walk (LPW), CTA size and face staging.  Each lane
+// owns every LPW-th face, so fewer lanes per walk means more walks read each
+// staged face row at once (less shared-memory traffic per FMA) but fewer
+// walks in flight.  Every candidate is costed as rounds of resident walks
+// (registers: 128 per lane; shared memory: the staged faces) times the
+// per-lane step cost (faces + normals + shuffle reductions); unstaged faces
+// are read through L1 at about 2.5x the cost.
+struct HnrShape {
+    int lpw, bt;
+    bool staged;
+};
+
+static HnrShape hnr_pick(int maxd, int d, int f, int64_t count, int num_sms, int optin) {
+    const HnrShape cands[5] = {{maxd, 128, true}, {maxd, 512, true}, {8, 512, true}, {4, 512, true}, {maxd, 128, false}};
+    const size_t smem = static_cast<size_t>(f) * (hnr_lda(d) + 1) * sizeof(double);
+    HnrShape best = {maxd, 128, false};
+    double best_t = 1e300;
+    for (const HnrShape& c : cands) {
+        if (c.lpw > maxd) continue;
+        if (c.bt == 512 && maxd > 16) continue;
+        if (c.lpw != maxd && !((c.lpw == 8 && maxd == 16) || (c.lpw == 4 && (maxd == 8 || maxd == 16)))) continue;
+        if (c.staged && smem > static_cast<size_t>(optin) - 2048) continue;
+        int per_sm = 65536 / (128 * c.bt);
+        if (c.staged) per_sm = std::min<int>(per_sm, static_cast<int>((228 * 1024) / (smem + 1024)));
+        if (per_sm < 1) continue;
+        const double walks = static_cast<double>(num_sms) * per_sm * (c.bt / c.lpw);
+        const double rounds = std::ceil(static_cast<double>(count) / walks);
+        const double face = std::ceil(static_cast<double>(f) / c.lpw) * (2.5 * d + 12.0) * (c.staged ? 1.0 : 2.5);
+        const double per_step = face + std::ceil(static_cast<double>(d) / c.lpw) * 180.0 +
+                                14.0 * std::log2(static_cast<double>(c.lpw)) + 60.0;
+        const double t = rounds * per_step;
+        if (t < best_t * 0.97) {
+            best_t = t;
+            best = c;
+        }
+    }
+    return best;
+}
+
+template <int MAXD>
+static int32_t launch_hnr(const ez_world* w, int rng, cudaStream_t s, const double* A, const double* b,
+                          const int32_t* F_dev, int F, int f_bound, int d, const double* seeds, int64_t n_seeds,
+                          const double* seg, int64_t count, int n_ms, uint64_t seed, uint64_t walk_offset, double* out,
+                          int32_t* status) {
+    int optin = 0, sms = 0;
+    if (w) {
+        optin = w->smem_optin;
+        sms = w->num_sms;
+    } else {
+        int dev = 0;
+        EZ_CUDA(cudaGetDevice(&dev));
+        cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    const int fmax = std::max(F, f_bound);
+    const HnrShape sh = hnr_pick(MAXD, d, fmax, count, sms, optin);
+    const int smem_faces = sh.staged ? fmax : 0;
+#define EZ_HNR_GO(LPW_, BT_)                                                                                      \
+    return (rng == EZ_RNG_PHILOX)                                                                                  \
+               ? launch_hnr_t<MAXD, EZ_RNG_PHILOX, LPW_, BT_>(s, A, b, F_dev, F, smem_faces, d, seeds, n_seeds,    \
+                                                               seg, count, n_ms, seed, walk_offset, out, status)    \
+               : launch_hnr_t<MAXD, EZ_RNG_COUNTER, LPW_, BT_>(s, A, b, F_dev, F, smem_faces, d, seeds, n_seeds,   \
+                                                                seg, count, n_ms, seed, walk_offset, out, status)
+    if constexpr (MAXD <= 16) {
+        if (sh.lpw == MAXD && sh.bt == 512) { EZ_HNR_GO(MAXD, 512); }
+    }
+    if constexpr (MAXD == 16 || MAXD == 8) {
+        if (sh.lpw == 4) { EZ_HNR_GO(4, 512); }
+        if constexpr (MAXD == 16) {
+            if (sh.lpw == 8) { EZ_HNR_GO(8, 512); }
+        }
+    }
+    EZ_HNR_GO(MAXD, 128);
+#undef EZ_HNR_GO
+}
+
+constexpr int kMmaFaces = 96;  // from this many faces on, walks run on the FP64 tensor cores
+
+template <int KC>
+static int32_t launch_hnr_mma(cudaStream_t s, const double* Ap, const int32_t* F_dev, int F, int d,
+                              const double* seeds, int64_t n_seeds, const double* seg, int64_t count, int n_ms,
+                              uint64_t seed, uint64_t walk_offset, double* out, int32_t* status) {
+    const int64_t warps = (count + 7) / 8;
+    k_hnr_mma<KC><<<static_cast<unsigned>((warps + 3) / 4), 128, 0, s>>>(Ap, F_dev, F, d, seeds, n_seeds, seg, count,
+                                                                          n_ms, seed, walk_offset, out, status);
+    EZ_CUDA(cudaGetLastError());
+    return EZ_OK;
+}
+
+// f_bound: largest face count the walk may see (faces live on the device in
+// the EI-ZO loop).  Ap: scratch of at least hnr_ap_words(f_bound, d) doubles
+// for the tensor-core path, or nullptr (allocated on the stream).
+static int32_t dispatch_hnr(const ez_world* w, int rng, cudaStream_t s, const double* A, const double* b,
+                            const int32_t* F_dev, int F, int f_bound, int d, const double* seeds, int64_t n_seeds,
+                            const double* seg, int64_t count, int n_ms, uint64_t seed, uint64_t walk_offset,
+                            double* out, int32_t* status, double* Ap = nullptr) {
+    const int fmax = std::max(F, f_bound);
+    if (rng == EZ_RNG_COUNTER && fmax >= kMmaFaces && d <= 31 && !getenv("EZ_HNR_NO_MMA")) {
+        const int kp = hnr_mma_kp(d);
+        double* ap = Ap;
+        if (!ap) EZ_CUDA(cudaMallocAsync(&ap, sizeof(double) * hnr_ap_words(fmax, d), s));
+        k_pack_faces<<<64, 256, 0, s>>>(A, b, F_dev, F, d, kp, ap);
+        int32_t st;
+        if (kp == 8) st = launch_hnr_mma<2>(s, ap, F_dev, F, d, seeds, n_seeds, seg, count, n_ms, seed, walk_offset, out, status);
+        else if (kp == 16) st = launch_hnr_mma<4>(s, ap, F_dev, F, d, seeds, n_seeds, seg, count, n_ms, seed, walk_offset, out, status);
+        else st = launch_hnr_mma<8>(s, ap, F_dev, F, d, seeds, n_seeds, seg, count, n_ms, seed, walk_offset, out, status);
+        if (!Ap) cudaFreeAsync(ap, s);
+        return st;
+    }
+    if (d <= 4) return launch_hnr<4>(w, rng, s, A, b, F_dev, F, f_bound, d, seeds, n_seeds, seg, count, n_ms, seed, walk_offset, out, status);
+    if (d <= 8) return launch_hnr<8>(w, rng, s, A, b, F_dev, F, f_bound, d, seeds, n_seeds, seg, count, n_ms, seed, walk_offset, out, status);
+    if (d <= 16) return launch_hnr<16>(w, rng, s, A, b, F_dev, F, f_bound, d, seeds, n_seeds, seg, count, n_ms, seed, walk_offset, out, status);
+    if (d <= 32) return launch_hnr<32>(w, rng, s, A, b, F_dev, F, f_bound, d, seeds, n_seeds, seg, count, n_ms, seed, walk_offset, out, status);
     return fail(EZ_UNSUPPORTED, "hit-and-run supports dimension <= 32");
 }
 
@@ -683,10 +995,11 @@ extern "C" int32_t ez_hit_and_run(const double* d_A, const double* d_b, int32_t 
     if (rng != EZ_RNG_COUNTER && rng != EZ_RNG_PHILOX) return fail(EZ_INVALID_ARGUMENT, "unknown rng");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     int32_t* d_status = nullptr;
+    EZ_TRY(retain_async_pool());
     EZ_CUDA(cudaMallocAsync(&d_status, 2 * sizeof(int32_t), s));  // (status, stop)
     EZ_CUDA(cudaMemsetAsync(d_status, 0, 2 * sizeof(int32_t), s));
     k_seed_check<<<static_cast<unsigned>((n_seeds + 127) / 128), 128, 0, s>>>(d_A, d_b, n_faces, dim, d_seeds, n_seeds, d_status);
-    int32_t st = dispatch_hnr(rng, s, d_A, d_b, nullptr, n_faces, n_faces, dim, d_seeds, n_seeds, nullptr, count, n_ms,
+    int32_t st = dispatch_hnr(nullptr, rng, s, d_A, d_b, nullptr, n_faces, n_faces, dim, d_seeds, n_seeds, nullptr, count, n_ms,
                               seed, walk_offset, d_out, d_status);
     int32_t h_status = 0;
     if (st == EZ_OK) {
@@ -776,8 +1089,8 @@ extern "C" int32_t ez_inflate_edge(ez_world* w, const double* h_v1, const double
         const int64_t n_s = std::max<int64_t>(p.n_p, m);
         int32_t* it = ws->rec + slot_offset(k);
         EZ_CUDA(cudaMemsetAsync(it, 0, 8 * sizeof(int32_t), s));
-        EZ_TRY(dispatch_hnr(rng, s, ws->A, ws->b, ws->rec + kFaces, f_known, f_known + 2 * p.n_f, d, nullptr, 1,
-                            ws->seg, n_s, p.n_ms, seed, woff, ws->X, ws->rec + kStatus));
+        EZ_TRY(dispatch_hnr(w, rng, s, ws->A, ws->b, ws->rec + kFaces, f_known, f_known + 2 * p.n_f, d, nullptr, 1,
+                            ws->seg, n_s, p.n_ms, seed, woff, ws->X, ws->rec + kStatus, ws->Ap));
         EZ_TRY(launch_check(w, ws->X, EZ_F64, n_s, d, ws->flags, precision, s, m, it + kColM));
         k_compact<<<1, 1024, 0, s>>>(ws->flags, n_s, p.n_p, thr, ws->rec, it, ws->col);
         EZ_CUDA(cudaGetLastError());

@@ -1029,6 +1029,7 @@ extern "C" int32_t ez_world_create(const ez_robot_desc* rb, const ez_scene_desc*
     if (rb->n_geoms > kMaxSpheres) return fail(EZ_UNSUPPORTED, "more than 1024 robot geometries");
     if (margin < 0.0) return fail(EZ_INVALID_ARGUMENT, "margin must be >= 0");
     EZ_CUDA(cudaSetDevice(device));
+    EZ_TRY(retain_async_pool());
 
     HModel hm;
     const int nj = rb->n_joints;

@@ -73,3 +73,53 @@ def test_many_faces_high_dim():
     poly = HPolytope(A, np.full(200, 0.5))
     sb = hit_and_run_sample(poly, np.zeros((1, d)), 5000, 40, seed=3)
     assert np.max(sb.points @ poly.A.T - poly.b) <= 1e-9
+
+
+# --- large polytopes: the FP64 tensor-core walk (k_hnr_mma, F >= 96 faces) ---------------
+
+def _random_poly(d, n_faces, seed, r=0.5):
+    rng = np.random.default_rng(seed)
+    A = rng.normal(size=(n_faces, d))
+    A /= np.linalg.norm(A, axis=1, keepdims=True)
+    return HPolytope(A, np.full(n_faces, r))
+
+
+@pytest.mark.parametrize("d,n_faces", [(7, 120), (14, 300), (20, 150)])
+def test_mma_walk_matches_oracle(d, n_faces):
+    from oracle import ref
+    poly = _random_poly(d, n_faces, seed=d)
+    seeds = np.zeros((1, d))
+    sb = hit_and_run_sample(poly, seeds, 257, 12, seed=5, walk_offset=3)
+    X = ref.hit_and_run(poly.A, poly.b, seeds, 257, 12, 5, walk_offset=3)
+    # rounding-level differences in the face sums only (tolerance as the goldens above)
+    assert np.max(np.abs(sb.points - X)) <= 1e-9
+    assert np.max(sb.points @ poly.A.T - poly.b) <= 1e-9
+
+
+def test_mma_walk_agrees_with_lane_walk(monkeypatch):
+    poly = _random_poly(14, 400, seed=2)
+    seeds = np.zeros((1, 14))
+    a = hit_and_run_sample(poly, seeds, 3000, 30, seed=8)
+    monkeypatch.setenv("EZ_HNR_NO_MMA", "1")
+    b = hit_and_run_sample(poly, seeds, 3000, 30, seed=8)
+    assert np.max(np.abs(a.points - b.points)) <= 1e-9
+
+
+def test_mma_walk_partition_invariance():
+    poly = _random_poly(14, 200, seed=3)
+    seeds = np.zeros((1, 14))
+    a = hit_and_run_sample(poly, seeds, 1000, 10, seed=77)
+    first = hit_and_run_sample(poly, seeds, 333, 10, seed=77, walk_offset=0)
+    second = hit_and_run_sample(poly, seeds, 667, 10, seed=77, walk_offset=333)
+    assert np.array_equal(np.vstack([first.points, second.points]), a.points)
+
+
+def test_mma_walk_errors():
+    poly = _random_poly(14, 128, seed=4)
+    with pytest.raises(SeedOutside):
+        hit_and_run_sample(poly, np.full((1, 14), 5.0), 10, 5, seed=0)
+    # two opposite faces leave an empty slab (x_0 <= -1e-10 and -x_0 <= -1e-10)
+    A = np.vstack([poly.A, np.eye(14)[:1], -np.eye(14)[:1]])
+    b = np.concatenate([poly.b, [-1e-10, -1e-10]])
+    with pytest.raises(EmptyChord):
+        hit_and_run_sample(HPolytope(A, b), np.zeros((1, 14)), 10, 5, seed=0)

@@ -1,0 +1,19 @@
+"""Profiling driver: config 4 (14-DOF bimanual) EI-ZO single-segment region, once or repeated."""
+import sys, time
+from pathlib import Path
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+from paper_2504_10783_b200 import fixtures as fx
+from paper_2504_10783_b200.eizo import InflationParams, Segment, inflate_edge
+from paper_2504_10783_b200.polytope import HPolytope
+
+w = fx.bimanual14_world()
+v1, v2 = fx.random_free_segment(w, seed=3)
+dom = HPolytope.from_bounds(w.lower, w.upper)
+p = InflationParams(**fx.FRANKA_PARAMS)
+reps = int(sys.argv[1]) if len(sys.argv) > 1 else 1
+ck = w.checker()
+for s in range(reps):
+    t0 = time.perf_counter()
+    r = inflate_edge(Segment(v1, v2), dom, p, ck, seed=7)
+    print(f"region {s}: {1e3*(time.perf_counter()-t0):.2f} ms wall, {r.device_ms:.2f} ms device, "
+          f"it={r.iterations} faces={r.hyperplanes_added} checks={r.collision_checks}", flush=True)
