@@ -275,7 +275,7 @@ __device__ __forceinline__ void chord_update(double sl, double h, double& hs, do
 }
 
 template <int KC>
-__global__ void __launch_bounds__(128)
+__global__ void __launch_bounds__(64, KC >= 8 ? 8 : 11)
 k_hnr_mma(const double* __restrict__ Ap, const int32_t* __restrict__ F_dev, int F, int d,
           const double* __restrict__ seeds, int64_t n_seeds, const double* __restrict__ seg, int64_t count,
           int n_ms, uint64_t seed, uint64_t walk_offset, double* __restrict__ out, int32_t* __restrict__ status) {
@@ -331,19 +331,29 @@ k_hnr_mma(const double* __restrict__ Ap, const int32_t* __restrict__ F_dev, int 
             if (4 * j + c < d) dr[j] = dr[j] / nrm;
         double hs[2] = {INFINITY, INFINITY}, hh[2] = {1.0, 1.0}, ls[2] = {INFINITY, INFINITY}, lh[2] = {-1.0, -1.0};
         bool outside = false;
-        int t = 0;
-        for (; t + 1 < tiles; t += 2) {
+        // two 8-face tiles per round, the next round's A fragments loaded
+        // ahead (L1 latency hidden behind the current round's MMAs)
+        double va[2][KC], vn[2][KC];
+#pragma unroll
+        for (int u = 0; u < 2; ++u)
+#pragma unroll
+            for (int j = 0; j < KC; ++j)
+                va[u][j] = (u < tiles) ? __ldg(arow + static_cast<int64_t>(u) * 8 * KP + 4 * j) : 0.0;
+        for (int t = 0; t < tiles; t += 2) {
+#pragma unroll
+            for (int u = 0; u < 2; ++u)
+#pragma unroll
+                for (int j = 0; j < KC; ++j)
+                    vn[u][j] = (t + 2 + u < tiles) ? __ldg(arow + static_cast<int64_t>(t + 2 + u) * 8 * KP + 4 * j) : 0.0;
             double g[2][2] = {{0.0, 0.0}, {0.0, 0.0}}, h[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
-            const double* a0 = arow + static_cast<int64_t>(t) * 8 * KP;
-            const double* a1 = a0 + 8 * KP;
 #pragma unroll
             for (int j = 0; j < KC; ++j) {
-                const double v0 = __ldg(a0 + 4 * j), v1 = __ldg(a1 + 4 * j);
-                dmma_8x8x4(g[0][0], g[0][1], v0, x[j]);
-                dmma_8x8x4(h[0][0], h[0][1], v0, dr[j]);
-                dmma_8x8x4(g[1][0], g[1][1], v1, x[j]);
-                dmma_8x8x4(h[1][0], h[1][1], v1, dr[j]);
+                dmma_8x8x4(g[0][0], g[0][1], va[0][j], x[j]);
+                dmma_8x8x4(h[0][0], h[0][1], va[0][j], dr[j]);
+                dmma_8x8x4(g[1][0], g[1][1], va[1][j], x[j]);
+                dmma_8x8x4(h[1][0], h[1][1], va[1][j], dr[j]);
             }
+            // a tile past the end has zero rows: h = 0 is masked, g = 0 is not outside
 #pragma unroll
             for (int u = 0; u < 2; ++u)
 #pragma unroll
@@ -351,19 +361,10 @@ k_hnr_mma(const double* __restrict__ Ap, const int32_t* __restrict__ F_dev, int 
                     outside |= check_seed && step == 0 && g[u][s2] > kMemberTol;
                     chord_update(-g[u][s2], h[u][s2], hs[s2], hh[s2], ls[s2], lh[s2]);
                 }
-        }
-        if (t < tiles) {
-            double g0 = 0.0, g1 = 0.0, h0 = 0.0, h1 = 0.0;
-            const double* a0 = arow + static_cast<int64_t>(t) * 8 * KP;
 #pragma unroll
-            for (int j = 0; j < KC; ++j) {
-                const double v0 = __ldg(a0 + 4 * j);
-                dmma_8x8x4(g0, g1, v0, x[j]);
-                dmma_8x8x4(h0, h1, v0, dr[j]);
-            }
-            outside |= check_seed && step == 0 && (g0 > kMemberTol || g1 > kMemberTol);
-            chord_update(-g0, h0, hs[0], hh[0], ls[0], lh[0]);
-            chord_update(-g1, h1, hs[1], hh[1], ls[1], lh[1]);
+            for (int u = 0; u < 2; ++u)
+#pragma unroll
+                for (int j = 0; j < KC; ++j) va[u][j] = vn[u][j];
         }
         // reduce over the 8 face rows (lanes with the same c)
 #pragma unroll
@@ -922,7 +923,7 @@ static int32_t launch_hnr_mma(cudaStream_t s, const double* Ap, const int32_t* F
                               const double* seeds, int64_t n_seeds, const double* seg, int64_t count, int n_ms,
                               uint64_t seed, uint64_t walk_offset, double* out, int32_t* status) {
     const int64_t warps = (count + 7) / 8;
-    k_hnr_mma<KC><<<static_cast<unsigned>((warps + 3) / 4), 128, 0, s>>>(Ap, F_dev, F, d, seeds, n_seeds, seg, count,
+    k_hnr_mma<KC><<<static_cast<unsigned>((warps + 1) / 2), 64, 0, s>>>(Ap, F_dev, F, d, seeds, n_seeds, seg, count,
                                                                           n_ms, seed, walk_offset, out, status);
     EZ_CUDA(cudaGetLastError());
     return EZ_OK;
