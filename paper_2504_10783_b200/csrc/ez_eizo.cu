@@ -266,12 +266,22 @@ __global__ void k_pack_faces(const double* __restrict__ A, const double* __restr
     }
 }
 
-__device__ __forceinline__ void chord_update(double sl, double h, double& hs, double& hh, double& ls, double& lh) {
-    if (h > kChordMask) {
-        if (sl * hh < hs * h) { hs = sl; hh = h; }
-    } else if (h < -kChordMask) {
-        if (sl * lh > ls * h) { ls = sl; lh = h; }
-    }
+// Running chord ends with the lower end folded onto the upper one: both keep
+// min of sl / |h| as a fraction (S, H), H > 0, over faces with h > mask (hi)
+// or h < -mask (lo); t_hi = S0 / H0, t_lo = -S1 / H1.  The comparisons are
+// the same products as the lane walk's (sl * lo_h > lo_s * h with
+// lo_h = -H1), so the selected faces are identical; branch-free, so lanes
+// with opposite signs of h do not diverge.
+__device__ __forceinline__ void chord_update(double sl, double h, double (&S)[2], double (&H)[2]) {
+    const bool neg = h < 0.0;
+    const double ah = fabs(h);
+    const double sc = neg ? S[1] : S[0], hc = neg ? H[1] : H[0];
+    const bool take = (ah > kChordMask) && (sl * hc < sc * ah);
+    const bool t0 = take && !neg, t1 = take && neg;
+    S[0] = t0 ? sl : S[0];
+    H[0] = t0 ? ah : H[0];
+    S[1] = t1 ? sl : S[1];
+    H[1] = t1 ? ah : H[1];
 }
 
 template <int KC>
@@ -329,7 +339,7 @@ k_hnr_mma(const double* __restrict__ Ap, const int32_t* __restrict__ F_dev, int 
 #pragma unroll
         for (int j = 0; j < KC; ++j)
             if (4 * j + c < d) dr[j] = dr[j] / nrm;
-        double hs[2] = {INFINITY, INFINITY}, hh[2] = {1.0, 1.0}, ls[2] = {INFINITY, INFINITY}, lh[2] = {-1.0, -1.0};
+        double cs[2][2] = {{INFINITY, INFINITY}, {INFINITY, INFINITY}}, ch[2][2] = {{1.0, 1.0}, {1.0, 1.0}};  // [slot][hi/lo]
         bool outside = false;
         // two 8-face tiles per round, the next round's A fragments loaded
         // ahead (L1 latency hidden behind the current round's MMAs)
@@ -359,7 +369,7 @@ k_hnr_mma(const double* __restrict__ Ap, const int32_t* __restrict__ F_dev, int 
 #pragma unroll
                 for (int s2 = 0; s2 < 2; ++s2) {
                     outside |= check_seed && step == 0 && g[u][s2] > kMemberTol;
-                    chord_update(-g[u][s2], h[u][s2], hs[s2], hh[s2], ls[s2], lh[s2]);
+                    chord_update(-g[u][s2], h[u][s2], cs[s2], ch[s2]);
                 }
 #pragma unroll
             for (int u = 0; u < 2; ++u)
@@ -370,20 +380,21 @@ k_hnr_mma(const double* __restrict__ Ap, const int32_t* __restrict__ F_dev, int 
 #pragma unroll
         for (int o = 4; o < 32; o <<= 1) {
 #pragma unroll
-            for (int s2 = 0; s2 < 2; ++s2) {
-                const double os = __shfl_xor_sync(0xffffffffu, hs[s2], o), oh = __shfl_xor_sync(0xffffffffu, hh[s2], o);
-                if (os * hh[s2] < hs[s2] * oh) { hs[s2] = os; hh[s2] = oh; }
-                const double qs = __shfl_xor_sync(0xffffffffu, ls[s2], o), qh = __shfl_xor_sync(0xffffffffu, lh[s2], o);
-                if (qs * lh[s2] > ls[s2] * qh) { ls[s2] = qs; lh[s2] = qh; }
-            }
+            for (int s2 = 0; s2 < 2; ++s2)
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    const double os = __shfl_xor_sync(0xffffffffu, cs[s2][e], o);
+                    const double oh = __shfl_xor_sync(0xffffffffu, ch[s2][e], o);
+                    if (os * ch[s2][e] < cs[s2][e] * oh) { cs[s2][e] = os; ch[s2][e] = oh; }
+                }
         }
         const bool any_out = __any_sync(0xffffffffu, outside);
         double tt[2];
         int err = EZ_OK;
 #pragma unroll
         for (int s2 = 0; s2 < 2; ++s2) {
-            double thi = hs[s2] / hh[s2];
-            double tlo = ls[s2] / lh[s2];
+            double thi = cs[s2][0] / ch[s2][0];
+            double tlo = -(cs[s2][1] / ch[s2][1]);
             if (thi < tlo - kChordTol) err = EZ_EMPTY_CHORD;
             tlo = fmin(tlo, 0.0);
             thi = fmax(thi, 0.0);
