@@ -1002,10 +1002,9 @@ using namespace ez;
 
 static void world_free(ez_world* w) {
     if (!w) return;
-    for (int i = 0; i < 2; ++i) {
-        cudaFree(w->d_blob[i]);
+    for (int i = 0; i < 2; ++i) cudaFree(w->d_blob[i]);
+    for (int i = 0; i < ez_world::kHostStages; ++i) {
         if (w->hstream[i]) cudaStreamDestroy(w->hstream[i]);
-        if (w->hevent[i]) cudaEventDestroy(w->hevent[i]);
         cudaFreeHost(w->h_stage_in[i]);
         cudaFreeHost(w->h_stage_out[i]);
         cudaFree(w->d_stage_in[i]);
@@ -1260,9 +1259,17 @@ extern "C" int32_t ez_check_batch_host(ez_world* w, const double* h_q, int64_t n
     std::lock_guard<std::mutex> lock(w->mu);
     EZ_CUDA(cudaSetDevice(w->device));
     const int dof = w->dof;
-    const int64_t chunk = 1 << 16;
+    // Chunks of `chunk` rows rotate over kHostStages streams: the H2D copy of
+    // one chunk overlaps the check and D2H of the previous ones, so the call
+    // runs at the PCIe rate of the fp64 input.
+    constexpr int NS = ez_world::kHostStages;
+    static const int64_t chunk = [] {
+        const char* e = getenv("EZ_HOST_CHUNK");
+        const int64_t v = e ? atoll(e) : 0;
+        return v >= 1024 ? v : int64_t(1) << 16;
+    }();
     if (w->stage_rows < chunk) {
-        for (int i = 0; i < 2; ++i) {
+        for (int i = 0; i < NS; ++i) {
             cudaFreeHost(w->h_stage_in[i]);
             cudaFreeHost(w->h_stage_out[i]);
             cudaFree(w->d_stage_in[i]);
@@ -1274,7 +1281,6 @@ extern "C" int32_t ez_check_batch_host(ez_world* w, const double* h_q, int64_t n
             EZ_CUDA(cudaMalloc(&w->d_stage_in[i], sizeof(double) * chunk * dof));
             EZ_CUDA(cudaMalloc(reinterpret_cast<void**>(&w->d_stage_out[i]), chunk));
             if (!w->hstream[i]) EZ_CUDA(cudaStreamCreateWithFlags(&w->hstream[i], cudaStreamNonBlocking));
-            if (!w->hevent[i]) EZ_CUDA(cudaEventCreateWithFlags(&w->hevent[i], cudaEventDisableTiming));
         }
         w->stage_rows = chunk;
     }
@@ -1284,9 +1290,10 @@ extern "C" int32_t ez_check_batch_host(ez_world* w, const double* h_q, int64_t n
     bool pinned_out = cudaPointerGetAttributes(&attr, h_free) == cudaSuccess && attr.type == cudaMemoryTypeHost;
     cudaGetLastError();
     const int64_t nchunks = (n + chunk - 1) / chunk;
-    int64_t pending_out[2] = {-1, -1};  // chunk index whose result sits in h_stage_out[b]
+    int64_t pending_out[NS];  // chunk index whose result sits in h_stage_out[b]
+    for (int b = 0; b < NS; ++b) pending_out[b] = -1;
     for (int64_t c = 0; c < nchunks; ++c) {
-        const int b = static_cast<int>(c & 1);
+        const int b = static_cast<int>(c % NS);
         cudaStream_t s = w->hstream[b];
         const int64_t r0 = c * chunk;
         const int64_t rows = std::min(chunk, n - r0);
@@ -1321,7 +1328,7 @@ extern "C" int32_t ez_check_batch_host(ez_world* w, const double* h_q, int64_t n
             pending_out[b] = c;
         }
     }
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < NS; ++b) {
         EZ_CUDA(cudaStreamSynchronize(w->hstream[b]));
         if (pending_out[b] >= 0) {
             const int64_t pr0 = pending_out[b] * chunk;

@@ -37,12 +37,12 @@ struct ez_world {
 
     // host-buffer check pipeline
     std::mutex mu;
-    cudaStream_t hstream[2] = {nullptr, nullptr};
-    cudaEvent_t hevent[2] = {nullptr, nullptr};
-    void* h_stage_in[2] = {nullptr, nullptr};
-    uint8_t* h_stage_out[2] = {nullptr, nullptr};
-    void* d_stage_in[2] = {nullptr, nullptr};
-    uint8_t* d_stage_out[2] = {nullptr, nullptr};
+    static constexpr int kHostStages = 4;
+    cudaStream_t hstream[kHostStages] = {};
+    void* h_stage_in[kHostStages] = {};
+    uint8_t* h_stage_out[kHostStages] = {};
+    void* d_stage_in[kHostStages] = {};
+    uint8_t* d_stage_out[kHostStages] = {};
     int64_t stage_rows = 0;
 
     ez_eizo_ws* eizo = nullptr;
