@@ -20,7 +20,9 @@
 #ifndef CORRIDOR_B200_H
 #define CORRIDOR_B200_H
 
+#ifndef __CUDACC_RTC__
 #include <stdint.h>
+#endif
 
 #ifdef __cplusplus
 extern "C" {
@@ -120,6 +122,7 @@ typedef struct ez_eizo_report {
     double device_ms;             /* GPU time of the whole inflation         */
 } ez_eizo_report;
 
+#ifndef __CUDACC_RTC__ /* the run-time compiled kernels need the types only */
 /* ---------------- library ---------------- */
 int32_t ez_abi_version(void);
 const char* ez_last_error(void);
@@ -137,6 +140,16 @@ int32_t ez_world_create(const ez_robot_desc* robot, const ez_scene_desc* scene,
                         double margin, int32_t device, ez_world** out);
 int32_t ez_world_destroy(ez_world* world);
 int32_t ez_world_get_info(const ez_world* world, ez_world_info* out);
+
+/* Model-specialised fp32 check kernel (no reference counterpart: the
+ * reference's _check_chunk, world.py:505-517, interprets the model per call).
+ * mode 1: generate CUDA for this world's robot model (literal constants,
+ * straight-line FK and pair tests), compile it with NVRTC for sm_100a and use
+ * it for fp32 batches; mode 0: query only; mode -1: go back to the generic
+ * kernel for good.  Returns EZ_OK if the specialised kernel is in use,
+ * EZ_UNSUPPORTED if it is not (robot boxes, NVRTC missing, disabled).
+ * fp32 batches of >= 2^18 rows specialise automatically unless EZ_JIT=0. */
+int32_t ez_world_specialize(ez_world* world, int32_t mode);
 
 /* Free mask (1 = collision-free) for n configurations.  d_q points at n rows
  * of `dof` values of type q_dtype with row stride ld (elements).  precision
@@ -232,6 +245,7 @@ int32_t ez_roadmap_export(const ez_roadmap* roadmap, int64_t* h_offsets, int32_t
 int32_t ez_collision_set(ez_roadmap* roadmap, const int32_t* d_vox_idx, int64_t n_vox,
                          const double* h_vmap_origin, double vmap_side, int32_t same_grid,
                          uint32_t* d_blocked_bits, int64_t* n_blocked, void* stream);
+#endif /* __CUDACC_RTC__ */
 
 #ifdef __cplusplus
 }

@@ -62,6 +62,7 @@ SIGNATURES = {
     "ez_world_create": (c_i32, [C.POINTER(RobotDesc), C.POINTER(SceneDesc), c_dbl, c_i32, C.POINTER(c_vp)]),
     "ez_world_destroy": (c_i32, [c_vp]),
     "ez_world_get_info": (c_i32, [c_vp, C.POINTER(WorldInfo)]),
+    "ez_world_specialize": (c_i32, [c_vp, c_i32]),
     "ez_check_batch": (c_i32, [c_vp, c_vp, c_i32, c_i64, c_i64, c_vp, c_i32, c_vp]),
     "ez_check_batch_host": (c_i32, [c_vp, c_vp, c_i64, c_i64, c_vp, c_i32]),
     "ez_fk_batch": (c_i32, [c_vp, c_vp, c_i64, c_vp, c_vp]),

@@ -1,0 +1,153 @@
+// ez_check_core.cuh — the tile loop of the fused FK + collision check,
+// shared by the generic kernel (model read from the staged blob) and the
+// per-model kernels compiled at run time (ez_jit.cu).  Replaces
+// corridor/world.py:483-517 (check_batch / _check_chunk).
+//
+// Two phases per tile of BT configurations:
+//   A) every thread: FK + the calibrated hot self pairs.  Most colliding
+//      configurations are decided here.
+//   B) survivors are appended (in index order) to a CTA ring buffer; whenever
+//      a full CTA's worth is queued, every thread takes one, reloads its row,
+//      recomputes FK and runs the obstacle tests and remaining pairs.  Phase
+//      B therefore always runs on full warps and no warp idles at a barrier
+//      while a few lanes finish the expensive tail.
+//
+// A policy P supplies the model:
+//   bool a(const Q* row, T* cen) const   phase A, true = collides
+//   bool b(const Q* row, T* cen) const   phase B, true = collides
+// `row` is the thread's staged configuration, `cen` its centre store
+// (element k at cen[k * BT]).
+#pragma once
+
+#include "ez_device.cuh"
+
+namespace ez {
+
+constexpr int kPrefetch = 8;  // registers per thread for the next tile's rows (dof*BT/BT <= 8)
+
+template <typename T, typename Q, int BT, class P>
+__device__ __forceinline__ void check_phase_b(const P& pol, int dof, const Q* __restrict__ q, int64_t ld, int64_t idx,
+                                              Q* row, T* cen, uint8_t* __restrict__ out, int64_t count_lim,
+                                              int32_t* n_col) {
+    Q v[32];
+#pragma unroll
+    for (int k = 0; k < 32; ++k)
+        if (k < dof) v[k] = q[idx * ld + k];
+#pragma unroll
+    for (int k = 0; k < 32; ++k)
+        if (k < dof) row[k] = v[k];
+    const bool c2 = pol.b(row, cen);
+    out[idx] = c2 ? 0 : 1;
+    if (n_col != nullptr && c2 && idx < count_lim) atomicAdd(n_col, 1);
+}
+
+// rows: BT * dof staging slots in shared memory; s_queue: 2 * BT entries;
+// s_warp: BT / 32 entries; cen: this thread's centre store.
+template <typename T, typename Q, int BT, class P>
+__device__ __forceinline__ void check_tiles(const P& pol, int dof, T* my_cen, Q* rows, int32_t* s_queue, int* s_warp,
+                                            const Q* __restrict__ q, int64_t n, int64_t ld,
+                                            uint8_t* __restrict__ out, int64_t count_lim, int32_t* __restrict__ n_col) {
+    constexpr int qcap = 2 * BT;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    Q* my_row = rows + threadIdx.x * dof;
+    const bool contiguous = (ld == dof) && (dof <= kPrefetch);
+    int qhead = 0, qn = 0;  // ring buffer state (uniform across the CTA)
+    const int64_t tiles = (n + BT - 1) / BT;
+    Q pf[kPrefetch];
+    auto prefetch = [&](int64_t tile) {
+        if (tile >= tiles) return;
+        const int64_t base = tile * BT;
+        const int tot = static_cast<int>(min(static_cast<int64_t>(BT), n - base)) * dof;
+        const Q* src = q + base * dof;
+#pragma unroll
+        for (int j = 0; j < kPrefetch; ++j) {
+            const int i = threadIdx.x + j * BT;
+            if (i < tot) pf[j] = src[i];
+        }
+    };
+    if (contiguous) prefetch(blockIdx.x);
+    for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+        const int64_t base = tile * BT;
+        const int nr = static_cast<int>(min(static_cast<int64_t>(BT), n - base));
+        __syncthreads();
+        if (contiguous) {
+            const int tot = nr * dof;
+#pragma unroll
+            for (int j = 0; j < kPrefetch; ++j) {
+                const int i = threadIdx.x + j * BT;
+                if (i < tot) rows[i] = pf[j];
+            }
+        } else {
+            for (int i = threadIdx.x; i < nr * dof; i += BT) {
+                const int r = i / dof, k = i - r * dof;
+                rows[i] = q[(base + r) * ld + k];
+            }
+        }
+        __syncthreads();
+        if (contiguous) prefetch(tile + gridDim.x);  // lands while this tile is checked
+        // phase A
+        const bool valid = threadIdx.x < nr;
+        bool col = false;
+        if (valid) {
+            col = pol.a(my_row, my_cen);
+            if (col) out[base + threadIdx.x] = 0;
+        }
+        if (n_col != nullptr) {
+            const unsigned m = __ballot_sync(0xffffffffu, col && (base + threadIdx.x) < count_lim);
+            if (lane == 0 && m) atomicAdd(n_col, __popc(m));
+        }
+        // append the survivors to the queue, in index order
+        const bool surv = valid && !col;
+        const unsigned sm = __ballot_sync(0xffffffffu, surv);
+        if (lane == 0) s_warp[wid] = __popc(sm);
+        __syncthreads();
+        int off = 0, add = 0;
+#pragma unroll
+        for (int w = 0; w < BT / 32; ++w) {
+            const int c = s_warp[w];
+            off += (w < wid) ? c : 0;
+            add += c;
+        }
+        if (surv)
+            s_queue[(qhead + qn + off + __popc(sm & ((1u << lane) - 1u))) % qcap] = static_cast<int32_t>(base + threadIdx.x);
+        qn += add;
+        __syncthreads();
+        // phase B on full CTAs; after the last tile, the partial rest
+        const bool last = tile + gridDim.x >= tiles;
+        while (qn >= BT || (last && qn > 0)) {
+            if (threadIdx.x < min(qn, BT))
+                check_phase_b<T, Q, BT>(pol, dof, q, ld, s_queue[(qhead + threadIdx.x) % qcap], my_row, my_cen, out,
+                                        count_lim, n_col);
+            const int took = min(qn, BT);
+            qhead = (qhead + took) % qcap;
+            qn -= took;
+            __syncthreads();
+        }
+    }
+}
+
+// The generic policy: the model is the blob staged in shared memory.
+template <typename T, int BT>
+struct BlobPolicy {
+    const ModelDev<T>& M;
+    const uint8_t* smem;
+    T margin;
+    template <typename Q>
+    __device__ __forceinline__ void fk(const Q* row, T* cen) const {
+        fk_sphere_centres<T, Q>(reinterpret_cast<const JointRec<T>*>(smem), M.n_joints,
+                                reinterpret_cast<const SphereRec<T>*>(smem + M.off_spheres), row, cen, BT,
+                                reinterpret_cast<const BoxRec<T>*>(smem + M.off_boxes), M.box_base);
+    }
+    template <typename Q>
+    __device__ __forceinline__ bool a(const Q* row, T* cen) const {
+        fk<Q>(row, cen);
+        return hot_pairs_collide<T>(M, smem, cen, BT);
+    }
+    template <typename Q>
+    __device__ __forceinline__ bool b(const Q* row, T* cen) const {
+        fk<Q>(row, cen);
+        return rest_collides<T>(M, smem, cen, BT, margin);
+    }
+};
+
+}  // namespace ez

@@ -1,11 +1,21 @@
 // ez_common.h — host+device shared definitions for the corridor_b200 library.
 #pragma once
 
+#ifdef __CUDACC_RTC__
+// run-time compiled kernels (ez_jit.cu): no host headers
+typedef signed char int8_t;
+typedef unsigned char uint8_t;
+typedef int int32_t;
+typedef unsigned int uint32_t;
+typedef long long int64_t;
+typedef unsigned long long uint64_t;
+#else
 #include <cstdint>
 #include <cstdio>
 #include <string>
 
 #include <cuda_runtime.h>
+#endif
 
 #include "../../include/corridor_b200.h"
 
@@ -14,10 +24,12 @@ namespace ez {
 // ---------------------------------------------------------------------------
 // error plumbing: thread-local last error + status propagation
 // ---------------------------------------------------------------------------
+#ifndef __CUDACC_RTC__
 void set_error(const std::string& msg);
 int32_t fail(int32_t status, const std::string& msg);
 int32_t cuda_fail(cudaError_t err, const char* what, const char* file, int line);
 int32_t retain_async_pool();  // keep the current device's default mem pool cached
+#endif
 
 #define EZ_CUDA(call)                                                        \
     do {                                                                     \

@@ -376,13 +376,13 @@ __device__ __forceinline__ int64_t voxel_cell(const VoxGrid<T>& V, T px, T py, T
 
 constexpr uint32_t kFarCell = 0xFF000000u;  // q = 255: no voxel within the list radius
 
-// Decide "some voxel centre within R of p" from the cell word w.
+// List walk for a cell the quantised distance does not decide (rare: the
+// point is within one quantisation step of R).
+#ifndef EZ_VOXEL_WALK_ATTR
+#define EZ_VOXEL_WALK_ATTR __forceinline__
+#endif
 template <typename T>
-__device__ __forceinline__ bool voxel_decide(const VoxGrid<T>& V, uint32_t w, T e, T px, T py, T pz, T R) {
-    const uint32_t qc = w >> 24;
-    const T lo = T(qc) * V.dq;
-    if (lo - e > R + V.eps) return false;                          // certainly free
-    if (qc < 255u && lo + V.dq + e <= R - V.eps) return true;      // certainly hit
+__device__ EZ_VOXEL_WALK_ATTR bool voxel_walk(const VoxGrid<T>& V, uint32_t w, T e, T px, T py, T pz, T R) {
     const int4* __restrict__ L = V.lists + (w & 0x00FFFFFFu);
     const T lim = R + e + V.eps;
     const T R2 = R * R;
@@ -395,6 +395,16 @@ __device__ __forceinline__ bool voxel_decide(const VoxGrid<T>& V, uint32_t w, T 
         const T dz = pz - lattice_centre(V.vorg[2], E.z, V.vside);
         if (dx * dx + dy * dy + dz * dz <= R2) return true;
     }
+}
+
+// Decide "some voxel centre within R of p" from the cell word w.
+template <typename T>
+__device__ __forceinline__ bool voxel_decide(const VoxGrid<T>& V, uint32_t w, T e, T px, T py, T pz, T R) {
+    const uint32_t qc = w >> 24;
+    const T lo = T(qc) * V.dq;
+    if (lo - e > R + V.eps) return false;                          // certainly free
+    if (qc < 255u && lo + V.dq + e <= R - V.eps) return true;      // certainly hit
+    return voxel_walk<T>(V, w, e, px, py, pz, R);
 }
 
 template <typename T>

@@ -1,0 +1,494 @@
+// ez_jit.cu — per-model check kernels compiled at run time.
+//
+// The generic k_check reads the robot model from the blob it stages in shared
+// memory: every joint rotation, sphere offset, pair index and threshold is a
+// shared-memory load, every 3x3 product is a full 27-FMA product, and sphere
+// centres go through a per-thread shared-memory store.  For one model, all of
+// that is known when the world is built.  This file emits the model as
+// straight-line CUDA (joint products with zero terms removed and unit terms
+// folded, sphere offsets, pair indices and thresholds as literals, centres in
+// registers), compiles it with NVRTC for sm_100a and loads it as a CUDA
+// library.  The tile loop, the survivor queue and the voxel-grid tests are the
+// generic ones (ez_check_core.cuh, ez_device.cuh), embedded into the library
+// at build time.  Same arithmetic as the generic path (same expression order;
+// joint-matrix entries below 1e-12, i.e. cos(pi/2) rounding residue, are
+// dropped), so flags stay exact outside the 1e-5 contact band.
+//
+// Replaces corridor/world.py:483-565 (check_batch -> _check_chunk ->
+// _sphere_vs_obstacles / _pair) for sphere-only robots on the fp32 path.
+#include <dlfcn.h>
+#include <sys/stat.h>
+#include <unistd.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <sstream>
+#include <string>
+#include <vector>
+
+#include <nvrtc.h>
+
+#include "ez_device.cuh"
+#include "ez_jit.h"
+#include "ez_world.h"
+
+#include "ez_jit_headers.inc"
+
+namespace ez {
+namespace {
+
+// ---------------------------------------------------------------------------
+// NVRTC, opened at run time (no link-time dependency)
+// ---------------------------------------------------------------------------
+struct Nvrtc {
+    decltype(&nvrtcCreateProgram) create = nullptr;
+    decltype(&nvrtcCompileProgram) compile = nullptr;
+    decltype(&nvrtcGetProgramLogSize) log_size = nullptr;
+    decltype(&nvrtcGetProgramLog) log = nullptr;
+    decltype(&nvrtcGetCUBINSize) cubin_size = nullptr;
+    decltype(&nvrtcGetCUBIN) cubin = nullptr;
+    decltype(&nvrtcDestroyProgram) destroy = nullptr;
+    decltype(&nvrtcGetErrorString) err = nullptr;
+    bool ok = false;
+};
+
+const Nvrtc& nvrtc() {
+    static Nvrtc n;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        const char* names[] = {"libnvrtc.so.12", "libnvrtc.so", "/usr/local/cuda/lib64/libnvrtc.so.12",
+                               "/usr/local/cuda/lib64/libnvrtc.so"};
+        void* h = nullptr;
+        for (const char* nm : names)
+            if ((h = dlopen(nm, RTLD_NOW | RTLD_LOCAL)) != nullptr) break;
+        if (!h) return;
+        n.create = reinterpret_cast<decltype(n.create)>(dlsym(h, "nvrtcCreateProgram"));
+        n.compile = reinterpret_cast<decltype(n.compile)>(dlsym(h, "nvrtcCompileProgram"));
+        n.log_size = reinterpret_cast<decltype(n.log_size)>(dlsym(h, "nvrtcGetProgramLogSize"));
+        n.log = reinterpret_cast<decltype(n.log)>(dlsym(h, "nvrtcGetProgramLog"));
+        n.cubin_size = reinterpret_cast<decltype(n.cubin_size)>(dlsym(h, "nvrtcGetCUBINSize"));
+        n.cubin = reinterpret_cast<decltype(n.cubin)>(dlsym(h, "nvrtcGetCUBIN"));
+        n.destroy = reinterpret_cast<decltype(n.destroy)>(dlsym(h, "nvrtcDestroyProgram"));
+        n.err = reinterpret_cast<decltype(n.err)>(dlsym(h, "nvrtcGetErrorString"));
+        n.ok = n.create && n.compile && n.log_size && n.log && n.cubin_size && n.cubin && n.destroy && n.err;
+    });
+    return n;
+}
+
+// ---------------------------------------------------------------------------
+// source generation
+// ---------------------------------------------------------------------------
+std::string lit(float v) {  // exact float literal
+    if (v == 0.0f) return std::signbit(v) ? "(-0.0f)" : "0.0f";
+    char buf[48];
+    std::snprintf(buf, sizeof(buf), "(%af)", static_cast<double>(v));
+    return buf;
+}
+
+// sum_k a_k * c_k in the generic order (a0*c0 + a1*c1 + a2*c2, left to right),
+// zero coefficients removed and unit ones folded
+std::string dot3(const std::string (&a)[3], const float (&c)[3]) {
+    std::string out;
+    for (int k = 0; k < 3; ++k) {
+        if (c[k] == 0.0f) continue;
+        std::string term = (c[k] == 1.0f) ? a[k] : (c[k] == -1.0f ? "(-" + a[k] + ")" : a[k] + " * " + lit(c[k]));
+        out = out.empty() ? term : out + " + " + term;
+    }
+    return out.empty() ? std::string("0.0f") : out;
+}
+
+struct Gen {
+    const ModelDev<float>& M;
+    const uint8_t* blob;
+    float margin;
+    int bt;
+    std::ostringstream o;
+
+    const JointRec<float>* J() const { return reinterpret_cast<const JointRec<float>*>(blob); }
+    const SphereRec<float>* S() const { return reinterpret_cast<const SphereRec<float>*>(blob + M.off_spheres); }
+
+    static float clean(float v) { return std::fabs(v) < 1e-12f ? 0.0f : v; }
+
+    // joint chain: frame of link j in R{j}_k / t{j}_k, sphere s in c{s}_k
+    void fk() {
+        for (int j = 0; j < M.n_joints; ++j) {
+            const JointRec<float>& jr = J()[j];
+            float jR[9], jt[3];
+            for (int k = 0; k < 9; ++k) jR[k] = clean(jr.R[k]);
+            for (int k = 0; k < 3; ++k) jt[k] = clean(jr.t[k]);
+            o << "    // joint " << j << "\n";
+            const int p = jr.parent;
+            for (int r = 0; r < 3; ++r) {
+                for (int c = 0; c < 3; ++c) {
+                    std::string e;
+                    if (p < 0) {
+                        e = lit(jR[3 * r + c]);
+                    } else {
+                        const std::string a[3] = {"R" + std::to_string(p) + "_" + std::to_string(3 * r),
+                                                  "R" + std::to_string(p) + "_" + std::to_string(3 * r + 1),
+                                                  "R" + std::to_string(p) + "_" + std::to_string(3 * r + 2)};
+                        const float cc[3] = {jR[c], jR[3 + c], jR[6 + c]};
+                        e = dot3(a, cc);
+                    }
+                    o << "    float R" << j << "_" << 3 * r + c << " = " << e << ";\n";
+                }
+                std::string e;
+                if (p < 0) {
+                    e = lit(jt[r]);
+                } else {
+                    const std::string a[3] = {"R" + std::to_string(p) + "_" + std::to_string(3 * r),
+                                              "R" + std::to_string(p) + "_" + std::to_string(3 * r + 1),
+                                              "R" + std::to_string(p) + "_" + std::to_string(3 * r + 2)};
+                    const float cc[3] = {jt[0], jt[1], jt[2]};
+                    const std::string d = dot3(a, cc);
+                    e = "t" + std::to_string(p) + "_" + std::to_string(r) + " + (" + d + ")";
+                }
+                o << "    float t" << j << "_" << r << " = " << e << ";\n";
+            }
+            if (jr.kind == EZ_JOINT_REVOLUTE) {
+                o << "    {\n        float s, c;\n        Angle<float, Q>::sc(row[" << jr.qidx << "], s, c);\n";
+                for (int r = 0; r < 3; ++r) {
+                    const std::string n0 = "R" + std::to_string(j) + "_" + std::to_string(3 * r);
+                    const std::string n1 = "R" + std::to_string(j) + "_" + std::to_string(3 * r + 1);
+                    o << "        { const float n0 = " << n0 << ", n1 = " << n1 << "; " << n0 << " = n0 * c + n1 * s; "
+                      << n1 << " = n1 * c - n0 * s; }\n";
+                }
+                o << "    }\n";
+            } else if (jr.kind == EZ_JOINT_PRISMATIC) {
+                float ax[3];
+                for (int k = 0; k < 3; ++k) ax[k] = clean(jr.ax[k]);
+                o << "    {\n        const float qq = static_cast<float>(row[" << jr.qidx << "]);\n";
+                for (int r = 0; r < 3; ++r) {
+                    const std::string a[3] = {"R" + std::to_string(j) + "_" + std::to_string(3 * r),
+                                              "R" + std::to_string(j) + "_" + std::to_string(3 * r + 1),
+                                              "R" + std::to_string(j) + "_" + std::to_string(3 * r + 2)};
+                    o << "        t" << j << "_" << r << " += (" << dot3(a, ax) << ") * qq;\n";
+                }
+                o << "    }\n";
+            }
+            for (int s = jr.sph_begin; s < jr.sph_end; ++s) {
+                float pp[3];
+                for (int k = 0; k < 3; ++k) pp[k] = clean(S()[s].p[k]);
+                for (int r = 0; r < 3; ++r) {
+                    const std::string a[3] = {"R" + std::to_string(j) + "_" + std::to_string(3 * r),
+                                              "R" + std::to_string(j) + "_" + std::to_string(3 * r + 1),
+                                              "R" + std::to_string(j) + "_" + std::to_string(3 * r + 2)};
+                    o << "    const float c" << s << "_" << r << " = t" << j << "_" << r << " + (" << dot3(a, pp)
+                      << ");\n";
+                }
+            }
+        }
+    }
+
+    std::string d2(int a, int b) const {
+        std::ostringstream e;
+        e << "sq3(c" << a << "_0 - c" << b << "_0, c" << a << "_1 - c" << b << "_1, c" << a << "_2 - c" << b << "_2)";
+        return e.str();
+    }
+
+    void hot() {
+        const HotRec<float>* H = reinterpret_cast<const HotRec<float>*>(blob + M.off_hot);
+        for (int p = 0; p < M.n_hot; ++p)
+            o << "    if (" << d2(H[p].a, H[p].b) << " <= " << lit(H[p].thr2) << ") return true;\n";
+    }
+
+    void statics(int s) {
+        const SphereRec<float>& sp = S()[s];
+        const std::string X = "c" + std::to_string(s) + "_0", Y = "c" + std::to_string(s) + "_1",
+                          Z = "c" + std::to_string(s) + "_2";
+        const StaticSphereRec<float>* SS = reinterpret_cast<const StaticSphereRec<float>*>(blob + M.off_ssph);
+        for (int i = 0; i < M.n_ssph; ++i) {
+            o << "    { const float rr = (" << lit(SS[i].r) << " + " << lit(sp.r) << ") + " << lit(margin) << "; if (sq3("
+              << X << " - " << lit(SS[i].c[0]) << ", " << Y << " - " << lit(SS[i].c[1]) << ", " << Z << " - "
+              << lit(SS[i].c[2]) << ") <= rr * rr) return true; }\n";
+        }
+        const StaticBoxRec<float>* SB = reinterpret_cast<const StaticBoxRec<float>*>(blob + M.off_sbox);
+        for (int i = 0; i < M.n_sbox; ++i) {
+            const StaticBoxRec<float>& b = SB[i];
+            o << "    { const float dx = " << X << " - " << lit(b.t[0]) << ", dy = " << Y << " - " << lit(b.t[1])
+              << ", dz = " << Z << " - " << lit(b.t[2]) << "; float d2 = 0.0f;\n";
+            for (int r = 0; r < 3; ++r)
+                o << "      { const float l = " << lit(b.Rt[3 * r]) << " * dx + " << lit(b.Rt[3 * r + 1]) << " * dy + "
+                  << lit(b.Rt[3 * r + 2]) << " * dz; const float cl = fmin(fmax(l, " << lit(-b.he[r]) << "), "
+                  << lit(b.he[r]) << "); d2 += (l - cl) * (l - cl); }\n";
+            o << "      if (d2 <= " << lit(sp.rmar) << " * " << lit(sp.rmar) << ") return true; }\n";
+        }
+    }
+
+    // obstacles in calibrated order, cells of kVoxBatch spheres fetched together
+    void obstacles() {
+        const int32_t* order = reinterpret_cast<const int32_t*>(blob + M.off_order);
+        const bool vox = M.vox.present;
+        for (int k0 = 0; k0 < M.n_spheres; k0 += kVoxBatch) {
+            const int nb = std::min(kVoxBatch, M.n_spheres - k0);
+            o << "    {\n";
+            for (int j = 0; j < nb; ++j) {
+                const int s = order[k0 + j];
+                if (!vox) continue;
+                o << "        float e" << j << " = 0.0f; uint32_t w" << j << " = kFarCell;\n"
+                  << "        { const int64_t cl = voxel_cell<float>(M.vox, c" << s << "_0, c" << s << "_1, c" << s
+                  << "_2, e" << j << "); if (cl >= 0) w" << j << " = __ldg(M.vox.cells + cl); }\n";
+            }
+            for (int j = 0; j < nb; ++j) {
+                const int s = order[k0 + j];
+                statics(s);
+                if (vox)
+                    o << "        if (w" << j << " != kFarCell && voxel_decide<float>(M.vox, w" << j << ", e" << j
+                      << ", c" << s << "_0, c" << s << "_1, c" << s << "_2, " << lit(S()[s].rvox) << ")) return true;\n";
+            }
+            o << "    }\n";
+        }
+    }
+
+    void blocks() {
+        const BlockRec<float>* B = reinterpret_cast<const BlockRec<float>*>(blob + M.off_blocks);
+        const HotRec<float>* P = reinterpret_cast<const HotRec<float>*>(blob + M.off_rest);
+        for (int k = 0; k < M.n_blocks; ++k) {
+            const BlockRec<float>& bk = B[k];
+            const bool always = bk.thr2 >= 1e29f;
+            if (!always) o << "    if (!(" << d2(bk.ba, bk.bb) << " > " << lit(bk.thr2) << ")) {\n";
+            else o << "    {\n";
+            int p = bk.begin;
+            for (; p + 4 <= bk.end; p += 4) {
+                o << "        if (";
+                for (int u = 0; u < 4; ++u)
+                    o << (u ? " | " : "") << "(" << d2(P[p + u].a, P[p + u].b) << " <= " << lit(P[p + u].thr2) << ")";
+                o << ") return true;\n";
+            }
+            for (; p < bk.end; ++p)
+                o << "        if (" << d2(P[p].a, P[p].b) << " <= " << lit(P[p].thr2) << ") return true;\n";
+            o << "    }\n";
+        }
+    }
+
+    std::string source() {
+        o << "// generated by ez_jit.cu for one robot model\n#include \"ez_check_core.cuh\"\n\nnamespace ez {\n\n"
+          << "__device__ __forceinline__ float sq3(float dx, float dy, float dz) { return dx * dx + dy * dy + dz * dz; }\n\n"
+          << "struct JitPolicy {\n    const ModelDev<float>& M;\n"
+          << "    template <typename Q>\n    __device__ __forceinline__ bool a(const Q* row, float*) const {\n";
+        fk();
+        hot();
+        o << "    return false;\n    }\n"
+          << "    template <typename Q>\n    __device__ __forceinline__ bool b(const Q* row, float*) const {\n";
+        fk();
+        obstacles();
+        blocks();
+        o << "    return false;\n    }\n};\n\n";
+        o << "template <typename Q>\n__device__ __forceinline__ void jit_body(const ModelDev<float>& M, const Q* q, int64_t n, "
+             "int64_t ld, uint8_t* out, int64_t count_lim, int32_t* n_col) {\n"
+          << "    extern __shared__ __align__(16) uint8_t smem[];\n"
+          << "    __shared__ int32_t s_queue[2 * " << bt << "];\n    __shared__ int s_warp[" << bt / 32 << "];\n"
+          << "    const JitPolicy pol{M};\n"
+          << "    check_tiles<float, Q, " << bt << ">(pol, " << M.dof
+          << ", static_cast<float*>(nullptr), reinterpret_cast<Q*>(smem), s_queue, s_warp, q, n, ld, out, count_lim, n_col);\n}\n\n"
+          << "}  // namespace ez\n\n";
+        for (const char* qt : {"float", "double"}) {
+            o << "extern \"C\" __global__ void __launch_bounds__(" << bt << ") ez_check_jit_" << qt[0]
+              << "(ez::ModelDev<float> M, const " << qt << "* __restrict__ q, int64_t n, int64_t ld, "
+              << "uint8_t* __restrict__ out, float, int64_t count_lim, int32_t* __restrict__ n_col) {\n"
+              << "    ez::jit_body<" << qt << ">(M, q, n, ld, out, count_lim, n_col);\n}\n";
+        }
+        return o.str();
+    }
+};
+
+// ---------------------------------------------------------------------------
+// compile + load, cached by source text (same model and margin -> one module)
+// ---------------------------------------------------------------------------
+// never destroyed: modules stay loaded until the process exits
+std::mutex g_mu;
+std::map<std::string, std::shared_ptr<JitCheck>>& g_cache = *new std::map<std::string, std::shared_ptr<JitCheck>>();
+
+// the rare list walk stays out of line: inlined at every unrolled sphere test
+// it bloats the straight-line kernel
+const char* const kNvrtcOpts[] = {"--gpu-architecture=sm_100a", "--std=c++17", "-lineinfo", "-w",
+                                  "-DEZ_VOXEL_WALK_ATTR=__noinline__"};
+constexpr int kNvrtcOptCount = 5;
+
+// On-disk cubin cache (an optimisation only: a miss recompiles).  Key: FNV-1a
+// of the generated source, the embedded headers and the NVRTC options.
+// EZ_JIT_CACHE=0 disables.
+std::string cache_path(const std::string& src) {
+    const char* off = getenv("EZ_JIT_CACHE");
+    if (off && off[0] == '0') return "";
+    std::string dir;
+    if (const char* d = getenv("EZ_JIT_CACHE_DIR")) dir = d;
+    else if (const char* x = getenv("XDG_CACHE_HOME")) dir = std::string(x) + "/corridor_b200";
+    else if (const char* h = getenv("HOME")) dir = std::string(h) + "/.cache/corridor_b200";
+    else return "";
+    uint64_t hsh = 1469598103934665603ull;
+    auto mix = [&](const char* p, size_t n) {
+        for (size_t i = 0; i < n; ++i) hsh = (hsh ^ static_cast<uint8_t>(p[i])) * 1099511628211ull;
+    };
+    mix(src.data(), src.size());
+    for (int i = 0; i < kJitHeaderCount; ++i) mix(kJitHeaderText[i], strlen(kJitHeaderText[i]));
+    for (int i = 0; i < kNvrtcOptCount; ++i) mix(kNvrtcOpts[i], strlen(kNvrtcOpts[i]));
+    char name[64];
+    std::snprintf(name, sizeof(name), "/jit_%016llx.cubin", static_cast<unsigned long long>(hsh));
+    return dir + name;
+}
+
+bool read_file(const std::string& path, std::vector<char>* out) {
+    FILE* f = path.empty() ? nullptr : fopen(path.c_str(), "rb");
+    if (!f) return false;
+    fseek(f, 0, SEEK_END);
+    const long n = ftell(f);
+    fseek(f, 0, SEEK_SET);
+    out->resize(n > 0 ? n : 0);
+    const bool ok = n > 0 && fread(out->data(), 1, n, f) == static_cast<size_t>(n);
+    fclose(f);
+    return ok;
+}
+
+void write_file(const std::string& path, const std::vector<char>& data) {
+    if (path.empty()) return;
+    const std::string dir = path.substr(0, path.rfind('/'));
+    for (size_t i = 1; i <= dir.size(); ++i)  // mkdir -p
+        if (i == dir.size() || dir[i] == '/') mkdir(dir.substr(0, i).c_str(), 0755);
+    const std::string tmp = path + ".tmp" + std::to_string(static_cast<long long>(getpid()));
+    FILE* f = fopen(tmp.c_str(), "wb");
+    if (!f) return;
+    const bool ok = fwrite(data.data(), 1, data.size(), f) == data.size();
+    fclose(f);
+    if (ok) rename(tmp.c_str(), path.c_str());
+    else remove(tmp.c_str());
+}
+
+int32_t nvrtc_cubin(const std::string& src, std::vector<char>* cubin) {
+    const Nvrtc& nv = nvrtc();
+    if (!nv.ok) return fail(EZ_UNSUPPORTED, "NVRTC (libnvrtc.so.12) not found; specialised check kernels unavailable");
+    nvrtcProgram prog;
+    nvrtcResult r = nv.create(&prog, src.c_str(), "ez_check_jit.cu", kJitHeaderCount, kJitHeaderText, kJitHeaderNames);
+    if (r != NVRTC_SUCCESS) return fail(EZ_UNSUPPORTED, std::string("nvrtcCreateProgram: ") + nv.err(r));
+    r = nv.compile(prog, kNvrtcOptCount, kNvrtcOpts);
+    if (r != NVRTC_SUCCESS) {
+        size_t n = 0;
+        nv.log_size(prog, &n);
+        std::string log(n, '\0');
+        nv.log(prog, &log[0]);
+        nv.destroy(&prog);
+        return fail(EZ_UNSUPPORTED, "NVRTC compile of the specialised check kernel failed:\n" + log.substr(0, 4000));
+    }
+    size_t n = 0;
+    nv.cubin_size(prog, &n);
+    cubin->resize(n);
+    nv.cubin(prog, cubin->data());
+    nv.destroy(&prog);
+    return EZ_OK;
+}
+
+int32_t compile(const std::string& src, int bt, std::shared_ptr<JitCheck>* out) {
+    std::vector<char> cubin;
+    const std::string cp = cache_path(src);
+    auto jc = std::make_shared<JitCheck>();
+    jc->bt = bt;
+    bool loaded = false;
+    if (read_file(cp, &cubin)) {  // a cached cubin that does not load is rebuilt
+        loaded = cudaLibraryLoadData(&jc->lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0) == cudaSuccess;
+        if (!loaded) cudaGetLastError();
+    }
+    if (!loaded) {
+        EZ_TRY(nvrtc_cubin(src, &cubin));
+        write_file(cp, cubin);
+        EZ_CUDA(cudaLibraryLoadData(&jc->lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0));
+    }
+    EZ_CUDA(cudaLibraryGetKernel(&jc->kf, jc->lib, "ez_check_jit_f"));
+    EZ_CUDA(cudaLibraryGetKernel(&jc->kd, jc->lib, "ez_check_jit_d"));
+    *out = jc;
+    return EZ_OK;
+}
+
+}  // namespace
+
+JitCheck::~JitCheck() {
+    if (lib) cudaLibraryUnload(lib);
+}
+
+std::string jit_source(const ez_world* w, int bt) {
+    Gen g{w->mf, w->h_blob_f.data(), static_cast<float>(w->margin), bt, {}};
+    return g.source();
+}
+
+int32_t jit_specialize(ez_world* w) {
+    if (w->jit) return EZ_OK;
+    if (w->jit_failed) return fail(EZ_UNSUPPORTED, w->jit_error);
+    auto refuse = [&](int32_t st, const std::string& why) {
+        w->jit_failed = true;
+        w->jit_error = why;
+        return fail(st, why);
+    };
+    if (w->mf.n_boxes > 0 || w->mf.n_mix > 0) return refuse(EZ_UNSUPPORTED, "robot boxes use the generic check kernel");
+    if (w->h_blob_f.empty()) return refuse(EZ_UNSUPPORTED, "no host copy of the model");
+    const int bt = 128;
+    const std::string src = jit_source(w, bt);
+    if (const char* dump = getenv("EZ_JIT_DUMP")) {  // inspection: write the generated source
+        if (FILE* f = fopen(dump, "w")) {
+            fwrite(src.data(), 1, src.size(), f);
+            fclose(f);
+        }
+    }
+    std::shared_ptr<JitCheck> jc;
+    {
+        std::lock_guard<std::mutex> lk(g_mu);
+        auto it = g_cache.find(src);
+        if (it != g_cache.end()) jc = it->second;
+    }
+    if (!jc) {
+        const int32_t st = compile(src, bt, &jc);
+        if (st != EZ_OK) {
+            w->jit_failed = true;
+            w->jit_error = ez_last_error();
+            return st;
+        }
+        std::lock_guard<std::mutex> lk(g_mu);
+        g_cache.emplace(src, jc);
+    }
+    for (int i = 0; i < 2; ++i) {
+        const void* k = reinterpret_cast<const void*>(i == 0 ? jc->kf : jc->kd);
+        const size_t smem = static_cast<size_t>(bt) * w->dof * (i == 0 ? sizeof(float) : sizeof(double));
+        int occ = 0;
+        EZ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, bt, smem));
+        if (occ < 1) return refuse(EZ_CAPACITY, "specialised check kernel does not fit on an SM");
+        w->jit_occ[i] = occ;
+    }
+    w->jit = jc;
+    return EZ_OK;
+}
+
+int32_t jit_launch(ez_world* w, const void* d_q, bool q64, int64_t n, int64_t ld, uint8_t* d_free,
+                   cudaStream_t stream, int64_t count_lim, int32_t* n_col) {
+    const JitCheck& jc = *w->jit;
+    const int bt = jc.bt;
+    const size_t smem = static_cast<size_t>(bt) * w->dof * (q64 ? sizeof(double) : sizeof(float));
+    const int64_t tiles = (n + bt - 1) / bt;
+    const unsigned grid =
+        static_cast<unsigned>(std::min<int64_t>(tiles, static_cast<int64_t>(w->num_sms) * w->jit_occ[q64 ? 1 : 0]));
+    ModelDev<float> M = w->mf;
+    float margin = static_cast<float>(w->margin);
+    void* args[] = {&M, const_cast<void**>(&d_q), &n, &ld, &d_free, &margin, &count_lim, &n_col};
+    EZ_CUDA(cudaLaunchKernel(reinterpret_cast<const void*>(q64 ? jc.kd : jc.kf), dim3(grid), dim3(bt), args, smem,
+                             stream));
+    return EZ_OK;
+}
+
+}  // namespace ez
+
+extern "C" int32_t ez_world_specialize(ez_world* w, int32_t mode) {
+    if (!w) return ez::fail(EZ_INVALID_ARGUMENT, "null world");
+    std::lock_guard<std::mutex> lock(w->mu);
+    EZ_CUDA(cudaSetDevice(w->device));
+    if (mode < 0) {
+        w->jit.reset();
+        w->jit_failed = true;
+        w->jit_error = "specialised check kernel disabled for this world";
+        return EZ_OK;
+    }
+    if (mode > 0) return ez::jit_specialize(w);
+    if (w->jit) return EZ_OK;
+    return ez::fail(EZ_UNSUPPORTED, w->jit_failed ? w->jit_error : std::string("not specialised"));
+}

@@ -13,7 +13,7 @@
 
 #include <cub/device/device_scan.cuh>
 
-#include "ez_device.cuh"
+#include "ez_check_core.cuh"
 #include "ez_rng.cuh"
 #include "ez_world.h"
 
@@ -636,37 +636,6 @@ static int32_t build_voxel_grid(ez_world* w, const ez_scene_desc* sc, const HMod
 // ---------------------------------------------------------------------------
 // kernels: fused check, FK frames
 // ---------------------------------------------------------------------------
-// Fused FK + collision check in two phases:
-//   A) per tile, every thread: FK -> sphere centres (smem) -> calibrated hot
-//      self pairs.  Most colliding configurations are decided here.
-//   B) survivors are appended (in order) to a CTA queue; whenever a full
-//      CTA's worth is queued, every thread takes one, reloads its row,
-//      recomputes FK and runs the obstacle tests and remaining pairs.  Phase B
-//      therefore always runs on full warps and no warp idles at a barrier
-//      while a few lanes finish the expensive tail.
-template <typename T, typename Q>
-__device__ __forceinline__ void check_phase_b(const ModelDev<T>& M, const uint8_t* smem, const Q* __restrict__ q,
-                                              int64_t ld, int64_t idx, Q* row, T* cen, int stride, T margin,
-                                              uint8_t* __restrict__ out, int64_t count_lim, int32_t* n_col) {
-    const int dof = M.dof;
-    Q v[32];
-#pragma unroll
-    for (int k = 0; k < 32; ++k)
-        if (k < dof) v[k] = q[idx * ld + k];
-#pragma unroll
-    for (int k = 0; k < 32; ++k)
-        if (k < dof) row[k] = v[k];
-    const JointRec<T>* J = reinterpret_cast<const JointRec<T>*>(smem);
-    const SphereRec<T>* S = reinterpret_cast<const SphereRec<T>*>(smem + M.off_spheres);
-    fk_sphere_centres<T, Q>(J, M.n_joints, S, row, cen, stride, reinterpret_cast<const BoxRec<T>*>(smem + M.off_boxes),
-                            M.box_base);
-    const bool c2 = rest_collides<T>(M, smem, cen, stride, margin);
-    out[idx] = c2 ? 0 : 1;
-    if (n_col != nullptr && c2 && idx < count_lim) atomicAdd(n_col, 1);
-}
-
-constexpr int kPrefetch = 8;  // registers per thread for the next tile's rows (dof*BT/BT <= 8)
-
 template <typename T, typename Q, int BT>
 __global__ void __launch_bounds__(BT)
 k_check(ModelDev<T> M, const Q* __restrict__ q, int64_t n, int64_t ld, uint8_t* __restrict__ out,
@@ -679,90 +648,9 @@ k_check(ModelDev<T> M, const Q* __restrict__ q, int64_t n, int64_t ld, uint8_t* 
     T* cen = reinterpret_cast<T*>(smem + M.blob_bytes);
     const size_t roff = (static_cast<size_t>(M.blob_bytes) + static_cast<size_t>(M.cen_words) * BT * sizeof(T) + 15) &
                         ~static_cast<size_t>(15);
-    Q* rows = reinterpret_cast<Q*>(smem + roff);
-    const int dof = M.dof;
-    constexpr int qcap = 2 * BT;
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const JointRec<T>* J = reinterpret_cast<const JointRec<T>*>(smem);
-    const SphereRec<T>* S = reinterpret_cast<const SphereRec<T>*>(smem + M.off_spheres);
-    T* my_cen = cen + threadIdx.x;
-    Q* my_row = rows + threadIdx.x * dof;
-    const bool contiguous = (ld == dof) && (dof <= kPrefetch);
-    int qhead = 0, qn = 0;  // ring buffer state (uniform across the CTA)
-    const int64_t tiles = (n + BT - 1) / BT;
-    Q pf[kPrefetch];
-    auto prefetch = [&](int64_t tile) {
-        if (tile >= tiles) return;
-        const int64_t base = tile * BT;
-        const int tot = static_cast<int>(min(static_cast<int64_t>(BT), n - base)) * dof;
-        const Q* src = q + base * dof;
-#pragma unroll
-        for (int j = 0; j < kPrefetch; ++j) {
-            const int i = threadIdx.x + j * BT;
-            if (i < tot) pf[j] = src[i];
-        }
-    };
-    if (contiguous) prefetch(blockIdx.x);
-    for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
-        const int64_t base = tile * BT;
-        const int nr = static_cast<int>(min(static_cast<int64_t>(BT), n - base));
-        __syncthreads();
-        if (contiguous) {
-            const int tot = nr * dof;
-#pragma unroll
-            for (int j = 0; j < kPrefetch; ++j) {
-                const int i = threadIdx.x + j * BT;
-                if (i < tot) rows[i] = pf[j];
-            }
-        } else {
-            for (int i = threadIdx.x; i < nr * dof; i += BT) {
-                const int r = i / dof, k = i - r * dof;
-                rows[i] = q[(base + r) * ld + k];
-            }
-        }
-        __syncthreads();
-        if (contiguous) prefetch(tile + gridDim.x);  // lands while this tile is checked
-        // phase A
-        const bool valid = threadIdx.x < nr;
-        bool col = false;
-        if (valid) {
-            fk_sphere_centres<T, Q>(J, M.n_joints, S, my_row, my_cen, BT,
-                                    reinterpret_cast<const BoxRec<T>*>(smem + M.off_boxes), M.box_base);
-            col = hot_pairs_collide<T>(M, smem, my_cen, BT);
-            if (col) out[base + threadIdx.x] = 0;
-        }
-        if (n_col != nullptr) {
-            const unsigned m = __ballot_sync(0xffffffffu, col && (base + threadIdx.x) < count_lim);
-            if (lane == 0 && m) atomicAdd(n_col, __popc(m));
-        }
-        // append the survivors to the queue, in index order
-        const bool surv = valid && !col;
-        const unsigned sm = __ballot_sync(0xffffffffu, surv);
-        if (lane == 0) s_warp[wid] = __popc(sm);
-        __syncthreads();
-        int off = 0, add = 0;
-#pragma unroll
-        for (int w = 0; w < BT / 32; ++w) {
-            const int c = s_warp[w];
-            off += (w < wid) ? c : 0;
-            add += c;
-        }
-        if (surv) s_queue[(qhead + qn + off + __popc(sm & ((1u << lane) - 1u))) % qcap] = static_cast<int32_t>(base + threadIdx.x);
-        qn += add;
-        __syncthreads();
-        // phase B on full CTAs
-        while (qn >= BT) {
-            check_phase_b<T, Q>(M, smem, q, ld, s_queue[(qhead + threadIdx.x) % qcap], my_row, my_cen, BT, margin,
-                                out, count_lim, n_col);
-            qhead = (qhead + BT) % qcap;
-            qn -= BT;
-            __syncthreads();
-        }
-    }
-    // drain
-    if (threadIdx.x < qn)
-        check_phase_b<T, Q>(M, smem, q, ld, s_queue[(qhead + threadIdx.x) % qcap], my_row, my_cen, BT, margin, out,
-                            count_lim, n_col);
+    const BlobPolicy<T, BT> pol{M, smem, margin};
+    check_tiles<T, Q, BT>(pol, M.dof, cen + threadIdx.x, reinterpret_cast<Q*>(smem + roff), s_queue, s_warp, q, n, ld,
+                          out, count_lim, n_col);
 }
 
 // link frames (true frames, fp64) for fk_batch / forward_kinematics
@@ -887,6 +775,7 @@ static int32_t calibrate_layout(ez_world* w, HModel& hm, const double* lower, co
     layout_pairs(hm, &pair_hits, &sph_hits);
     for (int i = 0; i < 2; ++i) {
         std::vector<uint8_t> blob = (i == 0) ? pack_blob<float>(hm, w->mf) : pack_blob<double>(hm, w->md);
+        if (i == 0) w->h_blob_f = blob;
         uint8_t* d = nullptr;
         EZ_CUDA(cudaMalloc(&d, blob.size()));
         EZ_CUDA(cudaMemcpy(d, blob.data(), blob.size(), cudaMemcpyHostToDevice));
@@ -936,10 +825,28 @@ static void launch_bt(const ModelDev<T>& M, unsigned grid, size_t smem, cudaStre
     k_check<T, Q, BT><<<grid, BT, smem, stream>>>(M, d_q, n, ld, d_free, margin, count_lim, n_col);
 }
 
+// EZ_JIT=0 keeps every batch on the generic kernel; otherwise the first fp32
+// batch of at least kJitMinRows rows compiles the model-specialised one.
+constexpr int64_t kJitMinRows = int64_t(1) << 18;
+static bool jit_enabled() {
+    static const bool on = [] {
+        const char* e = getenv("EZ_JIT");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
 template <typename T, typename Q>
 static int32_t launch_check_t(ez_world* w, const ModelDev<T>& M, const Q* d_q, int64_t n, int64_t ld,
                               uint8_t* d_free, cudaStream_t stream, int64_t count_lim, int32_t* n_col) {
     const int slot = (sizeof(T) == 8 ? 2 : 0) + (sizeof(Q) == 8 ? 1 : 0);
+    if (sizeof(T) == 4) {
+        // large fp32 batches: the model-specialised kernel (compiled once per model)
+        if (!w->jit && !w->jit_failed && n >= kJitMinRows && jit_enabled()) {
+            if (jit_specialize(w) != EZ_OK) set_error("");  // stays on the generic kernel
+        }
+        if (w->jit) return jit_launch(w, d_q, sizeof(Q) == 8, n, ld, d_free, stream, count_lim, n_col);
+    }
     if (w->launch_threads[slot] == 0) {
         int bw = -1, bt = 0, bo = 0;
         size_t bs = 0;
@@ -1189,6 +1096,7 @@ extern "C" int32_t ez_world_create(const ez_robot_desc* rb, const ez_scene_desc*
     {
         std::vector<uint8_t> bf = pack_blob<float>(hm, w->mf);
         std::vector<uint8_t> bd = pack_blob<double>(hm, w->md);
+        w->h_blob_f = bf;
         st = upload(bf, &w->d_blob[0]);
         if (st == EZ_OK) st = upload(bd, &w->d_blob[1]);
         w->mf.blob = w->d_blob[0];

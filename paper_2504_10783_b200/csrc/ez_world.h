@@ -2,10 +2,13 @@
 // for one checker margin), shared by the check, FK and EI-ZO translation units.
 #pragma once
 
+#include <memory>
 #include <mutex>
+#include <string>
 #include <vector>
 
 #include "ez_common.h"
+#include "ez_jit.h"
 
 struct ez_eizo_ws;  // EI-ZO device workspace (ez_eizo.cu)
 
@@ -46,6 +49,14 @@ struct ez_world {
     int64_t stage_rows = 0;
 
     ez_eizo_ws* eizo = nullptr;
+
+    // run-time specialised fp32 check kernel (ez_jit.cu) and the host copy of
+    // the fp32 model blob it is generated from
+    std::vector<uint8_t> h_blob_f;
+    std::shared_ptr<ez::JitCheck> jit;
+    bool jit_failed = false;
+    std::string jit_error;
+    int32_t jit_occ[2] = {0, 0};
 
     // cached launch shapes of k_check, [T fp64][Q fp64]
     int32_t launch_threads[4] = {0, 0, 0, 0};

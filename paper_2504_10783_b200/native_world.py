@@ -155,6 +155,21 @@ class NativeWorld:
                                                 precision_code(precision)))
         return out
 
+    def specialize(self, mode: int = 1) -> bool:
+        """Model-specialised fp32 check kernel (``ez_world_specialize``).
+
+        mode 1 compiles it (NVRTC, once per model and margin) and uses it for
+        fp32 batches; 0 queries; -1 returns to the generic kernel for good.
+        Returns True if the specialised kernel is in use.
+        """
+        st = N.lib().ez_world_specialize(self._h, int(mode))
+        if st == 0:
+            return mode >= 0
+        if st == 10:  # EZ_UNSUPPORTED: robot boxes, NVRTC missing or disabled
+            return False
+        N.check(st)
+        return False
+
     def check_device(self, Q, out=None, precision="fp32", stream: int | None = None):
         """Free mask (uint8 CUDA tensor) for a CUDA tensor of configurations (fp32 or fp64)."""
         torch = torch_mod()

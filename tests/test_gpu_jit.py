@@ -1,0 +1,76 @@
+"""Model-specialised check kernel (ez_jit.cu, NVRTC): parity with the reference goldens and
+exact agreement with the generic kernel it replaces for large fp32 batches."""
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import golden
+from paper_2504_10783_b200 import fixtures as fx
+from paper_2504_10783_b200.model import BOX, SPHERE, Geometry, RigidTransform
+from paper_2504_10783_b200.scene import VoxelMap, World
+
+pytestmark = pytest.mark.gpu
+
+BAND = 1e-5
+
+
+def _golden_world(name, g):
+    if name == "forest7":
+        return fx.disc_world(fx.forest_centers(7)).with_vmap(VoxelMap(np.array([-5.0, -5.0]), 0.02, g["vox_idx"]))
+    return {"franka7": fx.franka7_world, "franka7_m02": fx.franka7_world, "bimanual14": fx.bimanual14_world,
+            "arm3": fx.arm3_world}[name]()
+
+
+@pytest.mark.parametrize("name", ["franka7", "franka7_m02", "bimanual14", "arm3", "forest7"])
+def test_specialised_flags_match_reference(name):
+    g = golden(f"check_{name}.npz")
+    ck = _golden_world(name, g).checker(margin=float(g["margin"]))
+    assert ck.native.specialize(1), "NVRTC specialisation unavailable on this box"
+    free = ck.check_batch(g["Q"].astype(np.float64))
+    mism = (free != g["free"]) & (np.abs(g["clearance"]) >= BAND)
+    assert not mism.any(), f"{mism.sum()} flag mismatches outside the {BAND} band"
+
+
+def _statics_world():
+    """Franka arm among a static sphere, a static box and a voxel cloud."""
+    w = fx.franka7_world()
+    static = (Geometry(SPHERE, RigidTransform(np.eye(3), np.array([0.5, 0.3, 0.6])), radius=0.12),
+              Geometry(BOX, RigidTransform(np.eye(3), np.array([0.0, -0.5, 0.4])), half_extents=np.array([0.1, 0.2, 0.3])))
+    return World(w.model, static, w.vmap, w.lower, w.upper)
+
+
+@pytest.mark.parametrize("which", ["franka7", "bimanual14", "arm3", "statics"])
+@pytest.mark.parametrize("rows", ["float32", "float64"])
+def test_specialised_equals_generic(which, rows):
+    w = {"franka7": fx.franka7_world, "bimanual14": fx.bimanual14_world, "arm3": fx.arm3_world,
+         "statics": _statics_world}[which]()
+    gen, jit = w.checker(margin=0.01).native, w.checker(margin=0.01).native
+    gen.specialize(-1)
+    assert jit.specialize(1)
+    lo = torch.as_tensor(w.lower, dtype=torch.float64, device="cuda")
+    hi = torch.as_tensor(w.upper, dtype=torch.float64, device="cuda")
+    g = torch.Generator(device="cuda")
+    g.manual_seed(11)
+    Q = (lo + (hi - lo) * torch.rand((300_000, w.model.dof), generator=g, device="cuda", dtype=torch.float64))
+    Q = Q.to(getattr(torch, rows))
+    a, b = gen.check_device(Q), jit.check_device(Q)
+    assert 0.0 < float(a.float().mean()) < 1.0
+    assert torch.equal(a, b)
+
+
+def test_robot_boxes_stay_generic():
+    from oracle.make_scenes import box_arm3d
+    ck = World(box_arm3d()).checker()
+    assert not ck.native.specialize(1)
+    assert not ck.native.specialize(0)
+
+
+def test_large_batches_specialise_automatically():
+    w = fx.franka7_world()
+    nat = w.checker().native
+    assert not nat.specialize(0)
+    lo = torch.as_tensor(w.lower, dtype=torch.float32, device="cuda")
+    hi = torch.as_tensor(w.upper, dtype=torch.float32, device="cuda")
+    nat.check_device(lo + (hi - lo) * torch.rand((1 << 18, 7), device="cuda"))
+    assert nat.specialize(0)
