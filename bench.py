@@ -186,6 +186,7 @@ def bench_drm(n_nodes: int = 100_000, reps: int = 10, cpu: bool = True) -> dict:
 
     grid = Grid(np.array([-0.75, -1.02, -0.36]), 0.06, (25, 34, 26))
     base = fx.franka7_world(False)
+    sample_free_nodes(base, n_nodes, seed=0)  # warm-up: compiles the specialised check kernel once
     t0 = time.perf_counter()
     nodes = sample_free_nodes(base, n_nodes, seed=0)
     t_nodes = time.perf_counter() - t0

@@ -424,7 +424,11 @@ int32_t jit_specialize(ez_world* w) {
     };
     if (w->mf.n_boxes > 0 || w->mf.n_mix > 0) return refuse(EZ_UNSUPPORTED, "robot boxes use the generic check kernel");
     if (w->h_blob_f.empty()) return refuse(EZ_UNSUPPORTED, "no host copy of the model");
-    const int bt = 128;
+    static const int bt = [] {  // CTA size (EZ_JIT_BT: 64, 128 or 256)
+        const char* e = getenv("EZ_JIT_BT");
+        const int v = e ? atoi(e) : 128;
+        return (v == 64 || v == 256) ? v : 128;
+    }();
     const std::string src = jit_source(w, bt);
     if (const char* dump = getenv("EZ_JIT_DUMP")) {  // inspection: write the generated source
         if (FILE* f = fopen(dump, "w")) {

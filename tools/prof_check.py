@@ -7,11 +7,15 @@ from paper_2504_10783_b200 import fixtures as fx
 
 w = fx.franka7_world()
 nat = w.checker().native
+if "--generic" in sys.argv:
+    nat.specialize(-1)
+else:
+    print("specialised:", nat.specialize(1))
 lo = torch.as_tensor(w.lower, dtype=torch.float32, device="cuda")
 hi = torch.as_tensor(w.upper, dtype=torch.float32, device="cuda")
 g = torch.Generator(device="cuda"); g.manual_seed(1)
 Q = lo + (hi - lo) * torch.rand((1 << 20, 7), generator=g, device="cuda")
-prec = sys.argv[1] if len(sys.argv) > 1 else "fp32"
+prec = "fp64" if "fp64" in sys.argv else "fp32"
 for _ in range(4):
     out = nat.check_device(Q, precision=prec)
 torch.cuda.synchronize()
