@@ -3,7 +3,7 @@
 // per-model kernels compiled at run time (ez_jit.cu).  Replaces
 // corridor/world.py:483-517 (check_batch / _check_chunk).
 //
-// Two phases per tile of BT configurations:
+// Two phases per tile of bt configurations (one CTA):
 //   A) every thread: FK + the calibrated hot self pairs.  Most colliding
 //      configurations are decided here.
 //   B) survivors are appended (in index order) to a CTA ring buffer; whenever
@@ -41,44 +41,48 @@ __device__ __forceinline__ void check_phase_b(const P& pol, int dof, const Q* __
     if (n_col != nullptr && c2 && idx < count_lim) atomicAdd(n_col, 1);
 }
 
-// rows: BT * dof staging slots in shared memory; s_queue: 2 * BT entries;
-// s_warp: BT / 32 entries; cen: this thread's centre store.
+// rows: bt * dof staging slots in shared memory; s_queue: 2 * bt entries;
+// s_warp: bt / 32 entries; cen: this thread's centre store.  The CTA size bt
+// is BT, or blockDim.x for BT = 0 (one kernel launched at several sizes).
 template <typename T, typename Q, int BT, class P>
 __device__ __forceinline__ void check_tiles(const P& pol, int dof, T* my_cen, Q* rows, int32_t* s_queue, int* s_warp,
                                             const Q* __restrict__ q, int64_t n, int64_t ld,
                                             uint8_t* __restrict__ out, int64_t count_lim, int32_t* __restrict__ n_col) {
-    constexpr int qcap = 2 * BT;
+    const int bt = BT > 0 ? BT : static_cast<int>(blockDim.x);
+    const int qcap = 2 * bt;
+    // ring index; a run-time CTA size is a power of two
+    auto wrap = [&](int x) { return BT > 0 ? x % qcap : (x & (qcap - 1)); };
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     Q* my_row = rows + threadIdx.x * dof;
     const bool contiguous = (ld == dof) && (dof <= kPrefetch);
     int qhead = 0, qn = 0;  // ring buffer state (uniform across the CTA)
-    const int64_t tiles = (n + BT - 1) / BT;
+    const int64_t tiles = (n + bt - 1) / bt;
     Q pf[kPrefetch];
     auto prefetch = [&](int64_t tile) {
         if (tile >= tiles) return;
-        const int64_t base = tile * BT;
-        const int tot = static_cast<int>(min(static_cast<int64_t>(BT), n - base)) * dof;
+        const int64_t base = tile * bt;
+        const int tot = static_cast<int>(min(static_cast<int64_t>(bt), n - base)) * dof;
         const Q* src = q + base * dof;
 #pragma unroll
         for (int j = 0; j < kPrefetch; ++j) {
-            const int i = threadIdx.x + j * BT;
+            const int i = threadIdx.x + j * bt;
             if (i < tot) pf[j] = src[i];
         }
     };
     if (contiguous) prefetch(blockIdx.x);
     for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
-        const int64_t base = tile * BT;
-        const int nr = static_cast<int>(min(static_cast<int64_t>(BT), n - base));
+        const int64_t base = tile * bt;
+        const int nr = static_cast<int>(min(static_cast<int64_t>(bt), n - base));
         __syncthreads();
         if (contiguous) {
             const int tot = nr * dof;
 #pragma unroll
             for (int j = 0; j < kPrefetch; ++j) {
-                const int i = threadIdx.x + j * BT;
+                const int i = threadIdx.x + j * bt;
                 if (i < tot) rows[i] = pf[j];
             }
         } else {
-            for (int i = threadIdx.x; i < nr * dof; i += BT) {
+            for (int i = threadIdx.x; i < nr * dof; i += bt) {
                 const int r = i / dof, k = i - r * dof;
                 rows[i] = q[(base + r) * ld + k];
             }
@@ -102,24 +106,23 @@ __device__ __forceinline__ void check_tiles(const P& pol, int dof, T* my_cen, Q*
         if (lane == 0) s_warp[wid] = __popc(sm);
         __syncthreads();
         int off = 0, add = 0;
-#pragma unroll
-        for (int w = 0; w < BT / 32; ++w) {
+        for (int w = 0; w < bt / 32; ++w) {
             const int c = s_warp[w];
             off += (w < wid) ? c : 0;
             add += c;
         }
         if (surv)
-            s_queue[(qhead + qn + off + __popc(sm & ((1u << lane) - 1u))) % qcap] = static_cast<int32_t>(base + threadIdx.x);
+            s_queue[wrap(qhead + qn + off + __popc(sm & ((1u << lane) - 1u)))] = static_cast<int32_t>(base + threadIdx.x);
         qn += add;
         __syncthreads();
         // phase B on full CTAs; after the last tile, the partial rest
         const bool last = tile + gridDim.x >= tiles;
-        while (qn >= BT || (last && qn > 0)) {
-            if (threadIdx.x < min(qn, BT))
-                check_phase_b<T, Q, BT>(pol, dof, q, ld, s_queue[(qhead + threadIdx.x) % qcap], my_row, my_cen, out,
+        while (qn >= bt || (last && qn > 0)) {
+            if (threadIdx.x < min(qn, bt))
+                check_phase_b<T, Q, BT>(pol, dof, q, ld, s_queue[wrap(qhead + threadIdx.x)], my_row, my_cen, out,
                                         count_lim, n_col);
-            const int took = min(qn, BT);
-            qhead = (qhead + took) % qcap;
+            const int took = min(qn, bt);
+            qhead = wrap(qhead + took);
             qn -= took;
             __syncthreads();
         }

@@ -106,7 +106,6 @@ struct Gen {
     const ModelDev<float>& M;
     const uint8_t* blob;
     float margin;
-    int bt;
     std::ostringstream o;
 
     const JointRec<float>* J() const { return reinterpret_cast<const JointRec<float>*>(blob); }
@@ -279,20 +278,28 @@ struct Gen {
         obstacles();
         blocks();
         o << "    return false;\n    }\n};\n\n";
-        o << "template <typename Q>\n__device__ __forceinline__ void jit_body(const ModelDev<float>& M, const Q* q, int64_t n, "
-             "int64_t ld, uint8_t* out, int64_t count_lim, int32_t* n_col) {\n"
+        // per row type two kernels: 512 threads (compile-time CTA size, at most
+        // 128 registers) and up to 256 threads (CTA size from blockDim: 64..256,
+        // up to 255 registers); dynamic shared memory = rows, then the survivor
+        // ring of 2 * blockDim entries
+        o << "template <typename Q, int BT>\n__device__ __forceinline__ void jit_body(const ModelDev<float>& M, const Q* q, "
+             "int64_t n, int64_t ld, uint8_t* out, int64_t count_lim, int32_t* n_col) {\n"
           << "    extern __shared__ __align__(16) uint8_t smem[];\n"
-          << "    __shared__ int32_t s_queue[2 * " << bt << "];\n    __shared__ int s_warp[" << bt / 32 << "];\n"
+          << "    __shared__ int s_warp[16];\n"
+          << "    const size_t qoff = (static_cast<size_t>(BT > 0 ? BT : blockDim.x) * " << M.dof
+          << " * sizeof(Q) + 15) & ~size_t(15);\n"
           << "    const JitPolicy pol{M};\n"
-          << "    check_tiles<float, Q, " << bt << ">(pol, " << M.dof
-          << ", static_cast<float*>(nullptr), reinterpret_cast<Q*>(smem), s_queue, s_warp, q, n, ld, out, count_lim, n_col);\n}\n\n"
+          << "    check_tiles<float, Q, BT>(pol, " << M.dof
+          << ", static_cast<float*>(nullptr), reinterpret_cast<Q*>(smem), reinterpret_cast<int32_t*>(smem + qoff), s_warp, "
+             "q, n, ld, out, count_lim, n_col);\n}\n\n"
           << "}  // namespace ez\n\n";
-        for (const char* qt : {"float", "double"}) {
-            o << "extern \"C\" __global__ void __launch_bounds__(" << bt << ") ez_check_jit_" << qt[0]
-              << "(ez::ModelDev<float> M, const " << qt << "* __restrict__ q, int64_t n, int64_t ld, "
-              << "uint8_t* __restrict__ out, float, int64_t count_lim, int32_t* __restrict__ n_col) {\n"
-              << "    ez::jit_body<" << qt << ">(M, q, n, ld, out, count_lim, n_col);\n}\n";
-        }
+        for (const char* qt : {"float", "double"})
+            for (int bt : {256, 512}) {
+                o << "extern \"C\" __global__ void __launch_bounds__(" << bt << ") ez_check_jit_" << qt[0] << bt
+                  << "(ez::ModelDev<float> M, const " << qt << "* __restrict__ q, int64_t n, int64_t ld, "
+                  << "uint8_t* __restrict__ out, float, int64_t count_lim, int32_t* __restrict__ n_col) {\n"
+                  << "    ez::jit_body<" << qt << ", " << (bt == 512 ? 512 : 0) << ">(M, q, n, ld, out, count_lim, n_col);\n}\n";
+            }
         return o.str();
     }
 };
@@ -382,11 +389,10 @@ int32_t nvrtc_cubin(const std::string& src, std::vector<char>* cubin) {
     return EZ_OK;
 }
 
-int32_t compile(const std::string& src, int bt, std::shared_ptr<JitCheck>* out) {
+int32_t compile(const std::string& src, std::shared_ptr<JitCheck>* out) {
     std::vector<char> cubin;
     const std::string cp = cache_path(src);
     auto jc = std::make_shared<JitCheck>();
-    jc->bt = bt;
     bool loaded = false;
     if (read_file(cp, &cubin)) {  // a cached cubin that does not load is rebuilt
         loaded = cudaLibraryLoadData(&jc->lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0) == cudaSuccess;
@@ -397,8 +403,10 @@ int32_t compile(const std::string& src, int bt, std::shared_ptr<JitCheck>* out) 
         write_file(cp, cubin);
         EZ_CUDA(cudaLibraryLoadData(&jc->lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0));
     }
-    EZ_CUDA(cudaLibraryGetKernel(&jc->kf, jc->lib, "ez_check_jit_f"));
-    EZ_CUDA(cudaLibraryGetKernel(&jc->kd, jc->lib, "ez_check_jit_d"));
+    EZ_CUDA(cudaLibraryGetKernel(&jc->k[0][0], jc->lib, "ez_check_jit_f256"));
+    EZ_CUDA(cudaLibraryGetKernel(&jc->k[0][1], jc->lib, "ez_check_jit_f512"));
+    EZ_CUDA(cudaLibraryGetKernel(&jc->k[1][0], jc->lib, "ez_check_jit_d256"));
+    EZ_CUDA(cudaLibraryGetKernel(&jc->k[1][1], jc->lib, "ez_check_jit_d512"));
     *out = jc;
     return EZ_OK;
 }
@@ -409,10 +417,102 @@ JitCheck::~JitCheck() {
     if (lib) cudaLibraryUnload(lib);
 }
 
-std::string jit_source(const ez_world* w, int bt) {
-    Gen g{w->mf, w->h_blob_f.data(), static_cast<float>(w->margin), bt, {}};
+std::string jit_source(const ez_world* w) {
+    Gen g{w->mf, w->h_blob_f.data(), static_cast<float>(w->margin), {}};
     return g.source();
 }
+
+namespace {
+
+constexpr int kJitSizes[4] = {64, 128, 256, 512};
+
+size_t jit_smem(const ez_world* w, int bt, bool q64) {
+    const size_t rows = (static_cast<size_t>(bt) * w->dof * (q64 ? sizeof(double) : sizeof(float)) + 15) & ~size_t(15);
+    return rows + 2 * static_cast<size_t>(bt) * sizeof(int32_t);
+}
+
+// random rows in the joint box for the CTA-size pick
+__global__ void k_fill_box(float* q, int64_t n, int dof, const double* lo, const double* hi, uint64_t seed) {
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n * dof;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        uint64_t z = seed + static_cast<uint64_t>(i) * 0x9E3779B97F4A7C15ull;
+        z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+        z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+        z ^= z >> 31;
+        const int k = static_cast<int>(i % dof);
+        q[i] = static_cast<float>(lo[k] + (hi[k] - lo[k]) * ((z >> 11) * 0x1p-53));
+    }
+}
+
+int32_t launch_at(ez_world* w, int bt, const void* d_q, bool q64, int64_t n, int64_t ld, uint8_t* d_free,
+                  cudaStream_t stream, int64_t count_lim, int32_t* n_col) {
+    const JitCheck& jc = *w->jit;
+    int si = 0;
+    while (kJitSizes[si] != bt) ++si;
+    const cudaKernel_t kern = jc.k[q64 ? 1 : 0][bt == 512 ? 1 : 0];
+    const int64_t tiles = (n + bt - 1) / bt;
+    const unsigned grid = static_cast<unsigned>(
+        std::min<int64_t>(tiles, static_cast<int64_t>(w->num_sms) * w->jit_occ[q64 ? 1 : 0][si]));
+    ModelDev<float> M = w->mf;
+    float margin = static_cast<float>(w->margin);
+    void* args[] = {&M, const_cast<void**>(&d_q), &n, &ld, &d_free, &margin, &count_lim, &n_col};
+    EZ_CUDA(cudaLaunchKernel(reinterpret_cast<const void*>(kern), dim3(grid), dim3(bt), args, jit_smem(w, bt, q64),
+                             stream));
+    return EZ_OK;
+}
+
+// CTA size for large batches: one 512-thread CTA per SM keeps every warp of
+// the SM in the same region of the long straight-line kernel (instruction
+// cache), two 256-thread CTAs wait less at the tile barriers; time both.
+int32_t tune_bt(ez_world* w) {
+    const char* e = getenv("EZ_JIT_BT");
+    if (e && (atoi(e) == 256 || atoi(e) == 512)) {
+        w->jit_bt = atoi(e);
+        return EZ_OK;
+    }
+    const int64_t n = int64_t(1) << 19;
+    const int dof = w->dof;
+    float* d_q = nullptr;
+    double* d_box = nullptr;
+    uint8_t* d_out = nullptr;
+    cudaStream_t s = nullptr;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    int32_t st = EZ_OK;
+    auto ck = [&](cudaError_t r) {
+        if (r != cudaSuccess && st == EZ_OK) st = cuda_fail(r, "CTA-size pick", __FILE__, __LINE__);
+        return st == EZ_OK;
+    };
+    if (ck(cudaMalloc(&d_q, sizeof(float) * n * dof)) && ck(cudaMalloc(&d_out, n)) &&
+        ck(cudaMalloc(&d_box, sizeof(double) * 2 * dof)) &&
+        ck(cudaMemcpy(d_box, w->q_lo.data(), sizeof(double) * dof, cudaMemcpyHostToDevice)) &&
+        ck(cudaMemcpy(d_box + dof, w->q_hi.data(), sizeof(double) * dof, cudaMemcpyHostToDevice)) &&
+        ck(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking)) && ck(cudaEventCreate(&e0)) &&
+        ck(cudaEventCreate(&e1))) {
+        k_fill_box<<<256, 256, 0, s>>>(d_q, n, dof, d_box, d_box + dof, 0x7E57ull);
+        float best = 1e30f;
+        for (int bt : {512, 256}) {
+            for (int r = 0; r < 2 && st == EZ_OK; ++r) st = launch_at(w, bt, d_q, false, n, dof, d_out, s, 0, nullptr);
+            if (!ck(cudaEventRecord(e0, s))) break;
+            for (int r = 0; r < 3 && st == EZ_OK; ++r) st = launch_at(w, bt, d_q, false, n, dof, d_out, s, 0, nullptr);
+            float ms = 0.f;
+            if (!ck(cudaEventRecord(e1, s)) || !ck(cudaEventSynchronize(e1)) || !ck(cudaEventElapsedTime(&ms, e0, e1)))
+                break;
+            if (ms < best) {
+                best = ms;
+                w->jit_bt = bt;
+            }
+        }
+    }
+    cudaFree(d_q);
+    cudaFree(d_out);
+    cudaFree(d_box);
+    if (e0) cudaEventDestroy(e0);
+    if (e1) cudaEventDestroy(e1);
+    if (s) cudaStreamDestroy(s);
+    return st;
+}
+
+}  // namespace
 
 int32_t jit_specialize(ez_world* w) {
     if (w->jit) return EZ_OK;
@@ -424,12 +524,7 @@ int32_t jit_specialize(ez_world* w) {
     };
     if (w->mf.n_boxes > 0 || w->mf.n_mix > 0) return refuse(EZ_UNSUPPORTED, "robot boxes use the generic check kernel");
     if (w->h_blob_f.empty()) return refuse(EZ_UNSUPPORTED, "no host copy of the model");
-    static const int bt = [] {  // CTA size (EZ_JIT_BT: 64, 128 or 256)
-        const char* e = getenv("EZ_JIT_BT");
-        const int v = e ? atoi(e) : 128;
-        return (v == 64 || v == 256) ? v : 128;
-    }();
-    const std::string src = jit_source(w, bt);
+    const std::string src = jit_source(w);
     if (const char* dump = getenv("EZ_JIT_DUMP")) {  // inspection: write the generated source
         if (FILE* f = fopen(dump, "w")) {
             fwrite(src.data(), 1, src.size(), f);
@@ -443,7 +538,7 @@ int32_t jit_specialize(ez_world* w) {
         if (it != g_cache.end()) jc = it->second;
     }
     if (!jc) {
-        const int32_t st = compile(src, bt, &jc);
+        const int32_t st = compile(src, &jc);
         if (st != EZ_OK) {
             w->jit_failed = true;
             w->jit_error = ez_last_error();
@@ -453,31 +548,40 @@ int32_t jit_specialize(ez_world* w) {
         g_cache.emplace(src, jc);
     }
     for (int i = 0; i < 2; ++i) {
-        const void* k = reinterpret_cast<const void*>(i == 0 ? jc->kf : jc->kd);
-        const size_t smem = static_cast<size_t>(bt) * w->dof * (i == 0 ? sizeof(float) : sizeof(double));
-        int occ = 0;
-        EZ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, bt, smem));
-        if (occ < 1) return refuse(EZ_CAPACITY, "specialised check kernel does not fit on an SM");
-        w->jit_occ[i] = occ;
+        for (int v = 0; v < 2; ++v) {
+            const void* k = reinterpret_cast<const void*>(jc->k[i][v]);
+            EZ_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(jit_smem(w, v ? 512 : 256, i == 1))));
+        }
+        for (int si = 0; si < 4; ++si) {
+            const void* k = reinterpret_cast<const void*>(jc->k[i][kJitSizes[si] == 512 ? 1 : 0]);
+            int occ = 0;
+            EZ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, kJitSizes[si], jit_smem(w, kJitSizes[si], i == 1)));
+            if (occ < 1) return refuse(EZ_CAPACITY, "specialised check kernel does not fit on an SM");
+            w->jit_occ[i][si] = occ;
+        }
     }
     w->jit = jc;
-    return EZ_OK;
+    const int32_t st = tune_bt(w);
+    if (st != EZ_OK) w->jit.reset();
+    return st;
 }
 
+// Large batches run at the tuned CTA size; a batch too small to give every
+// SM a CTA at that size (host-path chunks, the EI-ZO loop's 1e4-row batches)
+// drops to the largest size that does, down to 64 threads.
 int32_t jit_launch(ez_world* w, const void* d_q, bool q64, int64_t n, int64_t ld, uint8_t* d_free,
                    cudaStream_t stream, int64_t count_lim, int32_t* n_col) {
-    const JitCheck& jc = *w->jit;
-    const int bt = jc.bt;
-    const size_t smem = static_cast<size_t>(bt) * w->dof * (q64 ? sizeof(double) : sizeof(float));
-    const int64_t tiles = (n + bt - 1) / bt;
-    const unsigned grid =
-        static_cast<unsigned>(std::min<int64_t>(tiles, static_cast<int64_t>(w->num_sms) * w->jit_occ[q64 ? 1 : 0]));
-    ModelDev<float> M = w->mf;
-    float margin = static_cast<float>(w->margin);
-    void* args[] = {&M, const_cast<void**>(&d_q), &n, &ld, &d_free, &margin, &count_lim, &n_col};
-    EZ_CUDA(cudaLaunchKernel(reinterpret_cast<const void*>(q64 ? jc.kd : jc.kf), dim3(grid), dim3(bt), args, smem,
-                             stream));
-    return EZ_OK;
+    int bt = 64;
+    for (int si = 3; si >= 0; --si) {
+        const int cand = kJitSizes[si];
+        if (cand > w->jit_bt) continue;
+        if ((n + cand - 1) / cand >= static_cast<int64_t>(w->num_sms)) {
+            bt = cand;
+            break;
+        }
+    }
+    return launch_at(w, bt, d_q, q64, n, ld, d_free, stream, count_lim, n_col);
 }
 
 }  // namespace ez

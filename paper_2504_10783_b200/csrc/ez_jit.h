@@ -9,21 +9,22 @@ struct ez_world;
 
 namespace ez {
 
-// One compiled module: the check kernel for one robot model (and margin), for
-// fp32 and fp64 configuration rows.  Kept for the life of the process.
+// One compiled module: the check kernels for one robot model (and margin).
+// k[rows f32/f64][0: 64..256 threads, 1: 512 threads].  Kept for the life of
+// the process.
 struct JitCheck {
     cudaLibrary_t lib = nullptr;
-    cudaKernel_t kf = nullptr;  // rows as float
-    cudaKernel_t kd = nullptr;  // rows as double
-    int bt = 128;
+    cudaKernel_t k[2][2] = {};
     ~JitCheck();
 };
 
 // Generate, compile (NVRTC, sm_100a) and load the world's specialised check
-// kernel; EZ_UNSUPPORTED if the model has robot boxes or NVRTC is missing.
+// kernel, then pick its CTA size for large batches by timing 256 and 512
+// threads on random configurations; EZ_UNSUPPORTED if the model has robot
+// boxes or NVRTC is missing.
 int32_t jit_specialize(ez_world* w);
 // CUDA source of the specialised kernel (for inspection and tests)
-std::string jit_source(const ez_world* w, int bt);
+std::string jit_source(const ez_world* w);
 // Launch it over n rows (fp32 arithmetic).
 int32_t jit_launch(ez_world* w, const void* d_q, bool q64, int64_t n, int64_t ld, uint8_t* d_free,
                    cudaStream_t stream, int64_t count_lim, int32_t* n_col);

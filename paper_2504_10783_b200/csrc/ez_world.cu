@@ -1115,6 +1115,13 @@ extern "C" int32_t ez_world_create(const ez_robot_desc* rb, const ez_scene_desc*
     if (st == EZ_OK && sc && sc->n_voxels > 0) st = build_voxel_grid(w, sc, hm, dim);
     if (st == EZ_OK && rb->joint_lower && rb->joint_upper && hm.dof > 0 && !hm.spheres.empty())
         st = calibrate_layout(w, hm, rb->joint_lower, rb->joint_upper);
+    w->q_lo.assign(hm.dof, -3.14159265358979);
+    w->q_hi.assign(hm.dof, 3.14159265358979);
+    if (rb->joint_lower && rb->joint_upper)
+        for (int k = 0; k < hm.dof; ++k) {
+            w->q_lo[k] = rb->joint_lower[k];
+            w->q_hi[k] = rb->joint_upper[k];
+        }
     if (st != EZ_OK) {
         world_free(w);
         return st;

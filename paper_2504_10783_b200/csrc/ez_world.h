@@ -53,10 +53,12 @@ struct ez_world {
     // run-time specialised fp32 check kernel (ez_jit.cu) and the host copy of
     // the fp32 model blob it is generated from
     std::vector<uint8_t> h_blob_f;
+    std::vector<double> q_lo, q_hi;  // joint box (the specialised kernel's CTA size is tuned on it)
     std::shared_ptr<ez::JitCheck> jit;
     bool jit_failed = false;
     std::string jit_error;
-    int32_t jit_occ[2] = {0, 0};
+    int32_t jit_bt = 512;            // CTA size for large batches
+    int32_t jit_occ[2][4] = {};      // [rows f32/f64][CTA size 64/128/256/512] resident CTAs per SM
 
     // cached launch shapes of k_check, [T fp64][Q fp64]
     int32_t launch_threads[4] = {0, 0, 0, 0};
