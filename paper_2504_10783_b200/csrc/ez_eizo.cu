@@ -44,23 +44,36 @@ __device__ __forceinline__ unsigned group_mask() {
 
 // A: faces, row f at A + f * lda.  VEC: rows are 16-byte aligned with lda
 // even (shared-memory staging), so a row is read as double2 pairs.
+// Zw: the walk's counter-stream draws (k_draws), element (step, k) at
+// Zw[(step * (d + 1) + k) * zs]; they are loaded one step ahead.
 template <int MAXD, int RNG, int LPW, bool VEC>
 __device__ __forceinline__ int hnr_walk(double (&x)[MAXD], int d, const double* __restrict__ A, int lda,
                                         const double* __restrict__ b, int F, int n_ms, uint64_t seed,
-                                        uint64_t walk, bool check_seed) {
+                                        uint64_t walk, bool check_seed, const double* __restrict__ Zw, int64_t zs) {
     constexpr int PER = (MAXD + LPW - 1) / LPW;  // normals drawn per lane
     const unsigned gm = group_mask<LPW>();
     const int lane = threadIdx.x & (LPW - 1);
-    const uint64_t key = (RNG == EZ_RNG_COUNTER) ? walk_key(seed, walk) : 0ull;
+    double nxt[PER], nxt_u = 0.0;
+    auto load_draws = [&](int step) {
+        if (RNG != EZ_RNG_COUNTER || step >= n_ms) return;
+        const double* z = Zw + static_cast<int64_t>(step) * (d + 1) * zs;
+#pragma unroll
+        for (int j = 0; j < PER; ++j) {
+            const int k = lane + j * LPW;
+            nxt[j] = (k < d) ? __ldg(z + k * zs) : 0.0;
+        }
+        nxt_u = __ldg(z + d * zs);
+    };
+    load_draws(0);
     for (int step = 0; step < n_ms; ++step) {
         double dir[MAXD];
+        double cur_u = 0.0;
         if (RNG == EZ_RNG_COUNTER) {
             double mine[PER];
 #pragma unroll
-            for (int j = 0; j < PER; ++j) {
-                const int k = lane + j * LPW;
-                mine[j] = (k < d) ? counter_normal(key, static_cast<uint64_t>(step), k) : 0.0;
-            }
+            for (int j = 0; j < PER; ++j) mine[j] = nxt[j];
+            cur_u = nxt_u;
+            load_draws(step + 1);  // in flight while this step runs
 #pragma unroll
             for (int k = 0; k < MAXD; ++k) dir[k] = __shfl_sync(gm, mine[k / LPW], k % LPW, LPW);
         } else {
@@ -162,7 +175,7 @@ __device__ __forceinline__ int hnr_walk(double (&x)[MAXD], int d, const double* 
         thi = fmax(thi, 0.0);
         double u;
         if (RNG == EZ_RNG_COUNTER) {
-            u = counter_uniform(key, static_cast<uint64_t>(step), d);
+            u = cur_u;
         } else {
             const Philox4 r = philox_draw(seed, walk, static_cast<uint32_t>(step), static_cast<uint32_t>((d + 3) / 4));
             u = philox_u53(r.x, r.y);
@@ -173,6 +186,26 @@ __device__ __forceinline__ int hnr_walk(double (&x)[MAXD], int d, const double* 
             if (k < d) x[k] = __dadd_rn(x[k], __dmul_rn(dir[k], tt));
     }
     return EZ_OK;
+}
+
+// All counter-stream draws of a walk batch, ahead of the walks:
+// Z[(step * (d + 1) + k) * count + i] is normal k (k < d) or the uniform
+// (k = d) of walk walk_offset + i at mixing step `step` (seeding.py:40-60).
+// They do not depend on the walk state, so generating them here (fully
+// parallel, throughput bound) leaves the walk's 60-step critical path with
+// loads issued a step ahead instead of hash + ndtri chains.
+__global__ void k_draws(uint64_t seed, uint64_t walk_offset, int64_t count, int d, int n_ms, double* __restrict__ Z,
+                        const int32_t* __restrict__ status) {
+    if (status && (status[0] != EZ_OK || status[1] != 0)) return;
+    const int64_t total = count * n_ms * (d + 1);
+    for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < total;
+         t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t i = t % count, sk = t / count;
+        const int k = static_cast<int>(sk % (d + 1));
+        const uint64_t step = static_cast<uint64_t>(sk / (d + 1));
+        const uint64_t key = walk_key(seed, walk_offset + static_cast<uint64_t>(i));
+        Z[t] = (k < d) ? counter_normal(key, step, k) : counter_uniform(key, step, d);
+    }
 }
 
 // Walk i starts at seeds[i % n_seeds] (explicit seeds) or at a point of the
@@ -187,7 +220,7 @@ __global__ void __launch_bounds__(BT)
 k_hnr(const double* __restrict__ A, const double* __restrict__ b, const int32_t* __restrict__ F_dev, int F,
       int d, const double* __restrict__ seeds, int64_t n_seeds, const double* __restrict__ seg, int64_t count,
       int n_ms, uint64_t seed, uint64_t walk_offset, double* __restrict__ out, int32_t* __restrict__ status,
-      int smem_faces, int lda) {
+      int smem_faces, int lda, const double* __restrict__ Z) {
     extern __shared__ __align__(16) double s_faces[];
     if (F_dev) F = *F_dev;
     if (status[0] != EZ_OK || status[1] != 0) return;  // (status, stop)
@@ -220,9 +253,11 @@ k_hnr(const double* __restrict__ A, const double* __restrict__ b, const int32_t*
 #pragma unroll
         for (int k = 0; k < MAXD; ++k) x[k] = (k < d) ? __dadd_rn(seg[k], __dmul_rn(alpha, seg[d + k])) : 0.0;
     }
+    const double* Zw = Z ? Z + i : nullptr;
     const int st = staged ? hnr_walk<MAXD, RNG, LPW, true>(x, d, s_faces, lda, s_faces + F * lda, F, n_ms, seed, walk,
-                                                           seeds == nullptr)
-                          : hnr_walk<MAXD, RNG, LPW, false>(x, d, A, d, b, F, n_ms, seed, walk, seeds == nullptr);
+                                                           seeds == nullptr, Zw, count)
+                          : hnr_walk<MAXD, RNG, LPW, false>(x, d, A, d, b, F, n_ms, seed, walk, seeds == nullptr, Zw,
+                                                            count);
     if (st != EZ_OK) {
         if (lane == 0) set_status(status, st);
         return;
@@ -288,7 +323,8 @@ template <int KC>
 __global__ void __launch_bounds__(64, KC >= 8 ? 8 : 11)
 k_hnr_mma(const double* __restrict__ Ap, const int32_t* __restrict__ F_dev, int F, int d,
           const double* __restrict__ seeds, int64_t n_seeds, const double* __restrict__ seg, int64_t count,
-          int n_ms, uint64_t seed, uint64_t walk_offset, double* __restrict__ out, int32_t* __restrict__ status) {
+          int n_ms, uint64_t seed, uint64_t walk_offset, double* __restrict__ out, int32_t* __restrict__ status,
+          const double* __restrict__ Z) {
     constexpr int KP = 4 * KC;
     if (F_dev) F = *F_dev;
     if (status[0] != EZ_OK || status[1] != 0) return;
@@ -298,11 +334,24 @@ k_hnr_mma(const double* __restrict__ Ap, const int32_t* __restrict__ F_dev, int 
     const int wl = lane >> 2, c = lane & 3;
     const int64_t wi = min(wbase + wl, count - 1);  // idle slots shadow the last walk
     const uint64_t key = walk_key(seed, walk_offset + static_cast<uint64_t>(wi));
-    // the walks whose C entries this lane owns
-    uint64_t skey[2];
+    // the walks whose C entries this lane owns (their uniforms)
+    int64_t sw[2];
 #pragma unroll
-    for (int s2 = 0; s2 < 2; ++s2)
-        skey[s2] = walk_key(seed, walk_offset + static_cast<uint64_t>(min(wbase + 2 * c + s2, count - 1)));
+    for (int s2 = 0; s2 < 2; ++s2) sw[s2] = min(wbase + 2 * c + s2, count - 1);
+    const int64_t zstep = static_cast<int64_t>(d + 1) * count;
+    double nd[KC], nu[2];
+    auto load_draws = [&](int step) {
+        if (step >= n_ms) return;
+        const double* z = Z + step * zstep;
+#pragma unroll
+        for (int j = 0; j < KC; ++j) {
+            const int k = 4 * j + c;
+            nd[j] = (k < d) ? __ldg(z + k * count + wi) : 0.0;
+        }
+#pragma unroll
+        for (int s2 = 0; s2 < 2; ++s2) nu[s2] = __ldg(z + d * count + sw[s2]);
+    };
+    load_draws(0);
     double x[KC], dr[KC];
     if (seeds) {
         const double* sp = seeds + (wi % n_seeds) * d;
@@ -323,11 +372,12 @@ k_hnr_mma(const double* __restrict__ Ap, const int32_t* __restrict__ F_dev, int 
     const int tiles = (F + 7) >> 3;
     const double* arow = Ap + static_cast<int64_t>(wl) * KP + c;
     for (int step = 0; step < n_ms; ++step) {
+        double cu[2];
 #pragma unroll
-        for (int j = 0; j < KC; ++j) {
-            const int k = 4 * j + c;
-            dr[j] = (k < d) ? counter_normal(key, static_cast<uint64_t>(step), k) : 0.0;
-        }
+        for (int j = 0; j < KC; ++j) dr[j] = nd[j];
+        cu[0] = nu[0];
+        cu[1] = nu[1];
+        load_draws(step + 1);  // in flight while this step runs
         // numpy-order norm: squares summed left to right over k
         double ss = 0.0;
 #pragma unroll
@@ -398,8 +448,7 @@ k_hnr_mma(const double* __restrict__ Ap, const int32_t* __restrict__ F_dev, int 
             if (thi < tlo - kChordTol) err = EZ_EMPTY_CHORD;
             tlo = fmin(tlo, 0.0);
             thi = fmax(thi, 0.0);
-            const double u = counter_uniform(skey[s2], static_cast<uint64_t>(step), d);
-            tt[s2] = __dadd_rn(tlo, __dmul_rn(u, thi - tlo));
+            tt[s2] = __dadd_rn(tlo, __dmul_rn(cu[s2], thi - tlo));
         }
         if (any_out) {
             if (lane == 0) set_status(status, EZ_SEED_OUTSIDE);
@@ -729,6 +778,8 @@ struct ez_eizo_ws {
     double* b = nullptr;
     double* Ap = nullptr;   // padded faces for the tensor-core walk
     int64_t ap_cap = 0;
+    double* Z = nullptr;    // counter-stream draws of one sample batch (k_draws)
+    int64_t z_cap = 0;
     double* X = nullptr;
     uint8_t* flags = nullptr;
     int32_t* col = nullptr;
@@ -750,6 +801,7 @@ void eizo_ws_free(ez_eizo_ws* ws) {
     cudaFree(ws->A);
     cudaFree(ws->b);
     cudaFree(ws->Ap);
+    cudaFree(ws->Z);
     cudaFree(ws->X);
     cudaFree(ws->flags);
     cudaFree(ws->col);
@@ -785,7 +837,7 @@ static ez_eizo_ws* g_ws[64] = {};
 
 static ez_eizo_ws*& device_ws(int device) { return g_ws[device & 63]; }
 
-static int32_t ws_reserve(ez_world* w, int d, int64_t n, int32_t c, int32_t f) {
+static int32_t ws_reserve(ez_world* w, int d, int64_t n, int32_t c, int32_t f, int n_ms) {
     ez_eizo_ws*& slot = device_ws(w->device);
     if (!slot) {
         slot = new ez_eizo_ws();
@@ -824,6 +876,10 @@ static int32_t ws_reserve(ez_world* w, int d, int64_t n, int32_t c, int32_t f) {
         EZ_TRY(grow(&ws->Ap, 0, hnr_ap_words(f, d), false));
         ws->ap_cap = hnr_ap_words(f, d);
     }
+    if (n * n_ms * (d + 1) > ws->z_cap) {
+        EZ_TRY(grow(&ws->Z, 0, n * n_ms * (d + 1), false));
+        ws->z_cap = n * n_ms * (d + 1);
+    }
     return EZ_OK;
 }
 
@@ -838,7 +894,7 @@ template <int MAXD, int RNG, int LPW, int BT>
 static int32_t launch_hnr_t(cudaStream_t s, const double* A, const double* b, const int32_t* F_dev,
                             int F, int smem_faces, int d, const double* seeds, int64_t n_seeds, const double* seg,
                             int64_t count, int n_ms, uint64_t seed, uint64_t walk_offset, double* out,
-                            int32_t* status) {
+                            int32_t* status, const double* Z) {
     auto k = k_hnr<MAXD, RNG, LPW, BT>;
     const int lda = hnr_lda(d);
     const size_t smem = static_cast<size_t>(smem_faces) * (lda + 1) * sizeof(double);
@@ -846,7 +902,7 @@ static int32_t launch_hnr_t(cudaStream_t s, const double* A, const double* b, co
     const int64_t threads = count * LPW;
     const unsigned grid = static_cast<unsigned>((threads + BT - 1) / BT);
     k<<<grid, BT, smem, s>>>(A, b, F_dev, F, d, seeds, n_seeds, seg, count, n_ms, seed, walk_offset, out, status,
-                             smem_faces, lda);
+                             smem_faces, lda, Z);
     EZ_CUDA(cudaGetLastError());
     return EZ_OK;
 }
@@ -854,17 +910,20 @@ static int32_t launch_hnr_t(cudaStream_t s, const double* A, const double* b, co
 // Launch shape: lanes per walk (LPW), CTA size and face staging.  Each lane
 // owns every LPW-th face, so fewer lanes per walk means more walks read each
 // staged face row at once (less shared-memory traffic per FMA) but fewer
-// walks in flight.  Every candidate is costed as rounds of resident walks
-// (registers: 128 per lane; shared memory: the staged faces) times the
-// per-lane step cost (faces + normals + shuffle reductions); unstaged faces
-// are read through L1 at about 2.5x the cost.
+// walks in flight.  Cost model per candidate: the per-lane step cost (faces +
+// draw loads + shuffle reductions; unstaged faces read through L1 cost about
+// 2.5x) times the busiest SM's load, as issue throughput (its warps at IPC 2)
+// or as latency (its rounds of resident CTAs, ~4 cycles per dependent
+// instruction), whichever is larger.  Small CTAs spread a 1e4-walk batch over
+// all SMs instead of leaving a third of them idle.
 struct HnrShape {
     int lpw, bt;
     bool staged;
 };
 
 static HnrShape hnr_pick(int maxd, int d, int f, int64_t count, int num_sms, int optin) {
-    const HnrShape cands[5] = {{maxd, 128, true}, {maxd, 512, true}, {8, 512, true}, {4, 512, true}, {maxd, 128, false}};
+    const HnrShape cands[8] = {{maxd, 128, true}, {maxd, 512, true}, {8, 512, true}, {8, 128, true},
+                               {4, 512, true},    {4, 128, true},    {maxd, 128, false}, {maxd, 512, false}};
     const size_t smem = static_cast<size_t>(f) * (hnr_lda(d) + 1) * sizeof(double);
     HnrShape best = {maxd, 128, false};
     double best_t = 1e300;
@@ -876,12 +935,13 @@ static HnrShape hnr_pick(int maxd, int d, int f, int64_t count, int num_sms, int
         int per_sm = 65536 / (128 * c.bt);
         if (c.staged) per_sm = std::min<int>(per_sm, static_cast<int>((228 * 1024) / (smem + 1024)));
         if (per_sm < 1) continue;
-        const double walks = static_cast<double>(num_sms) * per_sm * (c.bt / c.lpw);
-        const double rounds = std::ceil(static_cast<double>(count) / walks);
+        const double ctas = std::ceil(static_cast<double>(count) * c.lpw / c.bt);
         const double face = std::ceil(static_cast<double>(f) / c.lpw) * (2.5 * d + 12.0) * (c.staged ? 1.0 : 2.5);
-        const double per_step = face + std::ceil(static_cast<double>(d) / c.lpw) * 180.0 +
-                                14.0 * std::log2(static_cast<double>(c.lpw)) + 60.0;
-        const double t = rounds * per_step;
+        const double cost = face + std::ceil(static_cast<double>(d) / c.lpw) * 20.0 +
+                            14.0 * std::log2(static_cast<double>(c.lpw)) + 60.0;
+        const double thr = std::ceil(ctas / num_sms) * (c.bt / 32) * cost / 2.0;
+        const double lat = std::ceil(ctas / (static_cast<double>(num_sms) * per_sm)) * cost * 4.0;
+        const double t = std::max(thr, lat);
         if (t < best_t * 0.97) {
             best_t = t;
             best = c;
@@ -894,7 +954,7 @@ template <int MAXD>
 static int32_t launch_hnr(const ez_world* w, int rng, cudaStream_t s, const double* A, const double* b,
                           const int32_t* F_dev, int F, int f_bound, int d, const double* seeds, int64_t n_seeds,
                           const double* seg, int64_t count, int n_ms, uint64_t seed, uint64_t walk_offset, double* out,
-                          int32_t* status) {
+                          int32_t* status, const double* Z) {
     int optin = 0, sms = 0;
     if (w) {
         optin = w->smem_optin;
@@ -911,60 +971,86 @@ static int32_t launch_hnr(const ez_world* w, int rng, cudaStream_t s, const doub
 #define EZ_HNR_GO(LPW_, BT_)                                                                                      \
     return (rng == EZ_RNG_PHILOX)                                                                                  \
                ? launch_hnr_t<MAXD, EZ_RNG_PHILOX, LPW_, BT_>(s, A, b, F_dev, F, smem_faces, d, seeds, n_seeds,    \
-                                                               seg, count, n_ms, seed, walk_offset, out, status)    \
+                                                               seg, count, n_ms, seed, walk_offset, out, status, Z) \
                : launch_hnr_t<MAXD, EZ_RNG_COUNTER, LPW_, BT_>(s, A, b, F_dev, F, smem_faces, d, seeds, n_seeds,   \
-                                                                seg, count, n_ms, seed, walk_offset, out, status)
+                                                                seg, count, n_ms, seed, walk_offset, out, status, Z)
     if constexpr (MAXD <= 16) {
         if (sh.lpw == MAXD && sh.bt == 512) { EZ_HNR_GO(MAXD, 512); }
     }
     if constexpr (MAXD == 16 || MAXD == 8) {
-        if (sh.lpw == 4) { EZ_HNR_GO(4, 512); }
+        if (sh.lpw == 4 && sh.bt == 512) { EZ_HNR_GO(4, 512); }
+        if (sh.lpw == 4) { EZ_HNR_GO(4, 128); }
         if constexpr (MAXD == 16) {
-            if (sh.lpw == 8) { EZ_HNR_GO(8, 512); }
+            if (sh.lpw == 8 && sh.bt == 512) { EZ_HNR_GO(8, 512); }
+            if (sh.lpw == 8) { EZ_HNR_GO(8, 128); }
         }
     }
     EZ_HNR_GO(MAXD, 128);
 #undef EZ_HNR_GO
 }
 
-constexpr int kMmaFaces = 96;  // from this many faces on, walks run on the FP64 tensor cores
+// Counter-stream walks run on the FP64 tensor cores at every face count
+// (measured: 7-DOF region 3.34 -> 2.81 ms with 14-64 faces); the lane-per-face
+// walk serves the Philox stream (EZ_HNR_MMA_FACES / EZ_HNR_NO_MMA override).
+constexpr int kMmaFaces = 0;
 
 template <int KC>
 static int32_t launch_hnr_mma(cudaStream_t s, const double* Ap, const int32_t* F_dev, int F, int d,
                               const double* seeds, int64_t n_seeds, const double* seg, int64_t count, int n_ms,
-                              uint64_t seed, uint64_t walk_offset, double* out, int32_t* status) {
+                              uint64_t seed, uint64_t walk_offset, double* out, int32_t* status, const double* Z) {
     const int64_t warps = (count + 7) / 8;
     k_hnr_mma<KC><<<static_cast<unsigned>((warps + 1) / 2), 64, 0, s>>>(Ap, F_dev, F, d, seeds, n_seeds, seg, count,
-                                                                          n_ms, seed, walk_offset, out, status);
+                                                                          n_ms, seed, walk_offset, out, status, Z);
     EZ_CUDA(cudaGetLastError());
     return EZ_OK;
 }
 
 // f_bound: largest face count the walk may see (faces live on the device in
 // the EI-ZO loop).  Ap: scratch of at least hnr_ap_words(f_bound, d) doubles
-// for the tensor-core path, or nullptr (allocated on the stream).
+// for the tensor-core path, Z: scratch of hnr_draw_words(count, n_ms, d)
+// doubles for the counter-stream draws; nullptr = allocated on the stream.
+static int64_t hnr_draw_words(int64_t count, int n_ms, int d) { return count * n_ms * (d + 1); }
+
 static int32_t dispatch_hnr(const ez_world* w, int rng, cudaStream_t s, const double* A, const double* b,
                             const int32_t* F_dev, int F, int f_bound, int d, const double* seeds, int64_t n_seeds,
                             const double* seg, int64_t count, int n_ms, uint64_t seed, uint64_t walk_offset,
-                            double* out, int32_t* status, double* Ap = nullptr) {
+                            double* out, int32_t* status, double* Ap = nullptr, double* Z = nullptr) {
+    if (d > 32) return fail(EZ_UNSUPPORTED, "hit-and-run supports dimension <= 32");
     const int fmax = std::max(F, f_bound);
-    if (rng == EZ_RNG_COUNTER && fmax >= kMmaFaces && d <= 31 && !getenv("EZ_HNR_NO_MMA")) {
+    double* z = nullptr;
+    if (rng == EZ_RNG_COUNTER) {
+        z = Z;
+        if (!z) EZ_CUDA(cudaMallocAsync(&z, sizeof(double) * hnr_draw_words(count, n_ms, d), s));
+        const int64_t total = hnr_draw_words(count, n_ms, d);
+        const unsigned grid = static_cast<unsigned>(std::min<int64_t>((total + 255) / 256, 148 * 16));
+        k_draws<<<grid, 256, 0, s>>>(seed, walk_offset, count, d, n_ms, z, status);
+        EZ_CUDA(cudaGetLastError());
+    }
+    int32_t st;
+    static const int mma_faces = [] {
+        const char* e = getenv("EZ_HNR_MMA_FACES");
+        return e ? atoi(e) : kMmaFaces;
+    }();
+    if (rng == EZ_RNG_COUNTER && fmax >= mma_faces && d <= 31 && !getenv("EZ_HNR_NO_MMA")) {
         const int kp = hnr_mma_kp(d);
         double* ap = Ap;
         if (!ap) EZ_CUDA(cudaMallocAsync(&ap, sizeof(double) * hnr_ap_words(fmax, d), s));
         k_pack_faces<<<64, 256, 0, s>>>(A, b, F_dev, F, d, kp, ap);
-        int32_t st;
-        if (kp == 8) st = launch_hnr_mma<2>(s, ap, F_dev, F, d, seeds, n_seeds, seg, count, n_ms, seed, walk_offset, out, status);
-        else if (kp == 16) st = launch_hnr_mma<4>(s, ap, F_dev, F, d, seeds, n_seeds, seg, count, n_ms, seed, walk_offset, out, status);
-        else st = launch_hnr_mma<8>(s, ap, F_dev, F, d, seeds, n_seeds, seg, count, n_ms, seed, walk_offset, out, status);
+        if (kp == 8) st = launch_hnr_mma<2>(s, ap, F_dev, F, d, seeds, n_seeds, seg, count, n_ms, seed, walk_offset, out, status, z);
+        else if (kp == 16) st = launch_hnr_mma<4>(s, ap, F_dev, F, d, seeds, n_seeds, seg, count, n_ms, seed, walk_offset, out, status, z);
+        else st = launch_hnr_mma<8>(s, ap, F_dev, F, d, seeds, n_seeds, seg, count, n_ms, seed, walk_offset, out, status, z);
         if (!Ap) cudaFreeAsync(ap, s);
-        return st;
+    } else if (d <= 4) {
+        st = launch_hnr<4>(w, rng, s, A, b, F_dev, F, f_bound, d, seeds, n_seeds, seg, count, n_ms, seed, walk_offset, out, status, z);
+    } else if (d <= 8) {
+        st = launch_hnr<8>(w, rng, s, A, b, F_dev, F, f_bound, d, seeds, n_seeds, seg, count, n_ms, seed, walk_offset, out, status, z);
+    } else if (d <= 16) {
+        st = launch_hnr<16>(w, rng, s, A, b, F_dev, F, f_bound, d, seeds, n_seeds, seg, count, n_ms, seed, walk_offset, out, status, z);
+    } else {
+        st = launch_hnr<32>(w, rng, s, A, b, F_dev, F, f_bound, d, seeds, n_seeds, seg, count, n_ms, seed, walk_offset, out, status, z);
     }
-    if (d <= 4) return launch_hnr<4>(w, rng, s, A, b, F_dev, F, f_bound, d, seeds, n_seeds, seg, count, n_ms, seed, walk_offset, out, status);
-    if (d <= 8) return launch_hnr<8>(w, rng, s, A, b, F_dev, F, f_bound, d, seeds, n_seeds, seg, count, n_ms, seed, walk_offset, out, status);
-    if (d <= 16) return launch_hnr<16>(w, rng, s, A, b, F_dev, F, f_bound, d, seeds, n_seeds, seg, count, n_ms, seed, walk_offset, out, status);
-    if (d <= 32) return launch_hnr<32>(w, rng, s, A, b, F_dev, F, f_bound, d, seeds, n_seeds, seg, count, n_ms, seed, walk_offset, out, status);
-    return fail(EZ_UNSUPPORTED, "hit-and-run supports dimension <= 32");
+    if (z && !Z) cudaFreeAsync(z, s);
+    return st;
 }
 
 template <typename T, int MAXD>
@@ -1059,7 +1145,7 @@ extern "C" int32_t ez_inflate_edge(ez_world* w, const double* h_v1, const double
         if (worst >= 0.0) return fail(EZ_SEED_OUTSIDE_DOMAIN, "seed segment must be strictly inside the domain");
     }
     // capacity for 64 iterations up front: no allocation inside the loop
-    EZ_TRY(ws_reserve(w, d, std::max<int64_t>(p.n_p, batch_size(64, p)), p.n_p, n_faces0 + 64 * p.n_f));
+    EZ_TRY(ws_reserve(w, d, std::max<int64_t>(p.n_p, batch_size(64, p)), p.n_p, n_faces0 + 64 * p.n_f, p.n_ms));
     ez_eizo_ws* ws = device_ws(w->device);
     cudaStream_t s = ws->stream;
     std::vector<double> seg(3 * d);
@@ -1102,7 +1188,7 @@ extern "C" int32_t ez_inflate_edge(ez_world* w, const double* h_v1, const double
         int32_t* it = ws->rec + slot_offset(k);
         EZ_CUDA(cudaMemsetAsync(it, 0, 8 * sizeof(int32_t), s));
         EZ_TRY(dispatch_hnr(w, rng, s, ws->A, ws->b, ws->rec + kFaces, f_known, f_known + 2 * p.n_f, d, nullptr, 1,
-                            ws->seg, n_s, p.n_ms, seed, woff, ws->X, ws->rec + kStatus, ws->Ap));
+                            ws->seg, n_s, p.n_ms, seed, woff, ws->X, ws->rec + kStatus, ws->Ap, ws->Z));
         EZ_TRY(launch_check(w, ws->X, EZ_F64, n_s, d, ws->flags, precision, s, m, it + kColM));
         k_compact<<<1, 1024, 0, s>>>(ws->flags, n_s, p.n_p, thr, ws->rec, it, ws->col);
         EZ_CUDA(cudaGetLastError());
@@ -1168,7 +1254,7 @@ extern "C" int32_t ez_inflate_edge(ez_world* w, const double* h_v1, const double
         if (!fits) {  // grow the workspace, then continue without lookahead for this step
             EZ_CUDA(cudaStreamSynchronize(s));
             EZ_TRY(ws_reserve(w, d, std::max<int64_t>(ws->n_cap, std::max<int64_t>(p.n_p, batch_size(k + 64, p))),
-                              p.n_p, std::max(ws->f_cap, F + 64 * p.n_f)));
+                              p.n_p, std::max(ws->f_cap, F + 64 * p.n_f), p.n_ms));
             EZ_TRY(enqueue(k + 1, walk_offset, F));
         }
     }
@@ -1206,7 +1292,7 @@ extern "C" int32_t ez_refine_set(ez_world* w, const double* h_v1, const double* 
     std::lock_guard<std::mutex> lock(g_ws_mu);
     EZ_CUDA(cudaSetDevice(w->device));
     const int d = dim;
-    EZ_TRY(ws_reserve(w, d, n_cols, n_cols, n_faces + n_cols + 1));
+    EZ_TRY(ws_reserve(w, d, n_cols, n_cols, n_faces + n_cols + 1, 0));
     ez_eizo_ws* ws = device_ws(w->device);
     cudaStream_t s = ws->stream;
     std::vector<double> seg(3 * d);

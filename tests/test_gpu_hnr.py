@@ -75,7 +75,7 @@ def test_many_faces_high_dim():
     assert np.max(sb.points @ poly.A.T - poly.b) <= 1e-9
 
 
-# --- large polytopes: the FP64 tensor-core walk (k_hnr_mma, F >= 96 faces) ---------------
+# --- the FP64 tensor-core walk (k_hnr_mma; the lane-per-face walk under EZ_HNR_NO_MMA) -----
 
 def _random_poly(d, n_faces, seed, r=0.5):
     rng = np.random.default_rng(seed)
