@@ -780,6 +780,11 @@ struct ez_eizo_ws {
     int64_t ap_cap = 0;
     double* Z = nullptr;    // counter-stream draws of one sample batch (k_draws)
     int64_t z_cap = 0;
+    double* Z2[2] = {nullptr, nullptr};  // EI-ZO loop: draws of iterations k (even/odd), made on `side`
+    int64_t z2_cap = 0;
+    cudaStream_t side = nullptr;
+    cudaEvent_t ev_draws[2] = {nullptr, nullptr};
+    cudaEvent_t ev_walked[2] = {nullptr, nullptr};
     double* X = nullptr;
     uint8_t* flags = nullptr;
     int32_t* col = nullptr;
@@ -802,6 +807,13 @@ void eizo_ws_free(ez_eizo_ws* ws) {
     cudaFree(ws->b);
     cudaFree(ws->Ap);
     cudaFree(ws->Z);
+    cudaFree(ws->Z2[0]);
+    cudaFree(ws->Z2[1]);
+    if (ws->side) cudaStreamDestroy(ws->side);
+    for (cudaEvent_t e : ws->ev_draws)
+        if (e) cudaEventDestroy(e);
+    for (cudaEvent_t e : ws->ev_walked)
+        if (e) cudaEventDestroy(e);
     cudaFree(ws->X);
     cudaFree(ws->flags);
     cudaFree(ws->col);
@@ -849,6 +861,11 @@ static int32_t ws_reserve(ez_world* w, int d, int64_t n, int32_t c, int32_t f, i
         EZ_CUDA(cudaMalloc(&slot->rec, kRecInts * sizeof(int32_t)));
         EZ_CUDA(cudaMallocHost(&slot->h_rec, 2 * kRecInts * sizeof(int32_t)));
         EZ_CUDA(cudaMalloc(&slot->seg, sizeof(double) * 3 * 64));
+        EZ_CUDA(cudaStreamCreateWithFlags(&slot->side, cudaStreamNonBlocking));
+        for (int i = 0; i < 2; ++i) {
+            EZ_CUDA(cudaEventCreateWithFlags(&slot->ev_draws[i], cudaEventDisableTiming));
+            EZ_CUDA(cudaEventCreateWithFlags(&slot->ev_walked[i], cudaEventDisableTiming));
+        }
     }
     ez_eizo_ws* ws = slot;
     if (ws->d != d) {
@@ -876,9 +893,11 @@ static int32_t ws_reserve(ez_world* w, int d, int64_t n, int32_t c, int32_t f, i
         EZ_TRY(grow(&ws->Ap, 0, hnr_ap_words(f, d), false));
         ws->ap_cap = hnr_ap_words(f, d);
     }
-    if (n * n_ms * (d + 1) > ws->z_cap) {
-        EZ_TRY(grow(&ws->Z, 0, n * n_ms * (d + 1), false));
-        ws->z_cap = n * n_ms * (d + 1);
+    if (n * n_ms * (d + 1) > ws->z2_cap) {
+        // the side stream may still be filling a buffer of the previous call
+        if (ws->side) EZ_CUDA(cudaStreamSynchronize(ws->side));
+        for (int i = 0; i < 2; ++i) EZ_TRY(grow(&ws->Z2[i], 0, n * n_ms * (d + 1), false));
+        ws->z2_cap = n * n_ms * (d + 1);
     }
     return EZ_OK;
 }
@@ -1014,17 +1033,20 @@ static int64_t hnr_draw_words(int64_t count, int n_ms, int d) { return count * n
 static int32_t dispatch_hnr(const ez_world* w, int rng, cudaStream_t s, const double* A, const double* b,
                             const int32_t* F_dev, int F, int f_bound, int d, const double* seeds, int64_t n_seeds,
                             const double* seg, int64_t count, int n_ms, uint64_t seed, uint64_t walk_offset,
-                            double* out, int32_t* status, double* Ap = nullptr, double* Z = nullptr) {
+                            double* out, int32_t* status, double* Ap = nullptr, double* Z = nullptr,
+                            bool z_ready = false) {
     if (d > 32) return fail(EZ_UNSUPPORTED, "hit-and-run supports dimension <= 32");
     const int fmax = std::max(F, f_bound);
     double* z = nullptr;
-    if (rng == EZ_RNG_COUNTER) {
+    if (rng == EZ_RNG_COUNTER && !(Z && z_ready)) {
         z = Z;
         if (!z) EZ_CUDA(cudaMallocAsync(&z, sizeof(double) * hnr_draw_words(count, n_ms, d), s));
         const int64_t total = hnr_draw_words(count, n_ms, d);
         const unsigned grid = static_cast<unsigned>(std::min<int64_t>((total + 255) / 256, 148 * 16));
         k_draws<<<grid, 256, 0, s>>>(seed, walk_offset, count, d, n_ms, z, status);
         EZ_CUDA(cudaGetLastError());
+    } else if (rng == EZ_RNG_COUNTER) {
+        z = Z;
     }
     int32_t st;
     static const int mma_faces = [] {
@@ -1187,8 +1209,23 @@ extern "C" int32_t ez_inflate_edge(ez_world* w, const double* h_v1, const double
         const int64_t n_s = std::max<int64_t>(p.n_p, m);
         int32_t* it = ws->rec + slot_offset(k);
         EZ_CUDA(cudaMemsetAsync(it, 0, 8 * sizeof(int32_t), s));
+        // The walk's draws depend only on (seed, walk offset, batch size): they
+        // are made on the side stream into this iteration's buffer, overlapping
+        // the previous iteration's check, bisection and placement.
+        double* zb = nullptr;
+        if (rng == EZ_RNG_COUNTER) {
+            zb = ws->Z2[k & 1];
+            EZ_CUDA(cudaStreamWaitEvent(ws->side, ws->ev_walked[k & 1], 0));  // iteration k - 2 done reading
+            const int64_t total = hnr_draw_words(n_s, p.n_ms, d);
+            const unsigned grid = static_cast<unsigned>(std::min<int64_t>((total + 255) / 256, 148 * 16));
+            k_draws<<<grid, 256, 0, ws->side>>>(seed, woff, n_s, d, p.n_ms, zb, ws->rec + kStatus);
+            EZ_CUDA(cudaGetLastError());
+            EZ_CUDA(cudaEventRecord(ws->ev_draws[k & 1], ws->side));
+            EZ_CUDA(cudaStreamWaitEvent(s, ws->ev_draws[k & 1], 0));
+        }
         EZ_TRY(dispatch_hnr(w, rng, s, ws->A, ws->b, ws->rec + kFaces, f_known, f_known + 2 * p.n_f, d, nullptr, 1,
-                            ws->seg, n_s, p.n_ms, seed, woff, ws->X, ws->rec + kStatus, ws->Ap, ws->Z));
+                            ws->seg, n_s, p.n_ms, seed, woff, ws->X, ws->rec + kStatus, ws->Ap, zb, zb != nullptr));
+        if (zb) EZ_CUDA(cudaEventRecord(ws->ev_walked[k & 1], s));
         EZ_TRY(launch_check(w, ws->X, EZ_F64, n_s, d, ws->flags, precision, s, m, it + kColM));
         k_compact<<<1, 1024, 0, s>>>(ws->flags, n_s, p.n_p, thr, ws->rec, it, ws->col);
         EZ_CUDA(cudaGetLastError());
