@@ -80,6 +80,17 @@ const Nvrtc& nvrtc() {
     return n;
 }
 
+// CTA size of the large-batch kernel (EZ_JIT_BIG: 512, 640 or 768 threads;
+// the register cap is 65536 / size)
+int big_cta() {
+    static const int v = [] {
+        const char* e = getenv("EZ_JIT_BIG");
+        const int x = e ? atoi(e) : 512;
+        return (x == 640 || x == 768) ? x : 512;
+    }();
+    return v;
+}
+
 // ---------------------------------------------------------------------------
 // source generation
 // ---------------------------------------------------------------------------
@@ -285,7 +296,7 @@ struct Gen {
         o << "template <typename Q, int BT>\n__device__ __forceinline__ void jit_body(const ModelDev<float>& M, const Q* q, "
              "int64_t n, int64_t ld, uint8_t* out, int64_t count_lim, int32_t* n_col) {\n"
           << "    extern __shared__ __align__(16) uint8_t smem[];\n"
-          << "    __shared__ int s_warp[16];\n"
+          << "    __shared__ int s_warp[32];\n"
           << "    const size_t qoff = (static_cast<size_t>(BT > 0 ? BT : blockDim.x) * " << M.dof
           << " * sizeof(Q) + 15) & ~size_t(15);\n"
           << "    const JitPolicy pol{M};\n"
@@ -294,11 +305,11 @@ struct Gen {
              "q, n, ld, out, count_lim, n_col);\n}\n\n"
           << "}  // namespace ez\n\n";
         for (const char* qt : {"float", "double"})
-            for (int bt : {256, 512}) {
+            for (int bt : {256, big_cta()}) {
                 o << "extern \"C\" __global__ void __launch_bounds__(" << bt << ") ez_check_jit_" << qt[0] << bt
                   << "(ez::ModelDev<float> M, const " << qt << "* __restrict__ q, int64_t n, int64_t ld, "
                   << "uint8_t* __restrict__ out, float, int64_t count_lim, int32_t* __restrict__ n_col) {\n"
-                  << "    ez::jit_body<" << qt << ", " << (bt == 512 ? 512 : 0) << ">(M, q, n, ld, out, count_lim, n_col);\n}\n";
+                  << "    ez::jit_body<" << qt << ", " << (bt == 256 ? 0 : bt) << ">(M, q, n, ld, out, count_lim, n_col);\n}\n";
             }
         return o.str();
     }
@@ -404,9 +415,9 @@ int32_t compile(const std::string& src, std::shared_ptr<JitCheck>* out) {
         EZ_CUDA(cudaLibraryLoadData(&jc->lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0));
     }
     EZ_CUDA(cudaLibraryGetKernel(&jc->k[0][0], jc->lib, "ez_check_jit_f256"));
-    EZ_CUDA(cudaLibraryGetKernel(&jc->k[0][1], jc->lib, "ez_check_jit_f512"));
+    EZ_CUDA(cudaLibraryGetKernel(&jc->k[0][1], jc->lib, ("ez_check_jit_f" + std::to_string(big_cta())).c_str()));
     EZ_CUDA(cudaLibraryGetKernel(&jc->k[1][0], jc->lib, "ez_check_jit_d256"));
-    EZ_CUDA(cudaLibraryGetKernel(&jc->k[1][1], jc->lib, "ez_check_jit_d512"));
+    EZ_CUDA(cudaLibraryGetKernel(&jc->k[1][1], jc->lib, ("ez_check_jit_d" + std::to_string(big_cta())).c_str()));
     *out = jc;
     return EZ_OK;
 }
@@ -424,7 +435,7 @@ std::string jit_source(const ez_world* w) {
 
 namespace {
 
-constexpr int kJitSizes[4] = {64, 128, 256, 512};
+const int kJitSizes[4] = {64, 128, 256, big_cta()};
 
 size_t jit_smem(const ez_world* w, int bt, bool q64) {
     const size_t rows = (static_cast<size_t>(bt) * w->dof * (q64 ? sizeof(double) : sizeof(float)) + 15) & ~size_t(15);
@@ -449,7 +460,7 @@ int32_t launch_at(ez_world* w, int bt, const void* d_q, bool q64, int64_t n, int
     const JitCheck& jc = *w->jit;
     int si = 0;
     while (kJitSizes[si] != bt) ++si;
-    const cudaKernel_t kern = jc.k[q64 ? 1 : 0][bt == 512 ? 1 : 0];
+    const cudaKernel_t kern = jc.k[q64 ? 1 : 0][bt == big_cta() ? 1 : 0];
     const int64_t tiles = (n + bt - 1) / bt;
     const unsigned grid = static_cast<unsigned>(
         std::min<int64_t>(tiles, static_cast<int64_t>(w->num_sms) * w->jit_occ[q64 ? 1 : 0][si]));
@@ -466,7 +477,7 @@ int32_t launch_at(ez_world* w, int bt, const void* d_q, bool q64, int64_t n, int
 // cache), two 256-thread CTAs wait less at the tile barriers; time both.
 int32_t tune_bt(ez_world* w) {
     const char* e = getenv("EZ_JIT_BT");
-    if (e && (atoi(e) == 256 || atoi(e) == 512)) {
+    if (e && (atoi(e) == 256 || atoi(e) == big_cta())) {
         w->jit_bt = atoi(e);
         return EZ_OK;
     }
@@ -490,7 +501,7 @@ int32_t tune_bt(ez_world* w) {
         ck(cudaEventCreate(&e1))) {
         k_fill_box<<<256, 256, 0, s>>>(d_q, n, dof, d_box, d_box + dof, 0x7E57ull);
         float best = 1e30f;
-        for (int bt : {512, 256}) {
+        for (int bt : {big_cta(), 256}) {
             for (int r = 0; r < 2 && st == EZ_OK; ++r) st = launch_at(w, bt, d_q, false, n, dof, d_out, s, 0, nullptr);
             if (!ck(cudaEventRecord(e0, s))) break;
             for (int r = 0; r < 3 && st == EZ_OK; ++r) st = launch_at(w, bt, d_q, false, n, dof, d_out, s, 0, nullptr);
@@ -551,10 +562,10 @@ int32_t jit_specialize(ez_world* w) {
         for (int v = 0; v < 2; ++v) {
             const void* k = reinterpret_cast<const void*>(jc->k[i][v]);
             EZ_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(jit_smem(w, v ? 512 : 256, i == 1))));
+                                         static_cast<int>(jit_smem(w, v ? big_cta() : 256, i == 1))));
         }
         for (int si = 0; si < 4; ++si) {
-            const void* k = reinterpret_cast<const void*>(jc->k[i][kJitSizes[si] == 512 ? 1 : 0]);
+            const void* k = reinterpret_cast<const void*>(jc->k[i][kJitSizes[si] == big_cta() ? 1 : 0]);
             int occ = 0;
             EZ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, kJitSizes[si], jit_smem(w, kJitSizes[si], i == 1)));
             if (occ < 1) return refuse(EZ_CAPACITY, "specialised check kernel does not fit on an SM");
