@@ -74,3 +74,34 @@ def test_large_batches_specialise_automatically():
     hi = torch.as_tensor(w.upper, dtype=torch.float32, device="cuda")
     nat.check_device(lo + (hi - lo) * torch.rand((1 << 18, 7), device="cuda"))
     assert nat.specialize(0)
+
+
+def _oblique_world():
+    """Revolute, prismatic and oblique-axis joints (Q folding and the prismatic branch of the generator)."""
+    from paper_2504_10783_b200.model import Joint, Link, RobotModel, REVOLUTE, PRISMATIC
+    from oracle.make_scenes import pose
+    sph = lambda *p: Geometry(SPHERE, pose(p), radius=0.06)
+    joints = (Joint(REVOLUTE, -1, pose((-0.2, 0.0, 0.2)), axis=np.array([0.0, 0.0, 1.0])),
+              Joint(PRISMATIC, 0, pose((0.0, 0.0, 0.3), (0.3, 0.0, 0.0)), axis=np.array([0.3, 0.2, 0.93])),
+              Joint(REVOLUTE, 1, pose((0.2, 0.0, 0.1), (0.0, 0.4, 0.0)), axis=np.array([0.6, -0.64, 0.48])))
+    links = (Link((sph(0, 0, 0.1), sph(0, 0, 0.25))), Link((sph(0, 0, 0), sph(0.1, 0, 0))),
+             Link((sph(0.15, 0, 0), sph(0.3, 0, 0), sph(0.45, 0.05, 0))))
+    model = RobotModel(3, joints, links, np.array([-3.0, -0.2, -3.0]), np.array([3.0, 0.6, 3.0]),
+                       ((0, 5), (0, 6), (1, 6)))
+    base = fx.franka7_world()
+    static = (Geometry(SPHERE, RigidTransform(np.eye(3), np.array([-0.5, 0.2, 0.6])), radius=0.1),)
+    return World(model, static, base.vmap, model.lower, model.upper)
+
+
+@pytest.mark.parametrize("rows", ["float32", "float64"])
+def test_specialised_equals_generic_prismatic_oblique(rows):
+    w = _oblique_world()
+    gen, jit = w.checker().native, w.checker().native
+    gen.specialize(-1)
+    assert jit.specialize(1)
+    lo = torch.as_tensor(w.lower, dtype=torch.float64, device="cuda")
+    hi = torch.as_tensor(w.upper, dtype=torch.float64, device="cuda")
+    Q = (lo + (hi - lo) * torch.rand((200_000, 3), device="cuda", dtype=torch.float64)).to(getattr(torch, rows))
+    a, b = gen.check_device(Q), jit.check_device(Q)
+    assert 0.0 < float(a.float().mean()) < 1.0
+    assert torch.equal(a, b)
