@@ -135,6 +135,36 @@ def clustered_cloud(n_points: int, n_blobs: int, seed: int = 0) -> np.ndarray:
     return np.concatenate(pts)
 
 
+def bench_config1(cpu: bool = True) -> dict:
+    """Config 1: EI-ZO of the 3-DOF planar arm's segment with the reference's default parameters,
+    on the GPU and (CPU baseline) through the oracle port, the reference's own CPU-runnable case."""
+    from paper_2504_10783_b200 import fixtures as fx
+    from paper_2504_10783_b200.eizo import InflationParams, Segment, inflate_edge
+    from paper_2504_10783_b200.polytope import HPolytope
+
+    world = fx.arm3_world()
+    v1, v2 = fx.ARM3_SEGMENT
+    dom = HPolytope.from_bounds(world.lower, world.upper)
+    ck = world.checker()
+    inflate_edge(Segment(v1, v2), dom, InflationParams(), ck, seed=0)
+    walls = []
+    for _ in range(5):
+        t0 = time.perf_counter()
+        rep = inflate_edge(Segment(v1, v2), dom, InflationParams(), ck, seed=0)
+        walls.append((time.perf_counter() - t0) * 1e3)
+    out = {"ms_per_region_wall": float(np.median(walls)), "device_ms": rep.device_ms, "iterations": rep.iterations,
+           "faces": rep.hyperplanes_added, "collision_checks": rep.collision_checks,
+           "workload": "3-link planar arm among 3 discs + table, ARM3 segment, default InflationParams, seed 0"}
+    if cpu:
+        from oracle import ref
+        t0 = time.perf_counter()
+        r = ref.inflate_edge(v1, v2, dom.A, dom.b, ref.OracleChecker(world, workers=1), seed=0)
+        out["cpu_oracle_ms"] = (time.perf_counter() - t0) * 1e3
+        out["cpu_iterations"] = r["iterations"]
+        out["cpu_collision_checks"] = r["collision_checks"]
+    return out
+
+
 def bench_config4(checks_n: int = 1 << 20) -> dict:
     """Config 4: 14-DOF bimanual (66 spheres, 1,248 pairs): checks/s and one EI-ZO region."""
     import torch
@@ -409,6 +439,7 @@ def run_ours(args):
     peaks = _measured_peaks()
     extra = {}
     if world_size == 1 and not args.skip_extra:
+        extra["config1"] = bench_config1(cpu=not args.skip_cpu)
         extra["config4"] = bench_config4()
         extra["drm"] = bench_drm(cpu=not args.skip_cpu)
     line = {
