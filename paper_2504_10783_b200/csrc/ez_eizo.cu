@@ -319,8 +319,14 @@ __device__ __forceinline__ void chord_update(double sl, double h, double (&S)[2]
     H[1] = t1 ? ah : H[1];
 }
 
+#ifndef EZ_HNR_TPR
+#define EZ_HNR_TPR 2
+#endif
+#ifndef EZ_HNR_MINB
+#define EZ_HNR_MINB 8
+#endif
 template <int KC>
-__global__ void __launch_bounds__(64, KC >= 8 ? 8 : 11)
+__global__ void __launch_bounds__(64, KC >= 8 ? 8 : EZ_HNR_MINB)
 k_hnr_mma(const double* __restrict__ Ap, const int32_t* __restrict__ F_dev, int F, int d,
           const double* __restrict__ seeds, int64_t n_seeds, const double* __restrict__ seg, int64_t count,
           int n_ms, uint64_t seed, uint64_t walk_offset, double* __restrict__ out, int32_t* __restrict__ status,
@@ -391,38 +397,41 @@ k_hnr_mma(const double* __restrict__ Ap, const int32_t* __restrict__ F_dev, int 
             if (4 * j + c < d) dr[j] = dr[j] / nrm;
         double cs[2][2] = {{INFINITY, INFINITY}, {INFINITY, INFINITY}}, ch[2][2] = {{1.0, 1.0}, {1.0, 1.0}};  // [slot][hi/lo]
         bool outside = false;
-        // two 8-face tiles per round, the next round's A fragments loaded
+        // TPR 8-face tiles per round, the next round's A fragments loaded
         // ahead (L1 latency hidden behind the current round's MMAs)
-        double va[2][KC], vn[2][KC];
+        constexpr int TPR = EZ_HNR_TPR;
+        double va[TPR][KC], vn[TPR][KC];
 #pragma unroll
-        for (int u = 0; u < 2; ++u)
+        for (int u = 0; u < TPR; ++u)
 #pragma unroll
             for (int j = 0; j < KC; ++j)
                 va[u][j] = (u < tiles) ? __ldg(arow + static_cast<int64_t>(u) * 8 * KP + 4 * j) : 0.0;
-        for (int t = 0; t < tiles; t += 2) {
+        for (int t = 0; t < tiles; t += TPR) {
 #pragma unroll
-            for (int u = 0; u < 2; ++u)
+            for (int u = 0; u < TPR; ++u)
 #pragma unroll
                 for (int j = 0; j < KC; ++j)
-                    vn[u][j] = (t + 2 + u < tiles) ? __ldg(arow + static_cast<int64_t>(t + 2 + u) * 8 * KP + 4 * j) : 0.0;
-            double g[2][2] = {{0.0, 0.0}, {0.0, 0.0}}, h[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+                    vn[u][j] = (t + TPR + u < tiles) ? __ldg(arow + static_cast<int64_t>(t + TPR + u) * 8 * KP + 4 * j) : 0.0;
+            double g[TPR][2], h[TPR][2];
 #pragma unroll
-            for (int j = 0; j < KC; ++j) {
-                dmma_8x8x4(g[0][0], g[0][1], va[0][j], x[j]);
-                dmma_8x8x4(h[0][0], h[0][1], va[0][j], dr[j]);
-                dmma_8x8x4(g[1][0], g[1][1], va[1][j], x[j]);
-                dmma_8x8x4(h[1][0], h[1][1], va[1][j], dr[j]);
-            }
+            for (int u = 0; u < TPR; ++u) g[u][0] = g[u][1] = h[u][0] = h[u][1] = 0.0;
+#pragma unroll
+            for (int j = 0; j < KC; ++j)
+#pragma unroll
+                for (int u = 0; u < TPR; ++u) {
+                    dmma_8x8x4(g[u][0], g[u][1], va[u][j], x[j]);
+                    dmma_8x8x4(h[u][0], h[u][1], va[u][j], dr[j]);
+                }
             // a tile past the end has zero rows: h = 0 is masked, g = 0 is not outside
 #pragma unroll
-            for (int u = 0; u < 2; ++u)
+            for (int u = 0; u < TPR; ++u)
 #pragma unroll
                 for (int s2 = 0; s2 < 2; ++s2) {
                     outside |= check_seed && step == 0 && g[u][s2] > kMemberTol;
                     chord_update(-g[u][s2], h[u][s2], cs[s2], ch[s2]);
                 }
 #pragma unroll
-            for (int u = 0; u < 2; ++u)
+            for (int u = 0; u < TPR; ++u)
 #pragma unroll
                 for (int j = 0; j < KC; ++j) va[u][j] = vn[u][j];
         }
