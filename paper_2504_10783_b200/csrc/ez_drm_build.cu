@@ -199,8 +199,10 @@ extern "C" int32_t ez_roadmap_build(ez_world* w, const double* d_nodes, int64_t 
     EZ_CUDA(cudaFuncSetAttribute(k_node_voxels<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     EZ_CUDA(cudaFuncSetAttribute(k_node_voxels<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     const unsigned grid = static_cast<unsigned>(std::min<int64_t>((n_nodes + warps - 1) / warps, 148 * 8));
+    // temporaries come from the stream-ordered pool (kept mapped between builds)
+    EZ_TRY(retain_async_pool());
     unsigned long long* d_cnt = nullptr;
-    EZ_CUDA(cudaMalloc(&d_cnt, sizeof(unsigned long long)));
+    EZ_CUDA(cudaMallocAsync(&d_cnt, sizeof(unsigned long long), s));
     EZ_CUDA(cudaMemsetAsync(d_cnt, 0, sizeof(unsigned long long), s));
     if (n_nodes > 0)
         k_node_voxels<false><<<grid, warps * 32, smem, s>>>(M, d_nodes, n_nodes, g, nullptr, d_cnt);
@@ -224,19 +226,20 @@ extern "C" int32_t ez_roadmap_build(ez_world* w, const double* d_nodes, int64_t 
     void* tmp = nullptr;
     size_t tmp_bytes = 0, scan_bytes = 0;
     auto cleanup = [&]() {
-        cudaFree(keys);
-        cudaFree(keys_sorted);
-        cudaFree(counts);
-        cudaFree(excl);
-        cudaFree(tmp);
-        cudaFree(d_cnt);
+        cudaFreeAsync(keys, s);
+        cudaFreeAsync(keys_sorted, s);
+        cudaFreeAsync(counts, s);
+        cudaFreeAsync(excl, s);
+        cudaFreeAsync(tmp, s);
+        cudaFreeAsync(d_cnt, s);
+        cudaStreamSynchronize(s);
     };
     cudaError_t e = cudaSuccess;
     const size_t nk = std::max<unsigned long long>(1, nnz);
-    if (e == cudaSuccess) e = cudaMalloc(&keys, sizeof(unsigned long long) * nk);
-    if (e == cudaSuccess) e = cudaMalloc(&keys_sorted, sizeof(unsigned long long) * nk);
-    if (e == cudaSuccess) e = cudaMalloc(&counts, sizeof(unsigned long long) * n_vox);
-    if (e == cudaSuccess) e = cudaMalloc(&excl, sizeof(unsigned long long) * n_vox);
+    if (e == cudaSuccess) e = cudaMallocAsync(&keys, sizeof(unsigned long long) * nk, s);
+    if (e == cudaSuccess) e = cudaMallocAsync(&keys_sorted, sizeof(unsigned long long) * nk, s);
+    if (e == cudaSuccess) e = cudaMallocAsync(&counts, sizeof(unsigned long long) * n_vox, s);
+    if (e == cudaSuccess) e = cudaMallocAsync(&excl, sizeof(unsigned long long) * n_vox, s);
     if (e == cudaSuccess) e = cudaMalloc(&r->d_off, sizeof(int64_t) * (n_vox + 1));
     if (e == cudaSuccess) e = cudaMalloc(&r->d_ids, sizeof(int32_t) * nk);
     if (e == cudaSuccess) e = cudaMalloc(&r->d_vox_bits, sizeof(uint32_t) * ((n_vox + 31) / 32));
@@ -255,7 +258,7 @@ extern "C" int32_t ez_roadmap_build(ez_world* w, const double* d_nodes, int64_t 
         e = cub::DeviceRadixSort::SortKeys(nullptr, tmp_bytes, keys, keys_sorted, static_cast<int64_t>(nnz), 0, end_bit, s);
     if (e == cudaSuccess)
         e = cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, counts, excl, static_cast<int>(n_vox), s);
-    if (e == cudaSuccess) e = cudaMalloc(&tmp, std::max(tmp_bytes, scan_bytes));
+    if (e == cudaSuccess) e = cudaMallocAsync(&tmp, std::max(tmp_bytes, scan_bytes), s);
     if (e == cudaSuccess && nnz > 0)
         e = cub::DeviceRadixSort::SortKeys(tmp, tmp_bytes, keys, keys_sorted, static_cast<int64_t>(nnz), 0, end_bit, s);
     if (e == cudaSuccess && nnz > 0) {
