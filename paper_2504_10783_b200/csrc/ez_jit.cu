@@ -124,6 +124,14 @@ struct Gen {
 
     static float clean(float v) { return std::fabs(v) < 1e-12f ? 0.0f : v; }
 
+    // obstacle tests moved into phase A (the most frequently hitting spheres;
+    // EZ_JIT_A_OBST, for tuning); phase B tests the rest
+    int a_obst() const {
+        const char* e = getenv("EZ_JIT_A_OBST");
+        const int k = e ? atoi(e) : 0;
+        return std::max(0, std::min(k, M.n_spheres));
+    }
+
     // joint chain: frame of link j in R{j}_k / t{j}_k, sphere s in c{s}_k
     void fk() {
         for (int j = 0; j < M.n_joints; ++j) {
@@ -231,11 +239,12 @@ struct Gen {
     }
 
     // obstacles in calibrated order, cells of kVoxBatch spheres fetched together
-    void obstacles() {
+    // spheres order[k_begin, k_end)
+    void obstacles(int k_begin, int k_end) {
         const int32_t* order = reinterpret_cast<const int32_t*>(blob + M.off_order);
         const bool vox = M.vox.present;
-        for (int k0 = 0; k0 < M.n_spheres; k0 += kVoxBatch) {
-            const int nb = std::min(kVoxBatch, M.n_spheres - k0);
+        for (int k0 = k_begin; k0 < k_end; k0 += kVoxBatch) {
+            const int nb = std::min(kVoxBatch, k_end - k0);
             o << "    {\n";
             for (int j = 0; j < nb; ++j) {
                 const int s = order[k0 + j];
@@ -283,10 +292,11 @@ struct Gen {
           << "    template <typename Q>\n    __device__ __forceinline__ bool a(const Q* row, float*) const {\n";
         fk();
         hot();
+        obstacles(0, a_obst());
         o << "    return false;\n    }\n"
           << "    template <typename Q>\n    __device__ __forceinline__ bool b(const Q* row, float*) const {\n";
         fk();
-        obstacles();
+        obstacles(a_obst(), M.n_spheres);
         blocks();
         o << "    return false;\n    }\n};\n\n";
         // per row type two kernels: 512 threads (compile-time CTA size, at most

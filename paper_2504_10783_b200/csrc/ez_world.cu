@@ -128,11 +128,19 @@ struct HModel {
     int dof = 0, n_store = 0;
 };
 
-constexpr int kHotPairs = 16;
+// calibrated hot self pairs tested in phase A (EZ_HOT_PAIRS overrides, for tuning)
+int hot_pairs() {
+    static const int v = [] {
+        const char* e = getenv("EZ_HOT_PAIRS");
+        const int x = e ? atoi(e) : 16;
+        return (x >= 0 && x <= 256) ? x : 16;
+    }();
+    return v;
+}
 constexpr int kMinBlock = 3;   // smaller link-pair blocks are tested without the bounding-sphere skip
 
 // Pair/sphere layout.  Without statistics: no hot list, blocks in link order.
-// With per-pair and per-sphere hit counts: the kHotPairs most frequent self
+// With per-pair and per-sphere hit counts: the hot_pairs() most frequent self
 // pairs first (flat), the rest in link-pair blocks ordered by hits, spheres
 // tested against obstacles in decreasing hit frequency.
 void layout_pairs(HModel& hm, const std::vector<uint32_t>* pair_hits, const std::vector<uint32_t>* sph_hits) {
@@ -144,7 +152,7 @@ void layout_pairs(HModel& hm, const std::vector<uint32_t>* pair_hits, const std:
     hm.hot.clear();
     if (pair_hits) {
         std::stable_sort(rank.begin(), rank.end(), [&](int x, int y) { return hits(x) > hits(y); });
-        for (int k = 0; k < std::min(kHotPairs, np); ++k) {
+        for (int k = 0; k < std::min(hot_pairs(), np); ++k) {
             if (hits(rank[k]) == 0) break;
             is_hot[rank[k]] = 1;
             hm.hot.push_back(hm.all_pairs[rank[k]]);
