@@ -225,7 +225,8 @@ int32_t ez_refine_set(ez_world* world, const double* h_v1, const double* h_v2, i
  * ez_roadmap_create  uploads the CSR voxel->node map (drm.py:108-131).
  * ez_collision_set   replaces collision_set (drm.py:262-296): d_blocked_bits
  *                    receives the node bitmap (ceil(n_nodes/32) words),
- *                    *n_blocked its popcount. */
+ *                    *n_blocked its popcount (synchronises); with
+ *                    n_blocked = NULL the call stays asynchronous on stream. */
 int32_t ez_voxelize(const double* d_points, int64_t n, int32_t dim, const double* h_origin,
                     double side, int32_t* d_idx_out, int64_t* n_out, void* stream);
 int32_t ez_roadmap_create(const int64_t* h_cmap_offsets, const int32_t* h_cmap_ids,
@@ -245,6 +246,12 @@ int32_t ez_roadmap_export(const ez_roadmap* roadmap, int64_t* h_offsets, int32_t
 int32_t ez_collision_set(ez_roadmap* roadmap, const int32_t* d_vox_idx, int64_t n_vox,
                          const double* h_vmap_origin, double vmap_side, int32_t same_grid,
                          uint32_t* d_blocked_bits, int64_t* n_blocked, void* stream);
+/* Same, plus the blocked node ids in ascending order in d_ids (capacity
+ * n_nodes) and their count in *n_ids (synchronises).  What the Python
+ * collision_set returns, without unpacking the bitmap on the host. */
+int32_t ez_collision_set_ids(ez_roadmap* roadmap, const int32_t* d_vox_idx, int64_t n_vox,
+                             const double* h_vmap_origin, double vmap_side, int32_t same_grid,
+                             uint32_t* d_blocked_bits, int32_t* d_ids, int64_t* n_ids, void* stream);
 #endif /* __CUDACC_RTC__ */
 
 #ifdef __cplusplus

@@ -87,6 +87,7 @@ SIGNATURES = {
     "ez_roadmap_info": (c_i32, [c_vp, P_i64, P_i64, P_i64]),
     "ez_roadmap_export": (c_i32, [c_vp, P_i64, P_i32]),
     "ez_collision_set": (c_i32, [c_vp, c_vp, c_i64, P_dbl, c_dbl, c_i32, c_vp, P_i64, c_vp]),
+    "ez_collision_set_ids": (c_i32, [c_vp, c_vp, c_i64, P_dbl, c_dbl, c_i32, c_vp, c_vp, P_i64, c_vp]),
 }
 
 _lib = None

@@ -24,21 +24,32 @@ struct VoxParams {
     int32_t dim;
 };
 
+// bounding box of the indices: warp-reduced first, one atomic pair per warp
+// and axis (a per-point atomic on six addresses serialised 1e5 updates)
 __global__ void k_vox_index(const double* __restrict__ pts, int64_t n, VoxParams vp, int32_t* __restrict__ idx,
                             int32_t* __restrict__ bbox, int32_t* __restrict__ overflow) {
     const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (i >= n) return;
+    const bool in = i < n;
     for (int k = 0; k < vp.dim; ++k) {
-        // floor((p - origin) / side), fp64 as numpy (world.py:327)
-        const double f = floor((pts[i * vp.dim + k] - vp.org[k]) / vp.side);
-        if (!(f >= -2147483648.0 && f <= 2147483647.0)) {
-            atomicExch(overflow, 1);
-            return;
+        int32_t v = 0;
+        bool ok = in;
+        if (in) {
+            // floor((p - origin) / side), fp64 as numpy (world.py:327)
+            const double f = floor((pts[i * vp.dim + k] - vp.org[k]) / vp.side);
+            if (!(f >= -2147483648.0 && f <= 2147483647.0)) {
+                atomicExch(overflow, 1);
+                ok = false;
+            } else {
+                v = static_cast<int32_t>(f);
+                idx[i * vp.dim + k] = v;
+            }
         }
-        const int32_t v = static_cast<int32_t>(f);
-        idx[i * vp.dim + k] = v;
-        atomicMin(bbox + 2 * k, v);
-        atomicMax(bbox + 2 * k + 1, v);
+        const int32_t mn = __reduce_min_sync(0xffffffffu, ok ? v : INT_MAX);
+        const int32_t mx = __reduce_max_sync(0xffffffffu, ok ? v : INT_MIN);
+        if ((threadIdx.x & 31) == 0) {
+            if (mn != INT_MAX) atomicMin(bbox + 2 * k, mn);
+            if (mx != INT_MIN) atomicMax(bbox + 2 * k + 1, mx);
+        }
     }
 }
 
@@ -53,11 +64,16 @@ __device__ __forceinline__ int64_t lex_index(const int32_t* v, int dim, const Bo
     return r;
 }
 
+// occupancy bits; lanes hitting the same word (clustered clouds) merge their
+// bits first, one atomic per distinct word per warp
 __global__ void k_vox_mark(const int32_t* __restrict__ idx, int64_t n, int dim, BoxDims bd, uint32_t* __restrict__ bits) {
     const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    const int64_t li = lex_index(idx + i * dim, dim, bd);
-    atomicOr(bits + (li >> 5), 1u << (li & 31));
+    const bool in = i < n;
+    const int64_t li = in ? lex_index(idx + i * dim, dim, bd) : 0;
+    const unsigned long long word = in ? static_cast<unsigned long long>(li >> 5) : ~0ull;
+    const unsigned grp = __match_any_sync(0xffffffffu, word);
+    const unsigned orv = __reduce_or_sync(grp, in ? (1u << (li & 31)) : 0u);
+    if (in && static_cast<int>(threadIdx.x & 31) == __ffs(grp) - 1) atomicOr(bits + word, orv);
 }
 
 __global__ void k_popc(const uint32_t* __restrict__ bits, int64_t nw, uint32_t* __restrict__ cnt) {
@@ -152,6 +168,53 @@ __global__ void k_count_bits(const uint32_t* __restrict__ bits, int64_t nw, unsi
         c += __popc(bits[i]);
     for (int o = 16; o > 0; o >>= 1) c += __shfl_down_sync(0xffffffffu, c, o);
     if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, c);
+}
+
+// Blocked-node ids, ascending, from the node bitmap: one CTA walks the words in
+// chunks of 1024, a block-wide exclusive scan of the popcounts places each
+// word's ids (the host no longer unpacks 1e5 bits).  ids[n_out] = count.
+__global__ void __launch_bounds__(1024) k_bits_to_ids(const uint32_t* __restrict__ bits, int64_t nw,
+                                                      int32_t* __restrict__ ids, int64_t* __restrict__ n_out) {
+    __shared__ int s_warp[32];
+    __shared__ int64_t s_base;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    if (threadIdx.x == 0) s_base = 0;
+    __syncthreads();
+    for (int64_t w0 = 0; w0 < nw; w0 += 1024) {
+        const int64_t wi = w0 + threadIdx.x;
+        const uint32_t w = wi < nw ? bits[wi] : 0u;
+        const int c = __popc(w);
+        int incl = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        if (lane == 31) s_warp[wid] = incl;
+        __syncthreads();
+        if (wid == 0) {
+            const int v = s_warp[lane];
+            int wincl = v;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, wincl, o);
+                if (lane >= o) wincl += y;
+            }
+            s_warp[lane] = wincl - v;  // exclusive prefix of the warps
+        }
+        __syncthreads();
+        int64_t pos = s_base + s_warp[wid] + (incl - c);
+        uint32_t m = w;
+        while (m) {
+            const int b = __ffs(m) - 1;
+            m &= m - 1;
+            ids[pos++] = static_cast<int32_t>((wi << 5) + b);
+        }
+        __syncthreads();
+        if (threadIdx.x == 1023) s_base = pos;  // the last thread ends the chunk
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *n_out = s_base;
 }
 
 }  // namespace ez
@@ -286,8 +349,8 @@ extern "C" int32_t ez_roadmap_destroy(ez_roadmap* r) {
 extern "C" int32_t ez_collision_set(ez_roadmap* r, const int32_t* d_vox_idx, int64_t n_vox, const double* h_vmap_origin,
                                     double vmap_side, int32_t same_grid, uint32_t* d_blocked_bits, int64_t* n_blocked,
                                     void* stream) {
-    if (!r || !n_blocked) return fail(EZ_INVALID_ARGUMENT, "null argument");
-    *n_blocked = 0;
+    if (!r) return fail(EZ_INVALID_ARGUMENT, "null roadmap");
+    if (n_blocked) *n_blocked = 0;
     EZ_CUDA(cudaSetDevice(r->device));
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     const int64_t nbw = (r->n_nodes + 31) / 32;
@@ -295,7 +358,7 @@ extern "C" int32_t ez_collision_set(ez_roadmap* r, const int32_t* d_vox_idx, int
     if (n_vox == 0) return EZ_OK;
     const int64_t vbw = (r->n_voxels + 31) / 32;
     EZ_CUDA(cudaMemsetAsync(r->d_vox_bits, 0, sizeof(uint32_t) * vbw, s));
-    EZ_CUDA(cudaMemsetAsync(r->d_count, 0, sizeof(unsigned long long), s));
+    if (n_blocked) EZ_CUDA(cudaMemsetAsync(r->d_count, 0, sizeof(unsigned long long), s));
     PruneParams pp{};
     for (int k = 0; k < r->dim; ++k) {
         pp.vorg[k] = h_vmap_origin[k];
@@ -311,11 +374,31 @@ extern "C" int32_t ez_collision_set(ez_roadmap* r, const int32_t* d_vox_idx, int
     const int64_t want = std::min<int64_t>((r->n_voxels * 32 + 255) / 256, 148 * 16);
     k_gather<<<static_cast<unsigned>(std::max<int64_t>(1, want)), 256, 0, s>>>(r->d_vox_bits, r->n_voxels, r->d_off, r->d_ids,
                                                                             d_blocked_bits);
+    EZ_CUDA(cudaGetLastError());
+    if (!n_blocked) return EZ_OK;  // no count wanted: stays asynchronous on `stream`
     k_count_bits<<<static_cast<unsigned>(std::min<int64_t>(std::max<int64_t>(1, (nbw + 255) / 256), 296)), 256, 0, s>>>(
         d_blocked_bits, nbw, r->d_count);
     EZ_CUDA(cudaGetLastError());
     EZ_CUDA(cudaMemcpyAsync(r->h_count, r->d_count, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
     EZ_CUDA(cudaStreamSynchronize(s));
     *n_blocked = static_cast<int64_t>(*r->h_count);
+    return EZ_OK;
+}
+
+extern "C" int32_t ez_collision_set_ids(ez_roadmap* r, const int32_t* d_vox_idx, int64_t n_vox,
+                                        const double* h_vmap_origin, double vmap_side, int32_t same_grid,
+                                        uint32_t* d_blocked_bits, int32_t* d_ids, int64_t* n_ids, void* stream) {
+    if (!r || !n_ids) return fail(EZ_INVALID_ARGUMENT, "null argument");
+    *n_ids = 0;
+    EZ_TRY(ez_collision_set(r, d_vox_idx, n_vox, h_vmap_origin, vmap_side, same_grid, d_blocked_bits, nullptr, stream));
+    if (n_vox == 0) return EZ_OK;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const int64_t nbw = (r->n_nodes + 31) / 32;
+    int64_t* d_n = reinterpret_cast<int64_t*>(r->d_count);
+    k_bits_to_ids<<<1, 1024, 0, s>>>(d_blocked_bits, nbw, d_ids, d_n);
+    EZ_CUDA(cudaGetLastError());
+    EZ_CUDA(cudaMemcpyAsync(r->h_count, d_n, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    EZ_CUDA(cudaStreamSynchronize(s));
+    *n_ids = static_cast<int64_t>(*r->h_count);
     return EZ_OK;
 }

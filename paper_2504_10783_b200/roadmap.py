@@ -205,18 +205,39 @@ class DeviceRoadmap:
             except Exception:
                 pass
 
-    def blocked_bits(self, vmap: VoxelMap, same: bool):
-        """Blocked-node bitmap (CUDA uint32 tensor) and its popcount."""
+    def blocked_bits(self, vmap: VoxelMap, same: bool, count: bool = True):
+        """Blocked-node bitmap (CUDA uint32 tensor) and its popcount (None if not ``count``:
+        then the call does not synchronise)."""
         import torch
 
         dev = torch_device()
-        idx = torch.as_tensor(np.ascontiguousarray(vmap.index_array(), dtype=np.int32), device=dev)
+        idx = vmap.device_index()  # voxelize_point_cloud keeps its indices on the device
+        if idx is None or idx.device != dev:
+            idx = torch.as_tensor(np.ascontiguousarray(vmap.index_array(), dtype=np.int32), device=dev)
         bits = torch.empty(max(1, (self.n_nodes + 31) // 32), dtype=torch.int32, device=dev)
         n_blocked = C.c_int64(0)
         vorg = np.ascontiguousarray(vmap.origin, dtype=np.float64)
         N.check(N.lib().ez_collision_set(self._h, idx.data_ptr(), vmap.n_occupied, N.ptr(vorg), float(vmap.side),
-                                         1 if same else 0, bits.data_ptr(), C.byref(n_blocked), stream_handle()))
-        return bits, n_blocked.value
+                                         1 if same else 0, bits.data_ptr(), C.byref(n_blocked) if count else None,
+                                         stream_handle()))
+        return bits, (n_blocked.value if count else None)
+
+    def blocked_ids(self, vmap: VoxelMap, same: bool) -> np.ndarray:
+        """Blocked node ids, ascending (int64 host array), via ez_collision_set_ids."""
+        import torch
+
+        dev = torch_device()
+        idx = vmap.device_index()
+        if idx is None or idx.device != dev:
+            idx = torch.as_tensor(np.ascontiguousarray(vmap.index_array(), dtype=np.int32), device=dev)
+        bits = torch.empty(max(1, (self.n_nodes + 31) // 32), dtype=torch.int32, device=dev)
+        ids = torch.empty(max(1, self.n_nodes), dtype=torch.int32, device=dev)
+        n = C.c_int64(0)
+        vorg = np.ascontiguousarray(vmap.origin, dtype=np.float64)
+        N.check(N.lib().ez_collision_set_ids(self._h, idx.data_ptr(), vmap.n_occupied, N.ptr(vorg), float(vmap.side),
+                                             1 if same else 0, bits.data_ptr(), ids.data_ptr(), C.byref(n),
+                                             stream_handle()))
+        return ids[: n.value].cpu().numpy().astype(np.int64)
 
 
 def build_collision_map(world_or_model, nodes, grid: Grid):
@@ -265,10 +286,7 @@ def collision_set(drm: Drm, vmap: VoxelMap) -> CollisionSet:
     if vmap.n_occupied == 0:
         return CollisionSet(ids=np.zeros(0, dtype=np.int64))
     same = bool(np.allclose(vmap.origin, drm.grid.origin) and np.isclose(vmap.side, drm.grid.side))
-    bits, _ = drm.device_map().blocked_bits(vmap, same)
-    words = bits.cpu().numpy().view(np.uint32)
-    flags = np.unpackbits(words.view(np.uint8), bitorder="little")[: drm.n_nodes]
-    return CollisionSet(ids=np.flatnonzero(flags).astype(np.int64))
+    return CollisionSet(ids=drm.device_map().blocked_ids(vmap, same))
 
 
 # ---------------------------------------------------------------------------

@@ -48,19 +48,37 @@ class VoxelMap:
         vm._set = None
         return vm
 
+    @classmethod
+    def _from_device(cls, origin, side, d_idx) -> "VoxelMap":
+        """Map whose sorted indices live in a CUDA int32 tensor (voxelize_point_cloud); the host
+        copy is made on first use, so voxelize -> collision_set never leaves the device."""
+        vm = cls._from_sorted(origin, side, None)
+        vm._dev = d_idx
+        vm._n = int(d_idx.shape[0])
+        return vm
+
+    def _host_idx(self) -> np.ndarray:
+        if self._idx is None:
+            self._idx = self._dev.cpu().numpy().astype(np.int64)
+        return self._idx
+
+    def device_index(self):
+        """Sorted indices as a CUDA int32 tensor, if the map was made on the device (else None)."""
+        return getattr(self, "_dev", None)
+
     @property
     def occupied(self) -> frozenset:
         if self._set is None:
-            self._set = frozenset(map(tuple, self._idx.tolist()))
+            self._set = frozenset(map(tuple, self._host_idx().tolist()))
         return self._set
 
     @property
     def n_occupied(self) -> int:
-        return int(self._idx.shape[0])
+        return self._n if self._idx is None else int(self._idx.shape[0])
 
     def index_array(self) -> np.ndarray:
         """(n, dim) int64 occupied indices in sorted (lexicographic) order."""
-        return self._idx
+        return self._host_idx()
 
     @property
     def dim(self) -> int:
@@ -71,9 +89,10 @@ class VoxelMap:
         return 0.5 * self.side * math.sqrt(self.dim)
 
     def centers(self) -> np.ndarray:
-        if self._idx.shape[0] == 0:
+        idx = self._host_idx()
+        if idx.shape[0] == 0:
             return np.zeros((0, self.dim))
-        return self.origin + (self._idx.astype(float) + 0.5) * self.side
+        return self.origin + (idx.astype(float) + 0.5) * self.side
 
 
 def voxelize_point_cloud(points, bin_side: float, origin) -> VoxelMap:
@@ -99,8 +118,7 @@ def voxelize_point_cloud(points, bin_side: float, origin) -> VoxelMap:
     org = np.ascontiguousarray(origin)
     N.check(N.lib().ez_voxelize(d_pts.data_ptr(), pts.shape[0], dim, N.ptr(org), float(bin_side),
                                 d_idx.data_ptr(), C.byref(n_out), stream_handle()))
-    idx = d_idx[: n_out.value].cpu().numpy().astype(np.int64)
-    return VoxelMap._from_sorted(origin, bin_side, idx)
+    return VoxelMap._from_device(origin, bin_side, d_idx[: n_out.value])
 
 
 # ---------------------------------------------------------------------------
