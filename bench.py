@@ -323,6 +323,31 @@ def run_ours(args):
     specialised = nat.specialize(1)
     jit_ms = (time.perf_counter() - t_jit) * 1e3
 
+    # e2e through the public numpy API: pinned fp64 host buffers, H2D + D2H inside the timed region
+    pin = torch.empty((BATCH, 7), dtype=torch.float64, pin_memory=True)
+    pin.copy_(batches[0].double().cpu())
+    Qh = pin.numpy()
+    res_pin = torch.empty(BATCH, dtype=torch.uint8, pin_memory=True).numpy()
+    # measured before the device-timed region (the nvidia-smi clock sampler
+    # running beside it disturbs host-driven copies for a while); the median
+    # of three groups of calls
+    e2e_steps = max(3, min(args.steps, 10))
+    for _ in range(3):
+        nat.check_host(Qh, out=res_pin)
+    if world_size > 1:
+        dist.barrier()
+    groups = []
+    for _ in range(3):
+        t_e = time.perf_counter()
+        for _ in range(e2e_steps):
+            nat.check_host(Qh, out=res_pin)
+        groups.append(time.perf_counter() - t_e)
+    e2e_s = float(np.median(groups))
+    te = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+    if world_size > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_value = BATCH * e2e_steps * world_size / float(te.item())
+
     for i in range(max(3, args.warmup)):
         step(i)
     torch.cuda.synchronize()
@@ -351,25 +376,6 @@ def run_ours(args):
     checks = BATCH * args.steps * world_size
     value = checks / (max_ms * 1e-3)
     free_frac = float(out.float().mean().item())
-
-    # e2e through the public numpy API: pinned fp64 host buffers, H2D + D2H inside the timed region
-    pin = torch.empty((BATCH, 7), dtype=torch.float64, pin_memory=True)
-    pin.copy_(batches[0].double().cpu())
-    Qh = pin.numpy()
-    res_pin = torch.empty(BATCH, dtype=torch.uint8, pin_memory=True).numpy()
-    e2e_steps = max(3, min(args.steps, 10))
-    for _ in range(2):
-        nat.check_host(Qh, out=res_pin)
-    if world_size > 1:
-        dist.barrier()
-    t_e = time.perf_counter()
-    for _ in range(e2e_steps):
-        nat.check_host(Qh, out=res_pin)
-    e2e_s = time.perf_counter() - t_e
-    te = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
-    if world_size > 1:
-        dist.all_reduce(te, op=dist.ReduceOp.MAX)
-    e2e_value = BATCH * e2e_steps * world_size / float(te.item())
 
     # EI-ZO single-segment 7-DOF region (Franka parameters), latency per region
     eizo = None
