@@ -108,3 +108,29 @@ def test_franka7_region_contains_segment():
     assert P.contains(v1, 1e-9) and P.contains(v2, 1e-9)
     assert rep.iterations >= 2 and rep.hyperplanes_added >= 10
     assert np.allclose(np.linalg.norm(P.A, axis=1), 1.0, atol=1e-12)
+
+
+def test_degenerate_segment_matches_oracle():
+    # v1 == v2: projection alpha = 0, c_proj = v1 (inflation.py:129-132); fp64 checks give the
+    # oracle's (the reference algorithm's) iterations, faces and counters exactly
+    from oracle import ref
+    world = fx.disc_world([[0.0, 2.0]], 0.6)
+    v = np.array([0.3, 0.4])
+    dom = HPolytope.from_bounds(world.lower, world.upper)
+    rep = inflate_edge(Segment(v, v.copy()), dom, InflationParams(), world.checker(precision="fp64"), seed=5)
+    r = ref.inflate_edge(v, v.copy(), dom.A, dom.b, ref.OracleChecker(world), seed=5)
+    assert rep.iterations == r["iterations"] and rep.hyperplanes_added == r["hyperplanes_added"]
+    assert rep.collision_checks == r["collision_checks"]
+    assert np.allclose(rep.polytope.A, r["A"], atol=1e-9) and np.allclose(rep.polytope.b, r["b"], atol=1e-9)
+    assert rep.polytope.contains(v, 1e-9)
+
+
+def test_n_it_one_places_once_then_stops():
+    # n_it is checked after placement: exactly one round, "max_iterations" (inflation.py:314-316)
+    world = fx.disc_world([[0.0, 1.2], [0.0, -1.2], [2.0, 1.2]], 0.5)
+    seg = Segment(np.array([-1.0, 0.0]), np.array([1.0, 0.0]))
+    dom = HPolytope.from_bounds(world.lower, world.upper)
+    rep = inflate_edge(seg, dom, InflationParams(n_it=1), world.checker(), seed=2)
+    assert rep.iterations == 1 and rep.terminated_by == "max_iterations"
+    assert 0 < rep.hyperplanes_added <= InflationParams().n_f
+    assert rep.polytope.contains(seg.v1, 1e-9) and rep.polytope.contains(seg.v2, 1e-9)
