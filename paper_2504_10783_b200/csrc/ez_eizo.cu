@@ -560,35 +560,49 @@ k_compact(const uint8_t* __restrict__ free_flags, int64_t n, int n_p, double thr
     if (threadIdx.x == 0) it[kNumCand] = min(run, n_p);
 }
 
-// project_batch for one point (inflation.py:297-310)
-template <int MAXD>
-__device__ __forceinline__ double project(const double (&c)[MAXD], int d, const double* __restrict__ v1,
-                                          const double* __restrict__ e, double ee, double (&p)[MAXD]) {
+// project_batch for one point (inflation.py:124-137, used at :297-310) on a
+// point spread over a G-lane group: lane l holds components k = l + j G in
+// slot j.  The dot products run over k in order on every lane (components
+// gathered by shuffles), so every lane gets the serial loop's bits.
+template <int MAXD, int G>
+__device__ __forceinline__ double project_group(const double (&c)[(MAXD + G - 1) / G], int d,
+                                                const double* __restrict__ v1, const double* __restrict__ e,
+                                                double ee, double (&p)[(MAXD + G - 1) / G], int lane,
+                                                unsigned gm) {
+    constexpr int PER = (MAXD + G - 1) / G;
     double alpha = 0.0;
     if (ee != 0.0) {
         double dot = 0.0;
 #pragma unroll
-        for (int k = 0; k < MAXD; ++k)
-            if (k < d) dot = fma(c[k] - v1[k], e[k], dot);
+        for (int k = 0; k < MAXD; ++k) {
+            const double ck = __shfl_sync(gm, c[k / G], k % G, G);
+            if (k < d) dot = fma(ck - v1[k], e[k], dot);
+        }
         alpha = fmin(fmax(dot / ee, 0.0), 1.0);
+    }
+    double r[PER];
+#pragma unroll
+    for (int j = 0; j < PER; ++j) {
+        const int k = lane + j * G;
+        p[j] = (k < d) ? __dadd_rn(v1[k], __dmul_rn(alpha, e[k])) : 0.0;
+        r[j] = (k < d) ? c[j] - p[j] : 0.0;
     }
     double ss = 0.0;
 #pragma unroll
     for (int k = 0; k < MAXD; ++k) {
-        if (k < d) {
-            p[k] = __dadd_rn(v1[k], __dmul_rn(alpha, e[k]));
-            const double r = c[k] - p[k];
-            ss = fma(r, r, ss);
-        }
+        const double rk = __shfl_sync(gm, r[k / G], k % G, G);
+        if (k < d) ss = fma(rk, rk, ss);
     }
     return sqrt(ss);
 }
 
-// One group of G lanes per candidate: project, fail-fast check of the
-// projection, N_b bisection rounds (each a cooperative FK + collision check),
-// t_col guard.  The group shares the candidate's row and centre store.
 constexpr int kBisectLanes = 8;
 
+// One group of G lanes per candidate: project, fail-fast check of the
+// projection, N_b bisection rounds (each a cooperative FK + collision check),
+// t_col guard.  The group shares the candidate's row and centre store; each
+// lane keeps only its own components of the candidate, projection and
+// bracket (registers set the occupancy of this latency-bound kernel).
 template <typename T, int MAXD, int G>
 __global__ void __launch_bounds__(128)
 k_bisect(ModelDev<T> M, T margin, const double* __restrict__ X, int d, const int32_t* __restrict__ col,
@@ -598,6 +612,7 @@ k_bisect(ModelDev<T> M, T margin, const double* __restrict__ X, int d, const int
     extern __shared__ __align__(16) uint8_t smem[];
     __shared__ uint64_t bar;
     constexpr int CPB = 128 / G;  // candidates per CTA
+    constexpr int PER = (MAXD + G - 1) / G;
     const int C = it[kNumCand];
     if (rec[kStatus] != EZ_OK || rec[kStop] || static_cast<int64_t>(blockIdx.x) * CPB >= C) return;
     tma_stage(smem, M.blob, M.blob_bytes, &bar);
@@ -611,15 +626,19 @@ k_bisect(ModelDev<T> M, T margin, const double* __restrict__ X, int d, const int
     const unsigned gm = coop_mask<G>();
     const double* v1 = seg;
     const double* e = seg + d;
-    double c[MAXD], lo[MAXD], hi[MAXD];
+    double c[PER], lo[PER], hi[PER];
     const double* xc = X + static_cast<int64_t>(col[i]) * d;
 #pragma unroll
-    for (int k = 0; k < MAXD; ++k) c[k] = (k < d) ? xc[k] : 0.0;
-    project<MAXD>(c, d, v1, e, ee, lo);
+    for (int j = 0; j < PER; ++j) {
+        const int k = lane + j * G;
+        c[j] = (k < d) ? xc[k] : 0.0;
+    }
+    project_group<MAXD, G>(c, d, v1, e, ee, lo, lane, gm);
 #pragma unroll
-    for (int k = 0; k < MAXD; ++k) {
-        hi[k] = c[k];
-        if (k < d && (k % G) == lane) row[k] = lo[k];
+    for (int j = 0; j < PER; ++j) {
+        const int k = lane + j * G;
+        hi[j] = c[j];
+        if (k < d) row[k] = lo[j];
     }
     __syncwarp(gm);
     if (!config_free_coop<T, double, G>(M, smem, row, cen, margin)) {
@@ -627,29 +646,31 @@ k_bisect(ModelDev<T> M, T margin, const double* __restrict__ X, int d, const int
         return;
     }
     for (int r = 0; r < n_b; ++r) {
-        double mid[MAXD];
+        double mid[PER];
         __syncwarp(gm);
 #pragma unroll
-        for (int k = 0; k < MAXD; ++k) {
-            mid[k] = 0.5 * (lo[k] + hi[k]);
-            if (k < d && (k % G) == lane) row[k] = mid[k];
+        for (int j = 0; j < PER; ++j) {
+            const int k = lane + j * G;
+            mid[j] = 0.5 * (lo[j] + hi[j]);
+            if (k < d) row[k] = mid[j];
         }
         __syncwarp(gm);
         const bool fr = config_free_coop<T, double, G>(M, smem, row, cen, margin);
 #pragma unroll
-        for (int k = 0; k < MAXD; ++k) {
-            if (fr) lo[k] = mid[k];
-            else hi[k] = mid[k];
+        for (int j = 0; j < PER; ++j) {
+            if (fr) lo[j] = mid[j];
+            else hi[j] = mid[j];
         }
     }
-    double ps[MAXD];
-    const double ds = project<MAXD>(hi, d, v1, e, ee, ps);
+    double ps[PER];
+    const double ds = project_group<MAXD, G>(hi, d, v1, e, ee, ps, lane, gm);
     if (ds <= t_col && lane == 0) set_status(rec + kStatus, EZ_SEGMENT_IN_COLLISION);  // inflation.py:307-310
 #pragma unroll
-    for (int k = 0; k < MAXD; ++k) {
-        if (k < d && (k % G) == lane) {
-            star[static_cast<int64_t>(i) * d + k] = hi[k];
-            pstar[static_cast<int64_t>(i) * d + k] = ps[k];
+    for (int j = 0; j < PER; ++j) {
+        const int k = lane + j * G;
+        if (k < d) {
+            star[static_cast<int64_t>(i) * d + k] = hi[j];
+            pstar[static_cast<int64_t>(i) * d + k] = ps[j];
         }
     }
     if (lane == 0) dstar[i] = ds;
