@@ -680,12 +680,36 @@ __device__ __forceinline__ bool config_free_coop(const ModelDev<T>& M, const uin
     const int32_t* order = reinterpret_cast<const int32_t*>(blob + M.off_order);
     const StaticSphereRec<T>* SS = reinterpret_cast<const StaticSphereRec<T>*>(blob + M.off_ssph);
     const StaticBoxRec<T>* SB = reinterpret_cast<const StaticBoxRec<T>*>(blob + M.off_sbox);
-    for (int k0 = 0; k0 < M.n_spheres; k0 += G) {
-        const int k = k0 + lane;
+    // kVoxBatch spheres per lane per round: their distance-grid cells are
+    // fetched together (independent L2 loads in flight), then decided
+    const bool vox = M.vox.present;
+    for (int k0 = 0; k0 < M.n_spheres; k0 += kVoxBatch * G) {
+        T px[kVoxBatch], py[kVoxBatch], pz[kVoxBatch], e[kVoxBatch];
+        uint32_t w[kVoxBatch];
+        int sid[kVoxBatch];
+#pragma unroll
+        for (int j = 0; j < kVoxBatch; ++j) {
+            const int k = k0 + j * G + lane;
+            sid[j] = (k < M.n_spheres) ? order[k] : -1;
+            w[j] = kFarCell;
+            e[j] = T(0);
+            if (sid[j] >= 0) {
+                px[j] = cen[3 * sid[j]];
+                py[j] = cen[3 * sid[j] + 1];
+                pz[j] = cen[3 * sid[j] + 2];
+                if (vox) {
+                    const int64_t c = voxel_cell<T>(M.vox, px[j], py[j], pz[j], e[j]);
+                    if (c >= 0) w[j] = __ldg(M.vox.cells + c);
+                }
+            }
+        }
         bool hit = false;
-        if (k < M.n_spheres) {
-            const int s = order[k];
-            hit = sphere_hits_obstacles<T>(M, S[s], SS, SB, margin, cen[3 * s], cen[3 * s + 1], cen[3 * s + 2]);
+#pragma unroll
+        for (int j = 0; j < kVoxBatch; ++j) {
+            if (sid[j] < 0 || hit) continue;
+            const SphereRec<T>& sp = S[sid[j]];
+            hit = static_hits<T>(M, sp, SS, SB, margin, px[j], py[j], pz[j]) ||
+                  (w[j] != kFarCell && voxel_decide<T>(M.vox, w[j], e[j], px[j], py[j], pz[j], sp.rvox));
         }
         if (__ballot_sync(gm, hit)) return false;
     }
