@@ -761,15 +761,4 @@ __device__ __forceinline__ bool config_free_coop(const ModelDev<T>& M, const uin
     return true;
 }
 
-// Dynamic shared memory of a checking CTA: blob | sphere centres | staged rows.
-template <typename T>
-__host__ __device__ inline size_t check_smem_bytes(uint32_t blob_bytes, int n_spheres, int threads,
-                                                   int row_bytes) {
-    size_t b = blob_bytes;
-    b += static_cast<size_t>(3) * n_spheres * threads * sizeof(T);
-    b = (b + 15) & ~static_cast<size_t>(15);
-    b += static_cast<size_t>(threads) * row_bytes;
-    return (b + 15) & ~static_cast<size_t>(15);
-}
-
 }  // namespace ez
