@@ -197,14 +197,16 @@ __device__ __forceinline__ int hnr_walk(double (&x)[MAXD], int d, const double* 
 __global__ void k_draws(uint64_t seed, uint64_t walk_offset, int64_t count, int d, int n_ms, double* __restrict__ Z,
                         const int32_t* __restrict__ status) {
     if (status && (status[0] != EZ_OK || status[1] != 0)) return;
-    const int64_t total = count * n_ms * (d + 1);
+    // one thread per (walk, step): the walk's hash prefix once for its d + 1 draws
+    const int64_t total = count * n_ms;
     for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < total;
          t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        const int64_t i = t % count, sk = t / count;
-        const int k = static_cast<int>(sk % (d + 1));
-        const uint64_t step = static_cast<uint64_t>(sk / (d + 1));
+        const int64_t i = t % count;
+        const uint64_t step = static_cast<uint64_t>(t / count);
         const uint64_t key = walk_key(seed, walk_offset + static_cast<uint64_t>(i));
-        Z[t] = (k < d) ? counter_normal(key, step, k) : counter_uniform(key, step, d);
+        double* z = Z + static_cast<int64_t>(step) * (d + 1) * count + i;
+        for (int k = 0; k < d; ++k) z[k * count] = counter_normal(key, step, k);
+        z[d * count] = counter_uniform(key, step, d);
     }
 }
 
@@ -1071,7 +1073,7 @@ static int32_t dispatch_hnr(const ez_world* w, int rng, cudaStream_t s, const do
     if (rng == EZ_RNG_COUNTER && !(Z && z_ready)) {
         z = Z;
         if (!z) EZ_CUDA(cudaMallocAsync(&z, sizeof(double) * hnr_draw_words(count, n_ms, d), s));
-        const int64_t total = hnr_draw_words(count, n_ms, d);
+        const int64_t total = count * n_ms;
         const unsigned grid = static_cast<unsigned>(std::min<int64_t>((total + 255) / 256, 148 * 16));
         k_draws<<<grid, 256, 0, s>>>(seed, walk_offset, count, d, n_ms, z, status);
         EZ_CUDA(cudaGetLastError());
@@ -1246,7 +1248,7 @@ extern "C" int32_t ez_inflate_edge(ez_world* w, const double* h_v1, const double
         if (rng == EZ_RNG_COUNTER) {
             zb = ws->Z2[k & 1];
             EZ_CUDA(cudaStreamWaitEvent(ws->side, ws->ev_walked[k & 1], 0));  // iteration k - 2 done reading
-            const int64_t total = hnr_draw_words(n_s, p.n_ms, d);
+            const int64_t total = n_s * p.n_ms;
             const unsigned grid = static_cast<unsigned>(std::min<int64_t>((total + 255) / 256, 148 * 16));
             k_draws<<<grid, 256, 0, ws->side>>>(seed, woff, n_s, d, p.n_ms, zb, ws->rec + kStatus);
             EZ_CUDA(cudaGetLastError());
