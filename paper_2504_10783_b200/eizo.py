@@ -187,13 +187,12 @@ def compute_step_back(a, b_raw: float, seg: Segment, delta_max: float) -> float:
 
 def default_bisection_steps(domain: HPolytope, delta_max: float) -> int:
     """ceil(log2(L / delta_max)) with L the domain box diagonal (inflation.py:219-229)."""
-    spans = []
-    for i in range(domain.dim):
-        col = domain.A[:, i]
-        pos, neg = col > 1e-12, col < -1e-12
-        hi = np.min(domain.b[pos] / col[pos]) if np.any(pos) else np.inf
-        lo = np.max(domain.b[neg] / col[neg]) if np.any(neg) else -np.inf
-        spans.append(hi - lo if np.isfinite(hi) and np.isfinite(lo) else 1.0)
+    A, b = domain.A, domain.b
+    with np.errstate(divide="ignore", invalid="ignore"):
+        R = b[:, None] / A
+    hi = np.where(A > 1e-12, R, np.inf).min(axis=0, initial=np.inf)
+    lo = np.where(A < -1e-12, R, -np.inf).max(axis=0, initial=-np.inf)
+    spans = np.where(np.isfinite(hi) & np.isfinite(lo), hi - lo, 1.0)
     diag = float(np.linalg.norm(spans))
     return max(1, int(math.ceil(math.log2(max(diag, 2.0 * delta_max) / delta_max))))
 
