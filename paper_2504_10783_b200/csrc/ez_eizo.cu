@@ -885,7 +885,12 @@ static int32_t ws_reserve(ez_world* w, int d, int64_t n, int32_t c, int32_t f, i
     ez_eizo_ws*& slot = device_ws(w->device);
     if (!slot) {
         slot = new ez_eizo_ws();
-        EZ_CUDA(cudaStreamCreateWithFlags(&slot->stream, cudaStreamNonBlocking));
+        // the loop's critical path at high priority, the ahead-of-time draws
+        // (side stream) at low priority: they fill the gaps instead of
+        // competing with the walk, bisection and placement for SMs
+        int prio_lo = 0, prio_hi = 0;
+        EZ_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+        EZ_CUDA(cudaStreamCreateWithPriority(&slot->stream, cudaStreamNonBlocking, prio_hi));
         EZ_CUDA(cudaEventCreate(&slot->ev0));
         EZ_CUDA(cudaEventCreate(&slot->ev1));
         EZ_CUDA(cudaEventCreateWithFlags(&slot->ev_it[0], cudaEventDisableTiming));
@@ -893,7 +898,7 @@ static int32_t ws_reserve(ez_world* w, int d, int64_t n, int32_t c, int32_t f, i
         EZ_CUDA(cudaMalloc(&slot->rec, kRecInts * sizeof(int32_t)));
         EZ_CUDA(cudaMallocHost(&slot->h_rec, 2 * kRecInts * sizeof(int32_t)));
         EZ_CUDA(cudaMalloc(&slot->seg, sizeof(double) * 3 * 64));
-        EZ_CUDA(cudaStreamCreateWithFlags(&slot->side, cudaStreamNonBlocking));
+        EZ_CUDA(cudaStreamCreateWithPriority(&slot->side, cudaStreamNonBlocking, prio_lo));
         for (int i = 0; i < 2; ++i) {
             EZ_CUDA(cudaEventCreateWithFlags(&slot->ev_draws[i], cudaEventDisableTiming));
             EZ_CUDA(cudaEventCreateWithFlags(&slot->ev_walked[i], cudaEventDisableTiming));
