@@ -817,6 +817,7 @@ struct ez_eizo_ws {
     cudaStream_t side = nullptr;
     cudaEvent_t ev_draws[2] = {nullptr, nullptr};
     cudaEvent_t ev_walked[2] = {nullptr, nullptr};
+    cudaEvent_t ev_fork = nullptr;  // orders the side stream after an inflation's setup
     double* X = nullptr;
     uint8_t* flags = nullptr;
     int32_t* col = nullptr;
@@ -846,6 +847,7 @@ void eizo_ws_free(ez_eizo_ws* ws) {
         if (e) cudaEventDestroy(e);
     for (cudaEvent_t e : ws->ev_walked)
         if (e) cudaEventDestroy(e);
+    if (ws->ev_fork) cudaEventDestroy(ws->ev_fork);
     cudaFree(ws->X);
     cudaFree(ws->flags);
     cudaFree(ws->col);
@@ -873,38 +875,77 @@ static int32_t grow(Tp** p, int64_t old_n, int64_t new_n, bool keep) {
     return EZ_OK;
 }
 
-// One EI-ZO workspace per device, shared by every world on it (inflations on
-// a device are serialised by g_ws_mu), so repeated inflations with fresh
-// checkers never allocate inside the loop.
-static std::mutex g_ws_mu;
-static ez_eizo_ws* g_ws[64] = {};
+// EI-ZO workspaces: a small pool per device, shared by every world on it, so
+// repeated inflations with fresh checkers never allocate inside the loop and
+// independent inflations (several segments of a path) can run concurrently,
+// each on its own stream, from different host threads.
+struct WsPool {
+    std::mutex mu;
+    std::vector<ez_eizo_ws*> all;
+    std::vector<bool> busy;
+};
+static WsPool g_pool[64];
 
-static ez_eizo_ws*& device_ws(int device) { return g_ws[device & 63]; }
-
-static int32_t ws_reserve(ez_world* w, int d, int64_t n, int32_t c, int32_t f, int n_ms) {
-    ez_eizo_ws*& slot = device_ws(w->device);
-    if (!slot) {
-        slot = new ez_eizo_ws();
-        // the loop's critical path at high priority, the ahead-of-time draws
-        // (side stream) at low priority: they fill the gaps instead of
-        // competing with the walk, bisection and placement for SMs
-        int prio_lo = 0, prio_hi = 0;
-        EZ_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
-        EZ_CUDA(cudaStreamCreateWithPriority(&slot->stream, cudaStreamNonBlocking, prio_hi));
-        EZ_CUDA(cudaEventCreate(&slot->ev0));
-        EZ_CUDA(cudaEventCreate(&slot->ev1));
-        EZ_CUDA(cudaEventCreateWithFlags(&slot->ev_it[0], cudaEventDisableTiming));
-        EZ_CUDA(cudaEventCreateWithFlags(&slot->ev_it[1], cudaEventDisableTiming));
-        EZ_CUDA(cudaMalloc(&slot->rec, kRecInts * sizeof(int32_t)));
-        EZ_CUDA(cudaMallocHost(&slot->h_rec, 2 * kRecInts * sizeof(int32_t)));
-        EZ_CUDA(cudaMalloc(&slot->seg, sizeof(double) * 3 * 64));
-        EZ_CUDA(cudaStreamCreateWithPriority(&slot->side, cudaStreamNonBlocking, prio_lo));
-        for (int i = 0; i < 2; ++i) {
-            EZ_CUDA(cudaEventCreateWithFlags(&slot->ev_draws[i], cudaEventDisableTiming));
-            EZ_CUDA(cudaEventCreateWithFlags(&slot->ev_walked[i], cudaEventDisableTiming));
-        }
+static int32_t ws_create(ez_eizo_ws** out) {
+    ez_eizo_ws* slot = new ez_eizo_ws();
+    *out = slot;
+    // the loop's critical path at high priority, the ahead-of-time draws
+    // (side stream) at low priority: they fill the gaps instead of competing
+    // with the walk, bisection and placement for SMs
+    int prio_lo = 0, prio_hi = 0;
+    EZ_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+    EZ_CUDA(cudaStreamCreateWithPriority(&slot->stream, cudaStreamNonBlocking, prio_hi));
+    EZ_CUDA(cudaEventCreate(&slot->ev0));
+    EZ_CUDA(cudaEventCreate(&slot->ev1));
+    EZ_CUDA(cudaEventCreateWithFlags(&slot->ev_it[0], cudaEventDisableTiming));
+    EZ_CUDA(cudaEventCreateWithFlags(&slot->ev_it[1], cudaEventDisableTiming));
+    EZ_CUDA(cudaMalloc(&slot->rec, kRecInts * sizeof(int32_t)));
+    EZ_CUDA(cudaMallocHost(&slot->h_rec, 2 * kRecInts * sizeof(int32_t)));
+    EZ_CUDA(cudaMalloc(&slot->seg, sizeof(double) * 3 * 64));
+    EZ_CUDA(cudaStreamCreateWithPriority(&slot->side, cudaStreamNonBlocking, prio_lo));
+    for (int i = 0; i < 2; ++i) {
+        EZ_CUDA(cudaEventCreateWithFlags(&slot->ev_draws[i], cudaEventDisableTiming));
+        EZ_CUDA(cudaEventCreateWithFlags(&slot->ev_walked[i], cudaEventDisableTiming));
     }
-    ez_eizo_ws* ws = slot;
+    EZ_CUDA(cudaEventCreateWithFlags(&slot->ev_fork, cudaEventDisableTiming));
+    return EZ_OK;
+}
+
+// A workspace of the current device for the duration of one call.
+struct WsLease {
+    int device = 0;
+    ez_eizo_ws* ws = nullptr;
+    int32_t acquire(int dev) {
+        device = dev;
+        WsPool& P = g_pool[dev & 63];
+        std::lock_guard<std::mutex> lk(P.mu);
+        for (size_t i = 0; i < P.all.size(); ++i)
+            if (!P.busy[i]) {
+                P.busy[i] = true;
+                ws = P.all[i];
+                return EZ_OK;
+            }
+        ez_eizo_ws* n = nullptr;
+        const int32_t st = ws_create(&n);
+        if (st != EZ_OK) {
+            eizo_ws_free(n);
+            return st;
+        }
+        P.all.push_back(n);
+        P.busy.push_back(true);
+        ws = n;
+        return EZ_OK;
+    }
+    ~WsLease() {
+        if (!ws) return;
+        WsPool& P = g_pool[device & 63];
+        std::lock_guard<std::mutex> lk(P.mu);
+        for (size_t i = 0; i < P.all.size(); ++i)
+            if (P.all[i] == ws) P.busy[i] = false;
+    }
+};
+
+static int32_t ws_reserve(ez_eizo_ws* ws, int d, int64_t n, int32_t c, int32_t f, int n_ms) {
     if (ws->d != d) {
         ws->n_cap = ws->c_cap = ws->f_cap = 0;
         ws->d = d;
@@ -1113,9 +1154,8 @@ static int32_t dispatch_hnr(const ez_world* w, int rng, cudaStream_t s, const do
 }
 
 template <typename T, int MAXD>
-static int32_t launch_bisect_t(ez_world* w, const ModelDev<T>& M, cudaStream_t s, const int32_t* it, int n_p, int d,
-                               double ee, int n_b, double t_col) {
-    ez_eizo_ws* ws = device_ws(w->device);
+static int32_t launch_bisect_t(ez_world* w, ez_eizo_ws* ws, const ModelDev<T>& M, cudaStream_t s, const int32_t* it,
+                               int n_p, int d, double ee, int n_b, double t_col) {
     constexpr int G = kBisectLanes, CPB = 128 / G;
     size_t smem = M.blob_bytes + static_cast<size_t>(M.cen_words) * CPB * sizeof(T);
     smem = (smem + 15) & ~static_cast<size_t>(15);
@@ -1132,10 +1172,11 @@ static int32_t launch_bisect_t(ez_world* w, const ModelDev<T>& M, cudaStream_t s
 }
 
 template <int MAXD>
-static int32_t launch_bisect(ez_world* w, int precision, cudaStream_t s, const int32_t* it, int n_p, int d, double ee,
+static int32_t launch_bisect(ez_world* w, ez_eizo_ws* ws, int precision, cudaStream_t s, const int32_t* it, int n_p,
+                             int d, double ee,
                              int n_b, double t_col) {
-    if (precision == EZ_F64) return launch_bisect_t<double, MAXD>(w, w->md, s, it, n_p, d, ee, n_b, t_col);
-    return launch_bisect_t<float, MAXD>(w, w->mf, s, it, n_p, d, ee, n_b, t_col);
+    if (precision == EZ_F64) return launch_bisect_t<double, MAXD>(w, ws, w->md, s, it, n_p, d, ee, n_b, t_col);
+    return launch_bisect_t<float, MAXD>(w, ws, w->mf, s, it, n_p, d, ee, n_b, t_col);
 }
 
 }  // namespace ez
@@ -1189,7 +1230,6 @@ extern "C" int32_t ez_inflate_edge(ez_world* w, const double* h_v1, const double
     const ez_eizo_params& p = *params;
     if (p.n_p < 1 || p.n_f < 1 || p.n_b < 1 || p.n_ms < 1) return fail(EZ_INVALID_ARGUMENT, "counts must be >= 1");
     if (rng != EZ_RNG_COUNTER && rng != EZ_RNG_PHILOX) return fail(EZ_INVALID_ARGUMENT, "unknown rng");
-    std::lock_guard<std::mutex> lock(g_ws_mu);
     EZ_CUDA(cudaSetDevice(w->device));
     const int d = dim;
     // seed segment strictly inside the domain (inflation.py:274-277), fp64 on the host
@@ -1204,8 +1244,10 @@ extern "C" int32_t ez_inflate_edge(ez_world* w, const double* h_v1, const double
         if (worst >= 0.0) return fail(EZ_SEED_OUTSIDE_DOMAIN, "seed segment must be strictly inside the domain");
     }
     // capacity for 64 iterations up front: no allocation inside the loop
-    EZ_TRY(ws_reserve(w, d, std::max<int64_t>(p.n_p, batch_size(64, p)), p.n_p, n_faces0 + 64 * p.n_f, p.n_ms));
-    ez_eizo_ws* ws = device_ws(w->device);
+    WsLease lease;
+    EZ_TRY(lease.acquire(w->device));
+    ez_eizo_ws* ws = lease.ws;
+    EZ_TRY(ws_reserve(ws, d, std::max<int64_t>(p.n_p, batch_size(64, p)), p.n_p, n_faces0 + 64 * p.n_f, p.n_ms));
     cudaStream_t s = ws->stream;
     std::vector<double> seg(3 * d);
     double ee = 0.0;
@@ -1266,10 +1308,10 @@ extern "C" int32_t ez_inflate_edge(ez_world* w, const double* h_v1, const double
         EZ_TRY(launch_check(w, ws->X, EZ_F64, n_s, d, ws->flags, precision, s, m, it + kColM));
         k_compact<<<1, 1024, 0, s>>>(ws->flags, n_s, p.n_p, thr, ws->rec, it, ws->col);
         EZ_CUDA(cudaGetLastError());
-        if (d <= 4) EZ_TRY(launch_bisect<4>(w, precision, s, it, p.n_p, d, ee, p.n_b, p.t_col));
-        else if (d <= 8) EZ_TRY(launch_bisect<8>(w, precision, s, it, p.n_p, d, ee, p.n_b, p.t_col));
-        else if (d <= 16) EZ_TRY(launch_bisect<16>(w, precision, s, it, p.n_p, d, ee, p.n_b, p.t_col));
-        else EZ_TRY(launch_bisect<32>(w, precision, s, it, p.n_p, d, ee, p.n_b, p.t_col));
+        if (d <= 4) EZ_TRY(launch_bisect<4>(w, ws, precision, s, it, p.n_p, d, ee, p.n_b, p.t_col));
+        else if (d <= 8) EZ_TRY(launch_bisect<8>(w, ws, precision, s, it, p.n_p, d, ee, p.n_b, p.t_col));
+        else if (d <= 16) EZ_TRY(launch_bisect<16>(w, ws, precision, s, it, p.n_p, d, ee, p.n_b, p.t_col));
+        else EZ_TRY(launch_bisect<32>(w, ws, precision, s, it, p.n_p, d, ee, p.n_b, p.t_col));
         k_place<<<1, 1024, place_smem, s>>>(ws->A, ws->b, ws->rec, it, d, ws->star, ws->pstar, ws->dstar, ws->seg,
                                             p.delta_max, p.n_f, nullptr);
         EZ_CUDA(cudaGetLastError());
@@ -1291,6 +1333,11 @@ extern "C" int32_t ez_inflate_edge(ez_world* w, const double* h_v1, const double
     int32_t hyper = 0;
     int k = 1;
     int32_t terminated = 0;
+    // the side stream's draws read the status record this call just reset on
+    // `s`: without this edge a draw kernel could still see the previous
+    // inflation's stop flag and skip its work
+    EZ_CUDA(cudaEventRecord(ws->ev_fork, s));
+    EZ_CUDA(cudaStreamWaitEvent(ws->side, ws->ev_fork, 0));
     EZ_TRY(enqueue(1, 0, F));
     for (;; ++k) {
         const uint64_t next_offset = walk_offset + static_cast<uint64_t>(n_s_of[k & 1]);
@@ -1327,7 +1374,7 @@ extern "C" int32_t ez_inflate_edge(ez_world* w, const double* h_v1, const double
         }
         if (!fits) {  // grow the workspace, then continue without lookahead for this step
             EZ_CUDA(cudaStreamSynchronize(s));
-            EZ_TRY(ws_reserve(w, d, std::max<int64_t>(ws->n_cap, std::max<int64_t>(p.n_p, batch_size(k + 64, p))),
+            EZ_TRY(ws_reserve(ws, d, std::max<int64_t>(ws->n_cap, std::max<int64_t>(p.n_p, batch_size(k + 64, p))),
                               p.n_p, std::max(ws->f_cap, F + 64 * p.n_f), p.n_ms));
             EZ_TRY(enqueue(k + 1, walk_offset, F));
         }
@@ -1363,11 +1410,12 @@ extern "C" int32_t ez_refine_set(ez_world* w, const double* h_v1, const double* 
     if (n_cols < 1) return fail(EZ_INVALID_ARGUMENT, "refine_sets needs at least one collision");
     if (n_b < 1) return fail(EZ_INVALID_ARGUMENT, "n_b must be >= 1");
     if (dim > 32) return fail(EZ_UNSUPPORTED, "dimension <= 32");
-    std::lock_guard<std::mutex> lock(g_ws_mu);
     EZ_CUDA(cudaSetDevice(w->device));
     const int d = dim;
-    EZ_TRY(ws_reserve(w, d, n_cols, n_cols, n_faces + n_cols + 1, 0));
-    ez_eizo_ws* ws = device_ws(w->device);
+    WsLease lease;
+    EZ_TRY(lease.acquire(w->device));
+    ez_eizo_ws* ws = lease.ws;
+    EZ_TRY(ws_reserve(ws, d, n_cols, n_cols, n_faces + n_cols + 1, 0));
     cudaStream_t s = ws->stream;
     std::vector<double> seg(3 * d);
     double ee = 0.0;
@@ -1389,10 +1437,10 @@ extern "C" int32_t ez_refine_set(ez_world* w, const double* h_v1, const double* 
     EZ_CUDA(cudaMemcpyAsync(ws->col, iota.data(), sizeof(int32_t) * n_cols, cudaMemcpyHostToDevice, s));
     EZ_CUDA(cudaMemcpyAsync(ws->rec, rec0, sizeof(rec0), cudaMemcpyHostToDevice, s));
     const int32_t* it = ws->rec + slot_offset(0);
-    if (d <= 4) EZ_TRY(launch_bisect<4>(w, precision, s, it, n_cols, d, ee, n_b, t_col));
-    else if (d <= 8) EZ_TRY(launch_bisect<8>(w, precision, s, it, n_cols, d, ee, n_b, t_col));
-    else if (d <= 16) EZ_TRY(launch_bisect<16>(w, precision, s, it, n_cols, d, ee, n_b, t_col));
-    else EZ_TRY(launch_bisect<32>(w, precision, s, it, n_cols, d, ee, n_b, t_col));
+    if (d <= 4) EZ_TRY(launch_bisect<4>(w, ws, precision, s, it, n_cols, d, ee, n_b, t_col));
+    else if (d <= 8) EZ_TRY(launch_bisect<8>(w, ws, precision, s, it, n_cols, d, ee, n_b, t_col));
+    else if (d <= 16) EZ_TRY(launch_bisect<16>(w, ws, precision, s, it, n_cols, d, ee, n_b, t_col));
+    else EZ_TRY(launch_bisect<32>(w, ws, precision, s, it, n_cols, d, ee, n_b, t_col));
     const size_t place_smem = static_cast<size_t>(n_cols);
     if (place_smem > 200 * 1024) return fail(EZ_UNSUPPORTED, "more than 204800 collisions in one repair");
     if (place_smem > 48 * 1024)

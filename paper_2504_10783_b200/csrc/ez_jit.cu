@@ -536,6 +536,7 @@ int32_t tune_bt(ez_world* w) {
 }  // namespace
 
 int32_t jit_specialize(ez_world* w) {
+    std::lock_guard<std::mutex> cfg(w->cfg_mu);  // threads racing to the first large batch compile once
     if (w->jit) return EZ_OK;
     if (w->jit_failed) return fail(EZ_UNSUPPORTED, w->jit_error);
     auto refuse = [&](int32_t st, const std::string& why) {

@@ -4,6 +4,7 @@
 //   CollisionChecker.check_batch 483-495 (ez_check_batch / ez_check_batch_host)
 //   fk_batch                    195-223 (ez_fk_batch)
 #include <algorithm>
+#include <atomic>
 #include <climits>
 #include <cmath>
 #include <cstdlib>
@@ -856,18 +857,22 @@ static int32_t launch_check_t(ez_world* w, const ModelDev<T>& M, const Q* d_q, i
         if (w->jit) return jit_launch(w, d_q, sizeof(Q) == 8, n, ld, d_free, stream, count_lim, n_col);
     }
     if (w->launch_threads[slot] == 0) {
-        int bw = -1, bt = 0, bo = 0;
-        size_t bs = 0;
-        EZ_TRY((eval_bt<T, Q, 64>(w, M, &bw, &bt, &bs, &bo)));
-        EZ_TRY((eval_bt<T, Q, 96>(w, M, &bw, &bt, &bs, &bo)));
-        EZ_TRY((eval_bt<T, Q, 128>(w, M, &bw, &bt, &bs, &bo)));
-        EZ_TRY((eval_bt<T, Q, 160>(w, M, &bw, &bt, &bs, &bo)));
-        EZ_TRY((eval_bt<T, Q, 192>(w, M, &bw, &bt, &bs, &bo)));
-        EZ_TRY((eval_bt<T, Q, 256>(w, M, &bw, &bt, &bs, &bo)));
-        if (bt == 0) return fail(EZ_CAPACITY, "robot model too large for one checking CTA");
-        w->launch_threads[slot] = bt;
-        w->launch_smem[slot] = bs;
-        w->launch_occ[slot] = bo;
+        std::lock_guard<std::mutex> lk(w->cfg_mu);
+        if (w->launch_threads[slot] == 0) {
+            int bw = -1, bt = 0, bo = 0;
+            size_t bs = 0;
+            EZ_TRY((eval_bt<T, Q, 64>(w, M, &bw, &bt, &bs, &bo)));
+            EZ_TRY((eval_bt<T, Q, 96>(w, M, &bw, &bt, &bs, &bo)));
+            EZ_TRY((eval_bt<T, Q, 128>(w, M, &bw, &bt, &bs, &bo)));
+            EZ_TRY((eval_bt<T, Q, 160>(w, M, &bw, &bt, &bs, &bo)));
+            EZ_TRY((eval_bt<T, Q, 192>(w, M, &bw, &bt, &bs, &bo)));
+            EZ_TRY((eval_bt<T, Q, 256>(w, M, &bw, &bt, &bs, &bo)));
+            if (bt == 0) return fail(EZ_CAPACITY, "robot model too large for one checking CTA");
+            w->launch_smem[slot] = bs;
+            w->launch_occ[slot] = bo;
+            std::atomic_thread_fence(std::memory_order_release);
+            w->launch_threads[slot] = bt;  // published last: readers check it first
+        }
     }
     const int threads = w->launch_threads[slot];
     const size_t smem = w->launch_smem[slot];

@@ -60,7 +60,9 @@ struct ez_world {
     int32_t jit_bt = 512;            // CTA size for large batches
     int32_t jit_occ[2][4] = {};      // [rows f32/f64][CTA size 64/128/256/512] resident CTAs per SM
 
-    // cached launch shapes of k_check, [T fp64][Q fp64]
+    // cached launch shapes of k_check, [T fp64][Q fp64]; set once under cfg_mu
+    // (EI-ZO calls of several threads may race to the first launch)
+    std::mutex cfg_mu;
     int32_t launch_threads[4] = {0, 0, 0, 0};
     size_t launch_smem[4] = {0, 0, 0, 0};
     int32_t launch_occ[4] = {0, 0, 0, 0};

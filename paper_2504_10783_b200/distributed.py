@@ -278,11 +278,17 @@ def inflate_edge_sharded(seg: Segment, domain: HPolytope, params: InflationParam
 # segment sharding
 # ---------------------------------------------------------------------------
 def inflate_segments_sharded(path, domain: HPolytope, params: InflationParams, checker, seed: int = 0,
-                             comm: Comm | None = None, rng="counter", inflate_fn=None):
+                             comm: Comm | None = None, rng="counter", inflate_fn=None, concurrency: int = 6):
     """Inflate the path's segments round-robin over ranks, then replay the skip rule everywhere.
 
-    Returns ``(Scs, local_reports)``.  Every rank gets the same ``Scs``.
+    A rank runs up to ``concurrency`` of its segments at once (host threads;
+    each native inflation takes its own device workspace and stream, so
+    several latency-bound regions share the GPU).  Returns ``(Scs,
+    local_reports)``; every rank gets the same ``Scs``, whatever the
+    concurrency (segment-keyed seeds).
     """
+    from concurrent.futures import ThreadPoolExecutor
+
     from .corridor import Scs
 
     comm = comm or LocalComm()
@@ -290,10 +296,19 @@ def inflate_segments_sharded(path, domain: HPolytope, params: InflationParams, c
     n = knots.shape[0] - 1
     mine = {}
     inflate_fn = inflate_fn or inflate_edge
-    for k in shard_segments(n, comm.world_size, comm.rank):
+    own = list(shard_segments(n, comm.world_size, comm.rank))
+
+    def one(k):
         rep = inflate_fn(Segment(knots[k], knots[k + 1]), domain, params, checker,
                          seed=child_seed(seed, 0x5E7, k), rng=rng)
-        mine[k] = (rep.polytope.A, rep.polytope.b, rep.iterations, rep.hyperplanes_added, rep.collision_checks)
+        return k, (rep.polytope.A, rep.polytope.b, rep.iterations, rep.hyperplanes_added, rep.collision_checks)
+
+    workers = max(1, min(int(concurrency), len(own)))
+    if workers == 1:
+        mine.update(one(k) for k in own)
+    else:
+        with ThreadPoolExecutor(max_workers=workers) as ex:
+            mine.update(ex.map(one, own))
     allpolys = {}
     for part in comm.all_gather_object(mine):
         allpolys.update(part)

@@ -12,6 +12,7 @@ from __future__ import annotations
 
 import ctypes as C
 import math
+import threading
 from dataclasses import dataclass
 
 import numpy as np
@@ -200,6 +201,8 @@ def default_bisection_steps(domain: HPolytope, delta_max: float) -> int:
 # ---------------------------------------------------------------------------
 # the inflation loop (GPU)
 # ---------------------------------------------------------------------------
+_CALLS_LOCK = threading.Lock()
+
 def inflate_edge(seg: Segment, domain: HPolytope, params: InflationParams, checker, seed: int = 0,
                  rng="counter") -> InflationReport:
     """Grow a polytope around a collision-free segment inside the domain, on the GPU.
@@ -236,7 +239,8 @@ def inflate_edge(seg: Segment, domain: HPolytope, params: InflationParams, check
     N.check(N.lib().ez_inflate_edge(native.handle, N.ptr(v1), N.ptr(v2), d, N.ptr(A0), N.ptr(b0), domain.n_faces,
                                     C.byref(p), int(seed) & (2**64 - 1), precision_code(checker.precision),
                                     rng_mode(rng), C.byref(rep), N.ptr(A_out), N.ptr(b_out), cap))
-    checker.calls += int(rep.collision_checks)
+    with _CALLS_LOCK:  # inflations of several segments may run in threads
+        checker.calls += int(rep.collision_checks)
     F = rep.n_faces
     poly = HPolytope(A_out[:F], b_out[:F])
     return InflationReport(poly, rep.iterations, rep.hyperplanes_added, int(rep.collision_checks),

@@ -59,3 +59,25 @@ def test_segment_sharding_single_rank_covers_path():
     assert sorted(mine) == [0, 1, 2]
     for k, c in enumerate(scs.coverage):
         assert scs.sets[c].contains_segment(knots[k], knots[k + 1])
+
+
+def test_concurrent_segments_equal_sequential():
+    # several inflations in flight on one GPU (one workspace and stream each): same corridor
+    from paper_2504_10783_b200.distributed import inflate_segments_sharded
+    from paper_2504_10783_b200.eizo import InflationParams
+    from paper_2504_10783_b200.polytope import HPolytope
+    from paper_2504_10783_b200.roadmap import PwlPath
+
+    world = fx.franka7_world()
+    path = PwlPath(fx.random_free_path(world, 6, seed=5))
+    dom = HPolytope.from_bounds(world.lower, world.upper)
+    params = InflationParams(**fx.FRANKA_PARAMS)
+    ck = world.checker()
+    seq, mine1 = inflate_segments_sharded(path, dom, params, ck, seed=3, concurrency=1)
+    calls1 = ck.calls
+    par, mine4 = inflate_segments_sharded(path, dom, params, ck, seed=3, concurrency=4)
+    assert seq.coverage == par.coverage and len(seq.sets) == len(par.sets)
+    for a, b in zip(seq.sets, par.sets):
+        assert np.array_equal(a.A, b.A) and np.array_equal(a.b, b.b)
+    assert {k: v[4] for k, v in mine1.items()} == {k: v[4] for k, v in mine4.items()}
+    assert ck.calls == 2 * calls1
