@@ -166,6 +166,35 @@ def bench_config1(cpu: bool = True) -> dict:
     return out
 
 
+def bench_boxes(checks_n: int = 1 << 20) -> dict:
+    """Robot boxes: a Franka-like chain of 8 oriented boxes + a tool sphere
+    (scenes/box_arm3d.json) against the config-2 cloud; generic kernel (box SAT, box vs voxel
+    lattice through the occupancy bitmap)."""
+    import torch
+
+    from paper_2504_10783_b200 import fixtures as fx
+    from paper_2504_10783_b200.scene import World, load_scene
+
+    arm = load_scene(ROOT / "scenes" / "box_arm3d.json")
+    cloud = fx.franka7_world().vmap
+    world = World(arm.model, arm.static, cloud, arm.lower, arm.upper)
+    nat = world.checker().native
+    lo = torch.as_tensor(world.lower, dtype=torch.float32, device="cuda")
+    hi = torch.as_tensor(world.upper, dtype=torch.float32, device="cuda")
+    Q = lo + (hi - lo) * torch.rand((checks_n, world.model.dof), device="cuda")
+    for _ in range(3):
+        out = nat.check_device(Q)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(5):
+        nat.check_device(Q)
+    e1.record()
+    torch.cuda.synchronize()
+    return {"checks_per_s": 5 * checks_n / (e0.elapsed_time(e1) * 1e-3), "free_fraction": float(out.float().mean()),
+            "workload": "8 robot boxes + 1 sphere, 20 self pairs (box-box SAT, sphere-box), 1 static box, 10k voxels"}
+
+
 def bench_config4(checks_n: int = 1 << 20) -> dict:
     """Config 4: 14-DOF bimanual (66 spheres, 1,248 pairs): checks/s and one EI-ZO region."""
     import torch
@@ -456,6 +485,7 @@ def run_ours(args):
     if world_size == 1 and not args.skip_extra:
         extra["config1"] = bench_config1(cpu=not args.skip_cpu)
         extra["config4"] = bench_config4()
+        extra["boxes"] = bench_boxes()
         extra["drm"] = bench_drm(cpu=not args.skip_cpu)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world_size, "steps": args.steps,

@@ -299,16 +299,27 @@ __device__ __forceinline__ bool box_hits_obstacles(const ModelDev<T>& M, const u
         lo[k] = max(V.lbase[k], static_cast<int>(floor(a)) - 1);
         hi[k] = min(V.lbase[k] + V.L[k] - 1, static_cast<int>(floor(b)) + 1);
     }
+    // rows of the x-range, 32 lattice cells per bitmap word: empty words (most
+    // of a sparse cloud) are skipped whole, set bits visited by ffs
+    if (lo[0] > hi[0]) return false;
     for (int z = lo[2]; z <= hi[2]; ++z)
-        for (int y = lo[1]; y <= hi[1]; ++y)
-            for (int x = lo[0]; x <= hi[0]; ++x) {
-                const int64_t bit = (static_cast<int64_t>(z - V.lbase[2]) * V.L[1] + (y - V.lbase[1])) * V.L[0] +
-                                    (x - V.lbase[0]);
-                if (!((__ldg(V.occ + (bit >> 5)) >> (bit & 31)) & 1u)) continue;
-                if (point_box_d2<T>(R, t, he, lattice_centre(V.vorg[0], x, V.vside), lattice_centre(V.vorg[1], y, V.vside),
-                                    lattice_centre(V.vorg[2], z, V.vside)) <= R2)
-                    return true;
+        for (int y = lo[1]; y <= hi[1]; ++y) {
+            const int64_t row = (static_cast<int64_t>(z - V.lbase[2]) * V.L[1] + (y - V.lbase[1])) * V.L[0] - V.lbase[0];
+            const int64_t b0 = row + lo[0], b1 = row + hi[0];
+            for (int64_t wi = b0 >> 5; wi <= (b1 >> 5); ++wi) {
+                uint32_t word = __ldg(V.occ + wi);
+                if (wi == (b0 >> 5)) word &= ~0u << (b0 & 31);
+                if (wi == (b1 >> 5)) word &= ~0u >> (31 - (b1 & 31));
+                while (word) {
+                    const int bpos = __ffs(word) - 1;
+                    word &= word - 1;
+                    const int x = static_cast<int>((wi << 5) + bpos - row);
+                    if (point_box_d2<T>(R, t, he, lattice_centre(V.vorg[0], x, V.vside),
+                                        lattice_centre(V.vorg[1], y, V.vside), lattice_centre(V.vorg[2], z, V.vside)) <= R2)
+                        return true;
+                }
             }
+        }
     return false;
 }
 
