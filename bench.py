@@ -501,8 +501,15 @@ def run_ours(args):
                                 if specialised else "k_check<float,float>"),
                      "jit_compile_ms": jit_ms, "flop_per_check": FLOP_PER_CHECK,
                      "avg_launch_ms": avg_launch_ms,
+                     "frac_note": "of measured: the FP32 FMA peak of this GPU, measured in this run",
                      "peak_source": "ez_fp32_peak FMA microbenchmark measured in this run "
-                                    "(MEASURED_PEAKS.json has HBM %.0f GB/s and bf16 only)" % peaks.get("hbm_gbs", 0)},
+                                    "(MEASURED_PEAKS.json has HBM %.0f GB/s and bf16 only)" % peaks.get("hbm_gbs", 0),
+                     # the same launch on the HBM roofline (28 B in + 1 B out per check)
+                     "hbm": {"achieved": 29.0 * BATCH / (avg_launch_ms * 1e-3) / 1e9, "peak": peaks.get("hbm_gbs"),
+                             "unit": "GB/s",
+                             "frac": (29.0 * BATCH / (avg_launch_ms * 1e-3) / 1e9 / peaks["hbm_gbs"])
+                             if peaks.get("hbm_gbs") else None,
+                             "frac_note": "of measured (MEASURED_PEAKS.json hbm_gbs): not the bound"}},
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": BATCH * 7 * 8, "d2h_bytes_per_step": BATCH,
                 "api": "CollisionChecker.check_batch(numpy fp64, pinned) -> ez_check_batch_host"},
         "gpu_launches": args.steps,
