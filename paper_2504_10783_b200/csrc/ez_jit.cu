@@ -239,12 +239,19 @@ struct Gen {
     }
 
     // obstacles in calibrated order, cells of kVoxBatch spheres fetched together
+    // distance-grid cells fetched together per batch of spheres (EZ_JIT_VOXB)
+    static int vox_batch() {
+        const char* e = getenv("EZ_JIT_VOXB");
+        const int v = e ? atoi(e) : kVoxBatch;
+        return (v >= 1 && v <= 64) ? v : kVoxBatch;
+    }
+
     // spheres order[k_begin, k_end)
     void obstacles(int k_begin, int k_end) {
         const int32_t* order = reinterpret_cast<const int32_t*>(blob + M.off_order);
         const bool vox = M.vox.present;
-        for (int k0 = k_begin; k0 < k_end; k0 += kVoxBatch) {
-            const int nb = std::min(kVoxBatch, k_end - k0);
+        for (int k0 = k_begin; k0 < k_end; k0 += vox_batch()) {
+            const int nb = std::min(vox_batch(), k_end - k0);
             o << "    {\n";
             for (int j = 0; j < nb; ++j) {
                 const int s = order[k0 + j];
