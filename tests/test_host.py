@@ -4,10 +4,11 @@ import numpy as np
 import pytest
 
 from paper_2504_10783_b200 import fixtures as fx
-from paper_2504_10783_b200.eizo import (InflationParams, Segment, compute_step_back, default_bisection_steps,
+from paper_2504_10783_b200.eizo import (InflationParams, Segment, bisection_update, compute_step_back, default_bisection_steps,
                                         dist_gradient, dist_to_segment, project_to_segment, required_batch_size,
                                         unadaptive_test)
 from paper_2504_10783_b200.errors import DimensionMismatch, GradientUndefined
+from paper_2504_10783_b200.model import REVOLUTE, SPHERE, Geometry, Joint, Link, RigidTransform, RobotModel
 from paper_2504_10783_b200.polytope import HPolytope, dumps_polytopes, loads_polytopes
 from paper_2504_10783_b200.roadmap import Drm, Grid, load_drm, save_drm
 from paper_2504_10783_b200.scene import (VoxelMap, World, load_point_cloud, load_scene, save_point_cloud,
@@ -78,6 +79,33 @@ def test_batch_size_and_test():
     assert not unadaptive_test(required_batch_size(3, params), 3, params)[0]
 
 
+class _CountingChecker:
+    """Duck-typed checker over a numpy predicate, counting the configurations it is asked about."""
+
+    def __init__(self, free_fn):
+        self.free_fn, self.calls = free_fn, 0
+
+    def check_batch(self, Q):
+        Q = np.atleast_2d(Q)
+        self.calls += len(Q)
+        return self.free_fn(Q)
+
+
+def test_bisection_known_answers():
+    """Reference test_inflation.py:116-135: convergence bound, retention, one check per step."""
+    seg = Segment(np.array([0.0, 0.0]), np.array([0.0, 1.0]))
+    half = _CountingChecker(lambda Q: Q[:, 0] < 2.0)
+    star = bisection_update(np.array([4.0, 0.0]), seg, 20, half)
+    assert np.linalg.norm(star - [2.0, 0.0]) <= 2 * 4 / 2 ** 20
+    assert half.calls == 20
+    c = np.array([3.0, 0.0])
+    only_c = _CountingChecker(lambda Q: ~np.all(np.isclose(Q, c), axis=1))
+    assert np.array_equal(bisection_update(c.copy(), seg, 8, only_c), c)
+    one = _CountingChecker(lambda Q: Q[:, 0] < 2.0)
+    bisection_update(np.array([4.0, 0.0]), seg, 1, one)
+    assert one.calls == 1
+
+
 def test_step_back_identity_and_default_nb():
     seg = Segment(np.array([0.0, 0.0]), np.array([1.0, 0.0]))
     assert compute_step_back(np.array([0.0, 1.0]), 5.0, seg, 0.01) == 0.01
@@ -107,6 +135,15 @@ def test_params_validation():
         InflationParams(n_f=0)
     p = InflationParams.from_dict({"delta": 0.1, "eps": 0.02, "n_p": 500, "junk": 1})
     assert p.delta == 0.1 and p.n_p == 500 and InflationParams.from_dict(p.to_dict()) == p
+
+
+def test_self_pair_same_link_rejected():
+    """Reference test_world.py:114-119."""
+    joints = (Joint(REVOLUTE, -1, RigidTransform.identity(2)),)
+    links = (Link((Geometry(SPHERE, RigidTransform.identity(2), radius=0.1),
+                   Geometry(SPHERE, RigidTransform.planar(0.5, 0.0), radius=0.1))),)
+    with pytest.raises(ValueError):
+        RobotModel(2, joints, links, [-1.0], [1.0], self_pairs=((0, 1),))
 
 
 def test_scene_json_roundtrip(tmp_path):
