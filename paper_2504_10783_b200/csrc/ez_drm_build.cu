@@ -34,7 +34,7 @@ struct MapGrid {
 
 template <bool kEmit>
 __global__ void __launch_bounds__(256)
-k_node_voxels(ModelDev<double> M, const double* __restrict__ nodes, int64_t n, MapGrid g,
+k_node_voxels(const __grid_constant__ ModelDev<double> M, const double* __restrict__ nodes, int64_t n, MapGrid g,
               unsigned long long* __restrict__ keys, unsigned long long* __restrict__ n_keys) {
     extern __shared__ __align__(16) uint8_t smem[];
     __shared__ uint64_t bar;

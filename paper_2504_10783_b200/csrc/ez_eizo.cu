@@ -607,7 +607,7 @@ constexpr int kBisectLanes = 8;
 // bracket (registers set the occupancy of this latency-bound kernel).
 template <typename T, int MAXD, int G>
 __global__ void __launch_bounds__(128)
-k_bisect(ModelDev<T> M, T margin, const double* __restrict__ X, int d, const int32_t* __restrict__ col,
+k_bisect(const __grid_constant__ ModelDev<T> M, T margin, const double* __restrict__ X, int d, const int32_t* __restrict__ col,
          int32_t* __restrict__ rec, const int32_t* __restrict__ it, const double* __restrict__ seg, double ee,
          int n_b, double t_col,
          double* __restrict__ star, double* __restrict__ pstar, double* __restrict__ dstar) {

@@ -9,18 +9,21 @@ struct ez_world;
 
 namespace ez {
 
-// One compiled module: the check kernels for one robot model (and margin).
-// k[rows f32/f64][0: 64..256 threads, 1: 512 threads].  Kept for the life of
-// the process.
+// CTA sizes the specialised kernels launch at (ez_world::jit_occ columns)
+constexpr int kJitSizeCount = 5;  // 64, 128, 256, 512, 1024
+
+// The check kernels for one robot model (and margin), one library each:
+// k[rows f32/f64][0: 64..256 threads, 1: 512 threads, 2: 1024 threads].  Kept
+// for the life of the process.
 struct JitCheck {
-    cudaLibrary_t lib = nullptr;
-    cudaKernel_t k[2][2] = {};
+    cudaLibrary_t lib[2][3] = {};
+    cudaKernel_t k[2][3] = {};
     ~JitCheck();
 };
 
 // Generate, compile (NVRTC, sm_100a) and load the world's specialised check
-// kernel, then pick its CTA size for large batches by timing 256 and 512
-// threads on random configurations; EZ_UNSUPPORTED if the model has robot
+// kernels, then pick the CTA size for large batches by timing 256, 512 and
+// 1024 threads on random configurations; EZ_UNSUPPORTED if the model has robot
 // boxes or NVRTC is missing.
 int32_t jit_specialize(ez_world* w);
 // CUDA source of the specialised kernel (for inspection and tests)

@@ -647,7 +647,7 @@ static int32_t build_voxel_grid(ez_world* w, const ez_scene_desc* sc, const HMod
 // ---------------------------------------------------------------------------
 template <typename T, typename Q, int BT>
 __global__ void __launch_bounds__(BT)
-k_check(ModelDev<T> M, const Q* __restrict__ q, int64_t n, int64_t ld, uint8_t* __restrict__ out,
+k_check(const __grid_constant__ ModelDev<T> M, const Q* __restrict__ q, int64_t n, int64_t ld, uint8_t* __restrict__ out,
         T margin, int64_t count_lim, int32_t* __restrict__ n_col) {
     extern __shared__ __align__(16) uint8_t smem[];
     __shared__ uint64_t bar;
@@ -663,7 +663,7 @@ k_check(ModelDev<T> M, const Q* __restrict__ q, int64_t n, int64_t ld, uint8_t* 
 }
 
 // link frames (true frames, fp64) for fk_batch / forward_kinematics
-__global__ void k_fk_frames(ModelDev<double> M, const double* __restrict__ Qt, const double* __restrict__ q,
+__global__ void k_fk_frames(const __grid_constant__ ModelDev<double> M, const double* __restrict__ Qt, const double* __restrict__ q,
                             int64_t n, double* __restrict__ out) {
     const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= n) return;
@@ -719,7 +719,7 @@ __global__ void k_fk_frames(ModelDev<double> M, const double* __restrict__ Qt, c
 // Hit statistics of every self pair and every sphere-vs-obstacle test over
 // uniform samples of the joint box; used only to order the tests.
 __global__ void __launch_bounds__(128)
-k_calibrate(ModelDev<float> M, const float* __restrict__ lo, const float* __restrict__ hi, int n, uint64_t seed,
+k_calibrate(const __grid_constant__ ModelDev<float> M, const float* __restrict__ lo, const float* __restrict__ hi, int n, uint64_t seed,
             float margin, uint32_t* __restrict__ pcount, uint32_t* __restrict__ sph_hits) {
     extern __shared__ __align__(16) uint8_t smem[];
     __shared__ uint64_t bar;

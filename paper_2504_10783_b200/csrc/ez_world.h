@@ -58,7 +58,7 @@ struct ez_world {
     bool jit_failed = false;
     std::string jit_error;
     int32_t jit_bt = 512;            // CTA size for large batches
-    int32_t jit_occ[2][4] = {};      // [rows f32/f64][CTA size 64/128/256/512] resident CTAs per SM
+    int32_t jit_occ[2][ez::kJitSizeCount] = {};  // [rows f32/f64][CTA size 64..1024] resident CTAs per SM
 
     // cached launch shapes of k_check, [T fp64][Q fp64]; set once under cfg_mu
     // (EI-ZO calls of several threads may race to the first launch)
