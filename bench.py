@@ -230,6 +230,7 @@ def bench_config4(checks_n: int = 1 << 20) -> dict:
     rep = inflate_edge(Segment(v1, v2), dom, params, ck, seed=7)
     wall = (time.perf_counter() - t0) * 1e3
     return {"checks_per_s": rate, "flop_per_check": 13104, "specialised_kernel": specialised, "jit_compile_ms": jit_ms,
+            "cta": nat.info()["check_cta"],
             "eizo_ms_wall": wall, "eizo_device_ms": rep.device_ms, "iterations": rep.iterations,
             "faces": rep.hyperplanes_added, "collision_checks": rep.collision_checks,
             "terminated_by": rep.terminated_by,
@@ -503,7 +504,7 @@ def run_ours(args):
                      "frac": achieved_tf / peak_tf.value, "traffic": traffic,
                      "kernel": ("ez_check_jit_f (k_check specialised for the model at run time, NVRTC sm_100a)"
                                 if specialised else "k_check<float,float>"),
-                     "jit_compile_ms": jit_ms, "flop_per_check": FLOP_PER_CHECK,
+                     "jit_compile_ms": jit_ms, "cta": nat.info()["check_cta"], "flop_per_check": FLOP_PER_CHECK,
                      "avg_launch_ms": avg_launch_ms,
                      "frac_note": "of measured: the FP32 FMA peak of this GPU, measured in this run",
                      "peak_source": "ez_fp32_peak FMA microbenchmark measured in this run "

@@ -28,7 +28,7 @@
 extern "C" {
 #endif
 
-#define EZ_ABI_VERSION 1
+#define EZ_ABI_VERSION 2
 
 /* ---- status codes: mapped 1:1 onto corridor.errors (errors.py:4-64) ---- */
 typedef enum ez_status {
@@ -103,6 +103,9 @@ typedef struct ez_world_info {
     double cell_side;             /* h = voxel side / subdivision            */
     int64_t list_entries;         /* candidate-list entries (incl. sentinels)*/
     int64_t device_bytes;         /* bytes held on the device                */
+    int32_t check_cta;            /* CTA size of the specialised check kernel */
+                                  /* for large batches, 0 = generic kernel   */
+    int32_t reserved_;
 } ez_world_info;
 
 /* EI-ZO parameters: inflation.InflationParams (inflation.py:55-95). */

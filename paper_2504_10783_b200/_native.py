@@ -40,7 +40,8 @@ class SceneDesc(C.Structure):
 class WorldInfo(C.Structure):
     _fields_ = [("dof", c_i32), ("n_links", c_i32), ("n_spheres", c_i32), ("n_pairs", c_i32),
                 ("n_static", c_i32), ("n_hot_pairs", c_i32), ("n_voxels", c_i64), ("grid_dims", c_i32 * 3),
-                ("cell_side", c_dbl), ("list_entries", c_i64), ("device_bytes", c_i64)]
+                ("cell_side", c_dbl), ("list_entries", c_i64), ("device_bytes", c_i64),
+                ("check_cta", c_i32), ("reserved_", c_i32)]
 
 
 class EizoParams(C.Structure):
@@ -109,7 +110,7 @@ def load_library(path: Path | str | None = None) -> C.CDLL:
             fn = getattr(lib, name)
             fn.restype = res
             fn.argtypes = args
-        if lib.ez_abi_version() != 1:
+        if lib.ez_abi_version() != 2:
             raise NativeError("ABI version mismatch")
         if path is None:
             _lib = lib

@@ -1163,6 +1163,11 @@ extern "C" int32_t ez_world_get_info(const ez_world* w, ez_world_info* out) {
     out->cell_side = w->cell_h;
     out->list_entries = w->n_list;
     out->device_bytes = w->device_bytes;
+    {
+        std::lock_guard<std::mutex> lk(const_cast<ez_world*>(w)->cfg_mu);  // jit is published under cfg_mu
+        out->check_cta = w->jit ? w->jit_bt : 0;
+    }
+    out->reserved_ = 0;
     return EZ_OK;
 }
 

@@ -74,6 +74,25 @@ def test_large_batches_specialise_automatically():
     hi = torch.as_tensor(w.upper, dtype=torch.float32, device="cuda")
     nat.check_device(lo + (hi - lo) * torch.rand((1 << 18, 7), device="cuda"))
     assert nat.specialize(0)
+    assert nat.info()["check_cta"] in (256, 512, 1024)
+
+
+@pytest.mark.parametrize("cta", [256, 512, 1024])
+def test_every_kernel_shape_equals_generic(cta, monkeypatch):
+    """The 64..256, 512 x 2 and 1024 x 1 kernels (EZ_JIT_BT forces the large-batch size)."""
+    monkeypatch.setenv("EZ_JIT_BT", str(cta))
+    w = fx.bimanual14_world()
+    gen, jit = w.checker().native, w.checker().native
+    gen.specialize(-1)
+    assert gen.info()["check_cta"] == 0
+    assert jit.specialize(1) and jit.info()["check_cta"] == cta
+    lo = torch.as_tensor(w.lower, dtype=torch.float32, device="cuda")
+    hi = torch.as_tensor(w.upper, dtype=torch.float32, device="cuda")
+    g = torch.Generator(device="cuda")
+    g.manual_seed(cta)
+    Q = lo + (hi - lo) * torch.rand((1 << 19, 14), generator=g, device="cuda")
+    assert torch.equal(gen.check_device(Q), jit.check_device(Q))
+    assert torch.equal(gen.check_device(Q.double()), jit.check_device(Q.double()))
 
 
 def _oblique_world():
