@@ -15,8 +15,12 @@
 // A policy P supplies the model:
 //   bool a(const Q* row, T* cen) const   phase A, true = collides
 //   bool b(const Q* row, T* cen) const   phase B, true = collides
-// `row` is the thread's staged configuration, `cen` its centre store
-// (element k at cen[k * BT]).
+//   static constexpr bool kRegRows
+// `cen` is the thread's centre store (element k at cen[k * BT]).  With
+// kRegRows (a policy whose joint count is a compile-time constant: the
+// run-time compiled kernels) `row` is a register array loaded by the thread
+// itself, the next tile's row prefetched, and the CTA meets at two barriers
+// per tile; otherwise rows are staged through shared memory.
 #pragma once
 
 #include "ez_device.cuh"
@@ -39,6 +43,90 @@ __device__ __forceinline__ void check_phase_b(const P& pol, int dof, const Q* __
     const bool c2 = pol.b(row, cen);
     out[idx] = c2 ? 0 : 1;
     if (n_col != nullptr && c2 && idx < count_lim) atomicAdd(n_col, 1);
+}
+
+// Register-row variant (P::kRegRows): no shared-memory rows, so neither the
+// staging barriers nor a barrier per phase-B round.  The two barriers left per
+// tile publish the per-warp survivor counts and then the queue; a thread that
+// passes the first one of the next tile knows every thread has finished this
+// tile's rounds, so queue slots and s_warp are never overwritten early.
+template <typename T, typename Q, int BT, class P>
+__device__ __forceinline__ void check_tiles_reg(const P& pol, int dof, int32_t* s_queue, int* s_warp,
+                                                const Q* __restrict__ q, int64_t n, int64_t ld,
+                                                uint8_t* __restrict__ out, int64_t count_lim,
+                                                int32_t* __restrict__ n_col) {
+    const int bt = BT > 0 ? BT : static_cast<int>(blockDim.x);
+    const int qcap = 2 * bt;
+    auto wrap = [&](int x) { return BT > 0 ? x % qcap : (x & (qcap - 1)); };
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const bool pre = dof <= kPrefetch;  // prefetch the next tile's row in registers
+    int qhead = 0, qn = 0;
+    const int64_t tiles = (n + bt - 1) / bt;
+    Q nxt[kPrefetch];
+    auto prefetch = [&](int64_t tile) {
+        const int64_t r = tile * bt + threadIdx.x;
+        if (tile < tiles && r < n) {
+#pragma unroll
+            for (int k = 0; k < kPrefetch; ++k)
+                if (k < dof) nxt[k] = q[r * ld + k];
+        }
+    };
+    if (pre) prefetch(blockIdx.x);
+    for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+        const int64_t base = tile * bt;
+        const int nr = static_cast<int>(min(static_cast<int64_t>(bt), n - base));
+        const bool valid = threadIdx.x < nr;
+        bool col = false;
+        if (valid) {
+            Q row[32];
+            if (pre) {
+#pragma unroll
+                for (int k = 0; k < kPrefetch; ++k)
+                    if (k < dof) row[k] = nxt[k];
+            } else {
+#pragma unroll
+                for (int k = 0; k < 32; ++k)
+                    if (k < dof) row[k] = q[(base + threadIdx.x) * ld + k];
+            }
+            if (pre) prefetch(tile + gridDim.x);  // lands while this tile is checked
+            col = pol.a(row, static_cast<T*>(nullptr));
+            if (col) out[base + threadIdx.x] = 0;
+        }
+        if (n_col != nullptr) {
+            const unsigned m = __ballot_sync(0xffffffffu, col && (base + threadIdx.x) < count_lim);
+            if (lane == 0 && m) atomicAdd(n_col, __popc(m));
+        }
+        const bool surv = valid && !col;
+        const unsigned sm = __ballot_sync(0xffffffffu, surv);
+        if (lane == 0) s_warp[wid] = __popc(sm);
+        __syncthreads();
+        int off = 0, add = 0;
+        for (int w = 0; w < bt / 32; ++w) {
+            const int c = s_warp[w];
+            off += (w < wid) ? c : 0;
+            add += c;
+        }
+        if (surv)
+            s_queue[wrap(qhead + qn + off + __popc(sm & ((1u << lane) - 1u)))] = static_cast<int32_t>(base + threadIdx.x);
+        qn += add;
+        __syncthreads();
+        const bool last = tile + gridDim.x >= tiles;
+        while (qn >= bt || (last && qn > 0)) {
+            if (threadIdx.x < min(qn, bt)) {
+                const int64_t idx = s_queue[wrap(qhead + threadIdx.x)];
+                Q row[32];
+#pragma unroll
+                for (int k = 0; k < 32; ++k)
+                    if (k < dof) row[k] = q[idx * ld + k];
+                const bool c2 = pol.b(row, static_cast<T*>(nullptr));
+                out[idx] = c2 ? 0 : 1;
+                if (n_col != nullptr && c2 && idx < count_lim) atomicAdd(n_col, 1);
+            }
+            const int took = min(qn, bt);
+            qhead = wrap(qhead + took);
+            qn -= took;
+        }
+    }
 }
 
 // rows: bt * dof staging slots in shared memory; s_queue: 2 * bt entries;
@@ -132,6 +220,7 @@ __device__ __forceinline__ void check_tiles(const P& pol, int dof, T* my_cen, Q*
 // The generic policy: the model is the blob staged in shared memory.
 template <typename T, int BT>
 struct BlobPolicy {
+    static constexpr bool kRegRows = false;  // run-time joint count: rows stay in shared memory
     const ModelDev<T>& M;
     const uint8_t* smem;
     T margin;

@@ -312,7 +312,7 @@ struct Gen {
     std::string source() {
         o << "// generated by ez_jit.cu for one robot model\n#include \"ez_check_core.cuh\"\n\nnamespace ez {\n\n"
           << "__device__ __forceinline__ float sq3(float dx, float dy, float dz) { return dx * dx + dy * dy + dz * dz; }\n\n"
-          << "struct JitPolicy {\n    const ModelDev<float>& M;\n"
+          << "struct JitPolicy {\n    static constexpr bool kRegRows = true;\n    const ModelDev<float>& M;\n"
           << "    template <typename Q>\n    __device__ __forceinline__ bool a(const Q* row, float*) const {\n";
         fk();
         hot();
@@ -328,12 +328,9 @@ struct Gen {
              "int64_t n, int64_t ld, uint8_t* out, int64_t count_lim, int32_t* n_col) {\n"
           << "    extern __shared__ __align__(16) uint8_t smem[];\n"
           << "    __shared__ int s_warp[32];\n"
-          << "    const size_t qoff = (static_cast<size_t>(BT > 0 ? BT : blockDim.x) * " << M.dof
-          << " * sizeof(Q) + 15) & ~size_t(15);\n"
           << "    const JitPolicy pol{M};\n"
-          << "    check_tiles<float, Q, BT>(pol, " << M.dof
-          << ", static_cast<float*>(nullptr), reinterpret_cast<Q*>(smem), reinterpret_cast<int32_t*>(smem + qoff), s_warp, "
-             "q, n, ld, out, count_lim, n_col);\n}\n\n"
+          << "    check_tiles_reg<float, Q, BT>(pol, " << M.dof
+          << ", reinterpret_cast<int32_t*>(smem), s_warp, q, n, ld, out, count_lim, n_col);\n}\n\n"
           << "}  // namespace ez\n\n";
         return o.str();
     }
@@ -499,10 +496,9 @@ std::string jit_source(const ez_world* w) {
 
 namespace {
 
-size_t jit_smem(const ez_world* w, int bt, bool q64) {
-    const size_t rows = (static_cast<size_t>(bt) * w->dof * (q64 ? sizeof(double) : sizeof(float)) + 15) & ~size_t(15);
-    return rows + 2 * static_cast<size_t>(bt) * sizeof(int32_t);
-}
+// dynamic shared memory: the survivor ring of 2 * bt entries (rows live in
+// registers, check_tiles_reg)
+size_t jit_smem(const ez_world*, int bt, bool) { return 2 * static_cast<size_t>(bt) * sizeof(int32_t); }
 
 // random rows in the joint box for the CTA-size pick
 __global__ void k_fill_box(float* q, int64_t n, int dof, const double* lo, const double* hi, uint64_t seed) {
