@@ -14,6 +14,8 @@ v1, v2 = fx.random_free_segment(w, seed=3)
 dom = HPolytope.from_bounds(w.lower, w.upper)
 p = InflationParams(**fx.FRANKA_PARAMS)
 ck = w.checker()
+if "--jit" in sys.argv:
+    print("specialised:", ck.native.specialize(1))
 for _ in range(2):
     inflate_edge(Segment(v1, v2), dom, p, ck, seed=7)
 torch.cuda.synchronize()
@@ -39,5 +41,5 @@ for e in ev:
     k = e["name"].split("(")[0][:40]
     by[k] = by.get(k, 0.0) + e["dur"]
 print(f"region span {t1 - t0:.0f} us, GPU busy {busy:.0f} us ({100 * busy / (t1 - t0):.0f}%), device_ms {r.device_ms:.3f}")
-for k, v in sorted(by.items(), key=lambda x: -x[1])[:10]:
+for k, v in sorted(by.items(), key=lambda x: -x[1])[:14]:
     print(f"  {k:40s} {v:9.0f} us")
