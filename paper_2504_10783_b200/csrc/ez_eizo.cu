@@ -678,6 +678,114 @@ k_bisect(const __grid_constant__ ModelDev<T> M, T margin, const double* __restri
     if (lane == 0) dstar[i] = ds;
 }
 
+// Two bisection levels per round.  One warp per candidate, four 8-lane
+// subgroups: subgroup 0 checks the midpoint m of [lo, hi], subgroups 1 and 2
+// the midpoints of [lo, m] and [m, hi] (the two points the next binary step
+// can check), subgroup 3 the projection in the first round (the fail-fast
+// check).  The round then takes both binary steps the results decide.  The
+// quarter points are formed from the same end points with the same
+// operations as the one-step loop's next midpoint, so every checked point,
+// every decision and star/pstar are bit-identical to k_bisect's, in half the
+// dependent rounds.
+template <typename T, int MAXD>
+__global__ void __launch_bounds__(128)
+k_bisect2(const __grid_constant__ ModelDev<T> M, T margin, const double* __restrict__ X, int d,
+          const int32_t* __restrict__ col, int32_t* __restrict__ rec, const int32_t* __restrict__ it,
+          const double* __restrict__ seg, double ee, int n_b, double t_col, double* __restrict__ star,
+          double* __restrict__ pstar, double* __restrict__ dstar) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    __shared__ uint64_t bar;
+    constexpr int G = kBisectLanes;
+    constexpr int SLOTS = 128 / G;      // subgroups per CTA, each with a row and a centre store
+    constexpr int CPB = 128 / 32;       // candidates per CTA
+    constexpr int PER = (MAXD + G - 1) / G;
+    static_assert(G == 8, "four subgroups per warp");
+    const int C = it[kNumCand];
+    if (rec[kStatus] != EZ_OK || rec[kStop] || static_cast<int64_t>(blockIdx.x) * CPB >= C) return;
+    tma_stage(smem, M.blob, M.blob_bytes, &bar);
+    const int slot = threadIdx.x / G, lane = threadIdx.x & (G - 1), sub = slot & 3;
+    T* cen = reinterpret_cast<T*>(smem + M.blob_bytes) + static_cast<size_t>(slot) * M.cen_words;
+    const size_t roff = (static_cast<size_t>(M.blob_bytes) + static_cast<size_t>(M.cen_words) * SLOTS * sizeof(T) + 15) &
+                        ~static_cast<size_t>(15);
+    double* row = reinterpret_cast<double*>(smem + roff) + slot * d;
+    const int i = blockIdx.x * CPB + static_cast<int>(threadIdx.x >> 5);
+    if (i >= C) return;  // whole warps leave together
+    const unsigned gm = coop_mask<G>();
+    const double* v1 = seg;
+    const double* e = seg + d;
+    double c[PER], lo[PER], hi[PER];
+    const double* xc = X + static_cast<int64_t>(col[i]) * d;
+#pragma unroll
+    for (int j = 0; j < PER; ++j) {
+        const int k = lane + j * G;
+        c[j] = (k < d) ? xc[k] : 0.0;
+    }
+    project_group<MAXD, G>(c, d, v1, e, ee, lo, lane, gm);
+#pragma unroll
+    for (int j = 0; j < PER; ++j) hi[j] = c[j];
+    bool first = true;
+    for (int done = 0; first || done < n_b;) {
+        const int lv = min(2, n_b - done);  // binary steps taken this round
+        double m[PER], pt[PER];
+#pragma unroll
+        for (int j = 0; j < PER; ++j) {
+            m[j] = 0.5 * (lo[j] + hi[j]);
+            pt[j] = sub == 0 ? m[j] : (sub == 1 ? 0.5 * (lo[j] + m[j]) : (sub == 2 ? 0.5 * (m[j] + hi[j]) : lo[j]));
+        }
+        const bool active = sub == 0 ? lv >= 1 : (sub == 3 ? first : lv >= 2);
+        bool fr = true;
+        if (active) {
+#pragma unroll
+            for (int j = 0; j < PER; ++j) {
+                const int k = lane + j * G;
+                if (k < d) row[k] = pt[j];
+            }
+            __syncwarp(gm);
+            fr = config_free_coop<T, double, G>(M, smem, row, cen, margin);
+        }
+        const unsigned bal = __ballot_sync(0xffffffffu, fr && lane == 0);  // bits 0, 8, 16, 24
+        if (first) {
+            if (!((bal >> 24) & 1u)) {
+                if ((threadIdx.x & 31) == 0) set_status(rec + kStatus, EZ_SEGMENT_IN_COLLISION);  // inflation.py:303-305
+                return;
+            }
+            first = false;
+        }
+        if (lv >= 1) {
+            const bool f0 = bal & 1u;
+#pragma unroll
+            for (int j = 0; j < PER; ++j) {
+                if (f0) lo[j] = m[j];
+                else hi[j] = m[j];
+            }
+            if (lv >= 2) {
+                const bool f1 = (bal >> (f0 ? 16 : 8)) & 1u;
+#pragma unroll
+                for (int j = 0; j < PER; ++j) {
+                    const double q = 0.5 * (lo[j] + hi[j]);  // the point subgroup 1 or 2 checked
+                    if (f1) lo[j] = q;
+                    else hi[j] = q;
+                }
+            }
+            done += lv;
+        }
+        __syncwarp();
+    }
+    if (sub != 0) return;
+    double ps[PER];
+    const double ds = project_group<MAXD, G>(hi, d, v1, e, ee, ps, lane, gm);
+    if (ds <= t_col && lane == 0) set_status(rec + kStatus, EZ_SEGMENT_IN_COLLISION);  // inflation.py:307-310
+#pragma unroll
+    for (int j = 0; j < PER; ++j) {
+        const int k = lane + j * G;
+        if (k < d) {
+            star[static_cast<int64_t>(i) * d + k] = hi[j];
+            pstar[static_cast<int64_t>(i) * d + k] = ps[j];
+        }
+    }
+    if (lane == 0) dstar[i] = ds;
+}
+
 // Greedy hyperplane placement on one CTA (inflation.py:232-259): the closest
 // alive candidate (stable order == lexicographic (dist, index)) becomes a
 // tangent face pushed back by compute_step_back; candidates outside die.
@@ -1161,10 +1269,17 @@ static int32_t launch_bisect_t(ez_world* w, ez_eizo_ws* ws, const ModelDev<T>& M
     smem = (smem + 15) & ~static_cast<size_t>(15);
     smem += static_cast<size_t>(CPB) * d * sizeof(double);
     smem = (smem + 15) & ~static_cast<size_t>(15);
-    auto kern = k_bisect<T, MAXD, G>;
+    // two levels per round (k_bisect2, a warp per candidate) unless
+    // EZ_BISECT1=1 asks for the one-step loop (8 lanes per candidate)
+    static const bool one_step = [] {
+        const char* e = getenv("EZ_BISECT1");
+        return e && e[0] == '1';
+    }();
+    auto kern = one_step ? k_bisect<T, MAXD, G> : k_bisect2<T, MAXD>;
+    const int cpb = one_step ? CPB : 128 / 32;
     if (smem > static_cast<size_t>(w->smem_optin) - 1024) return fail(EZ_CAPACITY, "robot model too large for one bisection CTA");
     if (smem > 48 * 1024) EZ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    kern<<<static_cast<unsigned>((n_p + CPB - 1) / CPB), 128, smem, s>>>(M, static_cast<T>(w->margin), ws->X, d, ws->col,
+    kern<<<static_cast<unsigned>((n_p + cpb - 1) / cpb), 128, smem, s>>>(M, static_cast<T>(w->margin), ws->X, d, ws->col,
                                                                      ws->rec, it, ws->seg, ee, n_b, t_col, ws->star,
                                                                      ws->pstar, ws->dstar);
     EZ_CUDA(cudaGetLastError());

@@ -134,3 +134,37 @@ def test_n_it_one_places_once_then_stops():
     assert rep.iterations == 1 and rep.terminated_by == "max_iterations"
     assert 0 < rep.hyperplanes_added <= InflationParams().n_f
     assert rep.polytope.contains(seg.v1, 1e-9) and rep.polytope.contains(seg.v2, 1e-9)
+
+
+_BISECT_CHILD = r"""
+import sys, numpy as np
+sys.path.insert(0, {root!r})
+from paper_2504_10783_b200 import fixtures as fx
+from paper_2504_10783_b200.eizo import InflationParams, Segment, inflate_edge
+from paper_2504_10783_b200.polytope import HPolytope
+out = []
+for world, prec in ((fx.franka7_world(), "fp32"), (fx.arm3_world(), "fp64")):
+    v1, v2 = fx.random_free_segment(world, seed=3) if world.model.dof == 7 else fx.ARM3_SEGMENT
+    dom = HPolytope.from_bounds(world.lower, world.upper)
+    params = InflationParams(**fx.FRANKA_PARAMS) if world.model.dof == 7 else InflationParams()
+    rep = inflate_edge(Segment(v1, v2), dom, params, world.checker(precision=prec), seed=7)
+    out += [rep.polytope.A, rep.polytope.b, np.array([rep.collision_checks, rep.iterations])]
+np.savez({path!r}, *out)
+"""
+
+
+def test_two_level_bisection_equals_one_step(tmp_path):
+    """k_bisect2 (two binary levels per round) against the one-step loop (EZ_BISECT1=1): same regions."""
+    import os, subprocess, sys
+    from pathlib import Path
+    root = str(Path(__file__).resolve().parents[1])
+    res = []
+    for flag in ("0", "1"):
+        path = str(tmp_path / f"b{flag}.npz")
+        env = dict(os.environ, EZ_BISECT1=flag)
+        subprocess.run([sys.executable, "-c", _BISECT_CHILD.format(root=root, path=path)], env=env, check=True,
+                       timeout=600)
+        z = np.load(path)
+        res.append([z[k] for k in sorted(z.files, key=lambda s: int(s.split("_")[1]))])
+    for a, b in zip(*res):
+        assert np.array_equal(a, b)
