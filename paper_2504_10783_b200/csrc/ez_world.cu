@@ -129,19 +129,21 @@ struct HModel {
     int dof = 0, n_store = 0;
 };
 
-// calibrated hot self pairs tested in phase A (EZ_HOT_PAIRS overrides, for tuning)
-int hot_pairs() {
+// calibrated hot self pairs tested in phase A: 16, or one per 40 pairs up to
+// 32 for large models (measured: 7-DOF / 248 pairs best at 16, 14-DOF / 1,264
+// pairs +8% at 32); EZ_HOT_PAIRS overrides, for tuning
+int hot_pairs(int n_pairs) {
     static const int v = [] {
         const char* e = getenv("EZ_HOT_PAIRS");
-        const int x = e ? atoi(e) : 16;
-        return (x >= 0 && x <= 256) ? x : 16;
+        const int x = e ? atoi(e) : -1;
+        return (x >= 0 && x <= 256) ? x : -1;
     }();
-    return v;
+    return v >= 0 ? v : std::max(16, std::min(32, n_pairs / 40));
 }
 constexpr int kMinBlock = 3;   // smaller link-pair blocks are tested without the bounding-sphere skip
 
 // Pair/sphere layout.  Without statistics: no hot list, blocks in link order.
-// With per-pair and per-sphere hit counts: the hot_pairs() most frequent self
+// With per-pair and per-sphere hit counts: the hot_pairs(np) most frequent self
 // pairs first (flat), the rest in link-pair blocks ordered by hits, spheres
 // tested against obstacles in decreasing hit frequency.
 void layout_pairs(HModel& hm, const std::vector<uint32_t>* pair_hits, const std::vector<uint32_t>* sph_hits) {
@@ -153,7 +155,7 @@ void layout_pairs(HModel& hm, const std::vector<uint32_t>* pair_hits, const std:
     hm.hot.clear();
     if (pair_hits) {
         std::stable_sort(rank.begin(), rank.end(), [&](int x, int y) { return hits(x) > hits(y); });
-        for (int k = 0; k < std::min(hot_pairs(), np); ++k) {
+        for (int k = 0; k < std::min(hot_pairs(np), np); ++k) {
             if (hits(rank[k]) == 0) break;
             is_hot[rank[k]] = 1;
             hm.hot.push_back(hm.all_pairs[rank[k]]);
