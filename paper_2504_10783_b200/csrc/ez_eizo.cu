@@ -786,14 +786,24 @@ k_bisect2(const __grid_constant__ ModelDev<T> M, T margin, const double* __restr
     if (lane == 0) dstar[i] = ds;
 }
 
+// k_place's shared memory: candidate distances cached when they fit next to
+// the alive bytes (up to 200 KB in all)
+inline int place_dist_cap(int n) { return 9 * static_cast<size_t>(n) <= 200 * 1024 ? n : 0; }
+inline size_t place_smem_bytes(int n, int dcap) {
+    return static_cast<size_t>(dcap) * sizeof(double) + static_cast<size_t>(n);
+}
+
 // Greedy hyperplane placement on one CTA (inflation.py:232-259): the closest
 // alive candidate (stable order == lexicographic (dist, index)) becomes a
 // tangent face pushed back by compute_step_back; candidates outside die.
 __global__ void __launch_bounds__(1024)
 k_place(double* __restrict__ A, double* __restrict__ b, int32_t* __restrict__ rec, int32_t* __restrict__ it, int d,
         const double* __restrict__ star, const double* __restrict__ pstar, const double* __restrict__ dstar,
-        const double* __restrict__ seg, double delta_max, int n_f, const double* __restrict__ targets) {
-    extern __shared__ uint8_t alive[];
+        const double* __restrict__ seg, double delta_max, int n_f, const double* __restrict__ targets, int dcap) {
+    // dynamic shared memory: dcap cached distances, then one alive byte per candidate
+    extern __shared__ __align__(16) uint8_t smem_place[];
+    double* s_dist = reinterpret_cast<double*>(smem_place);
+    uint8_t* alive = smem_place + static_cast<size_t>(dcap) * sizeof(double);
     __shared__ double s_bd[32];
     __shared__ int s_bi[32];
     __shared__ double s_a[32];
@@ -802,23 +812,43 @@ k_place(double* __restrict__ A, double* __restrict__ b, int32_t* __restrict__ re
     if (rec[kStatus] != EZ_OK || rec[kStop]) return;
     const int C = it[kNumCand];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    for (int i = threadIdx.x; i < C; i += blockDim.x) alive[i] = 1;
+    const bool cached = C <= dcap;
+    for (int i = threadIdx.x; i < C; i += blockDim.x) {
+        alive[i] = 1;
+        if (cached) s_dist[i] = dstar[i];
+    }
     int F = rec[kFaces];
     int placed = 0;
     const double* v1 = seg;
     const double* e = seg + d;
+    const double* tg = targets ? targets : star;
+    double rhs = 0.0;
     for (int r = 0; r < n_f; ++r) {
         __syncthreads();
+        // one pass: the discard test of the face placed last round (on the
+        // anchors, or on the original collisions in a repair, planner.py:
+        // 191-192), then the arg-min over the survivors
         double bd = INFINITY;
         int bi = INT_MAX;
         for (int i = threadIdx.x; i < C; i += blockDim.x) {
             if (!alive[i]) continue;
-            const double di = dstar[i];
+            if (r > 0) {
+                const double* t = tg + static_cast<int64_t>(i) * d;
+                double dot = 0.0;
+                for (int k = 0; k < d; ++k) dot = fma(t[k], s_a[k], dot);
+                if (!(dot <= rhs)) {
+                    alive[i] = 0;
+                    continue;
+                }
+            }
+            const double di = cached ? s_dist[i] : dstar[i];
             if (di < bd || (di == bd && i < bi)) {
                 bd = di;
                 bi = i;
             }
         }
+        // (the barrier after the warp results also orders every read of s_a
+        // above before warp 0 overwrites it)
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
             const double od = __shfl_down_sync(0xffffffffu, bd, o);
@@ -846,57 +876,60 @@ k_place(double* __restrict__ A, double* __restrict__ b, int32_t* __restrict__ re
                     bi = oi;
                 }
             }
-            if (lane == 0) {
-                int best = (bi == INT_MAX) ? -1 : bi;
-                if (best >= 0) {
-                    const double dist = dstar[best];
-                    if (dist <= 1e-12) {
-                        set_status(rec + kStatus, EZ_GRADIENT_UNDEFINED);  // inflation.py:423-424
-                        best = -1;
-                    } else {
-                        const double* cs = star + static_cast<int64_t>(best) * d;
-                        const double* cp = pstar + static_cast<int64_t>(best) * d;
-                        double braw = 0.0, av1 = 0.0, av2 = 0.0, nn = 0.0;
-                        for (int k = 0; k < d; ++k) {
-                            const double ak = (cs[k] - cp[k]) / dist;
-                            s_a[k] = ak;
-                            braw = fma(ak, cs[k], braw);
-                            av1 = fma(ak, v1[k], av1);
-                            av2 = fma(ak, v1[k] + e[k], av2);
-                            nn = fma(ak, ak, nn);
-                        }
-                        // compute_step_back (inflation.py:203-212)
-                        const double rr = (fmax(av1, av2) - braw) + delta_max;
-                        const double delta = rr > 0.0 ? delta_max - rr : delta_max;
-                        double rhs = braw - delta;
-                        // HPolytope row normalisation (cpoly.py:32-38)
-                        const double norm = sqrt(nn);
-                        if (fabs(norm - 1.0) > 1e-12) {
-                            for (int k = 0; k < d; ++k) s_a[k] /= norm;
-                            rhs /= norm;
-                        }
-                        s_rhs = rhs;
-                        for (int k = 0; k < d; ++k) A[static_cast<int64_t>(F) * d + k] = s_a[k];
-                        b[F] = rhs;
-                    }
-                }
-                s_best = best;
+            // the face: lane k < d owns component k; the dot products run over k
+            // in order on every lane (values gathered by shuffles), the bits of
+            // the serial loop
+            bi = __shfl_sync(0xffffffffu, bi, 0);
+            bd = __shfl_sync(0xffffffffu, bd, 0);  // = dstar[best]
+            int best = (bi == INT_MAX) ? -1 : bi;
+            if (best >= 0 && bd <= 1e-12) {
+                if (lane == 0) set_status(rec + kStatus, EZ_GRADIENT_UNDEFINED);  // inflation.py:423-424
+                best = -1;
             }
+            if (best >= 0) {
+                const double dist = bd;
+                double ak = 0.0, ck = 0.0, vk = 0.0, ek = 0.0;
+                if (lane < d) {
+                    ck = star[static_cast<int64_t>(best) * d + lane];
+                    ak = (ck - pstar[static_cast<int64_t>(best) * d + lane]) / dist;
+                    vk = v1[lane];
+                    ek = e[lane];
+                }
+                double braw = 0.0, av1 = 0.0, av2 = 0.0, nn = 0.0;
+                for (int k = 0; k < d; ++k) {
+                    const double a = __shfl_sync(0xffffffffu, ak, k), c = __shfl_sync(0xffffffffu, ck, k);
+                    const double v = __shfl_sync(0xffffffffu, vk, k), w = __shfl_sync(0xffffffffu, ek, k);
+                    braw = fma(a, c, braw);
+                    av1 = fma(a, v, av1);
+                    av2 = fma(a, v + w, av2);
+                    nn = fma(a, a, nn);
+                }
+                // compute_step_back (inflation.py:203-212)
+                const double rr = (fmax(av1, av2) - braw) + delta_max;
+                const double delta = rr > 0.0 ? delta_max - rr : delta_max;
+                double rh = braw - delta;
+                // HPolytope row normalisation (cpoly.py:32-38)
+                const double norm = sqrt(nn);
+                if (fabs(norm - 1.0) > 1e-12) {
+                    ak /= norm;
+                    rh /= norm;
+                }
+                if (lane < d) {
+                    s_a[lane] = ak;
+                    A[static_cast<int64_t>(F) * d + lane] = ak;
+                }
+                if (lane == 0) {
+                    s_rhs = rh;
+                    b[F] = rh;
+                }
+            }
+            if (lane == 0) s_best = best;
         }
         __syncthreads();
         if (s_best < 0) break;
         ++F;
         ++placed;
-        const double rhs = s_rhs;
-        for (int i = threadIdx.x; i < C; i += blockDim.x) {
-            if (!alive[i]) continue;
-            // discard test on the anchors (inflation) or on the original collisions (repair,
-            // planner.py:191-192)
-            const double* t = (targets ? targets : star) + static_cast<int64_t>(i) * d;
-            double dot = 0.0;
-            for (int k = 0; k < d; ++k) dot = fma(t[k], s_a[k], dot);
-            alive[i] = dot <= rhs;
-        }
+        rhs = s_rhs;
     }
     if (threadIdx.x == 0) {
         rec[kFaces] = F;
@@ -1386,10 +1419,11 @@ extern "C" int32_t ez_inflate_edge(ez_world* w, const double* h_v1, const double
         EZ_CUDA(cudaMemcpyAsync(ws->rec + kFaces, &f0, sizeof(int32_t), cudaMemcpyHostToDevice, s));
     }
     EZ_CUDA(cudaEventRecord(ws->ev0, s));
-    const size_t place_smem = static_cast<size_t>(p.n_p);
+    if (p.n_p > 200 * 1024) return fail(EZ_UNSUPPORTED, "n_p above 204800 candidates");
+    const int place_dcap = place_dist_cap(p.n_p);
+    const size_t place_smem = place_smem_bytes(p.n_p, place_dcap);
     if (place_smem > 48 * 1024)
-        EZ_CUDA(cudaFuncSetAttribute(k_place, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(std::min<size_t>(place_smem, 200 * 1024))));
-    if (place_smem > 200 * 1024) return fail(EZ_UNSUPPORTED, "n_p above 204800 candidates");
+        EZ_CUDA(cudaFuncSetAttribute(k_place, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(place_smem)));
 
     // One iteration = hit-and-run, check (+ first-M count), compaction/test,
     // bisection, placement, and a 128-byte record copy.  Iteration k+1 is
@@ -1428,7 +1462,7 @@ extern "C" int32_t ez_inflate_edge(ez_world* w, const double* h_v1, const double
         else if (d <= 16) EZ_TRY(launch_bisect<16>(w, ws, precision, s, it, p.n_p, d, ee, p.n_b, p.t_col));
         else EZ_TRY(launch_bisect<32>(w, ws, precision, s, it, p.n_p, d, ee, p.n_b, p.t_col));
         k_place<<<1, 1024, place_smem, s>>>(ws->A, ws->b, ws->rec, it, d, ws->star, ws->pstar, ws->dstar, ws->seg,
-                                            p.delta_max, p.n_f, nullptr);
+                                            p.delta_max, p.n_f, nullptr, place_dcap);
         EZ_CUDA(cudaGetLastError());
         EZ_CUDA(cudaMemcpyAsync(ws->h_rec + kRecInts * (k & 1), ws->rec, kRecInts * sizeof(int32_t),
                                 cudaMemcpyDeviceToHost, s));
@@ -1556,12 +1590,13 @@ extern "C" int32_t ez_refine_set(ez_world* w, const double* h_v1, const double* 
     else if (d <= 8) EZ_TRY(launch_bisect<8>(w, ws, precision, s, it, n_cols, d, ee, n_b, t_col));
     else if (d <= 16) EZ_TRY(launch_bisect<16>(w, ws, precision, s, it, n_cols, d, ee, n_b, t_col));
     else EZ_TRY(launch_bisect<32>(w, ws, precision, s, it, n_cols, d, ee, n_b, t_col));
-    const size_t place_smem = static_cast<size_t>(n_cols);
-    if (place_smem > 200 * 1024) return fail(EZ_UNSUPPORTED, "more than 204800 collisions in one repair");
+    if (n_cols > 200 * 1024) return fail(EZ_UNSUPPORTED, "more than 204800 collisions in one repair");
+    const int place_dcap = place_dist_cap(static_cast<int>(n_cols));
+    const size_t place_smem = place_smem_bytes(static_cast<int>(n_cols), place_dcap);
     if (place_smem > 48 * 1024)
         EZ_CUDA(cudaFuncSetAttribute(k_place, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(place_smem)));
     k_place<<<1, 1024, place_smem, s>>>(ws->A, ws->b, ws->rec, ws->rec + slot_offset(0), d, ws->star, ws->pstar,
-                                        ws->dstar, ws->seg, delta_max, n_cols, ws->X);
+                                        ws->dstar, ws->seg, delta_max, n_cols, ws->X, place_dcap);
     EZ_CUDA(cudaGetLastError());
     EZ_CUDA(cudaMemcpyAsync(ws->h_rec, ws->rec, kRecInts * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
     EZ_CUDA(cudaStreamSynchronize(s));
