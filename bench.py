@@ -109,6 +109,18 @@ def _measured_peaks():
     return {}
 
 
+def cpu_model() -> str:
+    """The host CPU's model name (/proc/cpuinfo), for the CPU-baseline lines."""
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def cpu_oracle_rate(world, n: int, workers: int) -> dict:
     """The oracle port (numpy + cKDTree, oracle/ref.py) on a bounded sample of the same workload."""
     from oracle import ref
@@ -121,7 +133,8 @@ def cpu_oracle_rate(world, n: int, workers: int) -> dict:
     ck.check_batch(Q)  # cKDTree queries use `workers` threads; numpy FK / pairs are single threaded
     dt = time.perf_counter() - t0
     return {"value": n / dt, "unit": UNIT, "cores": workers, "kind": "port",
-            "sample": f"{n} uniform 7-DOF configs, oracle/ref.py (numpy+cKDTree restatement of world.py:483-565)"}
+            "sample": f"{n} uniform 7-DOF configs, oracle/ref.py (numpy+cKDTree restatement of world.py:483-565)",
+            "cpu": cpu_model(), "host_cpus": os.cpu_count()}
 
 
 def clustered_cloud(n_points: int, n_blobs: int, seed: int = 0) -> np.ndarray:
@@ -262,8 +275,10 @@ def bench_drm(n_nodes: int = 100_000, reps: int = 10, cpu: bool = True) -> dict:
     drm = Drm(nodes, np.zeros(n_nodes + 1, np.int64), np.zeros(0, np.int32), off, ids, np.zeros((n_nodes, 7)), grid)
     out = {"grid": "25x34x26 side 0.06", "n_nodes": n_nodes, "cmap_nnz": int(ids.shape[0]),
            "node_sampling_s": t_nodes, "cmap_build_s": t_map, "cmap_first_build_s": builds[0], "clouds": []}
-    for blobs in (3, 8):
-        pts = clustered_cloud(100_000, blobs, seed=blobs)
+    # 10^5-point clouds at the paper's ~360 active voxels, and the survey's
+    # stress case: 10^6 points, ~2k active voxels
+    for n_pts, blobs in ((100_000, 3), (100_000, 8), (1_000_000, 30)):
+        pts = clustered_cloud(n_pts, blobs, seed=blobs)
         vm = voxelize_point_cloud(pts, grid.side, grid.origin)
         cs = collision_set(drm, vm)
         times = []
@@ -312,7 +327,8 @@ def run_reference(args):
                        "sample_per_step": n},
             "impl": "reference",
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
-                             "sample": f"{n} configs per step, oracle/ref.py with {cores} threads"},
+                             "sample": f"{n} configs per step, oracle/ref.py with {cores} threads",
+                             "cpu": cpu_model(), "host_cpus": os.cpu_count()},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
