@@ -45,7 +45,7 @@ __device__ __forceinline__ unsigned group_mask() {
 // A: faces, row f at A + f * lda.  VEC: rows are 16-byte aligned with lda
 // even (shared-memory staging), so a row is read as double2 pairs.
 // Zw: the walk's counter-stream draws (k_draws), element (step, k) at
-// Zw[(step * (d + 1) + k) * zs]; they are loaded one step ahead.
+// Zw[(step * (d + 1) + k) * zs] (unit directions, then the uniform); loaded one step ahead.
 template <int MAXD, int RNG, int LPW, bool VEC>
 __device__ __forceinline__ int hnr_walk(double (&x)[MAXD], int d, const double* __restrict__ A, int lda,
                                         const double* __restrict__ b, int F, int n_ms, uint64_t seed,
@@ -99,26 +99,29 @@ __device__ __forceinline__ int hnr_walk(double (&x)[MAXD], int d, const double* 
                 dir[k] = (k < d) ? static_cast<double>(v) : 0.0;
             }
         }
-        // normalise like numpy (squares rounded, left-to-right sum, IEEE divide)
-        double ss = 0.0;
+        // normalise like numpy (squares rounded, left-to-right sum, IEEE divide);
+        // the counter stream's draws arrive normalised (k_draws)
+        if (RNG != EZ_RNG_COUNTER) {
+            double ss = 0.0;
 #pragma unroll
-        for (int k = 0; k < MAXD; ++k)
-            if (k < d) ss = __dadd_rn(ss, __dmul_rn(dir[k], dir[k]));
-        const double nrm = sqrt(ss);
-        // lane l divides components l, l + LPW, ... (IEEE division, as numpy);
-        // the quotients are broadcast back to the group
-        double qv[PER];
+            for (int k = 0; k < MAXD; ++k)
+                if (k < d) ss = __dadd_rn(ss, __dmul_rn(dir[k], dir[k]));
+            const double nrm = sqrt(ss);
+            // lane l divides components l, l + LPW, ... (IEEE division, as numpy);
+            // the quotients are broadcast back to the group
+            double qv[PER];
 #pragma unroll
-        for (int j = 0; j < PER; ++j) {
-            const int k = lane + j * LPW;
-            double v = 0.0;
+            for (int j = 0; j < PER; ++j) {
+                const int k = lane + j * LPW;
+                double v = 0.0;
 #pragma unroll
-            for (int kk = 0; kk < MAXD; ++kk)
-                if (kk == k) v = dir[kk];
-            qv[j] = (k < d) ? v / nrm : 0.0;
+                for (int kk = 0; kk < MAXD; ++kk)
+                    if (kk == k) v = dir[kk];
+                qv[j] = (k < d) ? v / nrm : 0.0;
+            }
+#pragma unroll
+            for (int k = 0; k < MAXD; ++k) dir[k] = __shfl_sync(gm, qv[k / LPW], k % LPW, LPW);
         }
-#pragma unroll
-        for (int k = 0; k < MAXD; ++k) dir[k] = __shfl_sync(gm, qv[k / LPW], k % LPW, LPW);
         // chord end points: t_hi = min over h > 0 of sl / h, t_lo = max over h < 0.
         // The arg-min/max is tracked as the fraction (sl, h), compared by
         // cross-multiplication, and divided once at the end.
@@ -194,6 +197,11 @@ __device__ __forceinline__ int hnr_walk(double (&x)[MAXD], int d, const double* 
 // They do not depend on the walk state, so generating them here (fully
 // parallel, throughput bound) leaves the walk's 60-step critical path with
 // loads issued a step ahead instead of hash + ndtri chains.
+// The draws are stored as the walk's unit direction (numpy's normalisation:
+// squares rounded, summed left to right, IEEE sqrt and divide; cpoly.py:163-164),
+// so the walks' critical path skips the norm.  Element (step, k) at
+// Z[(step * (d + 1) + k) * count + walk]; k = d holds the chord uniform.
+template <int MAXD>
 __global__ void k_draws(uint64_t seed, uint64_t walk_offset, int64_t count, int d, int n_ms, double* __restrict__ Z,
                         const int32_t* __restrict__ status) {
     if (status && (status[0] != EZ_OK || status[1] != 0)) return;
@@ -205,9 +213,28 @@ __global__ void k_draws(uint64_t seed, uint64_t walk_offset, int64_t count, int 
         const uint64_t step = static_cast<uint64_t>(t / count);
         const uint64_t key = walk_key(seed, walk_offset + static_cast<uint64_t>(i));
         double* z = Z + static_cast<int64_t>(step) * (d + 1) * count + i;
-        for (int k = 0; k < d; ++k) z[k * count] = counter_normal(key, step, k);
+        double v[MAXD];
+        double ss = 0.0;
+#pragma unroll
+        for (int k = 0; k < MAXD; ++k) {
+            v[k] = (k < d) ? counter_normal(key, step, k) : 0.0;
+            if (k < d) ss = __dadd_rn(ss, __dmul_rn(v[k], v[k]));
+        }
+        const double nrm = sqrt(ss);
+#pragma unroll
+        for (int k = 0; k < MAXD; ++k)
+            if (k < d) z[k * count] = v[k] / nrm;
         z[d * count] = counter_uniform(key, step, d);
     }
+}
+
+static void launch_draws(cudaStream_t s, uint64_t seed, uint64_t walk_offset, int64_t count, int d, int n_ms,
+                         double* z, const int32_t* status) {
+    const int64_t total = count * n_ms;
+    const unsigned grid = static_cast<unsigned>(std::min<int64_t>((total + 255) / 256, 148 * 16));
+    if (d <= 8) k_draws<8><<<grid, 256, 0, s>>>(seed, walk_offset, count, d, n_ms, z, status);
+    else if (d <= 16) k_draws<16><<<grid, 256, 0, s>>>(seed, walk_offset, count, d, n_ms, z, status);
+    else k_draws<32><<<grid, 256, 0, s>>>(seed, walk_offset, count, d, n_ms, z, status);
 }
 
 // Walk i starts at seeds[i % n_seeds] (explicit seeds) or at a point of the
@@ -342,12 +369,8 @@ k_hnr_mma(const double* __restrict__ Ap, const int32_t* __restrict__ F_dev, int 
     const int wl = lane >> 2, c = lane & 3;
     const int64_t wi = min(wbase + wl, count - 1);  // idle slots shadow the last walk
     const uint64_t key = walk_key(seed, walk_offset + static_cast<uint64_t>(wi));
-    // the walks whose C entries this lane owns (their uniforms)
-    int64_t sw[2];
-#pragma unroll
-    for (int s2 = 0; s2 < 2; ++s2) sw[s2] = min(wbase + 2 * c + s2, count - 1);
     const int64_t zstep = static_cast<int64_t>(d + 1) * count;
-    double nd[KC], nu[2];
+    double nd[KC], nu;  // walk wl's direction components k = 4 j + c and its chord uniform
     auto load_draws = [&](int step) {
         if (step >= n_ms) return;
         const double* z = Z + step * zstep;
@@ -356,8 +379,7 @@ k_hnr_mma(const double* __restrict__ Ap, const int32_t* __restrict__ F_dev, int 
             const int k = 4 * j + c;
             nd[j] = (k < d) ? __ldg(z + k * count + wi) : 0.0;
         }
-#pragma unroll
-        for (int s2 = 0; s2 < 2; ++s2) nu[s2] = __ldg(z + d * count + sw[s2]);
+        nu = __ldg(z + d * count + wi);
     };
     load_draws(0);
     double x[KC], dr[KC];
@@ -380,23 +402,11 @@ k_hnr_mma(const double* __restrict__ Ap, const int32_t* __restrict__ F_dev, int 
     const int tiles = (F + 7) >> 3;
     const double* arow = Ap + static_cast<int64_t>(wl) * KP + c;
     for (int step = 0; step < n_ms; ++step) {
-        double cu[2];
 #pragma unroll
         for (int j = 0; j < KC; ++j) dr[j] = nd[j];
-        cu[0] = nu[0];
-        cu[1] = nu[1];
+        const double cu = nu;
         load_draws(step + 1);  // in flight while this step runs
-        // numpy-order norm: squares summed left to right over k
-        double ss = 0.0;
-#pragma unroll
-        for (int k = 0; k < KP; ++k) {
-            const double v = __shfl_sync(0xffffffffu, dr[k >> 2], (lane & ~3) | (k & 3));
-            if (k < d) ss = __dadd_rn(ss, __dmul_rn(v, v));
-        }
-        const double nrm = sqrt(ss);
-#pragma unroll
-        for (int j = 0; j < KC; ++j)
-            if (4 * j + c < d) dr[j] = dr[j] / nrm;
+        // dr is already the unit direction (k_draws normalises)
         double cs[2][2] = {{INFINITY, INFINITY}, {INFINITY, INFINITY}}, ch[2][2] = {{1.0, 1.0}, {1.0, 1.0}};  // [slot][hi/lo]
         bool outside = false;
         // TPR 8-face tiles per round, the next round's A fragments loaded
@@ -437,30 +447,50 @@ k_hnr_mma(const double* __restrict__ Ap, const int32_t* __restrict__ F_dev, int 
 #pragma unroll
                 for (int j = 0; j < KC; ++j) va[u][j] = vn[u][j];
         }
-        // reduce over the 8 face rows (lanes with the same c)
+        // Reduce over the 8 face rows (lane bits 2-4) as a reduce-scatter: the
+        // 4 running ends (slot s2, end e) halve at each butterfly level, so
+        // lane bits 4 and 3 pick the end a lane keeps ((s2, e) = (bit 4, bit 3))
+        // and the last level exchanges it whole.  16 shuffles instead of 48,
+        // and each lane divides one fraction instead of four.
+        const bool b4 = (lane >> 4) & 1, b3 = (lane >> 3) & 1;
+        auto merge = [](double& S, double& H, double os, double oh) {
+            if (os * H < S * oh) { S = os; H = oh; }
+        };
+        // level 1 (xor 16): keep slot b4, send slot !b4 (both ends)
+        double kS[2], kH[2];
 #pragma unroll
-        for (int o = 4; o < 32; o <<= 1) {
-#pragma unroll
-            for (int s2 = 0; s2 < 2; ++s2)
-#pragma unroll
-                for (int e = 0; e < 2; ++e) {
-                    const double os = __shfl_xor_sync(0xffffffffu, cs[s2][e], o);
-                    const double oh = __shfl_xor_sync(0xffffffffu, ch[s2][e], o);
-                    if (os * ch[s2][e] < cs[s2][e] * oh) { cs[s2][e] = os; ch[s2][e] = oh; }
-                }
+        for (int e = 0; e < 2; ++e) {
+            const double sendS = b4 ? cs[0][e] : cs[1][e], sendH = b4 ? ch[0][e] : ch[1][e];
+            kS[e] = b4 ? cs[1][e] : cs[0][e];
+            kH[e] = b4 ? ch[1][e] : ch[0][e];
+            const double os = __shfl_xor_sync(0xffffffffu, sendS, 16);
+            const double oh = __shfl_xor_sync(0xffffffffu, sendH, 16);
+            merge(kS[e], kH[e], os, oh);
+        }
+        // level 2 (xor 8): keep end b3, send end !b3
+        double S1 = b3 ? kS[1] : kS[0], H1 = b3 ? kH[1] : kH[0];
+        {
+            const double os = __shfl_xor_sync(0xffffffffu, b3 ? kS[0] : kS[1], 8);
+            const double oh = __shfl_xor_sync(0xffffffffu, b3 ? kH[0] : kH[1], 8);
+            merge(S1, H1, os, oh);
+        }
+        // level 3 (xor 4): both lanes hold the same end
+        {
+            const double os = __shfl_xor_sync(0xffffffffu, S1, 4);
+            const double oh = __shfl_xor_sync(0xffffffffu, H1, 4);
+            merge(S1, H1, os, oh);
         }
         const bool any_out = __any_sync(0xffffffffu, outside);
-        double tt[2];
-        int err = EZ_OK;
-#pragma unroll
-        for (int s2 = 0; s2 < 2; ++s2) {
-            double thi = cs[s2][0] / ch[s2][0];
-            double tlo = -(cs[s2][1] / ch[s2][1]);
-            if (thi < tlo - kChordTol) err = EZ_EMPTY_CHORD;
-            tlo = fmin(tlo, 0.0);
-            thi = fmax(thi, 0.0);
-            tt[s2] = __dadd_rn(tlo, __dmul_rn(cu[s2], thi - tlo));
-        }
+        // this lane's fraction: t_hi (e = 0) or -t_lo (e = 1) of walk 2c + b4
+        const double q = S1 / H1;
+        // walk wl = 2c' + s2 reads t_hi from lane 16 s2 + c' and -t_lo from lane 16 s2 + 8 + c'
+        const int src = 16 * (wl & 1) + (wl >> 1);
+        double thi = __shfl_sync(0xffffffffu, q, src);
+        double tlo = -__shfl_sync(0xffffffffu, q, src + 8);
+        const int err = (thi < tlo - kChordTol) ? EZ_EMPTY_CHORD : EZ_OK;
+        tlo = fmin(tlo, 0.0);
+        thi = fmax(thi, 0.0);
+        const double mine = __dadd_rn(tlo, __dmul_rn(cu, thi - tlo));
         if (any_out) {
             if (lane == 0) set_status(status, EZ_SEED_OUTSIDE);
             return;
@@ -469,9 +499,6 @@ k_hnr_mma(const double* __restrict__ Ap, const int32_t* __restrict__ F_dev, int 
             if (err != EZ_OK) set_status(status, err);
             return;
         }
-        // walk wl's step length lives in lanes with c == wl / 2, slot wl & 1
-        const double t0 = __shfl_sync(0xffffffffu, tt[0], wl >> 1), t1 = __shfl_sync(0xffffffffu, tt[1], wl >> 1);
-        const double mine = (wl & 1) ? t1 : t0;
 #pragma unroll
         for (int j = 0; j < KC; ++j)
             if (4 * j + c < d) x[j] = __dadd_rn(x[j], __dmul_rn(dr[j], mine));
@@ -1260,9 +1287,7 @@ static int32_t dispatch_hnr(const ez_world* w, int rng, cudaStream_t s, const do
     if (rng == EZ_RNG_COUNTER && !(Z && z_ready)) {
         z = Z;
         if (!z) EZ_CUDA(cudaMallocAsync(&z, sizeof(double) * hnr_draw_words(count, n_ms, d), s));
-        const int64_t total = count * n_ms;
-        const unsigned grid = static_cast<unsigned>(std::min<int64_t>((total + 255) / 256, 148 * 16));
-        k_draws<<<grid, 256, 0, s>>>(seed, walk_offset, count, d, n_ms, z, status);
+        launch_draws(s, seed, walk_offset, count, d, n_ms, z, status);
         EZ_CUDA(cudaGetLastError());
     } else if (rng == EZ_RNG_COUNTER) {
         z = Z;
@@ -1444,9 +1469,7 @@ extern "C" int32_t ez_inflate_edge(ez_world* w, const double* h_v1, const double
         if (rng == EZ_RNG_COUNTER) {
             zb = ws->Z2[k & 1];
             EZ_CUDA(cudaStreamWaitEvent(ws->side, ws->ev_walked[k & 1], 0));  // iteration k - 2 done reading
-            const int64_t total = n_s * p.n_ms;
-            const unsigned grid = static_cast<unsigned>(std::min<int64_t>((total + 255) / 256, 148 * 16));
-            k_draws<<<grid, 256, 0, ws->side>>>(seed, woff, n_s, d, p.n_ms, zb, ws->rec + kStatus);
+            launch_draws(ws->side, seed, woff, n_s, d, p.n_ms, zb, ws->rec + kStatus);
             EZ_CUDA(cudaGetLastError());
             EZ_CUDA(cudaEventRecord(ws->ev_draws[k & 1], ws->side));
             EZ_CUDA(cudaStreamWaitEvent(s, ws->ev_draws[k & 1], 0));
