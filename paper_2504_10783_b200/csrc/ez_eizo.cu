@@ -15,6 +15,8 @@
 #include <type_traits>
 #include <vector>
 
+#include <cooperative_groups.h>
+
 #include "ez_device.cuh"
 #include "ez_rng.cuh"
 #include "ez_world.h"
@@ -964,6 +966,183 @@ k_place(double* __restrict__ A, double* __restrict__ b, int32_t* __restrict__ re
     }
 }
 
+// The same placement on a cluster of kPlaceCl CTAs (EI-ZO loop).  One CTA
+// re-read every anchor row from L2 in each of the N_f rounds (a single SM's
+// L2 bandwidth bound it: ~4 us per round at 10^4 x 7 anchors).  Here CTA r
+// owns the contiguous candidate range [r C / K, (r + 1) C / K): its rows,
+// distances and alive bytes are staged in its shared memory once; per round
+// each CTA takes its arg-min, rank 0 reduces the K results through
+// distributed shared memory, builds the face exactly as k_place does and
+// broadcasts it; two cluster barriers per round.  Same decisions and bits as
+// k_place (global index tie-break, same dot-product order).
+constexpr int kPlaceCl = 8;
+constexpr int kPlaceClThreads = 512;
+__host__ __device__ inline int place_cl_slice(int n) { return (n + kPlaceCl - 1) / kPlaceCl; }
+inline size_t place_cl_smem_bytes(int n, int d) {
+    return static_cast<size_t>(place_cl_slice(n)) * (static_cast<size_t>(d) + 1) * sizeof(double) +
+           static_cast<size_t>(place_cl_slice(n));
+}
+
+__global__ void __cluster_dims__(kPlaceCl, 1, 1) __launch_bounds__(kPlaceClThreads)
+k_place_cl(double* __restrict__ A, double* __restrict__ b, int32_t* __restrict__ rec, int32_t* __restrict__ it, int d,
+           const double* __restrict__ star, const double* __restrict__ pstar, const double* __restrict__ dstar,
+           const double* __restrict__ seg, double delta_max, int n_f) {
+    namespace cg = cooperative_groups;
+    cg::cluster_group cluster = cg::this_cluster();
+    extern __shared__ __align__(16) uint8_t smem_pcl[];
+    __shared__ double s_bd[32];
+    __shared__ int s_bi[32];
+    __shared__ double s_cbd[kPlaceCl];  // rank 0: the CTAs' results
+    __shared__ int s_cbi[kPlaceCl];
+    __shared__ double s_a[32];
+    __shared__ double s_rhs;
+    __shared__ int s_best;
+    if (rec[kStatus] != EZ_OK || rec[kStop]) return;  // the same for every CTA of the cluster
+    const int C = it[kNumCand];
+    const int rank = static_cast<int>(cluster.block_rank());
+    const int slice = place_cl_slice(C);
+    const int lo = min(C, rank * slice), n = min(C, lo + slice) - lo;
+    double* s_rows = reinterpret_cast<double*>(smem_pcl);
+    double* s_dist = s_rows + static_cast<size_t>(slice) * d;
+    uint8_t* alive = reinterpret_cast<uint8_t*>(s_dist + slice);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    for (int i = threadIdx.x; i < n * d; i += blockDim.x) s_rows[i] = star[static_cast<int64_t>(lo) * d + i];
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        s_dist[i] = dstar[lo + i];
+        alive[i] = 1;
+    }
+    cluster.sync();  // every CTA of the cluster is running before any DSMEM access
+    int F = rec[kFaces];
+    int placed = 0;
+    const double* v1 = seg;
+    const double* e = seg + d;
+    double rhs = 0.0;
+    for (int r = 0; r < n_f; ++r) {
+        __syncthreads();
+        double bd = INFINITY;
+        int bi = INT_MAX;
+        for (int i = threadIdx.x; i < n; i += blockDim.x) {
+            if (!alive[i]) continue;
+            if (r > 0) {
+                const double* t = s_rows + static_cast<size_t>(i) * d;
+                double dot = 0.0;
+                for (int k = 0; k < d; ++k) dot = fma(t[k], s_a[k], dot);
+                if (!(dot <= rhs)) {
+                    alive[i] = 0;
+                    continue;
+                }
+            }
+            const double di = s_dist[i];
+            if (di < bd) {  // ascending i per thread: ties keep the lower index
+                bd = di;
+                bi = lo + i;
+            }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const double od = __shfl_down_sync(0xffffffffu, bd, o);
+            const int oi = __shfl_down_sync(0xffffffffu, bi, o);
+            if (od < bd || (od == bd && oi < bi)) {
+                bd = od;
+                bi = oi;
+            }
+        }
+        if (lane == 0) {
+            s_bd[wid] = bd;
+            s_bi[wid] = bi;
+        }
+        __syncthreads();
+        if (wid == 0) {
+            const int nw = blockDim.x >> 5;
+            bd = lane < nw ? s_bd[lane] : INFINITY;
+            bi = lane < nw ? s_bi[lane] : INT_MAX;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                const double od = __shfl_down_sync(0xffffffffu, bd, o);
+                const int oi = __shfl_down_sync(0xffffffffu, bi, o);
+                if (od < bd || (od == bd && oi < bi)) {
+                    bd = od;
+                    bi = oi;
+                }
+            }
+            if (lane == 0) {
+                *cluster.map_shared_rank(&s_cbd[rank], 0) = bd;
+                *cluster.map_shared_rank(&s_cbi[rank], 0) = bi;
+            }
+        }
+        cluster.sync();
+        if (rank == 0 && wid == 0) {
+            bd = lane < kPlaceCl ? s_cbd[lane] : INFINITY;
+            bi = lane < kPlaceCl ? s_cbi[lane] : INT_MAX;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                const double od = __shfl_down_sync(0xffffffffu, bd, o);
+                const int oi = __shfl_down_sync(0xffffffffu, bi, o);
+                if (od < bd || (od == bd && oi < bi)) {
+                    bd = od;
+                    bi = oi;
+                }
+            }
+            bi = __shfl_sync(0xffffffffu, bi, 0);
+            bd = __shfl_sync(0xffffffffu, bd, 0);  // = dstar[best]
+            int best = (bi == INT_MAX) ? -1 : bi;
+            if (best >= 0 && bd <= 1e-12) {
+                if (lane == 0) set_status(rec + kStatus, EZ_GRADIENT_UNDEFINED);  // inflation.py:423-424
+                best = -1;
+            }
+            double ak = 0.0, rh = 0.0;
+            if (best >= 0) {
+                const double dist = bd;
+                double ck = 0.0, vk = 0.0, ek = 0.0;
+                if (lane < d) {
+                    ck = star[static_cast<int64_t>(best) * d + lane];
+                    ak = (ck - pstar[static_cast<int64_t>(best) * d + lane]) / dist;
+                    vk = v1[lane];
+                    ek = e[lane];
+                }
+                double braw = 0.0, av1 = 0.0, av2 = 0.0, nn = 0.0;
+                for (int k = 0; k < d; ++k) {
+                    const double a = __shfl_sync(0xffffffffu, ak, k), c = __shfl_sync(0xffffffffu, ck, k);
+                    const double v = __shfl_sync(0xffffffffu, vk, k), w = __shfl_sync(0xffffffffu, ek, k);
+                    braw = fma(a, c, braw);
+                    av1 = fma(a, v, av1);
+                    av2 = fma(a, v + w, av2);
+                    nn = fma(a, a, nn);
+                }
+                // compute_step_back (inflation.py:203-212)
+                const double rr = (fmax(av1, av2) - braw) + delta_max;
+                const double delta = rr > 0.0 ? delta_max - rr : delta_max;
+                rh = braw - delta;
+                // HPolytope row normalisation (cpoly.py:32-38)
+                const double norm = sqrt(nn);
+                if (fabs(norm - 1.0) > 1e-12) {
+                    ak /= norm;
+                    rh /= norm;
+                }
+                if (lane < d) A[static_cast<int64_t>(F) * d + lane] = ak;
+                if (lane == 0) b[F] = rh;
+            }
+            // broadcast the face (or the stop) to every CTA of the cluster
+            for (int q = 0; q < kPlaceCl; ++q) {
+                if (best >= 0 && lane < d) *cluster.map_shared_rank(&s_a[lane], q) = ak;
+                if (lane == 0) {
+                    *cluster.map_shared_rank(&s_rhs, q) = rh;
+                    *cluster.map_shared_rank(&s_best, q) = best;
+                }
+            }
+        }
+        cluster.sync();
+        if (s_best < 0) break;
+        ++F;
+        ++placed;
+        rhs = s_rhs;
+    }
+    if (rank == 0 && threadIdx.x == 0) {
+        rec[kFaces] = F;
+        it[kPlaced] = placed;
+    }
+}
+
 }  // namespace ez
 
 // ---------------------------------------------------------------------------
@@ -1449,6 +1628,12 @@ extern "C" int32_t ez_inflate_edge(ez_world* w, const double* h_v1, const double
     const size_t place_smem = place_smem_bytes(p.n_p, place_dcap);
     if (place_smem > 48 * 1024)
         EZ_CUDA(cudaFuncSetAttribute(k_place, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(place_smem)));
+    // the cluster placement when a CTA's share of the anchors fits in shared memory
+    const size_t place_cl_smem = place_cl_smem_bytes(p.n_p, d);
+    const bool place_cl = place_cl_smem <= 200 * 1024 && !getenv("EZ_PLACE_1CTA");
+    if (place_cl && place_cl_smem > 48 * 1024)
+        EZ_CUDA(cudaFuncSetAttribute(k_place_cl, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(place_cl_smem)));
 
     // One iteration = hit-and-run, check (+ first-M count), compaction/test,
     // bisection, placement, and a 128-byte record copy.  Iteration k+1 is
@@ -1484,8 +1669,13 @@ extern "C" int32_t ez_inflate_edge(ez_world* w, const double* h_v1, const double
         else if (d <= 8) EZ_TRY(launch_bisect<8>(w, ws, precision, s, it, p.n_p, d, ee, p.n_b, p.t_col));
         else if (d <= 16) EZ_TRY(launch_bisect<16>(w, ws, precision, s, it, p.n_p, d, ee, p.n_b, p.t_col));
         else EZ_TRY(launch_bisect<32>(w, ws, precision, s, it, p.n_p, d, ee, p.n_b, p.t_col));
-        k_place<<<1, 1024, place_smem, s>>>(ws->A, ws->b, ws->rec, it, d, ws->star, ws->pstar, ws->dstar, ws->seg,
-                                            p.delta_max, p.n_f, nullptr, place_dcap);
+        if (place_cl)
+            k_place_cl<<<kPlaceCl, kPlaceClThreads, place_cl_smem, s>>>(ws->A, ws->b, ws->rec, it, d, ws->star,
+                                                                         ws->pstar, ws->dstar, ws->seg, p.delta_max,
+                                                                         p.n_f);
+        else
+            k_place<<<1, 1024, place_smem, s>>>(ws->A, ws->b, ws->rec, it, d, ws->star, ws->pstar, ws->dstar,
+                                                ws->seg, p.delta_max, p.n_f, nullptr, place_dcap);
         EZ_CUDA(cudaGetLastError());
         EZ_CUDA(cudaMemcpyAsync(ws->h_rec + kRecInts * (k & 1), ws->rec, kRecInts * sizeof(int32_t),
                                 cudaMemcpyDeviceToHost, s));
