@@ -716,8 +716,11 @@ k_bisect(const __grid_constant__ ModelDev<T> M, T margin, const double* __restri
 // operations as the one-step loop's next midpoint, so every checked point,
 // every decision and star/pstar are bit-identical to k_bisect's, in half the
 // dependent rounds.
+// Up to 8 DOF the kernel is capped at 64 registers (8 CTAs, 32 warps per SM,
+// no spills): 7-DOF bisection 618 -> 522 us per region.  The 16-DOF
+// instance lost 9% under the same cap and keeps its registers.
 template <typename T, int MAXD>
-__global__ void __launch_bounds__(128)
+__global__ void __launch_bounds__(128, MAXD <= 8 ? 8 : 1)
 k_bisect2(const __grid_constant__ ModelDev<T> M, T margin, const double* __restrict__ X, int d,
           const int32_t* __restrict__ col, int32_t* __restrict__ rec, const int32_t* __restrict__ it,
           const double* __restrict__ seg, double ee, int n_b, double t_col, double* __restrict__ star,
