@@ -409,11 +409,25 @@ k_hnr_mma(const double* __restrict__ Ap, const int32_t* __restrict__ F_dev, int 
         const double cu = nu;
         load_draws(step + 1);  // in flight while this step runs
         // dr is already the unit direction (k_draws normalises)
-        double cs[2][2] = {{INFINITY, INFINITY}, {INFINITY, INFINITY}}, ch[2][2] = {{1.0, 1.0}, {1.0, 1.0}};  // [slot][hi/lo]
-        bool outside = false;
         // TPR 8-face tiles per round, the next round's A fragments loaded
-        // ahead (L1 latency hidden behind the current round's MMAs)
+        // ahead (L1 latency hidden behind the current round's MMAs).  For
+        // d < 8 tile u of a round updates its own running ends
+        // [u][slot][hi/lo], so the TPR compare-select chains are independent
+        // until the merge below (7-DOF walk -2%; at d >= 8 the registers cost
+        // more than the chains: 14-DOF +4%, so one chain)
         constexpr int TPR = EZ_HNR_TPR;
+        constexpr int NCH = KC <= 2 ? TPR : 1;
+        double cs[NCH][2][2], ch[NCH][2][2];
+#pragma unroll
+        for (int u = 0; u < NCH; ++u)
+#pragma unroll
+            for (int s2 = 0; s2 < 2; ++s2)
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    cs[u][s2][e] = INFINITY;
+                    ch[u][s2][e] = 1.0;
+                }
+        bool outside = false;
         double va[TPR][KC], vn[TPR][KC];
 #pragma unroll
         for (int u = 0; u < TPR; ++u)
@@ -442,7 +456,7 @@ k_hnr_mma(const double* __restrict__ Ap, const int32_t* __restrict__ F_dev, int 
 #pragma unroll
                 for (int s2 = 0; s2 < 2; ++s2) {
                     outside |= check_seed && step == 0 && g[u][s2] > kMemberTol;
-                    chord_update(-g[u][s2], h[u][s2], cs[s2], ch[s2]);
+                    chord_update(-g[u][s2], h[u][s2], cs[u % NCH][s2], ch[u % NCH][s2]);
                 }
 #pragma unroll
             for (int u = 0; u < TPR; ++u)
@@ -458,13 +472,19 @@ k_hnr_mma(const double* __restrict__ Ap, const int32_t* __restrict__ F_dev, int 
         auto merge = [](double& S, double& H, double os, double oh) {
             if (os * H < S * oh) { S = os; H = oh; }
         };
+#pragma unroll
+        for (int u = 1; u < NCH; ++u)
+#pragma unroll
+            for (int s2 = 0; s2 < 2; ++s2)
+#pragma unroll
+                for (int e = 0; e < 2; ++e) merge(cs[0][s2][e], ch[0][s2][e], cs[u][s2][e], ch[u][s2][e]);
         // level 1 (xor 16): keep slot b4, send slot !b4 (both ends)
         double kS[2], kH[2];
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
-            const double sendS = b4 ? cs[0][e] : cs[1][e], sendH = b4 ? ch[0][e] : ch[1][e];
-            kS[e] = b4 ? cs[1][e] : cs[0][e];
-            kH[e] = b4 ? ch[1][e] : ch[0][e];
+            const double sendS = b4 ? cs[0][0][e] : cs[0][1][e], sendH = b4 ? ch[0][0][e] : ch[0][1][e];
+            kS[e] = b4 ? cs[0][1][e] : cs[0][0][e];
+            kH[e] = b4 ? ch[0][1][e] : ch[0][0][e];
             const double os = __shfl_xor_sync(0xffffffffu, sendS, 16);
             const double oh = __shfl_xor_sync(0xffffffffu, sendH, 16);
             merge(kS[e], kH[e], os, oh);
