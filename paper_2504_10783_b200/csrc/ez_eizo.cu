@@ -204,39 +204,38 @@ __device__ __forceinline__ int hnr_walk(double (&x)[MAXD], int d, const double* 
 // so the walks' critical path skips the norm.  Element (step, k) at
 // Z[(step * (d + 1) + k) * count + walk]; k = d holds the chord uniform.
 template <int MAXD>
-__global__ void k_draws(uint64_t seed, uint64_t walk_offset, int64_t count, int d, int n_ms, double* __restrict__ Z,
+__global__ void k_draws(uint64_t seed, uint64_t walk_offset, int64_t count, int d, int step0, double* __restrict__ Z,
                         const int32_t* __restrict__ status) {
     if (status && (status[0] != EZ_OK || status[1] != 0)) return;
-    // one thread per (walk, step): the walk's hash prefix once for its d + 1 draws
-    const int64_t total = count * n_ms;
-    for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < total;
-         t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        const int64_t i = t % count;
-        const uint64_t step = static_cast<uint64_t>(t / count);
-        const uint64_t key = walk_key(seed, walk_offset + static_cast<uint64_t>(i));
-        double* z = Z + static_cast<int64_t>(step) * (d + 1) * count + i;
-        double v[MAXD];
-        double ss = 0.0;
+    // one thread per (walk, step), the step from blockIdx.y (no 64-bit
+    // division): the walk's hash prefix once for its d + 1 draws
+    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (i >= count) return;
+    const uint64_t step = static_cast<uint64_t>(step0) + blockIdx.y;
+    const uint64_t key = walk_key(seed, walk_offset + static_cast<uint64_t>(i));
+    double* z = Z + static_cast<int64_t>(step) * (d + 1) * count + i;
+    double v[MAXD];
+    double ss = 0.0;
 #pragma unroll
-        for (int k = 0; k < MAXD; ++k) {
-            v[k] = (k < d) ? counter_normal(key, step, k) : 0.0;
-            if (k < d) ss = __dadd_rn(ss, __dmul_rn(v[k], v[k]));
-        }
-        const double nrm = sqrt(ss);
-#pragma unroll
-        for (int k = 0; k < MAXD; ++k)
-            if (k < d) z[k * count] = v[k] / nrm;
-        z[d * count] = counter_uniform(key, step, d);
+    for (int k = 0; k < MAXD; ++k) {
+        v[k] = (k < d) ? counter_normal(key, step, k) : 0.0;
+        if (k < d) ss = __dadd_rn(ss, __dmul_rn(v[k], v[k]));
     }
+    const double nrm = sqrt(ss);
+#pragma unroll
+    for (int k = 0; k < MAXD; ++k)
+        if (k < d) z[k * count] = v[k] / nrm;
+    z[d * count] = counter_uniform(key, step, d);
 }
 
 static void launch_draws(cudaStream_t s, uint64_t seed, uint64_t walk_offset, int64_t count, int d, int n_ms,
                          double* z, const int32_t* status) {
-    const int64_t total = count * n_ms;
-    const unsigned grid = static_cast<unsigned>(std::min<int64_t>((total + 255) / 256, 148 * 16));
-    if (d <= 8) k_draws<8><<<grid, 256, 0, s>>>(seed, walk_offset, count, d, n_ms, z, status);
-    else if (d <= 16) k_draws<16><<<grid, 256, 0, s>>>(seed, walk_offset, count, d, n_ms, z, status);
-    else k_draws<32><<<grid, 256, 0, s>>>(seed, walk_offset, count, d, n_ms, z, status);
+    for (int step0 = 0; step0 < n_ms; step0 += 65535) {  // gridDim.y limit
+        const dim3 grid(static_cast<unsigned>((count + 255) / 256), static_cast<unsigned>(std::min(n_ms - step0, 65535)));
+        if (d <= 8) k_draws<8><<<grid, 256, 0, s>>>(seed, walk_offset, count, d, step0, z, status);
+        else if (d <= 16) k_draws<16><<<grid, 256, 0, s>>>(seed, walk_offset, count, d, step0, z, status);
+        else k_draws<32><<<grid, 256, 0, s>>>(seed, walk_offset, count, d, step0, z, status);
+    }
 }
 
 // Walk i starts at seeds[i % n_seeds] (explicit seeds) or at a point of the
