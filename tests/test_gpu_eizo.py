@@ -168,3 +168,22 @@ def test_two_level_bisection_equals_one_step(tmp_path):
         res.append([z[k] for k in sorted(z.files, key=lambda s: int(s.split("_")[1]))])
     for a, b in zip(*res):
         assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("which", ["franka7", "bimanual14"])
+def test_cluster_placement_equals_one_cta(which, monkeypatch):
+    """k_place_cl (8-CTA cluster, anchors in shared memory) against k_place (one CTA,
+    EZ_PLACE_1CTA=1, read per call): identical regions and counters."""
+    world = fx.franka7_world() if which == "franka7" else fx.bimanual14_world()
+    v1, v2 = fx.random_free_segment(world, seed=3)
+    dom = HPolytope.from_bounds(world.lower, world.upper)
+    params = InflationParams(**{**fx.FRANKA_PARAMS, **({"n_it": 4} if which == "bimanual14" else {})})
+    ck = world.checker()
+    reps = []
+    for flag in (None, "1"):
+        if flag:
+            monkeypatch.setenv("EZ_PLACE_1CTA", flag)
+        reps.append(inflate_edge(Segment(v1, v2), dom, params, ck, seed=7))
+    a, b = reps
+    assert (a.iterations, a.hyperplanes_added, a.collision_checks) == (b.iterations, b.hyperplanes_added, b.collision_checks)
+    assert np.array_equal(a.polytope.A, b.polytope.A) and np.array_equal(a.polytope.b, b.polytope.b)
