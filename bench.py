@@ -45,7 +45,8 @@ def _rank():
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """nvidia-smi clocks / throttle reasons, sampled every 100 ms over a window of untimed steps
+    that brackets the (millisecond-long) timed region."""
 
     FIELDS = "clocks.sm,clocks.max.sm,clocks_event_reasons.active"
 
@@ -65,6 +66,12 @@ class ClockSampler:
         except Exception:
             self._p = None
         return self
+
+    def wait_first(self, timeout: float = 15.0) -> None:
+        """Block until nvidia-smi has produced a sample (its start-up can take a second)."""
+        t_end = time.perf_counter() + timeout
+        while self._p is not None and not self.samples and time.perf_counter() < t_end:
+            time.sleep(0.01)
 
     def _read(self):
         for line in self._p.stdout:
@@ -96,7 +103,8 @@ class ClockSampler:
                  0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
                  0x100: "display_clock_setting"}
         reasons = [n for b, n in names.items() if bits & b]
-        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": reasons}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": reasons, "samples": len(sm),
+                "window": "0.4 s of untimed steps, the timed region, 0.4 s of untimed steps"}
 
 
 def _measured_peaks():
@@ -378,7 +386,24 @@ def run_ours(args):
     if world_size > 1:
         dist.barrier()
     torch.cuda.synchronize()
+    def busy(seconds: float) -> None:
+        # untimed steps around the timed region, so the 100 ms clock samples
+        # see the GPU under this load (the timed region itself is milliseconds)
+        t_end = time.perf_counter() + seconds
+        i = 0
+        while time.perf_counter() < t_end:
+            step(i)
+            i += 1
+            if i % 64 == 0:
+                torch.cuda.synchronize()
+        torch.cuda.synchronize()
+
     with ClockSampler(local_rank) as clk:
+        clk.wait_first()
+        busy(0.4)
+        if world_size > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
         t0 = torch.cuda.Event(enable_timing=True)
         t1 = torch.cuda.Event(enable_timing=True)
         t0.record(stream)
@@ -388,6 +413,9 @@ def run_ours(args):
             ev[i][1].record(stream)
         t1.record(stream)
         torch.cuda.synchronize()
+        if world_size > 1:
+            dist.barrier()
+        busy(0.4)
     if world_size > 1:
         dist.barrier()
     total_ms = t0.elapsed_time(t1)
