@@ -187,3 +187,28 @@ def test_cluster_placement_equals_one_cta(which, monkeypatch):
     a, b = reps
     assert (a.iterations, a.hyperplanes_added, a.collision_checks) == (b.iterations, b.hyperplanes_added, b.collision_checks)
     assert np.array_equal(a.polytope.A, b.polytope.A) and np.array_equal(a.polytope.b, b.polytope.b)
+
+
+def test_franka7_region_eps_audit_independent_sampler():
+    """SURVEY 8(c)(ii) audit in 7-D: the region's collision fraction, measured on an
+    independent hit-and-run stream (other seed, 200 mixing steps) with flags from the CPU
+    oracle, is at most eps (0.005; the survey measured 0.0025 on this region)."""
+    from oracle import ref
+    from paper_2504_10783_b200.polytope import hit_and_run_sample
+    world = fx.franka7_world()
+    v1, v2 = fx.random_free_segment(world, seed=3)
+    dom = HPolytope.from_bounds(world.lower, world.upper)
+    rep = inflate_edge(Segment(v1, v2), dom, InflationParams(**fx.FRANKA_PARAMS), world.checker(), seed=7)
+    P = rep.polytope
+    assert P.contains(v1, 1e-9) and P.contains(v2, 1e-9)
+    X = hit_and_run_sample(P, (0.5 * (v1 + v2))[None, :], 20_000, 200, seed=424_242).points
+    assert P.contains_many(X, 1e-9).all()
+    colliding = ~ref.OracleChecker(world).check_batch(X)
+    assert colliding.mean() <= FRANKA_EPS
+    # the GPU checker agrees with the oracle on these samples outside the contact band
+    clr = ref.OracleChecker(world).clearance(X)
+    free = world.checker().check_batch(X)
+    assert not ((free != (clr > 0)) & (np.abs(clr) >= 1e-5)).any()
+
+
+FRANKA_EPS = fx.FRANKA_PARAMS["eps"]
