@@ -997,8 +997,14 @@ k_place(double* __restrict__ A, double* __restrict__ b, int32_t* __restrict__ re
 // distributed shared memory, builds the face exactly as k_place does and
 // broadcasts it; two cluster barriers per round.  Same decisions and bits as
 // k_place (global index tie-break, same dot-product order).
-constexpr int kPlaceCl = 8;
-constexpr int kPlaceClThreads = 512;
+#ifndef EZ_PLACE_CL
+#define EZ_PLACE_CL 8
+#endif
+#ifndef EZ_PLACE_CL_THREADS
+#define EZ_PLACE_CL_THREADS 512
+#endif
+constexpr int kPlaceCl = EZ_PLACE_CL;
+constexpr int kPlaceClThreads = EZ_PLACE_CL_THREADS;
 __host__ __device__ inline int place_cl_slice(int n) { return (n + kPlaceCl - 1) / kPlaceCl; }
 inline size_t place_cl_smem_bytes(int n, int d) {
     return static_cast<size_t>(place_cl_slice(n)) * (static_cast<size_t>(d) + 1) * sizeof(double) +
