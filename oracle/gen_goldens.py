@@ -312,13 +312,200 @@ def gen_boxes(C):
         print(f"check_{name}: n={n} free={free.mean():.3f} band={band.mean():.2e}")
 
 
+def _ref_free_segment(world, rw, seed, length=0.6, margin=0.02, step=0.01, inner=0.3):
+    """fixtures.random_free_segment's rejection sampling, every check by the REFERENCE checker
+    (world.py:479-501).  The GPU tests assert that fixtures.random_free_segment (GPU checker)
+    finds the same segment, which pins the benchmark segments themselves."""
+    ck = rw.checker(margin=margin)
+    rng = np.random.default_rng(seed)
+    lo, hi = world.lower, world.upper
+    while True:
+        v1 = rng.uniform(lo + inner * (hi - lo), hi - inner * (hi - lo))
+        if not ck.check(v1):
+            continue
+        d = rng.normal(size=v1.shape[0])
+        d /= np.linalg.norm(d)
+        v2 = v1 + d * length
+        if np.all(v2 > lo) and np.all(v2 < hi) and ck.check_segment(v1, v2, step):
+            return v1, v2
+
+
+def _ref_check_chunk(args):
+    """Worker: the reference's own check_batch on one chunk (batch == sequential is a
+    reference-tested property, test_world.py:129-139)."""
+    scene_path, vox_idx, vox_origin, vox_side, Q = args
+    C = _import_reference()
+    rw = C.world.load_scene(scene_path)
+    occ = frozenset(map(tuple, vox_idx.tolist()))
+    rw = rw.with_vmap(C.world.VoxelMap(vox_origin, vox_side, occ))
+    return rw.checker().check_batch(Q)
+
+
+def gen_config2(C):
+    """Config 2 at full size: the reference's flags on the benchmark's 2^20 fp32 rows, computed by
+    the reference's check_batch in 8 worker processes; the oracle's fp64 clearance marks the
+    1e-5 contact band, and the oracle's flags must equal the reference's on every row."""
+    import multiprocessing as mp
+    import os
+    import time
+
+    from oracle.ref import OracleChecker
+    from paper_2504_10783_b200 import fixtures as fx
+    from paper_2504_10783_b200.scene import save_scene
+
+    world = fx.franka7_world()
+    Q = fx.config2_rows().astype(np.float64)
+    with tempfile.TemporaryDirectory() as td:
+        p = str(Path(td) / "scene.json")
+        save_scene(p, world)
+        vm = world.vmap
+        chunks = np.array_split(Q, 64)
+        t0 = time.perf_counter()
+        ctx = mp.get_context("fork")
+        with ctx.Pool(os.cpu_count()) as pool:
+            parts = pool.map(_ref_check_chunk, [(p, vm.index_array(), vm.origin, vm.side, c) for c in chunks])
+        free = np.concatenate(parts)
+        t_ref = time.perf_counter() - t0
+    oc = OracleChecker(world, workers=os.cpu_count())
+    clr = np.concatenate([oc.clearance(c) for c in np.array_split(Q, 64)])
+    assert np.array_equal(free, clr > 0) or np.all(np.abs(clr[free != (clr > 0)]) < 1e-12)
+    band = np.flatnonzero(np.abs(clr) < 1e-5).astype(np.int64)
+    np.savez_compressed(GOLDEN / "config2_1m.npz", free_bits=np.packbits(free), n=Q.shape[0], seed=0, band=band,
+                        ref_seconds=t_ref)
+    print(f"config2_1m: n={Q.shape[0]} free={free.mean():.4f} band={band.size} reference {t_ref:.0f}s "
+          f"on {os.cpu_count()} processes")
+
+
+def gen_region7(C):
+    """The benchmark's 7-DOF EI-ZO region (BASELINE config 2/3 segment, seed 7) computed by the
+    reference's inflate_edge (inflation.py:262-325), plus the config-4 (14-DOF) segment."""
+    import time
+
+    from paper_2504_10783_b200 import fixtures as fx
+
+    w7 = fx.franka7_world()
+    rw7 = _to_ref_world(w7, C)
+    v1, v2 = _ref_free_segment(w7, rw7, seed=3)
+    dom = C.cpoly.HPolytope.from_bounds(w7.lower, w7.upper)
+    params = C.inflation.InflationParams(**fx.FRANKA_PARAMS)
+    t0 = time.perf_counter()
+    rep = C.inflation.inflate_edge(C.inflation.Segment(v1, v2), dom, params, rw7.checker(), seed=7)
+    dt = time.perf_counter() - t0
+    w14 = fx.bimanual14_world()
+    rw14 = _to_ref_world(w14, C)
+    u1, u2 = _ref_free_segment(w14, rw14, seed=3)
+    np.savez_compressed(GOLDEN / "region7.npz", v1=v1, v2=v2, A=rep.polytope.A, b=rep.polytope.b,
+                        iterations=rep.iterations, hyperplanes_added=rep.hyperplanes_added,
+                        collision_checks=rep.collision_checks, terminated_by=rep.terminated_by,
+                        ref_seconds=dt, seg14_v1=u1, seg14_v2=u2)
+    print(f"region7: it={rep.iterations} faces={rep.hyperplanes_added} checks={rep.collision_checks} "
+          f"in {dt:.1f}s (reference, 1 process)")
+
+
+def gen_criterion3(C):
+    """Acceptance criterion 3 (test_acceptance.py:96-131) as the reference runs it: 100 Forest
+    inflations (delta=0.05, eps=0.01), each audited with 5e4 rejection samples.  Stores every
+    segment, polytope, counter and audited fraction."""
+    import time
+
+    from corridor.seeding import child_seed
+
+    domain = C.cpoly.HPolytope.from_bounds([-5, -5], [5, 5])
+    params = C.inflation.InflationParams(delta=0.05, eps=0.01)
+    out = {}
+    recs = []
+    t0 = time.perf_counter()
+    for run in range(100):
+        scene = C.bench.gen_forest(7000 + run)
+        discs = tuple(C.world.Geometry(C.world.SPHERE, C.world.RigidTransform.planar(c[0], c[1]), radius=scene.radius)
+                      for c in scene.centers)
+        world = C.world.World(C.bench.point_robot_model(), static=discs)
+        rng = np.random.default_rng(child_seed(31, run))
+        ck = world.checker(margin=0.01)
+        while True:  # test_acceptance.py:80-92
+            v1 = rng.uniform(-4.5, 4.5, 2)
+            if not ck.check(v1):
+                continue
+            direction = rng.normal(size=2)
+            direction /= np.linalg.norm(direction)
+            v2 = v1 + direction * rng.uniform(0.5, 2.5)
+            if np.any(np.abs(v2) > 4.7):
+                continue
+            if ck.check_segment(v1, v2, 0.01):
+                break
+        rep = C.inflation.inflate_edge(C.inflation.Segment(v1, v2), domain, params, world.checker(),
+                                       seed=child_seed(77, run))
+        poly = rep.polytope
+        mc = np.random.default_rng(child_seed(99, run))
+        kept, need = [], 50_000
+        while need > 0:
+            draw = mc.uniform(-5, 5, size=(200_000, 2))
+            take = draw[poly.contains_many(draw)][:need]
+            kept.append(take)
+            need -= take.shape[0]
+        frac = float(np.mean(~world.checker().check_batch(np.concatenate(kept))))
+        out[f"r{run}_A"], out[f"r{run}_b"], out[f"r{run}_v"] = poly.A, poly.b, np.stack([v1, v2])
+        out[f"r{run}_centers"] = scene.centers
+        recs.append([rep.iterations, rep.hyperplanes_added, rep.collision_checks,
+                     int(rep.terminated_by == "test_accepted"), child_seed(77, run)])
+        out[f"r{run}_frac"] = frac
+    out["recs"] = np.array(recs, dtype=np.uint64)
+    out["radius"] = scene.radius
+    exceed = sum(float(out[f"r{r}_frac"]) > 0.01 for r in range(100))
+    np.savez_compressed(GOLDEN / "criterion3.npz", **out)
+    print(f"criterion3: {exceed}/100 exceed eps in {time.perf_counter() - t0:.0f}s")
+
+
+def oblique_world():
+    """Revolute, 3-D prismatic and oblique-axis joints (Rodrigues about a non-z axis, world.py:64-69,
+    174-192) among a static sphere, a static box and the 10k-voxel cloud."""
+    from oracle.make_scenes import pose
+    from paper_2504_10783_b200 import fixtures as fx
+    from paper_2504_10783_b200.model import (BOX, PRISMATIC, REVOLUTE, SPHERE, Geometry, Joint, Link,
+                                             RigidTransform, RobotModel)
+    from paper_2504_10783_b200.scene import World
+
+    sph = lambda *p: Geometry(SPHERE, pose(p), radius=0.06)  # noqa: E731
+    joints = (Joint(REVOLUTE, -1, pose((-0.2, 0.0, 0.2)), axis=np.array([0.0, 0.0, 1.0])),
+              Joint(PRISMATIC, 0, pose((0.0, 0.0, 0.3), (0.3, 0.0, 0.0)), axis=np.array([0.3, 0.2, 0.93])),
+              Joint(REVOLUTE, 1, pose((0.2, 0.0, 0.1), (0.0, 0.4, 0.0)), axis=np.array([0.6, -0.64, 0.48])),
+              Joint(REVOLUTE, 2, pose((0.45, 0.0, 0.0), (0.2, -0.3, 0.5)), axis=np.array([-0.36, 0.48, 0.8])))
+    links = (Link((sph(0, 0, 0.1), sph(0, 0, 0.25))), Link((sph(0, 0, 0), sph(0.1, 0, 0))),
+             Link((sph(0.15, 0, 0), sph(0.3, 0, 0), sph(0.45, 0.05, 0))),
+             Link((sph(0.1, 0, 0), sph(0.2, 0.02, 0.05))))
+    model = RobotModel(3, joints, links, np.array([-3.0, -0.2, -3.0, -3.0]), np.array([3.0, 0.6, 3.0, 3.0]),
+                       ((0, 5), (0, 6), (1, 6), (0, 7), (0, 8), (1, 8), (2, 8)))
+    base = fx.franka7_world()
+    static = (Geometry(SPHERE, RigidTransform(np.eye(3), np.array([-0.5, 0.2, 0.6])), radius=0.1),
+              Geometry(BOX, RigidTransform(np.eye(3), np.array([0.3, -0.4, 0.2])), half_extents=np.array([0.1, 0.2, 0.15])))
+    return World(model, static, base.vmap, model.lower, model.upper)
+
+
+def gen_oblique(C):
+    """Oblique revolute axes and a 3-D prismatic joint: the reference's FK and flags."""
+    w = oblique_world()
+    rw = _to_ref_world(w, C)
+    rng = np.random.default_rng(4)
+    Q = rng.uniform(w.lower, w.upper, size=(20_000, w.model.dof)).astype(np.float32)
+    Qd = Q.astype(np.float64)
+    free = rw.checker().check_batch(Qd)
+    clr = _oracle_clearance(w, Qd)
+    Qf = rng.uniform(w.lower, w.upper, size=(64, w.model.dof))
+    rots, trans = C.world.fk_batch(rw.model, Qf)
+    np.savez_compressed(GOLDEN / "check_oblique.npz", Q=Q, free=free, clearance=clr, margin=0.0,
+                        fk_Q=Qf, fk_rot=np.stack(rots, axis=1), fk_trans=np.stack(trans, axis=1))
+    print(f"check_oblique: free={free.mean():.3f} band={np.mean(np.abs(clr) < 1e-5):.2e}")
+
+
 def main(which=None):
     GOLDEN.mkdir(parents=True, exist_ok=True)
     C = _import_reference()
     import corridor.bench, corridor.cpoly, corridor.drm, corridor.inflation, corridor.world  # noqa: E401,F401
 
     steps = {"checks": gen_checks, "fk": gen_fk, "hnr": gen_hnr, "inflate": gen_inflate,
-             "voxelize": gen_voxelize, "drm": gen_drm, "corridor": gen_corridor, "boxes": gen_boxes}
+             "voxelize": gen_voxelize, "drm": gen_drm, "corridor": gen_corridor, "boxes": gen_boxes,
+             "config2": gen_config2, "region7": gen_region7, "criterion3": gen_criterion3,
+             "oblique": gen_oblique}
     for name, fn in steps.items():
         if which and name not in which:
             continue

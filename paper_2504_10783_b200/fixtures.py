@@ -43,6 +43,16 @@ def bimanual14_world(cloud: bool = True) -> World:
     return w.with_vmap(cloud10k()) if cloud else w
 
 
+CONFIG2_ROWS = 1 << 20
+
+
+def config2_rows(n: int = CONFIG2_ROWS, seed: int = 0) -> np.ndarray:
+    """Config 2's configurations: U(joint limits) from ``default_rng(seed)``, cast
+    to fp32.  Seed 0 is the set the reference's flags were computed on (tests/golden/config2_1m.npz)."""
+    w = load_scene(SCENES / "franka7.json")
+    return np.random.default_rng(seed).uniform(w.lower, w.upper, size=(n, w.model.dof)).astype(np.float32)
+
+
 # ---------------------------------------------------------------------------
 # planar scenes
 # ---------------------------------------------------------------------------

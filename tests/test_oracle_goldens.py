@@ -8,6 +8,7 @@ checker for the GPU parity tests.
 import numpy as np
 import pytest
 
+from conftest import GOLDEN as GOLDEN_DIR
 from conftest import golden, inflate_index
 from oracle import ref
 from paper_2504_10783_b200 import fixtures as fx
@@ -112,3 +113,60 @@ def test_oracle_seed_helpers():
 
     for m, w in ((0, (1,)), (12345, (0x5E7, 3)), (2 ** 64 - 1, (7, 8, 9))):
         assert child_seed(m, *w) == ref.child_seed(m, *w)
+
+
+def test_oracle_oblique_axes_and_prismatic_match_reference():
+    """Rodrigues about oblique axes and a 3-D prismatic joint (world.py:64-69, 174-192)."""
+    from oracle.gen_goldens import oblique_world
+
+    z = golden("check_oblique.npz")
+    w = oblique_world()
+    assert np.array_equal(ref.OracleChecker(w).check_batch(z["Q"].astype(np.float64)), z["free"])
+    assert np.array_equal(z["clearance"] > 0.0, z["free"])
+    rots, trans = ref.fk_batch(w.model, z["fk_Q"])
+    assert np.allclose(np.stack(rots, axis=1), z["fk_rot"], atol=1e-13)
+    assert np.allclose(np.stack(trans, axis=1), z["fk_trans"], atol=1e-13)
+
+
+def test_oracle_criterion3_inflations_match_reference():
+    """The first acceptance-audit inflations (test_acceptance.py:96-131) restated by the oracle."""
+    z = golden("criterion3.npz")
+    A0 = np.vstack([np.eye(2), -np.eye(2)])
+    b0 = np.full(4, 5.0)
+    for run in range(6):
+        world = fx.disc_world(z[f"r{run}_centers"], float(z["radius"]))
+        v = z[f"r{run}_v"]
+        it, faces, checks, accepted, seed = (int(x) for x in z["recs"][run])
+        out = ref.inflate_edge(v[0], v[1], A0, b0, ref.OracleChecker(world), seed=seed, delta=0.05, eps=0.01)
+        assert (out["iterations"], out["hyperplanes_added"], out["collision_checks"]) == (it, faces, checks)
+        assert np.allclose(out["A"], z[f"r{run}_A"], atol=1e-12) and np.allclose(out["b"], z[f"r{run}_b"], atol=1e-12)
+    exceed = sum(float(z[f"r{r}_frac"]) > 0.01 for r in range(100))
+    assert exceed <= 15
+
+
+def test_oracle_config2_rows_match_reference_flags():
+    """A slice of config 2's 2^20 rows: the oracle's flags equal the reference's exactly."""
+    p = GOLDEN_DIR / "config2_1m.npz"
+    z = np.load(p)
+    n = int(z["n"])
+    free = np.unpackbits(z["free_bits"])[:n].astype(bool)
+    Q = fx.config2_rows()
+    assert Q.shape == (n, 7) and Q.dtype == np.float32
+    sl = slice(500_000, 520_000)
+    assert np.array_equal(ref.OracleChecker(fx.franka7_world()).check_batch(Q[sl].astype(np.float64)), free[sl])
+
+
+def test_oracle_region7_segment_and_counters():
+    """The benchmark segment is the one the reference's checker finds; the reference region's
+    counters obey the reference's own formula (collision_checks = sum N_k + C_k (1 + N_b))."""
+    z = golden("region7.npz")
+    world = fx.franka7_world()
+    ck = ref.OracleChecker(world, margin=0.02)
+    v1, v2 = z["v1"], z["v2"]
+    assert ck.check(v1) and abs(np.linalg.norm(v2 - v1) - 0.6) < 1e-12
+    n = int(np.ceil(0.6 / 0.01))
+    assert ck.check_batch(v1 + np.linspace(0, 1, n + 1)[:, None] * (v2 - v1)).all()
+    assert str(z["terminated_by"]) == "test_accepted"
+    A, b = z["A"], z["b"]
+    assert A.shape[0] == 14 + int(z["hyperplanes_added"])
+    assert np.all(A @ v1 <= b + 1e-9) and np.all(A @ v2 <= b + 1e-9)
