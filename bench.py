@@ -1,19 +1,25 @@
 #!/usr/bin/env python
 """Benchmark of the EI-ZO hot path (BASELINE.json): collision checks/s, 7-DOF vs 10k voxel spheres.
 
-One step = one pass of the fused FK + collision kernel over a batch of 1M
-7-DOF configurations (config 2 of BASELINE.json) per GPU.  Weak scaling:
-under torchrun every rank checks its own 1M-config batches (no data-path
-collective); the whole-job value is all configurations / max-over-ranks
-device time.  Inputs are 8 resident batches (224 MB > the 126 MB L2) used in
-rotation, so no step reads its configurations from L2.
+One step = one pass of the fused FK + collision kernel over a batch of 2^20
+7-DOF configurations (config 2 of BASELINE.json) per GPU.  Weak scaling: each
+rank checks its own batches (no data-path collective); the whole-job value is
+all configurations / the max-over-ranks device time.  Inputs are 8 resident
+batches (224 MB > the 126 MB L2) used in rotation, so no step reads its
+configurations from L2.  Batch 0 of rank 0 is ``fixtures.config2_rows()``, the
+rows whose reference flags tests/golden/config2_1m.npz holds.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
 
+``--gpus N`` outside torchrun re-launches itself under torch.distributed.run
+with N ranks (one per GPU, NCCL).
+
 Extra keys: ``roofline`` (FP32-FMA bound; measured FMA peak), ``cpu_baseline``
-(the oracle port on this host, bounded sample), ``e2e`` (public numpy API
-with pinned host buffers, copies inside the timed region), ``eizo`` (7-DOF
-single-segment region latency), ``clocks``.
+(the oracle port on this host, bounded sample), ``e2e`` (the drop-in numpy
+call ``CollisionChecker.check_batch`` on pageable fp32 rows, copies inside the
+timed region; pinned and fp64 variants beside it), ``eizo`` (7-DOF region
+latency, its roofline and CPU baseline), ``config1``/``config3``/``config4``/
+``drm``/``boxes``, ``clocks``.
 """
 
 from __future__ import annotations
@@ -216,7 +222,7 @@ def bench_boxes(checks_n: int = 1 << 20) -> dict:
             "workload": "8 robot boxes + 1 sphere, 20 self pairs (box-box SAT, sphere-box), 1 static box, 10k voxels"}
 
 
-def bench_config4(checks_n: int = 1 << 20) -> dict:
+def bench_config4(checks_n: int = 1 << 20, cpu: bool = True) -> dict:
     """Config 4: 14-DOF bimanual (66 spheres, 1,248 pairs): checks/s and one EI-ZO region."""
     import torch
 
@@ -225,14 +231,14 @@ def bench_config4(checks_n: int = 1 << 20) -> dict:
     from paper_2504_10783_b200.polytope import HPolytope
 
     world = fx.bimanual14_world()
-    ck = world.checker()
+    t_jit = time.perf_counter()
+    ck = world.checker()  # "auto" specialisation at creation; also used by the EI-ZO loop below
+    nat = ck.native
+    jit_ms = (time.perf_counter() - t_jit) * 1e3
+    specialised = nat.specialize(0)
     lo = torch.as_tensor(world.lower, dtype=torch.float32, device="cuda")
     hi = torch.as_tensor(world.upper, dtype=torch.float32, device="cuda")
     Q = lo + (hi - lo) * torch.rand((checks_n, 14), device="cuda")
-    nat = ck.native
-    t_jit = time.perf_counter()
-    specialised = nat.specialize(1)  # model-specialised kernel, also used by the EI-ZO loop below
-    jit_ms = (time.perf_counter() - t_jit) * 1e3
     for _ in range(3):
         nat.check_device(Q)
     torch.cuda.synchronize()
@@ -250,12 +256,33 @@ def bench_config4(checks_n: int = 1 << 20) -> dict:
     t0 = time.perf_counter()
     rep = inflate_edge(Segment(v1, v2), dom, params, ck, seed=7)
     wall = (time.perf_counter() - t0) * 1e3
-    return {"checks_per_s": rate, "flop_per_check": 13104, "specialised_kernel": specialised, "jit_compile_ms": jit_ms,
-            "cta": nat.info()["check_cta"],
-            "eizo_ms_wall": wall, "eizo_device_ms": rep.device_ms, "iterations": rep.iterations,
-            "faces": rep.hyperplanes_added, "collision_checks": rep.collision_checks,
-            "terminated_by": rep.terminated_by,
-            "workload": "14-DOF bimanual sphere model vs 10k voxels; EI-ZO single segment, Franka (eps, delta)"}
+    flop, walk_gemm = region_flop(rep, params, 14, dom.n_faces, 13104)
+    out = {"checks_per_s": rate, "flop_per_check": 13104, "specialised_kernel": specialised, "jit_compile_ms": jit_ms,
+           "cta": nat.info()["check_cta"],
+           "eizo_ms_wall": wall, "eizo_device_ms": rep.device_ms, "iterations": rep.iterations,
+           "faces": rep.hyperplanes_added, "collision_checks": rep.collision_checks,
+           "terminated_by": rep.terminated_by,
+           "eizo_roofline": {"bound": "FP64 tensor (DMMA) in the walk", "flop_per_region": flop,
+                             "walk_gemm_flop": walk_gemm,
+                             "achieved_tflops": flop / (rep.device_ms * 1e-3) / 1e12,
+                             "note": "93% of the region is the walk over up to 1,860 faces; an LP analysis "
+                                     "(tools/redundancy.py) finds <3% of the faces redundant"},
+           "workload": "14-DOF bimanual sphere model vs 10k voxels; EI-ZO single segment, Franka (eps, delta)"}
+    if cpu:
+        from oracle import ref
+
+        oc = ref.OracleChecker(world, workers=os.cpu_count() or 1)
+        rows = np.random.default_rng(2).uniform(world.lower, world.upper, size=(4000, 14))
+        t0 = time.perf_counter()
+        oc.check_batch(rows)
+        t_chk = (time.perf_counter() - t0) / rows.shape[0]
+        out["cpu_baseline"] = {"kind": "port", "cores": os.cpu_count(), "cpu": cpu_model(),
+                               "checks_per_s": 1.0 / t_chk,
+                               "sample": "4,000 uniform 14-DOF configs through oracle/ref.py",
+                               "region_checks_alone_s": rep.collision_checks * t_chk,
+                               "note": "the full region (187 iterations, walks over up to 1,860 faces) is "
+                                       "not affordable on the CPU; its checks alone take region_checks_alone_s"}
+    return out
 
 
 def bench_drm(n_nodes: int = 100_000, reps: int = 10, cpu: bool = True) -> dict:
@@ -341,11 +368,202 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def region_flop(rep, params, d: int, f0: int, flop_per_check: float, n_b: int = 11):
+    """SURVEY.md §8(d) algorithmic FLOP of one EI-ZO region from its report:
+    sum_k N_k N_ms (4 F_k d + 2 F_k + 6 d) + checks * F_check + C N_f 2 d, with N_k = max(N_p, M_k)
+    (inflation.py:156-161, 288-290), F_k = F_0 + faces placed before iteration k, and the
+    candidates C from the reference's own count (collision_checks = sum N_k + C (1 + N_b)).
+    Returns (total, walk GEMM part sum_k N_k N_ms 4 F_k d)."""
+    from paper_2504_10783_b200.eizo import required_batch_size
+
+    walks, walk_total, walk_gemm, faces, placed = 0, 0.0, 0.0, f0, 0
+    for k in range(1, rep.iterations + 1):
+        n_k = max(params.n_p, required_batch_size(k, params))
+        walks += n_k
+        walk_gemm += n_k * params.n_ms * 4.0 * faces * d
+        walk_total += n_k * params.n_ms * (4.0 * faces * d + 2.0 * faces + 6.0 * d)
+        step = min(params.n_f, rep.hyperplanes_added - placed)
+        placed += step
+        faces += step
+    cands = max(0, rep.collision_checks - walks) / (1 + n_b)
+    total = walk_total + rep.collision_checks * flop_per_check + cands * params.n_f * 2.0 * d
+    return total, walk_gemm
+
+
+def _peak(fn_name: str, device: int) -> float:
+    from paper_2504_10783_b200 import _native as N
+
+    tf, ms = N.C.c_double(0.0), N.C.c_double(0.0)
+    N.check(getattr(N.lib(), fn_name)(device, N.C.byref(tf), N.C.byref(ms)))
+    return float(tf.value)
+
+
+def bench_eizo7(world, ck, cpu: bool, fp64_peak: float) -> dict:
+    """7-DOF single-segment region (Franka parameters): latency, roofline, CPU baseline."""
+    from paper_2504_10783_b200 import fixtures as fx
+    from paper_2504_10783_b200.eizo import InflationParams, Segment, inflate_edge
+    from paper_2504_10783_b200.polytope import HPolytope
+
+    v1, v2 = fx.random_free_segment(world, seed=3)
+    dom = HPolytope.from_bounds(world.lower, world.upper)
+    params = InflationParams(**fx.FRANKA_PARAMS)
+    inflate_edge(Segment(v1, v2), dom, params, ck, seed=6)  # warm-up (module load, workspace)
+    times, reps = [], []
+    for s_ in range(5):
+        t_r = time.perf_counter()
+        rep = inflate_edge(Segment(v1, v2), dom, params, ck, seed=7 + (s_ % 4))
+        times.append((time.perf_counter() - t_r) * 1e3)
+        reps.append(rep)
+    seed7 = reps[0]
+    flop, walk_flop = region_flop(seed7, params, 7, dom.n_faces, FLOP_PER_CHECK)
+    out = {"ms_per_region_wall": float(np.median(times)),
+           "device_ms": float(np.median([r.device_ms for r in reps])),
+           "seed7": {"iterations": seed7.iterations, "faces": seed7.hyperplanes_added,
+                     "collision_checks": seed7.collision_checks, "device_ms": seed7.device_ms,
+                     "matches_reference_counters": [seed7.iterations, seed7.hyperplanes_added,
+                                                    seed7.collision_checks] == [6, 50, 295128]},
+           "iterations": [r.iterations for r in reps], "faces": [r.hyperplanes_added for r in reps],
+           "collision_checks": [r.collision_checks for r in reps],
+           "segment": "7-DOF Franka-like + 10k voxels, length 0.6, free with margin 0.02 (default_rng(3))",
+           "params": "delta=eps=0.005, N_p=1e4, N_f=10, N_ms=60, delta_max=0.01, N_b=11",
+           "target_ms": 5.0,
+           "roofline": {"bound": "critical path (latency); FP64 tensor (walk)",
+                        "flop_per_region": flop, "walk_gemm_flop": walk_flop,
+                        "achieved": flop / (seed7.device_ms * 1e-3) / 1e12, "unit": "TFLOP/s",
+                        "peak": fp64_peak, "frac": flop / (seed7.device_ms * 1e-3) / 1e12 / fp64_peak,
+                        "peak_source": "ez_fp64_tc_peak (DMMA m8n8k4) measured in this run",
+                        "note": "SURVEY 8(d) per-region FLOP / device time; the region is a chain of "
+                                "~6 dependent iterations of 5 kernels, see profiles/r01_eizo7_region_trace.txt"}}
+    if cpu:
+        from oracle import ref
+
+        t0 = time.perf_counter()
+        r1 = ref.inflate_edge(v1, v2, dom.A, dom.b, ref.OracleChecker(world, workers=os.cpu_count() or 1),
+                              seed=7, n_it=1, **{k: v for k, v in fx.FRANKA_PARAMS.items()})
+        t1 = time.perf_counter() - t0
+        out["cpu_baseline"] = {
+            "kind": "port", "cores": os.cpu_count(), "cpu": cpu_model(),
+            "sample": "iteration 1 of the same region (oracle/ref.py inflate_edge, n_it=1, seed 7): "
+                      f"{r1['collision_checks']} checks, {r1['hyperplanes_added']} faces",
+            "first_iteration_s": t1,
+            "reference_full_region_s": 93.7,
+            "reference_full_region_note": "the reference package's own inflate_edge on this segment/seed, "
+                                          "measured in the build container (tests/golden/region7.npz ref_seconds)"}
+    return out
+
+
+def bench_config3(world, ck, comm, world_size: int, rank: int) -> dict:
+    """Config 3: 10-segment 7-DOF paths.  Latency of one path (sequential drop-in inflate_path and
+    segment-sharded speculation, both with the reference's seeding) and segments/s over a stream
+    of paths sharded across ranks (weak scaling: 4 paths per rank)."""
+    import torch
+
+    from paper_2504_10783_b200 import fixtures as fx
+    from paper_2504_10783_b200.corridor import inflate_path
+    from paper_2504_10783_b200.distributed import inflate_paths_sharded, inflate_segments_sharded
+    from paper_2504_10783_b200.eizo import InflationParams
+    from paper_2504_10783_b200.polytope import HPolytope
+    from paper_2504_10783_b200.roadmap import PwlPath
+
+    dist = torch.distributed if world_size > 1 else None
+    path = PwlPath(fx.random_free_path(world, 10, seed=3))
+    dom = HPolytope.from_bounds(world.lower, world.upper)
+    params = InflationParams(**fx.FRANKA_PARAMS)
+
+    def max_over_ranks(x):
+        if world_size == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def barrier():
+        if world_size > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    out = {"segments": 10, "path": "10 chained 0.6-long segments, free with margin 0.02 (default_rng(3))"}
+    seq = inflate_path(path, dom, params, ck, seed=11)  # warm-up
+    t0 = time.perf_counter()
+    seq = inflate_path(path, dom, params, ck, seed=11)
+    out["sequential_drop_in_ms"] = (time.perf_counter() - t0) * 1e3
+    out["sets_kept"] = len(seq.sets)
+    inflate_segments_sharded(path, dom, params, ck, seed=11, comm=comm)  # warm-up
+    barrier()
+    t0 = time.perf_counter()
+    scs, mine = inflate_segments_sharded(path, dom, params, ck, seed=11, comm=comm)
+    torch.cuda.synchronize()
+    out["sharded_speculative_ms_max_over_ranks"] = max_over_ranks((time.perf_counter() - t0) * 1e3)
+    out["sharded_equals_sequential"] = (scs.coverage == seq.coverage and all(
+        np.array_equal(a.A, b.A) for a, b in zip(scs.sets, seq.sets)))
+    out["sharded_reinflated"] = scs.reinflated
+    out["path_latency_ms"] = min(out["sequential_drop_in_ms"], out["sharded_speculative_ms_max_over_ranks"])
+    # throughput: a stream of paths, 4 per rank, each through inflate_path (reference semantics)
+    per_rank = 4
+    paths = [PwlPath(fx.random_free_path(world, 10, seed=100 + p)) for p in range(per_rank * world_size)]
+    inflate_paths_sharded(paths[:world_size], dom, params, ck, seed=5, comm=comm)  # warm-up
+    barrier()
+    t0 = time.perf_counter()
+    got = inflate_paths_sharded(paths, dom, params, ck, seed=5, comm=comm, concurrency=per_rank)
+    torch.cuda.synchronize()
+    dt = max_over_ranks(time.perf_counter() - t0)
+    out["stream"] = {"paths": len(paths), "paths_per_rank": per_rank, "segments": 10 * len(paths),
+                     "inflations_on_rank0": sum(len(s.sets) for s in got.values()) if rank == 0 else None,
+                     "seconds_max_over_ranks": dt, "segments_per_s": 10 * len(paths) / dt,
+                     "scaling": "weak (4 paths per rank, no collective)"}
+    return out
+
+
+def bench_e2e(ck, host_batches, world_size: int, steps: int) -> dict:
+    """End to end through the drop-in call: ``CollisionChecker.check_batch(numpy)`` -> one
+    ``ez_check_batch_host`` per step; the H2D copy of the step's rows and the D2H read of its
+    flags are inside the timed region.  Pageable fp32 (the headline), pinned fp32, pinned fp64."""
+    import torch
+    import torch.distributed as dist
+
+    def timed(batches, label):
+        gc.collect()
+        t_w, n_w = time.perf_counter(), 0
+        while n_w < 3 or time.perf_counter() - t_w < 1.0:  # copies run slower in a buffer's first second
+            ck.check_batch(batches[n_w % len(batches)])
+            n_w += 1
+        if world_size > 1:
+            dist.barrier()
+        groups = []
+        for _ in range(3):
+            t_e = time.perf_counter()
+            for i in range(steps):
+                ck.check_batch(batches[i % len(batches)])
+            groups.append(time.perf_counter() - t_e)
+        t = torch.tensor([float(np.median(groups))], dtype=torch.float64, device="cuda")
+        if world_size > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return BATCH * steps * world_size / float(t.item())
+
+    pageable = host_batches
+    pinned32 = []
+    for hb in host_batches[:2]:
+        t = torch.empty(hb.shape, dtype=torch.float32, pin_memory=True)
+        t.numpy()[:] = hb
+        pinned32.append(t.numpy())
+    pinned64 = []
+    for hb in host_batches[:2]:
+        t = torch.empty(hb.shape, dtype=torch.float64, pin_memory=True)
+        t.numpy()[:] = hb
+        pinned64.append(t.numpy())
+    e_steps = max(3, min(steps, 10))
+    return {"pageable_fp32": timed(pageable, "pageable"), "pinned_fp32": timed(pinned32, "pinned"),
+            "pinned_fp64": timed(pinned64, "pinned64"), "steps": e_steps,
+            "h2d_bytes_per_step": BATCH * 7 * 4, "d2h_bytes_per_step": BATCH}
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
 
     rank, world_size, local_rank = _rank()
+    if world_size != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world_size}")
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     if world_size > 1:
@@ -353,30 +571,24 @@ def run_ours(args):
 
     from paper_2504_10783_b200 import _native as N
     from paper_2504_10783_b200 import fixtures as fx
-    from paper_2504_10783_b200.eizo import InflationParams, Segment, inflate_edge
-    from paper_2504_10783_b200.polytope import HPolytope
+    from paper_2504_10783_b200.distributed import LocalComm, TorchComm
 
     world = fx.franka7_world()
-    ck = world.checker()
+    t_jit = time.perf_counter()
+    ck = world.checker()  # "auto": the model-specialised kernel is compiled with the device world
     nat = ck.native
-    lo = torch.as_tensor(world.lower, dtype=torch.float32, device=dev)
-    hi = torch.as_tensor(world.upper, dtype=torch.float32, device=dev)
-    gen = torch.Generator(device=dev)
-    gen.manual_seed(1234 + rank)
-    batches = [lo + (hi - lo) * torch.rand((BATCH, 7), generator=gen, device=dev) for _ in range(N_BATCHES)]
+    jit_ms = (time.perf_counter() - t_jit) * 1e3
+    specialised = nat.specialize(0)
+    # config 2 rows: U(joint limits) from default_rng, fp32; rank 0 batch 0 = the golden rows
+    host_batches = [fx.config2_rows(BATCH, seed=rank * N_BATCHES + i) for i in range(N_BATCHES)]
+    batches = [torch.as_tensor(h, device=dev) for h in host_batches]
     out = torch.empty(BATCH, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream(dev)
     sh = stream.cuda_stream
 
-    def step(i):
+    def step(i, precision=0):
         N.check(N.lib().ez_check_batch(nat.handle, batches[i % N_BATCHES].data_ptr(), 0, BATCH, 7, out.data_ptr(),
-                                       0, sh))
-
-    # model-specialised check kernel (NVRTC, ez_world_specialize); compiled
-    # before the warm-up, outside every timed region
-    t_jit = time.perf_counter()
-    specialised = nat.specialize(1)
-    jit_ms = (time.perf_counter() - t_jit) * 1e3
+                                       precision, sh))
 
     gc.collect()
     for i in range(max(3, args.warmup)):
@@ -386,6 +598,7 @@ def run_ours(args):
     if world_size > 1:
         dist.barrier()
     torch.cuda.synchronize()
+
     def busy(seconds: float) -> None:
         # untimed steps around the timed region, so the 100 ms clock samples
         # see the GPU under this load (the timed region itself is milliseconds)
@@ -426,97 +639,34 @@ def run_ours(args):
     max_ms = float(t.item())
     checks = BATCH * args.steps * world_size
     value = checks / (max_ms * 1e-3)
+    step(0)
     free_frac = float(out.float().mean().item())
+    # the reference's own arithmetic (fp64 kinematics and distances) on the same rows
+    e64a, e64b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    step(0, 1)
+    e64a.record(stream)
+    for i in range(4):
+        step(i, 1)
+    e64b.record(stream)
+    torch.cuda.synchronize()
+    fp64_rate = 4 * BATCH / (e64a.elapsed_time(e64b) * 1e-3)
 
-    # EI-ZO single-segment 7-DOF region (Franka parameters), latency per region
-    eizo = None
-    if not args.skip_eizo:
-        v1, v2 = fx.random_free_segment(world, seed=3)
-        dom = HPolytope.from_bounds(world.lower, world.upper)
-        params = InflationParams(**fx.FRANKA_PARAMS)
-        times, reps = [], []
-        eck = ck  # the specialised checker: EI-ZO's checks run the per-model kernel
-        inflate_edge(Segment(v1, v2), dom, params, eck, seed=6)  # warm-up (module load, workspace)
-        for s in range(4):
-            t_r = time.perf_counter()
-            rep = inflate_edge(Segment(v1, v2), dom, params, eck, seed=7 + s)
-            times.append((time.perf_counter() - t_r) * 1e3)
-            reps.append(rep)
-        eizo = {"ms_per_region_wall": float(np.median(times)),
-                "device_ms": float(np.median([r.device_ms for r in reps])),
-                "iterations": [r.iterations for r in reps], "faces": [r.hyperplanes_added for r in reps],
-                "collision_checks": [r.collision_checks for r in reps],
-                "segment": "7-DOF Franka-like + 10k voxels, length 0.6, free with margin 0.02 (default_rng(3))",
-                "params": "delta=eps=0.005, N_p=1e4, N_f=10, N_ms=60, delta_max=0.01, N_b=11"}
-
-    # config 3: a 10-segment 7-DOF path, segments sharded round-robin over the ranks
-    config3 = None
-    if not args.skip_eizo:
-        from paper_2504_10783_b200.distributed import LocalComm, TorchComm, inflate_segments_sharded
-        from paper_2504_10783_b200.roadmap import PwlPath
-
-        knots = fx.random_free_path(world, 10, seed=3)
-        path = PwlPath(knots)
-        dom = HPolytope.from_bounds(world.lower, world.upper)
-        params = InflationParams(**fx.FRANKA_PARAMS)
-        comm = TorchComm() if world_size > 1 else LocalComm()
-        eck = ck  # the specialised checker: EI-ZO's checks run the per-model kernel
-        inflate_segments_sharded(path, dom, params, eck, seed=11, comm=comm)  # warm-up
-        if world_size > 1:
-            dist.barrier()
-        torch.cuda.synchronize()
-        t_p = time.perf_counter()
-        scs, mine = inflate_segments_sharded(path, dom, params, eck, seed=11, comm=comm)
-        torch.cuda.synchronize()
-        dt = torch.tensor([time.perf_counter() - t_p], dtype=torch.float64, device=dev)
-        if world_size > 1:
-            dist.all_reduce(dt, op=dist.ReduceOp.MAX)
-        config3 = {"segments": 10, "path_ms_wall_max_over_ranks": float(dt.item()) * 1e3,
-                   "segments_per_s": 10 / float(dt.item()), "sets_kept": len(scs.sets),
-                   "segments_on_rank0": sorted(mine), "scaling": "strong (fixed 10-segment path)",
-                   "note": "segment-keyed seeds child_seed(seed, 0x5E7, k); skip rule replayed on every rank"}
-
-    # e2e through the public numpy API: pinned fp64 host buffers, H2D + D2H inside the timed region
-    pin = torch.empty((BATCH, 7), dtype=torch.float64, pin_memory=True)
-    pin.copy_(batches[0].double().cpu())
-    Qh = pin.numpy()
-    res_pin = torch.empty(BATCH, dtype=torch.uint8, pin_memory=True).numpy()
-    # measured last, away from the nvidia-smi clock sampler and seconds after
-    # the CUDA context came up (host-driven copies ran slower in the first
-    # second of a process, tools/diag_e2e3.py); the median of three groups
-    e2e_steps = max(3, min(args.steps, 10))
-    # collect the garbage of the sections above first: a collection inside the
-    # timed calls would run their checkers' destructors (cudaFree, unpinning)
-    # there (measured: 1.2 -> 1.7 ms per call)
-    gc.collect()
-    # warm-up by time, not count: copies from a freshly pinned buffer ran ~25%
-    # slower for about a second (tools/diag_e2e5.py)
-    t_w, n_w = time.perf_counter(), 0
-    while n_w < 3 or time.perf_counter() - t_w < 1.5:
-        nat.check_host(Qh, out=res_pin)
-        n_w += 1
-    if world_size > 1:
-        dist.barrier()
-    groups = []
-    for _ in range(3):
-        t_e = time.perf_counter()
-        for _ in range(e2e_steps):
-            nat.check_host(Qh, out=res_pin)
-        groups.append(time.perf_counter() - t_e)
-    e2e_s = float(np.median(groups))
-    te = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
-    if world_size > 1:
-        dist.all_reduce(te, op=dist.ReduceOp.MAX)
-    e2e_value = BATCH * e2e_steps * world_size / float(te.item())
+    e2e = bench_e2e(ck, host_batches, world_size, max(3, min(args.steps, 10)))
+    comm = TorchComm() if world_size > 1 else LocalComm()
+    fp64_peak = _peak("ez_fp64_tc_peak", local_rank) if rank == 0 else 0.0
+    eizo = None if args.skip_eizo else bench_eizo7(world, ck, cpu=(world_size == 1 and not args.skip_cpu),
+                                                   fp64_peak=fp64_peak)
+    config3 = None if args.skip_eizo else bench_config3(world, ck, comm, world_size, rank)
+    config4_sharded = None
+    if world_size > 1 and not args.skip_extra:
+        config4_sharded = bench_config4_sharded(comm, world_size)
 
     if rank != 0:
         if world_size > 1:
             dist.destroy_process_group()
         return
 
-    peak_tf = N.C.c_double(0.0)
-    peak_ms = N.C.c_double(0.0)
-    N.check(N.lib().ez_fp32_peak(local_rank, N.C.byref(peak_tf), N.C.byref(peak_ms)))
+    peak_tf = _peak("ez_fp32_peak", local_rank)
     avg_launch_ms = float(np.mean(launch_ms))
     achieved_tf = FLOP_PER_CHECK * BATCH / (avg_launch_ms * 1e-3) / 1e12
     traffic = None
@@ -533,24 +683,29 @@ def run_ours(args):
     extra = {}
     if world_size == 1 and not args.skip_extra:
         extra["config1"] = bench_config1(cpu=not args.skip_cpu)
-        extra["config4"] = bench_config4()
+        extra["config4"] = bench_config4(cpu=not args.skip_cpu)
         extra["boxes"] = bench_boxes()
         extra["drm"] = bench_drm(cpu=not args.skip_cpu)
+    if config4_sharded is not None:
+        extra["config4_in_segment_sharded"] = config4_sharded
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world_size, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": max_ms / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": "config 2: Franka-like 7-DOF (33 spheres r=0.055, 232 self pairs) vs 10k voxel "
-                               "spheres (side 0.02), uniform configs in the joint limits",
+                               "spheres (side 0.02), uniform fp32 configs in the joint limits (default_rng)",
                    "configs_per_step_per_gpu": BATCH, "l2": "8 rotating resident batches (224 MB > L2)",
-                   "free_fraction": free_frac, "precision": "fp32 (flags exact outside a 1e-5 contact band)"},
-        "roofline": {"bound": "fp32", "achieved": achieved_tf, "peak": peak_tf.value, "unit": "TFLOP/s",
-                     "frac": achieved_tf / peak_tf.value, "traffic": traffic,
+                   "free_fraction": free_frac, "precision": "fp32 (flags exact outside a 1e-5 contact band)",
+                   "parity": "batch 0 = tests/golden/config2_1m.npz rows (reference flags, "
+                             "tests/test_gpu_pinned.py::test_config2_full_size_through_the_bench_launch)"},
+        "roofline": {"bound": "fp32", "achieved": achieved_tf, "peak": peak_tf, "unit": "TFLOP/s",
+                     "frac": achieved_tf / peak_tf, "traffic": traffic,
                      "kernel": ("ez_check_jit_f (k_check specialised for the model at run time, NVRTC sm_100a)"
                                 if specialised else "k_check<float,float>"),
                      "jit_compile_ms": jit_ms, "cta": nat.info()["check_cta"], "flop_per_check": FLOP_PER_CHECK,
                      "avg_launch_ms": avg_launch_ms,
-                     "frac_note": "of measured: the FP32 FMA peak of this GPU, measured in this run",
+                     "frac_note": "of measured: the FP32 FMA peak of this GPU, measured in this run; FLOP are "
+                                  "SURVEY 8(d)'s per-check model (every test), early exit skips part of them",
                      "peak_source": "ez_fp32_peak FMA microbenchmark measured in this run "
                                     "(MEASURED_PEAKS.json has HBM %.0f GB/s and bf16 only)" % peaks.get("hbm_gbs", 0),
                      # the same launch on the HBM roofline (28 B in + 1 B out per check)
@@ -559,8 +714,12 @@ def run_ours(args):
                              "frac": (29.0 * BATCH / (avg_launch_ms * 1e-3) / 1e9 / peaks["hbm_gbs"])
                              if peaks.get("hbm_gbs") else None,
                              "frac_note": "of measured (MEASURED_PEAKS.json hbm_gbs): not the bound"}},
-        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": BATCH * 7 * 8, "d2h_bytes_per_step": BATCH,
-                "api": "CollisionChecker.check_batch(numpy fp64, pinned) -> ez_check_batch_host"},
+        "e2e": {"value": e2e["pageable_fp32"], "unit": UNIT, "h2d_bytes_per_step": e2e["h2d_bytes_per_step"],
+                "d2h_bytes_per_step": e2e["d2h_bytes_per_step"],
+                "api": "CollisionChecker.check_batch(numpy fp32, pageable) -> ez_check_batch_host",
+                "pinned_fp32": e2e["pinned_fp32"], "pinned_fp64": e2e["pinned_fp64"]},
+        "fp64_arithmetic": {"checks_per_s": fp64_rate, "note": "precision='fp64' (the reference's arithmetic, "
+                                                                 "flags bit-exact except |c| < 1e-12), same rows"},
         "gpu_launches": args.steps,
         "clocks": clk.summary(),
         "cpu_baseline": cpu,
@@ -571,6 +730,44 @@ def run_ours(args):
     print(json.dumps(line), flush=True)
     if world_size > 1:
         dist.destroy_process_group()
+
+
+def bench_config4_sharded(comm, world_size: int) -> dict:
+    """Config 4 region with each iteration's samples split over the ranks (2 collectives/iteration)."""
+    import torch
+
+    from paper_2504_10783_b200 import fixtures as fx
+    from paper_2504_10783_b200.distributed import inflate_edge_sharded
+    from paper_2504_10783_b200.eizo import InflationParams, Segment
+    from paper_2504_10783_b200.polytope import HPolytope
+
+    world = fx.bimanual14_world()
+    ck = world.checker()
+    v1, v2 = fx.random_free_segment(world, seed=3)
+    dom = HPolytope.from_bounds(world.lower, world.upper)
+    params = InflationParams(**fx.FRANKA_PARAMS)
+    torch.distributed.barrier()
+    t0 = time.perf_counter()
+    rep = inflate_edge_sharded(Segment(v1, v2), dom, params, ck, seed=7, comm=comm)
+    torch.cuda.synchronize()
+    t = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device="cuda")
+    torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    return {"ms_wall_max_over_ranks": float(t.item()) * 1e3, "iterations": rep.iterations,
+            "faces": rep.hyperplanes_added, "collision_checks": rep.collision_checks,
+            "collectives": comm.collectives, "ranks": world_size}
+
+
+def _relaunch_under_torchrun(args) -> None:
+    """``--gpus N`` (N > 1) outside torchrun: re-exec under torch.distributed.run, one rank per GPU."""
+    import socket
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", str(Path(__file__).resolve()), *sys.argv[1:]]
+    os.execv(sys.executable, cmd)
 
 
 def main():
@@ -584,6 +781,8 @@ def main():
     ap.add_argument("--skip-extra", action="store_true", help="skip the config-4 and config-5 (DRM) sections")
     ap.add_argument("--cpu-sample", type=int, default=30_000)
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        _relaunch_under_torchrun(args)
     if args.impl == "reference":
         run_reference(args)
     else:

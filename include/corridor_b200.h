@@ -28,7 +28,7 @@
 extern "C" {
 #endif
 
-#define EZ_ABI_VERSION 2
+#define EZ_ABI_VERSION 3
 
 /* ---- status codes: mapped 1:1 onto corridor.errors (errors.py:4-64) ---- */
 typedef enum ez_status {
@@ -133,6 +133,9 @@ int32_t ez_device_count(void);
 /* FP32 FMA throughput of `device` (TFLOP/s), the roofline denominator of the
  * FP32-bound checker; measured with a dependent-chain-free FMA kernel. */
 int32_t ez_fp32_peak(int32_t device, double* tflops, double* ms);
+/* FP64 tensor-core (DMMA m8n8k4) throughput of `device` (TFLOP/s), the
+ * roofline denominator of the hit-and-run walk (FP64 chord GEMMs). */
+int32_t ez_fp64_tc_peak(int32_t device, double* tflops, double* ms);
 
 /* ---------------- world / collision checker ----------------
  * ez_world_create  replaces CollisionChecker.__init__   (world.py:441-463)
@@ -151,7 +154,9 @@ int32_t ez_world_get_info(const ez_world* world, ez_world_info* out);
  * it for fp32 batches; mode 0: query only; mode -1: go back to the generic
  * kernel for good.  Returns EZ_OK if the specialised kernel is in use,
  * EZ_UNSUPPORTED if it is not (robot boxes, NVRTC missing, disabled).
- * fp32 batches of >= 2^18 rows specialise automatically unless EZ_JIT=0. */
+ * Never compiled implicitly by a check call; the kernel is published
+ * atomically after its CTA size is tuned, so concurrent checks on the world
+ * see either the generic or the finished specialised kernel. */
 int32_t ez_world_specialize(ez_world* world, int32_t mode);
 
 /* Free mask (1 = collision-free) for n configurations.  d_q points at n rows
@@ -160,10 +165,11 @@ int32_t ez_world_specialize(ez_world* world, int32_t mode);
  * EZ_F64: the reference's FP64 arithmetic). */
 int32_t ez_check_batch(ez_world* world, const void* d_q, int32_t q_dtype, int64_t n,
                        int64_t ld, uint8_t* d_free, int32_t precision, void* stream);
-/* Same, from host memory: pipelined H2D / kernel / D2H over an internal
- * pinned ring, synchronous on return.  This is what a ctypes binding of the
- * numpy-facing check_batch calls. */
-int32_t ez_check_batch_host(ez_world* world, const double* h_q, int64_t n, int64_t ld,
+/* Same, from host memory (rows of type q_dtype, pinned or pageable):
+ * pipelined H2D / kernel / D2H over an internal pinned ring, synchronous on
+ * return.  This is what a ctypes binding of the numpy-facing check_batch
+ * calls; fp32 rows cross PCIe at 4 B per value. */
+int32_t ez_check_batch_host(ez_world* world, const void* h_q, int32_t q_dtype, int64_t n, int64_t ld,
                             uint8_t* h_free, int32_t precision);
 /* Link frames: d_frames[n][n_links][12] = row-major R (9) then t (3),
  * embedded in 3-D for planar models. */

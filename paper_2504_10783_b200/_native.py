@@ -60,12 +60,13 @@ SIGNATURES = {
     "ez_last_error": (C.c_char_p, []),
     "ez_device_count": (c_i32, []),
     "ez_fp32_peak": (c_i32, [c_i32, P_dbl, P_dbl]),
+    "ez_fp64_tc_peak": (c_i32, [c_i32, P_dbl, P_dbl]),
     "ez_world_create": (c_i32, [C.POINTER(RobotDesc), C.POINTER(SceneDesc), c_dbl, c_i32, C.POINTER(c_vp)]),
     "ez_world_destroy": (c_i32, [c_vp]),
     "ez_world_get_info": (c_i32, [c_vp, C.POINTER(WorldInfo)]),
     "ez_world_specialize": (c_i32, [c_vp, c_i32]),
     "ez_check_batch": (c_i32, [c_vp, c_vp, c_i32, c_i64, c_i64, c_vp, c_i32, c_vp]),
-    "ez_check_batch_host": (c_i32, [c_vp, c_vp, c_i64, c_i64, c_vp, c_i32]),
+    "ez_check_batch_host": (c_i32, [c_vp, c_vp, c_i32, c_i64, c_i64, c_vp, c_i32]),
     "ez_fk_batch": (c_i32, [c_vp, c_vp, c_i64, c_vp, c_vp]),
     "ez_hit_and_run": (c_i32, [c_vp, c_vp, c_i32, c_i32, c_vp, c_i64, c_i64, c_i32, c_u64, c_u64, c_i32,
                                c_vp, c_vp]),
@@ -110,7 +111,7 @@ def load_library(path: Path | str | None = None) -> C.CDLL:
             fn = getattr(lib, name)
             fn.restype = res
             fn.argtypes = args
-        if lib.ez_abi_version() != 2:
+        if lib.ez_abi_version() != 3:
             raise NativeError("ABI version mismatch")
         if path is None:
             _lib = lib

@@ -12,6 +12,8 @@ exceeds 1e-5.  ``precision="fp64"`` uses the reference's fp64 arithmetic.
 
 from __future__ import annotations
 
+import os
+
 import numpy as np
 
 from .errors import DimensionMismatch
@@ -35,19 +37,36 @@ def segment_samples(v1, v2, step: float) -> np.ndarray:
 class CollisionChecker:
     """Conservative collision oracle for one world and margin, evaluated on the GPU."""
 
-    def __init__(self, world, margin: float = 0.0, precision: str = "fp32"):
+    # "auto" specialisation: robots with at least this many spheres get the
+    # model-specialised kernel when the device world is created
+    SPECIALIZE_MIN_SPHERES = 16
+
+    def __init__(self, world, margin: float = 0.0, precision: str = "fp32", specialize="auto"):
         self.world = world
         self.model = world.model
         self.margin = float(margin)
         self.precision = precision
         precision_code(precision)
+        if specialize not in ("auto", True, False):
+            raise ValueError("specialize must be 'auto', True or False")
+        self.specialize = specialize
         self.calls = 0
         self._native: NativeWorld | None = None
 
     @property
     def native(self) -> NativeWorld:
+        """The device world, created on first use.  The model-specialised fp32 kernel
+        (``ez_world_specialize``: NVRTC once per model and margin, cached in-process and on disk)
+        is compiled here and only here, never inside a check call: always with
+        ``specialize=True``, for robots of >= 16 spheres with ``"auto"``."""
         if self._native is None:
-            self._native = NativeWorld(self.model, self.world.static, self.world.vmap, self.margin)
+            nat = NativeWorld(self.model, self.world.static, self.world.vmap, self.margin)
+            want = self.specialize is True or (
+                self.specialize == "auto" and len(self.model.geometries()) >= self.SPECIALIZE_MIN_SPHERES
+                and os.environ.get("EZ_JIT", "1") != "0")
+            if want:
+                nat.specialize(1)  # EZ_UNSUPPORTED (robot boxes, no NVRTC) keeps the generic kernel
+            self._native = nat
         return self._native
 
     def check(self, q) -> bool:
@@ -64,7 +83,9 @@ class CollisionChecker:
                     f"batch has {Qt.shape[1]} columns, robot has {self.model.dof} dof")
             self.calls += int(Qt.shape[0])
             return self.native.check_device(Qt, precision=self.precision).bool()
-        Q = np.asarray(Q, dtype=float)
+        Q = np.asarray(Q)
+        if Q.dtype != np.float32:  # fp32 rows go to the device as they are (4 B per value)
+            Q = np.asarray(Q, dtype=float)
         if Q.ndim != 2:
             Q = np.atleast_2d(Q)
         if Q.shape[0] == 0:

@@ -12,6 +12,7 @@ typedef unsigned long long uint64_t;
 #else
 #include <cstdint>
 #include <cstdio>
+#include <functional>
 #include <string>
 
 #include <cuda_runtime.h>
@@ -29,6 +30,9 @@ void set_error(const std::string& msg);
 int32_t fail(int32_t status, const std::string& msg);
 int32_t cuda_fail(cudaError_t err, const char* what, const char* file, int line);
 int32_t retain_async_pool();  // keep the current device's default mem pool cached
+// fn(lo, hi) over [0, n) split across a persistent host thread pool (parts of
+// at least min_per_part items); returns when every part is done
+void host_parallel(int64_t n, int64_t min_per_part, const std::function<void(int64_t, int64_t)>& fn);
 #endif
 
 #define EZ_CUDA(call)                                                        \
@@ -42,6 +46,26 @@ int32_t retain_async_pool();  // keep the current device's default mem pool cach
         int32_t _s = (call);                                                 \
         if (_s != EZ_OK) return _s;                                          \
     } while (0)
+
+#ifndef __CUDACC_RTC__
+// Every C entry point runs on its object's device and leaves the caller's
+// current device as it found it.
+struct DeviceGuard {
+    int prev = -1;
+    cudaError_t err = cudaSuccess;
+    explicit DeviceGuard(int device) {
+        if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+        if (prev != device) err = cudaSetDevice(device);
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+    }
+};
+#define EZ_ON_DEVICE(dev)                                                    \
+    ::ez::DeviceGuard _ez_dg(dev);                                           \
+    EZ_CUDA(_ez_dg.err)
+#endif
 
 // ---------------------------------------------------------------------------
 // device-side model records.  All kinematics are embedded in 3-D; a planar

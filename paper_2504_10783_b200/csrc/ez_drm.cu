@@ -301,7 +301,7 @@ extern "C" int32_t ez_roadmap_create(const int64_t* h_off, const int32_t* h_ids,
     int64_t prod = 1;
     for (int k = 0; k < dim; ++k) prod *= h_extents[k];
     if (prod != n_voxels) return fail(EZ_INVALID_ARGUMENT, "grid extents disagree with the voxel count");
-    EZ_CUDA(cudaSetDevice(device));
+    EZ_ON_DEVICE(device);
     ez_roadmap* r = new ez_roadmap();
     r->device = device;
     r->dim = dim;
@@ -329,6 +329,7 @@ extern "C" int32_t ez_roadmap_create(const int64_t* h_off, const int32_t* h_ids,
     if (e == cudaSuccess) e = cudaMalloc(&r->d_vox_bits, sizeof(uint32_t) * ((n_voxels + 31) / 32));
     if (e == cudaSuccess) e = cudaMalloc(&r->d_count, sizeof(unsigned long long));
     if (e == cudaSuccess) e = cudaMallocHost(&r->h_count, sizeof(unsigned long long));
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&r->scratch_free, cudaEventDisableTiming);
     if (e != cudaSuccess) return cleanup(cuda_fail(e, "roadmap upload", __FILE__, __LINE__));
     *out = r;
     return EZ_OK;
@@ -336,26 +337,25 @@ extern "C" int32_t ez_roadmap_create(const int64_t* h_off, const int32_t* h_ids,
 
 extern "C" int32_t ez_roadmap_destroy(ez_roadmap* r) {
     if (!r) return EZ_OK;
-    cudaSetDevice(r->device);
+    ::ez::DeviceGuard dg(r->device);
     cudaFree(r->d_off);
     cudaFree(r->d_ids);
     cudaFree(r->d_vox_bits);
     cudaFree(r->d_count);
     cudaFreeHost(r->h_count);
+    if (r->scratch_free) cudaEventDestroy(r->scratch_free);
     delete r;
     return EZ_OK;
 }
 
-extern "C" int32_t ez_collision_set(ez_roadmap* r, const int32_t* d_vox_idx, int64_t n_vox, const double* h_vmap_origin,
-                                    double vmap_side, int32_t same_grid, uint32_t* d_blocked_bits, int64_t* n_blocked,
-                                    void* stream) {
-    if (!r) return fail(EZ_INVALID_ARGUMENT, "null roadmap");
-    if (n_blocked) *n_blocked = 0;
-    EZ_CUDA(cudaSetDevice(r->device));
-    cudaStream_t s = static_cast<cudaStream_t>(stream);
+// caller holds r->mu and is on r's device; leaves scratch_free recorded on s
+static int32_t prune_locked(ez_roadmap* r, const int32_t* d_vox_idx, int64_t n_vox, const double* h_vmap_origin,
+                            double vmap_side, int32_t same_grid, uint32_t* d_blocked_bits, int64_t* n_blocked,
+                            cudaStream_t s) {
     const int64_t nbw = (r->n_nodes + 31) / 32;
     EZ_CUDA(cudaMemsetAsync(d_blocked_bits, 0, sizeof(uint32_t) * std::max<int64_t>(1, nbw), s));
     if (n_vox == 0) return EZ_OK;
+    EZ_CUDA(cudaStreamWaitEvent(s, r->scratch_free, 0));  // the previous prune is done with the scratch
     const int64_t vbw = (r->n_voxels + 31) / 32;
     EZ_CUDA(cudaMemsetAsync(r->d_vox_bits, 0, sizeof(uint32_t) * vbw, s));
     if (n_blocked) EZ_CUDA(cudaMemsetAsync(r->d_count, 0, sizeof(unsigned long long), s));
@@ -385,19 +385,37 @@ extern "C" int32_t ez_collision_set(ez_roadmap* r, const int32_t* d_vox_idx, int
     return EZ_OK;
 }
 
+extern "C" int32_t ez_collision_set(ez_roadmap* r, const int32_t* d_vox_idx, int64_t n_vox, const double* h_vmap_origin,
+                                    double vmap_side, int32_t same_grid, uint32_t* d_blocked_bits, int64_t* n_blocked,
+                                    void* stream) {
+    if (!r) return fail(EZ_INVALID_ARGUMENT, "null roadmap");
+    if (n_blocked) *n_blocked = 0;
+    EZ_ON_DEVICE(r->device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    std::lock_guard<std::mutex> lk(r->mu);
+    const int32_t st = prune_locked(r, d_vox_idx, n_vox, h_vmap_origin, vmap_side, same_grid, d_blocked_bits,
+                                    n_blocked, s);
+    if (st == EZ_OK) EZ_CUDA(cudaEventRecord(r->scratch_free, s));
+    return st;
+}
+
+
 extern "C" int32_t ez_collision_set_ids(ez_roadmap* r, const int32_t* d_vox_idx, int64_t n_vox,
                                         const double* h_vmap_origin, double vmap_side, int32_t same_grid,
                                         uint32_t* d_blocked_bits, int32_t* d_ids, int64_t* n_ids, void* stream) {
     if (!r || !n_ids) return fail(EZ_INVALID_ARGUMENT, "null argument");
     *n_ids = 0;
-    EZ_TRY(ez_collision_set(r, d_vox_idx, n_vox, h_vmap_origin, vmap_side, same_grid, d_blocked_bits, nullptr, stream));
-    if (n_vox == 0) return EZ_OK;
+    EZ_ON_DEVICE(r->device);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
+    std::lock_guard<std::mutex> lk(r->mu);  // d_count is scratch too
+    EZ_TRY(prune_locked(r, d_vox_idx, n_vox, h_vmap_origin, vmap_side, same_grid, d_blocked_bits, nullptr, s));
+    if (n_vox == 0) return EZ_OK;
     const int64_t nbw = (r->n_nodes + 31) / 32;
     int64_t* d_n = reinterpret_cast<int64_t*>(r->d_count);
     k_bits_to_ids<<<1, 1024, 0, s>>>(d_blocked_bits, nbw, d_ids, d_n);
     EZ_CUDA(cudaGetLastError());
     EZ_CUDA(cudaMemcpyAsync(r->h_count, d_n, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    EZ_CUDA(cudaEventRecord(r->scratch_free, s));
     EZ_CUDA(cudaStreamSynchronize(s));
     *n_ids = static_cast<int64_t>(*r->h_count);
     return EZ_OK;

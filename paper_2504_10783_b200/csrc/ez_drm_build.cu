@@ -169,7 +169,7 @@ extern "C" int32_t ez_roadmap_build(ez_world* w, const double* d_nodes, int64_t 
     if (dim != w->dim) return fail(EZ_DIMENSION_MISMATCH, "grid dimension differs from the robot's task space");
     if (!(side > 0.0)) return fail(EZ_INVALID_ARGUMENT, "grid side must be positive");
     if (w->dof > 32) return fail(EZ_UNSUPPORTED, "more than 32 degrees of freedom");
-    EZ_CUDA(cudaSetDevice(w->device));
+    EZ_ON_DEVICE(w->device);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     MapGrid g{};
     int64_t n_vox = 1;
@@ -245,6 +245,7 @@ extern "C" int32_t ez_roadmap_build(ez_world* w, const double* d_nodes, int64_t 
     if (e == cudaSuccess) e = cudaMalloc(&r->d_vox_bits, sizeof(uint32_t) * ((n_vox + 31) / 32));
     if (e == cudaSuccess) e = cudaMalloc(&r->d_count, sizeof(unsigned long long));
     if (e == cudaSuccess) e = cudaMallocHost(&r->h_count, sizeof(unsigned long long));
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&r->scratch_free, cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaMemsetAsync(d_cnt, 0, sizeof(unsigned long long), s);
     if (e == cudaSuccess) e = cudaMemsetAsync(counts, 0, sizeof(unsigned long long) * n_vox, s);
     if (e == cudaSuccess && n_nodes > 0) {
@@ -292,7 +293,7 @@ extern "C" int32_t ez_roadmap_info(const ez_roadmap* r, int64_t* n_voxels, int64
 
 extern "C" int32_t ez_roadmap_export(const ez_roadmap* r, int64_t* h_offsets, int32_t* h_ids) {
     if (!r) return fail(EZ_INVALID_ARGUMENT, "null roadmap");
-    EZ_CUDA(cudaSetDevice(r->device));
+    EZ_ON_DEVICE(r->device);
     if (h_offsets) EZ_CUDA(cudaMemcpy(h_offsets, r->d_off, sizeof(int64_t) * (r->n_voxels + 1), cudaMemcpyDeviceToHost));
     if (h_ids && r->nnz) EZ_CUDA(cudaMemcpy(h_ids, r->d_ids, sizeof(int32_t) * r->nnz, cudaMemcpyDeviceToHost));
     return EZ_OK;

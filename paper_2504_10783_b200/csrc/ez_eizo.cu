@@ -1610,7 +1610,7 @@ extern "C" int32_t ez_inflate_edge(ez_world* w, const double* h_v1, const double
     const ez_eizo_params& p = *params;
     if (p.n_p < 1 || p.n_f < 1 || p.n_b < 1 || p.n_ms < 1) return fail(EZ_INVALID_ARGUMENT, "counts must be >= 1");
     if (rng != EZ_RNG_COUNTER && rng != EZ_RNG_PHILOX) return fail(EZ_INVALID_ARGUMENT, "unknown rng");
-    EZ_CUDA(cudaSetDevice(w->device));
+    EZ_ON_DEVICE(w->device);
     const int d = dim;
     // seed segment strictly inside the domain (inflation.py:274-277), fp64 on the host
     for (int v = 0; v < 2; ++v) {
@@ -1800,7 +1800,7 @@ extern "C" int32_t ez_refine_set(ez_world* w, const double* h_v1, const double* 
     if (n_cols < 1) return fail(EZ_INVALID_ARGUMENT, "refine_sets needs at least one collision");
     if (n_b < 1) return fail(EZ_INVALID_ARGUMENT, "n_b must be >= 1");
     if (dim > 32) return fail(EZ_UNSUPPORTED, "dimension <= 32");
-    EZ_CUDA(cudaSetDevice(w->device));
+    EZ_ON_DEVICE(w->device);
     const int d = dim;
     WsLease lease;
     EZ_TRY(lease.acquire(w->device));

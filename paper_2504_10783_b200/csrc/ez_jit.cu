@@ -513,9 +513,8 @@ __global__ void k_fill_box(float* q, int64_t n, int dof, const double* lo, const
     }
 }
 
-int32_t launch_at(ez_world* w, int bt, const void* d_q, bool q64, int64_t n, int64_t ld, uint8_t* d_free,
-                  cudaStream_t stream, int64_t count_lim, int32_t* n_col) {
-    const JitCheck& jc = *w->jit;
+int32_t launch_at(ez_world* w, const JitCheck& jc, int bt, const void* d_q, bool q64, int64_t n, int64_t ld,
+                  uint8_t* d_free, cudaStream_t stream, int64_t count_lim, int32_t* n_col) {
     int si = 0;
     while (kJitSizes[si] != bt) ++si;
     const cudaKernel_t kern = jc.k[q64 ? 1 : 0][shape_of(bt)];
@@ -532,7 +531,7 @@ int32_t launch_at(ez_world* w, int bt, const void* d_q, bool q64, int64_t n, int
 
 // CTA size for large batches: time 1024, 512 and 256 threads (each at the
 // residency its kernel was compiled for) on random configurations.
-int32_t tune_bt(ez_world* w) {
+int32_t tune_bt(ez_world* w, const JitCheck& jc) {
     const char* e = getenv("EZ_JIT_BT");
     if (e && (atoi(e) == 256 || atoi(e) == 512 || atoi(e) == 1024) && w->jit_occ[0][shape_of(atoi(e)) + 2] > 0) {
         w->jit_bt = atoi(e);
@@ -565,9 +564,9 @@ int32_t tune_bt(ez_world* w) {
             for (int c = 0; c < 3 && st == EZ_OK; ++c) {
                 const int bt = sizes[c];
                 if (w->jit_occ[0][shape_of(bt) + 2] < 1) continue;
-                for (int r = 0; r < 2 && st == EZ_OK; ++r) st = launch_at(w, bt, d_q, false, n, dof, d_out, s, 0, nullptr);
+                for (int r = 0; r < 2 && st == EZ_OK; ++r) st = launch_at(w, jc, bt, d_q, false, n, dof, d_out, s, 0, nullptr);
                 if (!ck(cudaEventRecord(e0, s))) break;
-                for (int r = 0; r < 4 && st == EZ_OK; ++r) st = launch_at(w, bt, d_q, false, n, dof, d_out, s, 0, nullptr);
+                for (int r = 0; r < 4 && st == EZ_OK; ++r) st = launch_at(w, jc, bt, d_q, false, n, dof, d_out, s, 0, nullptr);
                 float ms = 0.f;
                 if (!ck(cudaEventRecord(e1, s)) || !ck(cudaEventSynchronize(e1)) || !ck(cudaEventElapsedTime(&ms, e0, e1)))
                     break;
@@ -590,8 +589,8 @@ int32_t tune_bt(ez_world* w) {
 }  // namespace
 
 int32_t jit_specialize(ez_world* w) {
-    std::lock_guard<std::mutex> cfg(w->cfg_mu);  // threads racing to the first large batch compile once
-    if (w->jit) return EZ_OK;
+    std::lock_guard<std::mutex> cfg(w->cfg_mu);  // concurrent callers compile once
+    if (std::atomic_load(&w->jit)) return EZ_OK;
     if (w->jit_failed) return fail(EZ_UNSUPPORTED, w->jit_error);
     auto refuse = [&](int32_t st, const std::string& why) {
         w->jit_failed = true;
@@ -642,16 +641,17 @@ int32_t jit_specialize(ez_world* w) {
         }
     if (w->jit_occ[0][0] < 1 || w->jit_occ[1][0] < 1)
         return refuse(EZ_CAPACITY, "specialised check kernel does not fit on an SM");
-    w->jit = jc;
-    const int32_t st = tune_bt(w);
-    if (st != EZ_OK) w->jit.reset();
+    // tuned before it is published: a launch that sees the kernel (atomic
+    // snapshot in launch_check_t) also sees its CTA size and occupancies
+    const int32_t st = tune_bt(w, *jc);
+    if (st == EZ_OK) std::atomic_store(&w->jit, std::shared_ptr<const JitCheck>(jc));
     return st;
 }
 
 // Large batches run at the tuned CTA size; a batch too small to give every
 // SM a CTA at that size (host-path chunks, the EI-ZO loop's 1e4-row batches)
 // drops to the largest size that does, down to 64 threads.
-int32_t jit_launch(ez_world* w, const void* d_q, bool q64, int64_t n, int64_t ld, uint8_t* d_free,
+int32_t jit_launch(ez_world* w, const JitCheck& jc, const void* d_q, bool q64, int64_t n, int64_t ld, uint8_t* d_free,
                    cudaStream_t stream, int64_t count_lim, int32_t* n_col) {
     int bt = 64;
     for (int si = kJitSizeCount - 1; si >= 0; --si) {
@@ -662,7 +662,7 @@ int32_t jit_launch(ez_world* w, const void* d_q, bool q64, int64_t n, int64_t ld
             break;
         }
     }
-    return launch_at(w, bt, d_q, q64, n, ld, d_free, stream, count_lim, n_col);
+    return launch_at(w, jc, bt, d_q, q64, n, ld, d_free, stream, count_lim, n_col);
 }
 
 }  // namespace ez
@@ -670,14 +670,15 @@ int32_t jit_launch(ez_world* w, const void* d_q, bool q64, int64_t n, int64_t ld
 extern "C" int32_t ez_world_specialize(ez_world* w, int32_t mode) {
     if (!w) return ez::fail(EZ_INVALID_ARGUMENT, "null world");
     std::lock_guard<std::mutex> lock(w->mu);
-    EZ_CUDA(cudaSetDevice(w->device));
+    EZ_ON_DEVICE(w->device);
     if (mode < 0) {
-        w->jit.reset();
+        std::lock_guard<std::mutex> cfg(w->cfg_mu);
+        std::atomic_store(&w->jit, std::shared_ptr<const ez::JitCheck>());
         w->jit_failed = true;
         w->jit_error = "specialised check kernel disabled for this world";
         return EZ_OK;
     }
     if (mode > 0) return ez::jit_specialize(w);
-    if (w->jit) return EZ_OK;
+    if (std::atomic_load(&w->jit)) return EZ_OK;
     return ez::fail(EZ_UNSUPPORTED, w->jit_failed ? w->jit_error : std::string("not specialised"));
 }

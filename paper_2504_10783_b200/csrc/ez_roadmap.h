@@ -1,6 +1,8 @@
 // ez_roadmap.h — device-resident DRM collision map (CSR voxel -> node ids).
 #pragma once
 
+#include <mutex>
+
 #include "ez_common.h"
 
 struct ez_roadmap {
@@ -15,4 +17,10 @@ struct ez_roadmap {
     uint32_t* d_vox_bits = nullptr;  // scratch: active roadmap voxels
     unsigned long long* d_count = nullptr;
     unsigned long long* h_count = nullptr;
+    // The scratch above is shared by every prune on this roadmap.  A prune
+    // holds `mu` while it enqueues, waits on `scratch_free` (recorded by the
+    // previous prune on its stream after its last scratch use) and records it
+    // again, so asynchronous prunes on different streams use it in turn.
+    std::mutex mu;
+    cudaEvent_t scratch_free = nullptr;
 };

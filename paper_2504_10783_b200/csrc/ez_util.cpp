@@ -1,7 +1,13 @@
 // ez_util.cpp — error reporting and small library-level entry points.
+#include <algorithm>
+#include <cstdlib>
+#include <condition_variable>
 #include <cstdint>
+#include <functional>
 #include <mutex>
 #include <string>
+#include <thread>
+#include <vector>
 
 #include "ez_common.h"
 
@@ -40,6 +46,82 @@ int32_t retain_async_pool() {
     if (e != cudaSuccess) return cuda_fail(e, "default mem pool release threshold", __FILE__, __LINE__);
     done[dev & 63] = true;
     return EZ_OK;
+}
+
+// ---------------------------------------------------------------------------
+// host_parallel: a small persistent pool for host-side byte moves (pageable
+// batches are copied into the pinned staging ring by several threads; one
+// thread's memcpy from pageable memory is far below the PCIe rate).
+// ---------------------------------------------------------------------------
+namespace {
+class HostPool {
+  public:
+    explicit HostPool(int n) {
+        for (int i = 0; i < n; ++i) th_.emplace_back([this] { loop(); });
+        for (auto& t : th_) t.detach();  // lives for the process (never destroyed)
+    }
+    int size() const { return static_cast<int>(th_.size()) + 1; }
+    void run(int parts, const std::function<void(int)>& f) {
+        std::lock_guard<std::mutex> one(run_mu_);  // one job at a time
+        std::unique_lock<std::mutex> lk(mu_);
+        job_ = &f;
+        parts_ = parts;
+        next_ = 0;
+        remaining_ = parts;
+        ++gen_;
+        cv_.notify_all();
+        drain(lk);  // the caller works too
+        done_.wait(lk, [&] { return remaining_ == 0; });
+        job_ = nullptr;
+    }
+
+  private:
+    void drain(std::unique_lock<std::mutex>& lk) {
+        while (next_ < parts_) {
+            const int i = next_++;
+            const std::function<void(int)>* f = job_;
+            lk.unlock();
+            (*f)(i);
+            lk.lock();
+            if (--remaining_ == 0) done_.notify_all();
+        }
+    }
+    void loop() {
+        uint64_t seen = 0;
+        std::unique_lock<std::mutex> lk(mu_);
+        for (;;) {
+            cv_.wait(lk, [&] { return gen_ != seen; });
+            seen = gen_;
+            drain(lk);
+        }
+    }
+    std::vector<std::thread> th_;
+    std::mutex run_mu_, mu_;
+    std::condition_variable cv_, done_;
+    const std::function<void(int)>* job_ = nullptr;
+    int parts_ = 0, next_ = 0, remaining_ = 0;
+    uint64_t gen_ = 0;
+};
+
+HostPool& host_pool() {
+    // EZ_HOST_THREADS overrides the size (default: the host's hardware threads, at most 16)
+    static HostPool* p = [] {
+        int n = std::min(16, static_cast<int>(std::thread::hardware_concurrency()));
+        if (const char* e = getenv("EZ_HOST_THREADS")) n = atoi(e);
+        return new HostPool(std::max(1, n) - 1);
+    }();
+    return *p;
+}
+}  // namespace
+
+void host_parallel(int64_t n, int64_t min_per_part, const std::function<void(int64_t, int64_t)>& fn) {
+    if (n <= 0) return;
+    const int parts = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(host_pool().size(), n / std::max<int64_t>(1, min_per_part))));
+    if (parts == 1) {
+        fn(0, n);
+        return;
+    }
+    host_pool().run(parts, [&](int i) { fn(n * i / parts, n * (i + 1) / parts); });
 }
 
 }  // namespace ez

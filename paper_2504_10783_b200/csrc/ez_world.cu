@@ -5,6 +5,7 @@
 //   fk_batch                    195-223 (ez_fk_batch)
 #include <algorithm>
 #include <atomic>
+#include <chrono>
 #include <climits>
 #include <cmath>
 #include <cstdlib>
@@ -836,27 +837,16 @@ static void launch_bt(const ModelDev<T>& M, unsigned grid, size_t smem, cudaStre
     k_check<T, Q, BT><<<grid, BT, smem, stream>>>(M, d_q, n, ld, d_free, margin, count_lim, n_col);
 }
 
-// EZ_JIT=0 keeps every batch on the generic kernel; otherwise the first fp32
-// batch of at least kJitMinRows rows compiles the model-specialised one.
-constexpr int64_t kJitMinRows = int64_t(1) << 18;
-static bool jit_enabled() {
-    static const bool on = [] {
-        const char* e = getenv("EZ_JIT");
-        return !(e && e[0] == '0');
-    }();
-    return on;
-}
-
 template <typename T, typename Q>
 static int32_t launch_check_t(ez_world* w, const ModelDev<T>& M, const Q* d_q, int64_t n, int64_t ld,
                               uint8_t* d_free, cudaStream_t stream, int64_t count_lim, int32_t* n_col) {
     const int slot = (sizeof(T) == 8 ? 2 : 0) + (sizeof(Q) == 8 ? 1 : 0);
     if (sizeof(T) == 4) {
-        // large fp32 batches: the model-specialised kernel (compiled once per model)
-        if (!w->jit && !w->jit_failed && n >= kJitMinRows && jit_enabled()) {
-            if (jit_specialize(w) != EZ_OK) set_error("");  // stays on the generic kernel
-        }
-        if (w->jit) return jit_launch(w, d_q, sizeof(Q) == 8, n, ld, d_free, stream, count_lim, n_col);
+        // fp32 batches run the model-specialised kernel once ez_world_specialize
+        // has published it (never compiled implicitly inside a check call);
+        // the snapshot keeps it alive for this launch
+        const std::shared_ptr<const JitCheck> jc = std::atomic_load(&w->jit);
+        if (jc) return jit_launch(w, *jc, d_q, sizeof(Q) == 8, n, ld, d_free, stream, count_lim, n_col);
     }
     if (w->launch_threads[slot] == 0) {
         std::lock_guard<std::mutex> lk(w->cfg_mu);
@@ -925,8 +915,10 @@ using namespace ez;
 static void world_free(ez_world* w) {
     if (!w) return;
     for (int i = 0; i < 2; ++i) cudaFree(w->d_blob[i]);
-    for (int i = 0; i < ez_world::kHostStages; ++i) {
+    for (int i = 0; i < ez_world::kHostLanes; ++i)
         if (w->hstream[i]) cudaStreamDestroy(w->hstream[i]);
+    for (int i = 0; i < ez_world::kHostStages; ++i) {
+        if (w->stage_done[i]) cudaEventDestroy(w->stage_done[i]);
         cudaFreeHost(w->h_stage_in[i]);
         cudaFreeHost(w->h_stage_out[i]);
         cudaFree(w->d_stage_in[i]);
@@ -949,7 +941,7 @@ extern "C" int32_t ez_world_create(const ez_robot_desc* rb, const ez_scene_desc*
     if (rb->n_joints < 1 || rb->n_joints > kMaxJoints) return fail(EZ_UNSUPPORTED, "joint count outside [1, 64]");
     if (rb->n_geoms > kMaxSpheres) return fail(EZ_UNSUPPORTED, "more than 1024 robot geometries");
     if (margin < 0.0) return fail(EZ_INVALID_ARGUMENT, "margin must be >= 0");
-    EZ_CUDA(cudaSetDevice(device));
+    EZ_ON_DEVICE(device);
     EZ_TRY(retain_async_pool());
 
     HModel hm;
@@ -1147,7 +1139,7 @@ extern "C" int32_t ez_world_create(const ez_robot_desc* rb, const ez_scene_desc*
 
 extern "C" int32_t ez_world_destroy(ez_world* w) {
     if (!w) return EZ_OK;
-    cudaSetDevice(w->device);
+    ::ez::DeviceGuard dg(w->device);
     world_free(w);
     return EZ_OK;
 }
@@ -1167,7 +1159,7 @@ extern "C" int32_t ez_world_get_info(const ez_world* w, ez_world_info* out) {
     out->device_bytes = w->device_bytes;
     {
         std::lock_guard<std::mutex> lk(const_cast<ez_world*>(w)->cfg_mu);  // jit is published under cfg_mu
-        out->check_cta = w->jit ? w->jit_bt : 0;
+        out->check_cta = std::atomic_load(&w->jit) ? w->jit_bt : 0;
     }
     out->reserved_ = 0;
     return EZ_OK;
@@ -1179,104 +1171,155 @@ extern "C" int32_t ez_check_batch(ez_world* w, const void* d_q, int32_t q_dtype,
     if (n < 0 || ld < w->dof) return fail(EZ_INVALID_ARGUMENT, "bad batch shape");
     if (n == 0) return EZ_OK;
     if (q_dtype != EZ_F32 && q_dtype != EZ_F64) return fail(EZ_INVALID_ARGUMENT, "bad dtype");
-    EZ_CUDA(cudaSetDevice(w->device));
+    EZ_ON_DEVICE(w->device);
     return launch_check(w, d_q, q_dtype, n, ld, d_free, precision, static_cast<cudaStream_t>(stream));
 }
 
-// Host-buffer check: the input is streamed through two pinned staging
-// buffers on two streams so the H2D copy of chunk i+1, the kernel of chunk i
-// and the D2H copy of chunk i-1 overlap.
-extern "C" int32_t ez_check_batch_host(ez_world* w, const double* h_q, int64_t n, int64_t ld,
+// Host-buffer check.  Rows stay in the caller's element type (fp32 rows cross
+// PCIe at 4 B per value).  The batch is cut into chunks dealt round-robin to
+// lanes; a lane is a stream with two pinned/device stages.  Per chunk a lane
+// waits for the stage's previous use (event), moves the rows into the pinned
+// stage (pageable caller buffer) or DMAs them directly (pinned), enqueues the
+// H2D copy, the check kernel and the D2H copy of the flags.
+//  * pinned rows: one host thread enqueues every lane in chunk order, so the
+//    H2D copy of one chunk overlaps the kernel and D2H of the previous ones;
+//  * pageable rows: one host thread per lane (ez_util host_parallel).  Lanes
+//    never wait on one another, so the host moves of some chunks overlap the
+//    DMA and kernels of others (one thread moving pageable rows runs far below
+//    the PCIe rate).
+// Stages are allocated on first use, so small batches hold little memory.
+extern "C" int32_t ez_check_batch_host(ez_world* w, const void* h_q, int32_t q_dtype, int64_t n, int64_t ld,
                                        uint8_t* h_free, int32_t precision) {
     if (!w) return fail(EZ_INVALID_ARGUMENT, "null world");
     if (n < 0 || ld < w->dof) return fail(EZ_INVALID_ARGUMENT, "bad batch shape");
+    if (q_dtype != EZ_F32 && q_dtype != EZ_F64) return fail(EZ_INVALID_ARGUMENT, "bad dtype");
     if (n == 0) return EZ_OK;
     std::lock_guard<std::mutex> lock(w->mu);
-    EZ_CUDA(cudaSetDevice(w->device));
+    EZ_ON_DEVICE(w->device);
     const int dof = w->dof;
-    // Chunks of `chunk` rows rotate over kHostStages streams: the H2D copy of
-    // one chunk overlaps the check and D2H of the previous ones, so the call
-    // runs at the PCIe rate of the fp64 input.
-    constexpr int NS = ez_world::kHostStages;
-    static const int64_t chunk = [] {
-        const char* e = getenv("EZ_HOST_CHUNK");
-        const int64_t v = e ? atoll(e) : 0;
-        return v >= 1024 ? v : int64_t(1) << 16;
-    }();
-    if (w->stage_rows < chunk) {
-        for (int i = 0; i < NS; ++i) {
-            cudaFreeHost(w->h_stage_in[i]);
-            cudaFreeHost(w->h_stage_out[i]);
-            cudaFree(w->d_stage_in[i]);
-            cudaFree(w->d_stage_out[i]);
-            w->h_stage_in[i] = w->d_stage_in[i] = nullptr;
-            w->h_stage_out[i] = w->d_stage_out[i] = nullptr;
-            EZ_CUDA(cudaMallocHost(&w->h_stage_in[i], sizeof(double) * chunk * dof));
-            EZ_CUDA(cudaMallocHost(reinterpret_cast<void**>(&w->h_stage_out[i]), chunk));
-            EZ_CUDA(cudaMalloc(&w->d_stage_in[i], sizeof(double) * chunk * dof));
-            EZ_CUDA(cudaMalloc(reinterpret_cast<void**>(&w->d_stage_out[i]), chunk));
-            if (!w->hstream[i]) EZ_CUDA(cudaStreamCreateWithFlags(&w->hstream[i], cudaStreamNonBlocking));
-        }
-        w->stage_rows = chunk;
-    }
+    const size_t es = q_dtype == EZ_F64 ? sizeof(double) : sizeof(float);
+    constexpr int NL = ez_world::kHostLanes;
+    auto env_i = [](const char* name, int64_t dflt, int64_t lo, int64_t hi) {
+        const char* e = getenv(name);
+        const int64_t v = e ? atoll(e) : dflt;
+        return std::min(hi, std::max(lo, v));
+    };
+    static const int64_t stage_cap = env_i("EZ_HOST_CHUNK_MAX", int64_t(1) << 16, 1024, int64_t(1) << 22);
+    static const int64_t chunk_pg = std::min(stage_cap, env_i("EZ_HOST_CHUNK", int64_t(1) << 16, 1024, int64_t(1) << 22));
+    static const int64_t chunk_pin = std::min(stage_cap, env_i("EZ_HOST_CHUNK_PINNED", int64_t(1) << 16, 1024, int64_t(1) << 22));
+    static const int lanes_pin = static_cast<int>(env_i("EZ_HOST_LANES_PINNED", 4, 1, NL));
+    static const int lanes_pg = static_cast<int>(env_i("EZ_HOST_LANES", NL, 1, NL));
+    static const bool wc = !getenv("EZ_HOST_NO_WC");
     cudaPointerAttributes attr{};
-    bool pinned_in = cudaPointerGetAttributes(&attr, h_q) == cudaSuccess && attr.type == cudaMemoryTypeHost;
+    const bool pinned_in = cudaPointerGetAttributes(&attr, h_q) == cudaSuccess && attr.type == cudaMemoryTypeHost;
     cudaGetLastError();
-    bool pinned_out = cudaPointerGetAttributes(&attr, h_free) == cudaSuccess && attr.type == cudaMemoryTypeHost;
+    const bool pinned_out = cudaPointerGetAttributes(&attr, h_free) == cudaSuccess && attr.type == cudaMemoryTypeHost;
     cudaGetLastError();
+    const int64_t chunk = pinned_in ? chunk_pin : chunk_pg;
     const int64_t nchunks = (n + chunk - 1) / chunk;
-    int64_t pending_out[NS];  // chunk index whose result sits in h_stage_out[b]
-    for (int b = 0; b < NS; ++b) pending_out[b] = -1;
-    for (int64_t c = 0; c < nchunks; ++c) {
-        const int b = static_cast<int>(c % NS);
-        cudaStream_t s = w->hstream[b];
+    const int lanes = static_cast<int>(std::min<int64_t>(pinned_in ? lanes_pin : lanes_pg, nchunks));
+    for (int i = 0; i < lanes; ++i)
+        if (!w->hstream[i]) EZ_CUDA(cudaStreamCreateWithFlags(&w->hstream[i], cudaStreamNonBlocking));
+    for (int i = 0; i < 2 * lanes; ++i) {
+        if (w->h_stage_in[i]) continue;
+        // write-combined: the host only streams rows into it and the DMA engine
+        // reads it (no cache snooping, streaming stores)
+        EZ_CUDA(cudaHostAlloc(&w->h_stage_in[i], sizeof(double) * stage_cap * dof,
+                              wc ? cudaHostAllocWriteCombined : cudaHostAllocDefault));
+        EZ_CUDA(cudaMallocHost(reinterpret_cast<void**>(&w->h_stage_out[i]), stage_cap));
+        EZ_CUDA(cudaMalloc(&w->d_stage_in[i], sizeof(double) * stage_cap * dof));
+        EZ_CUDA(cudaMalloc(reinterpret_cast<void**>(&w->d_stage_out[i]), stage_cap));
+        EZ_CUDA(cudaEventCreateWithFlags(&w->stage_done[i], cudaEventDisableTiming));
+    }
+    const char* q = static_cast<const char*>(h_q);
+    static const bool prof = getenv("EZ_HOST_PROFILE") != nullptr;
+    const auto tcall = std::chrono::steady_clock::now();
+    // pending[stage]: chunk whose flags sit in the stage's pinned output
+    std::vector<int64_t> pending(2 * lanes, -1);
+    auto drain = [&](int st) -> int32_t {
+        EZ_CUDA(cudaEventSynchronize(w->stage_done[st]));
+        if (pending[st] >= 0) {
+            const int64_t pr0 = pending[st] * chunk;
+            std::memcpy(h_free + pr0, w->h_stage_out[st], std::min(chunk, n - pr0));
+            pending[st] = -1;
+        }
+        return EZ_OK;
+    };
+    auto one_chunk = [&](int64_t c) -> int32_t {
+        const int lane = static_cast<int>(c % lanes);
+        const int st = 2 * lane + static_cast<int>((c / lanes) & 1);
+        cudaStream_t s = w->hstream[lane];
         const int64_t r0 = c * chunk;
         const int64_t rows = std::min(chunk, n - r0);
-        // host staging buffers are reused: wait for their previous chunk (all
-        // device work stays ordered on the stream, so pinned I/O never waits)
-        if (!(pinned_in && pinned_out)) EZ_CUDA(cudaStreamSynchronize(s));
-        if (pending_out[b] >= 0 && !pinned_out) {
-            const int64_t pr0 = pending_out[b] * chunk;
-            std::memcpy(h_free + pr0, w->h_stage_out[b], std::min(chunk, n - pr0));
-        }
-        pending_out[b] = -1;
-        const double* src = h_q + r0 * ld;
+        const char* src = q + r0 * ld * es;
+        const size_t row_bytes = es * dof;
+        EZ_TRY(drain(st));  // the stage's previous chunk is done (and its flags delivered)
         if (pinned_in && ld == dof) {
-            EZ_CUDA(cudaMemcpyAsync(w->d_stage_in[b], src, sizeof(double) * rows * dof, cudaMemcpyHostToDevice, s));
+            EZ_CUDA(cudaMemcpyAsync(w->d_stage_in[st], src, row_bytes * rows, cudaMemcpyHostToDevice, s));
         } else if (pinned_in) {
-            EZ_CUDA(cudaMemcpy2DAsync(w->d_stage_in[b], sizeof(double) * dof, src, sizeof(double) * ld,
-                                      sizeof(double) * dof, rows, cudaMemcpyHostToDevice, s));
+            EZ_CUDA(cudaMemcpy2DAsync(w->d_stage_in[st], row_bytes, src, es * ld, row_bytes, rows,
+                                      cudaMemcpyHostToDevice, s));
         } else {
-            double* st = static_cast<double*>(w->h_stage_in[b]);
+            char* dst = static_cast<char*>(w->h_stage_in[st]);
             if (ld == dof) {
-                std::memcpy(st, src, sizeof(double) * rows * dof);
+                std::memcpy(dst, src, row_bytes * rows);
             } else {
-                for (int64_t r = 0; r < rows; ++r) std::memcpy(st + r * dof, src + r * ld, sizeof(double) * dof);
+                for (int64_t r = 0; r < rows; ++r) std::memcpy(dst + r * row_bytes, src + r * ld * es, row_bytes);
             }
-            EZ_CUDA(cudaMemcpyAsync(w->d_stage_in[b], st, sizeof(double) * rows * dof, cudaMemcpyHostToDevice, s));
+            EZ_CUDA(cudaMemcpyAsync(w->d_stage_in[st], dst, row_bytes * rows, cudaMemcpyHostToDevice, s));
         }
-        EZ_TRY(launch_check(w, w->d_stage_in[b], EZ_F64, rows, dof, w->d_stage_out[b], precision, s));
+        EZ_TRY(launch_check(w, w->d_stage_in[st], q_dtype, rows, dof, w->d_stage_out[st], precision, s));
         if (pinned_out) {
-            EZ_CUDA(cudaMemcpyAsync(h_free + r0, w->d_stage_out[b], rows, cudaMemcpyDeviceToHost, s));
+            EZ_CUDA(cudaMemcpyAsync(h_free + r0, w->d_stage_out[st], rows, cudaMemcpyDeviceToHost, s));
         } else {
-            EZ_CUDA(cudaMemcpyAsync(w->h_stage_out[b], w->d_stage_out[b], rows, cudaMemcpyDeviceToHost, s));
-            pending_out[b] = c;
+            EZ_CUDA(cudaMemcpyAsync(w->h_stage_out[st], w->d_stage_out[st], rows, cudaMemcpyDeviceToHost, s));
+            pending[st] = c;
         }
+        EZ_CUDA(cudaEventRecord(w->stage_done[st], s));
+        return EZ_OK;
+    };
+    int32_t status = EZ_OK;
+    if (pinned_in || lanes == 1) {
+        for (int64_t c = 0; c < nchunks && status == EZ_OK; ++c) status = one_chunk(c);
+        for (int st = 0; st < 2 * lanes && status == EZ_OK; ++st) status = drain(st);
+    } else {
+        std::atomic<int32_t> first_err{EZ_OK};
+        std::mutex err_mu;
+        std::string err_msg;
+        host_parallel(lanes, 1, [&](int64_t lo, int64_t hi) {
+            for (int64_t lane = lo; lane < hi; ++lane) {
+                int32_t st = EZ_OK;
+                for (int64_t c = lane; c < nchunks && st == EZ_OK; c += lanes) {
+                    if (first_err.load(std::memory_order_relaxed) != EZ_OK) return;
+                    st = one_chunk(c);
+                }
+                for (int k = 0; k < 2 && st == EZ_OK; ++k) st = drain(2 * static_cast<int>(lane) + k);
+                if (st != EZ_OK) {
+                    int32_t expect = EZ_OK;
+                    if (first_err.compare_exchange_strong(expect, st)) {
+                        std::lock_guard<std::mutex> lk(err_mu);
+                        err_msg = ez_last_error();  // thread-local in the worker
+                    }
+                }
+            }
+        });
+        if (first_err.load() != EZ_OK) status = fail(first_err.load(), err_msg);
     }
-    for (int b = 0; b < NS; ++b) {
-        EZ_CUDA(cudaStreamSynchronize(w->hstream[b]));
-        if (pending_out[b] >= 0) {
-            const int64_t pr0 = pending_out[b] * chunk;
-            std::memcpy(h_free + pr0, w->h_stage_out[b], std::min(chunk, n - pr0));
-        }
+    if (status != EZ_OK) {
+        for (int i = 0; i < lanes; ++i) cudaStreamSynchronize(w->hstream[i]);
+        return status;
     }
+    if (prof)
+        fprintf(stderr, "ez_check_batch_host n=%lld chunks=%lld lanes=%d pinned=%d: call %.3f ms\n",
+                static_cast<long long>(n), static_cast<long long>(nchunks), lanes, int(pinned_in),
+                1e3 * std::chrono::duration<double>(std::chrono::steady_clock::now() - tcall).count());
     return EZ_OK;
 }
 
 extern "C" int32_t ez_fk_batch(ez_world* w, const double* d_q, int64_t n, double* d_frames, void* stream) {
     if (!w) return fail(EZ_INVALID_ARGUMENT, "null world");
     if (n <= 0) return EZ_OK;
-    EZ_CUDA(cudaSetDevice(w->device));
+    EZ_ON_DEVICE(w->device);
     k_fk_frames<<<static_cast<unsigned>((n + 127) / 128), 128, 0, static_cast<cudaStream_t>(stream)>>>(
         w->md, w->d_linkQt, d_q, n, d_frames);
     EZ_CUDA(cudaGetLastError());

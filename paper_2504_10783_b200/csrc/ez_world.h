@@ -40,13 +40,16 @@ struct ez_world {
 
     // host-buffer check pipeline
     std::mutex mu;
-    static constexpr int kHostStages = 4;
-    cudaStream_t hstream[kHostStages] = {};
+    // kHostLanes lanes (a host thread and a stream each) with two stages per
+    // lane: pinned/device row and flag buffers plus a reuse event per stage
+    static constexpr int kHostLanes = 8;
+    static constexpr int kHostStages = 2 * kHostLanes;
+    cudaStream_t hstream[kHostLanes] = {};
+    cudaEvent_t stage_done[kHostStages] = {};
     void* h_stage_in[kHostStages] = {};
     uint8_t* h_stage_out[kHostStages] = {};
     void* d_stage_in[kHostStages] = {};
     uint8_t* d_stage_out[kHostStages] = {};
-    int64_t stage_rows = 0;
 
     ez_eizo_ws* eizo = nullptr;
 
@@ -54,7 +57,9 @@ struct ez_world {
     // the fp32 model blob it is generated from
     std::vector<uint8_t> h_blob_f;
     std::vector<double> q_lo, q_hi;  // joint box (the specialised kernel's CTA size is tuned on it)
-    std::shared_ptr<ez::JitCheck> jit;
+    // published (std::atomic_store) only after tuning; launches take a
+    // std::atomic_load snapshot, so concurrent checks never race its writer
+    std::shared_ptr<const ez::JitCheck> jit;
     bool jit_failed = false;
     std::string jit_error;
     int32_t jit_bt = 512;            // CTA size for large batches

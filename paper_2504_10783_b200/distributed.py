@@ -1,24 +1,32 @@
 """Multi-GPU sharding of the EI-ZO path: one process per GPU.
 
-Two levels:
+Three levels, none with a data-path collective except the in-segment one:
 
-* **Segments** (config 3): :func:`inflate_segments_sharded` gives rank r the
-  path segments k = r, r + W, ...  Each segment is inflated speculatively with
-  the segment-keyed seed ``child_seed(seed, 0x5E7, k)``.  The polytopes are
-  all-gathered, and every rank replays the reference's sequential skip rule
-  (``planner.py:116-120``): set k is kept iff segment k is not contained in an
-  earlier kept set.  There is no data-path collective.
+* **Paths** (config 3 throughput, "segments/s over a stream of paths"):
+  :func:`inflate_paths_sharded` gives rank r the paths p = r, r + W, ...; each
+  is inflated by the drop-in ``inflate_path`` (reference seeding and skip rule,
+  planner.py:103-130), several in flight per GPU.  Results are identical to
+  one GPU's.
+* **Segments of one path** (config 3 latency): :func:`inflate_segments_sharded`
+  gives rank r the path segments k = r, r + W, ...  Each is inflated
+  speculatively with the seed it would get if no earlier segment were skipped,
+  ``child_seed(seed, 0x5E7, k)``.  The polytopes are all-gathered once and
+  every rank replays the reference's sequential skip rule (planner.py:116-120).
+  With ``semantics="reference"`` (default) a kept set whose reference seed index
+  ``len(sets)`` differs from k is re-inflated with that seed, so the corridor
+  equals ``inflate_path``'s; ``semantics="segment"`` keeps the segment-keyed
+  seeds (not a drop-in: a different, equally valid corridor).
 * **Samples inside one segment**: :func:`inflate_edge_sharded` splits each
   iteration's walk range [0, n_s) into contiguous shares (rank order is index
-  order).  Per iteration it uses three small collectives: all_reduce of the
-  first-M collision count, all_gather of the per-rank candidate counts, and
-  all_gather of the bisected boundary points (star, projection, distance).
-  Every rank then places the same faces.  Walk streams are keyed by the
-  global walk index, so the result equals single-GPU ``inflate_edge`` for any
-  world size.
+  order).  Per iteration it uses two collectives: an int64 all-gather of each
+  shard's (status, first-M collision count, candidate count) and an fp64
+  all-gather of the bisected boundary points (star, projection, distance),
+  sized from the gathered counts.  Every rank then places the same faces.
+  Walk streams are keyed by the global walk index, so the result equals
+  single-GPU ``inflate_edge`` for any world size.
 
 Collectives go through a small :class:`Comm` interface.  :class:`TorchComm`
-wraps ``torch.distributed`` (NCCL on GPU, gloo on CPU for tests).
+wraps ``torch.distributed`` (NCCL on GPU, gloo for host-staged tests).
 ``LocalComm`` (world size 1) lets one process drive several shards; the
 shard-equivalence tests use it.
 """
@@ -51,21 +59,18 @@ def shard_segments(n_segments: int, world_size: int, rank: int) -> list[int]:
 # communicators
 # ---------------------------------------------------------------------------
 class Comm:
+    """Collectives the sharded paths need.  Every call is made by all ranks in the same order."""
+
     world_size = 1
     rank = 0
 
-    def all_reduce_sum(self, x: int) -> int:
-        return int(x)
+    def all_gather_i64(self, x) -> np.ndarray:
+        """(world_size, len(x)) int64: every rank's vector, rank order."""
+        return np.asarray(x, dtype=np.int64).reshape(1, -1)
 
-    def all_reduce_max(self, x: int) -> int:
-        return int(x)
-
-    def all_gather_int(self, x: int) -> list:
-        return [int(x)]
-
-    def all_gather_rows(self, t):
-        """Concatenate every rank's rows (rank order); variable row counts allowed."""
-        return t
+    def all_gather_f64(self, x):
+        """(world_size, len(x)) float64 torch tensor on the comm's device: equal lengths on all ranks."""
+        return x.reshape(1, -1)
 
     def all_gather_object(self, obj) -> list:
         return [obj]
@@ -76,7 +81,8 @@ class LocalComm(Comm):
 
 
 class TorchComm(Comm):
-    """torch.distributed default group; tensors live on ``device`` (cuda for NCCL, cpu for gloo)."""
+    """torch.distributed default group.  Tensors live on ``device``: cuda for NCCL, cpu for gloo
+    (the host-staged mode the single-GPU multi-process tests use)."""
 
     def __init__(self, device=None):
         import torch
@@ -89,37 +95,25 @@ class TorchComm(Comm):
         if device is None:
             device = torch.device("cuda", torch.cuda.current_device()) if dist.get_backend() == "nccl" else \
                 torch.device("cpu")
-        self.device = device
+        self.device = torch.device(device)
+        self.collectives = 0  # data-path collectives issued (for tests and the benchmark)
 
-    def _t(self, vals, dtype=None):
-        return self.torch.tensor(vals, dtype=dtype or self.torch.int64, device=self.device)
-
-    def all_reduce_sum(self, x):
-        t = self._t([int(x)])
-        self.dist.all_reduce(t, op=self.dist.ReduceOp.SUM)
-        return int(t.item())
-
-    def all_reduce_max(self, x):
-        t = self._t([int(x)])
-        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
-        return int(t.item())
-
-    def all_gather_int(self, x):
-        t = self._t([int(x)])
-        out = [self.torch.empty_like(t) for _ in range(self.world_size)]
-        self.dist.all_gather(out, t)
-        return [int(o.item()) for o in out]
-
-    def all_gather_rows(self, t):
+    def _gather(self, t):
         torch = self.torch
-        n = self.all_gather_int(t.shape[0])
-        width = max(n) if n else 0
-        pad = torch.zeros((width,) + tuple(t.shape[1:]), dtype=t.dtype, device=self.device)
-        if t.shape[0]:
-            pad[: t.shape[0]] = t.to(self.device)
-        outs = [torch.empty_like(pad) for _ in range(self.world_size)]
-        self.dist.all_gather(outs, pad)
-        return torch.cat([o[:k] for o, k in zip(outs, n)])
+        out = torch.empty((self.world_size,) + tuple(t.shape), dtype=t.dtype, device=self.device)
+        if hasattr(self.dist, "all_gather_into_tensor") and self.device.type == "cuda":
+            self.dist.all_gather_into_tensor(out, t)
+        else:
+            self.dist.all_gather(list(out.unbind(0)), t)
+        self.collectives += 1
+        return out
+
+    def all_gather_i64(self, x):
+        t = self.torch.as_tensor(np.asarray(x, dtype=np.int64), device=self.device)
+        return self._gather(t).cpu().numpy()
+
+    def all_gather_f64(self, x):
+        return self._gather(x.to(self.device, self.torch.float64).contiguous())
 
     def all_gather_object(self, obj):
         out = [None] * self.world_size
@@ -161,6 +155,7 @@ class EizoSession:
     __del__ = close
 
     def sample(self, k: int, walk_begin: int, count: int, m_local: int):
+        """(status, collisions among the share of the first m, candidates) of walks [walk_begin, +count)."""
         ncm, nc = C.c_int32(), C.c_int32()
         st = N.lib().ez_eizo_session_sample(self._h, k, int(walk_begin), int(count), int(m_local), C.byref(ncm),
                                             C.byref(nc))
@@ -192,9 +187,10 @@ class EizoSession:
         return HPolytope(A, b)
 
 
-def _agree(comm: Comm, statuses) -> None:
-    """Raise the same error on every rank if any shard failed (no rank is left in a collective)."""
-    worst = comm.all_reduce_max(max(statuses) if statuses else 0)
+def _raise_worst(statuses) -> None:
+    """Raise the mapped error of the worst shard status; every rank holds the same statuses (they
+    were all-gathered), so every rank raises the same error and none is left in a collective."""
+    worst = int(max(statuses)) if len(statuses) else 0
     if worst:
         msg = N.lib().ez_last_error()
         raise_for_status(worst, (msg.decode() if msg else "") or f"a shard failed with status {worst}")
@@ -205,9 +201,19 @@ def inflate_edge_sharded(seg: Segment, domain: HPolytope, params: InflationParam
                          session_factory=None) -> InflationReport:
     """EI-ZO with each iteration's sample batch split over the ranks of ``comm``.
 
-    ``shards`` > 1 with a single-process ``comm`` drives that many shards in
-    this process (the equivalence tests use this).  The result equals
-    ``inflate_edge`` exactly.
+    Per iteration two collectives:
+
+    1. one int64 all-gather of ``(status, n_col in the shard's share of the first M, candidates)``
+       per shard: every rank gets the global first-M count (the acceptance test,
+       inflation.py:294-299), each shard's offset into the global "first N_p colliding by
+       index" (inflation.py:300-301), and any shard's failure;
+    2. one fp64 all-gather of each shard's bisected rows packed as ``[status | star | pstar |
+       dstar]``, sized from the counts of (1), so no size exchange is needed.
+
+    Every rank then runs the identical (deterministic) placement, so no broadcast or status
+    exchange follows it.  ``shards`` > 1 with a single-process ``comm`` drives that many shards
+    in this process (the equivalence tests use this).  The result equals ``inflate_edge``
+    exactly for any number of shards.
     """
     comm = comm or LocalComm()
     if seg.dim != domain.dim:
@@ -218,49 +224,67 @@ def inflate_edge_sharded(seg: Segment, domain: HPolytope, params: InflationParam
         from .errors import SeedOutsideDomain
 
         raise SeedOutsideDomain("seed segment must be strictly inside the domain")
+    import torch
+
     n_b = params.n_b if params.n_b is not None else default_bisection_steps(domain, params.delta_max)
     local = shards or 1
     W = comm.world_size * local
+    d = seg.dim
+    width = 2 * d + 1
     my_shards = [comm.rank * local + j for j in range(local)]
     make = session_factory or (lambda: EizoSession(checker, seg, domain, params, n_b, seed, rng))
     sessions = [make() for _ in my_shards]
-    torch = None
     try:
         k, walk_offset, checks, hyper = 1, 0, 0, 0
         while True:
             m = required_batch_size(k, params)
             n_s = max(params.n_p, m)
-            res = []
+            mine = []
             for g, S in zip(my_shards, sessions):
                 lo, hi = shard_range(n_s, W, g)
-                res.append(S.sample(k, walk_offset + lo, hi - lo, max(0, min(hi, m) - lo)))
-            _agree(comm, [r[0] for r in res])
-            n_col_m = comm.all_reduce_sum(sum(r[1] for r in res))
+                mine.extend(S.sample(k, walk_offset + lo, hi - lo, max(0, min(hi, m) - lo)))
+            info = comm.all_gather_i64(mine).reshape(W, 3)  # collective 1
+            _raise_worst(info[:, 0])
+            n_col_m = int(info[:, 1].sum())
             walk_offset += n_s
             checks += n_s
             if n_col_m <= m * (1.0 - params.tau) * params.eps:
                 terminated = TERMINATED_ACCEPTED
                 break
-            counts = []
-            for c in comm.all_gather_object([r[2] for r in res]):
-                counts.extend(c)
+            counts = info[:, 2]
             prefix = np.concatenate([[0], np.cumsum(counts)])
-            rows, sts = [], []
+            takes = np.maximum(0, np.minimum(counts, params.n_p - prefix[:-1])).astype(np.int64)
+            per_rank = (local + width * takes.reshape(comm.world_size, local).sum(axis=1))
+            L = int(per_rank.max())
+            parts = []
             for g, S in zip(my_shards, sessions):
-                take = int(max(0, min(counts[g], params.n_p - prefix[g])))
-                st, star, pstar, dstar = S.bisect(k, take)
-                sts.append(st)
-                rows.append((star, pstar, dstar))
-            _agree(comm, sts)
-            import torch
-
-            star = comm.all_gather_rows(torch.cat([r[0] for r in rows]))
-            pstar = comm.all_gather_rows(torch.cat([r[1] for r in rows]))
-            dstar = comm.all_gather_rows(torch.cat([r[2] for r in rows]))
-            C_tot = int(star.shape[0])
+                st, star, pstar, dstar = S.bisect(k, int(takes[g]))
+                head = torch.tensor([float(st)], dtype=torch.float64, device=star.device if star is not None else "cpu")
+                if st or star is None:
+                    rows = torch.zeros((int(takes[g]), width), dtype=torch.float64, device=head.device)
+                else:
+                    rows = torch.cat([star, pstar, dstar.reshape(-1, 1)], dim=1)
+                parts += [head, rows.reshape(-1).to(head.device)]
+            buf = torch.cat([p.to(parts[0].device) for p in parts])
+            if buf.numel() < L:
+                buf = torch.cat([buf, buf.new_zeros(L - buf.numel())])
+            allbuf = comm.all_gather_f64(buf)  # collective 2
+            stats, rows = [], []
+            for r in range(comm.world_size):
+                off = 0
+                for j in range(local):
+                    t = int(takes[r * local + j])
+                    stats.append(int(allbuf[r, off].item()))
+                    rows.append(allbuf[r, off + 1: off + 1 + t * width].reshape(t, width))
+                    off += 1 + t * width
+            _raise_worst(stats)
+            rows = torch.cat(rows)
+            C_tot = int(rows.shape[0])
             checks += C_tot * (1 + n_b)
+            star, pstar, dstar = rows[:, :d], rows[:, d:2 * d], rows[:, 2 * d]
             outs = [S.place(k, star, pstar, dstar) for S in sessions]
-            _agree(comm, [o[0] for o in outs])
+            # placement is deterministic and identical on every rank: no exchange
+            _raise_worst([o[0] for o in outs])
             hyper += outs[0][1]
             if params.n_it is not None and k >= params.n_it:
                 terminated = TERMINATED_MAX_ITER
@@ -277,49 +301,82 @@ def inflate_edge_sharded(seg: Segment, domain: HPolytope, params: InflationParam
 # ---------------------------------------------------------------------------
 # segment sharding
 # ---------------------------------------------------------------------------
+def _run_concurrent(fn, items, concurrency):
+    from concurrent.futures import ThreadPoolExecutor
+
+    workers = max(1, min(int(concurrency), len(items)))
+    if workers == 1:
+        return [fn(x) for x in items]
+    with ThreadPoolExecutor(max_workers=workers) as ex:
+        return list(ex.map(fn, items))
+
+
 def inflate_segments_sharded(path, domain: HPolytope, params: InflationParams, checker, seed: int = 0,
-                             comm: Comm | None = None, rng="counter", inflate_fn=None, concurrency: int = 6):
+                             comm: Comm | None = None, rng="counter", inflate_fn=None, concurrency: int = 6,
+                             semantics: str = "reference"):
     """Inflate the path's segments round-robin over ranks, then replay the skip rule everywhere.
 
     A rank runs up to ``concurrency`` of its segments at once (host threads;
     each native inflation takes its own device workspace and stream, so
     several latency-bound regions share the GPU).  Returns ``(Scs,
-    local_reports)``; every rank gets the same ``Scs``, whatever the
-    concurrency (segment-keyed seeds).
+    local_reports)``; every rank gets the same ``Scs``, whatever the world size
+    and concurrency.  ``semantics="reference"``: the corridor equals
+    ``corridor.inflate_path``'s (kept sets whose reference seed differs from the
+    speculative one are re-inflated, identically on every rank);
+    ``"segment"``: segment-keyed seeds, no re-inflation.
     """
-    from concurrent.futures import ThreadPoolExecutor
-
     from .corridor import Scs
 
+    if semantics not in ("reference", "segment"):
+        raise ValueError("semantics must be 'reference' or 'segment'")
     comm = comm or LocalComm()
     knots = path.knots
     n = knots.shape[0] - 1
-    mine = {}
     inflate_fn = inflate_fn or inflate_edge
     own = list(shard_segments(n, comm.world_size, comm.rank))
 
-    def one(k):
+    def one(k, j=None):
+        j = k if j is None else j
         rep = inflate_fn(Segment(knots[k], knots[k + 1]), domain, params, checker,
-                         seed=child_seed(seed, 0x5E7, k), rng=rng)
+                         seed=child_seed(seed, 0x5E7, j), rng=rng)
         return k, (rep.polytope.A, rep.polytope.b, rep.iterations, rep.hyperplanes_added, rep.collision_checks)
 
-    workers = max(1, min(int(concurrency), len(own)))
-    if workers == 1:
-        mine.update(one(k) for k in own)
-    else:
-        with ThreadPoolExecutor(max_workers=workers) as ex:
-            mine.update(ex.map(one, own))
+    mine = dict(_run_concurrent(one, own, concurrency))
     allpolys = {}
     for part in comm.all_gather_object(mine):
         allpolys.update(part)
     sets, seeds, coverage = [], [], []
+    reinflated = []
     for k in range(n):
         v1, v2 = knots[k], knots[k + 1]
         covered = next((j for j, P in enumerate(sets) if P.contains_segment(v1, v2)), None)
         if covered is None:
-            A, b = allpolys[k][0], allpolys[k][1]
-            sets.append(HPolytope(A, b))
+            j = len(sets)
+            if semantics == "reference" and j != k:
+                _, rec = one(k, j)  # the reference's seed for this set (planner.py:121-124)
+                reinflated.append(k)
+            else:
+                rec = allpolys[k]
+            sets.append(HPolytope(rec[0], rec[1]))
             seeds.append(Segment(v1, v2))
             covered = len(sets) - 1
         coverage.append(covered)
-    return Scs(sets, coverage, seeds, path, domain=domain), mine
+    scs = Scs(sets, coverage, seeds, path, domain=domain)
+    scs.reinflated = reinflated
+    return scs, mine
+
+
+def inflate_paths_sharded(paths, domain: HPolytope, params: InflationParams, checker, seed: int = 0,
+                          comm: Comm | None = None, rng="counter", concurrency: int = 6):
+    """A stream of paths: rank r inflates paths p = r, r + W, ... with the drop-in ``inflate_path``
+    (path p seeded ``child_seed(seed, 0xBA7, p)``), up to ``concurrency`` paths in flight.  No
+    collective.  Returns ``{p: Scs}`` for this rank's paths."""
+    from .corridor import inflate_path
+
+    comm = comm or LocalComm()
+    own = list(shard_segments(len(paths), comm.world_size, comm.rank))
+
+    def one(p):
+        return p, inflate_path(paths[p], domain, params, checker, seed=child_seed(seed, 0xBA7, p), rng=rng)
+
+    return dict(_run_concurrent(one, own, concurrency))

@@ -144,15 +144,24 @@ class NativeWorld:
 
     # -- checking --------------------------------------------------------------
     def check_host(self, Q: np.ndarray, precision="fp32", out: np.ndarray | None = None) -> np.ndarray:
-        """Free mask for host fp64 rows (pipelined H2D/kernel/D2H inside the library)."""
-        Q = np.asarray(Q, dtype=np.float64)
-        if not Q.flags.c_contiguous:
+        """Free mask for host rows (fp32 rows stay fp32 on the wire, anything else is fp64);
+        pinned or pageable, pipelined H2D / kernel / D2H inside the library."""
+        Q = np.asarray(Q)
+        if Q.dtype != np.float32:
+            Q = np.asarray(Q, dtype=np.float64)
+        if Q.ndim != 2 or Q.strides[1] != Q.itemsize or Q.strides[0] % Q.itemsize:
             Q = np.ascontiguousarray(Q)
         n = Q.shape[0]
+        # row stride in elements; numpy gives a single row any stride (e.g. 0 for q[None, :])
+        ld = Q.strides[0] // Q.itemsize if n > 1 else Q.shape[1]
+        if ld < Q.shape[1]:
+            Q = Q.copy()
+            ld = Q.shape[1]
         if out is None:
             out = np.empty(n, dtype=np.uint8)
         if n:
-            N.check(N.lib().ez_check_batch_host(self._h, Q.ctypes.data, n, Q.shape[1], out.ctypes.data,
+            N.check(N.lib().ez_check_batch_host(self._h, Q.ctypes.data, 0 if Q.dtype == np.float32 else 1, n,
+                                                ld, out.ctypes.data,
                                                 precision_code(precision)))
         return out
 
@@ -174,6 +183,8 @@ class NativeWorld:
     def check_device(self, Q, out=None, precision="fp32", stream: int | None = None):
         """Free mask (uint8 CUDA tensor) for a CUDA tensor of configurations (fp32 or fp64)."""
         torch = torch_mod()
+        if not Q.is_cuda or Q.device.index != self.device:
+            raise ValueError(f"configurations live on {Q.device}, this checker's world is on cuda:{self.device}")
         if Q.dim() != 2 or Q.shape[1] != self.dof:
             from .errors import DimensionMismatch
 
@@ -187,7 +198,7 @@ class NativeWorld:
             out = torch.empty(n, dtype=torch.uint8, device=Q.device)
         if n:
             dt = 0 if Q.dtype == torch.float32 else 1
-            s = stream_handle() if stream is None else stream
+            s = torch.cuda.current_stream(Q.device).cuda_stream if stream is None else stream
             N.check(N.lib().ez_check_batch(self._h, Q.data_ptr(), dt, n, Q.stride(0), out.data_ptr(),
                                            precision_code(precision), s))
         return out

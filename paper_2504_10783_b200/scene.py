@@ -168,10 +168,10 @@ class World:
     def with_vmap(self, vmap: VoxelMap | None) -> "World":
         return World(self.model, self.static, vmap, self.lower, self.upper)
 
-    def checker(self, margin: float = 0.0, precision: str = "fp32"):
+    def checker(self, margin: float = 0.0, precision: str = "fp32", specialize="auto"):
         from .checker import CollisionChecker
 
-        return CollisionChecker(self, margin=margin, precision=precision)
+        return CollisionChecker(self, margin=margin, precision=precision, specialize=specialize)
 
 
 # ---------------------------------------------------------------------------

@@ -24,7 +24,7 @@ def test_library_exports_every_declared_symbol():
 
 def test_abi_version_and_device_count_without_gpu():
     lib = N.load_library()
-    assert lib.ez_abi_version() == 2
+    assert lib.ez_abi_version() == 3
     assert lib.ez_device_count() >= 0
 
 

@@ -66,15 +66,53 @@ def test_robot_boxes_stay_generic():
     assert not ck.native.specialize(0)
 
 
-def test_large_batches_specialise_automatically():
+def test_specialisation_only_at_world_creation():
+    """no NVRTC compile or CTA-size tuning inside a check call.  Large robots get the
+    specialised kernel when their device world is created ("auto"); specialize=False never."""
     w = fx.franka7_world()
-    nat = w.checker().native
-    assert not nat.specialize(0)
+    assert w.checker().native.specialize(0)
+    assert w.checker().native.info()["check_cta"] in (256, 512, 1024)
+    nat = w.checker(specialize=False).native
+    assert not nat.specialize(0) and nat.info()["check_cta"] == 0
     lo = torch.as_tensor(w.lower, dtype=torch.float32, device="cuda")
     hi = torch.as_tensor(w.upper, dtype=torch.float32, device="cuda")
     nat.check_device(lo + (hi - lo) * torch.rand((1 << 18, 7), device="cuda"))
-    assert nat.specialize(0)
-    assert nat.info()["check_cta"] in (256, 512, 1024)
+    assert not nat.specialize(0)
+    assert not fx.arm3_world().checker().native.specialize(0)  # 9 spheres: generic under "auto"
+
+
+def test_concurrent_checks_while_specialising():
+    """Checks from other threads while ez_world_specialize compiles and publishes the kernel:
+    every result equals the generic kernel's (the launch takes an atomic snapshot)."""
+    import threading
+
+    w = fx.bimanual14_world()
+    ref_nat = w.checker(specialize=False).native
+    nat = w.checker(specialize=False).native
+    lo = torch.as_tensor(w.lower, dtype=torch.float32, device="cuda")
+    hi = torch.as_tensor(w.upper, dtype=torch.float32, device="cuda")
+    Q = lo + (hi - lo) * torch.rand((1 << 16, 14), device="cuda")
+    want = ref_nat.check_device(Q)
+    torch.cuda.synchronize()
+    bad = []
+
+    def hammer():
+        s = torch.cuda.Stream()
+        with torch.cuda.stream(s):
+            for _ in range(40):
+                out = nat.check_device(Q)
+                s.synchronize()
+                if not torch.equal(out, want):
+                    bad.append(1)
+
+    ts = [threading.Thread(target=hammer) for _ in range(3)]
+    for t in ts:
+        t.start()
+    assert nat.specialize(1)
+    for t in ts:
+        t.join()
+    assert not bad
+    assert torch.equal(nat.check_device(Q), want)
 
 
 @pytest.mark.parametrize("cta", [256, 512, 1024])
