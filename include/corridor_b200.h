@@ -250,6 +250,17 @@ int32_t ez_roadmap_destroy(ez_roadmap* roadmap);
 int32_t ez_roadmap_build(ez_world* world, const double* d_nodes, int64_t n_nodes, int32_t dim,
                          const double* h_origin, double side, const int32_t* h_extents, void* stream,
                          ez_roadmap** out);
+/* Roadmap adjacency on the GPU (replaces build_drm's edge construction,
+ * drm.py:219-248): for each node its nearest min(n, 4k+1) nodes in fp64
+ * configuration distance (cKDTree order), the first skipped, stop at the
+ * first distance > d_cs, skip end-effector distance > d_ts (d_ee:
+ * [n_nodes][ee_dim] end-effector positions), keep at most k; symmetrised and
+ * returned as CSR in d_adj_offsets[n_nodes + 1] (int64) and d_adj_ids
+ * (int32, capacity 2 * k * n_nodes, ids ascending per row), *nnz entries.
+ * Synchronises on `stream`. */
+int32_t ez_roadmap_adjacency(const double* d_nodes, int64_t n_nodes, int32_t dof, const double* d_ee,
+                             int32_t ee_dim, int32_t k, double d_cs, double d_ts, int64_t* d_adj_offsets,
+                             int32_t* d_adj_ids, int64_t* nnz, void* stream);
 int32_t ez_roadmap_info(const ez_roadmap* roadmap, int64_t* n_voxels, int64_t* n_nodes, int64_t* nnz);
 int32_t ez_roadmap_export(const ez_roadmap* roadmap, int64_t* h_offsets, int32_t* h_ids);
 int32_t ez_collision_set(ez_roadmap* roadmap, const int32_t* d_vox_idx, int64_t n_vox,

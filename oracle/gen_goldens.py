@@ -197,6 +197,7 @@ def gen_drm(C):
     base = C.world.World(C.bench.point_robot_model())
     d2 = C.drm.build_drm(base.model, base.checker(), base.lower, base.upper, 200, 10, 10.0, 10.0, grid, seed=8)
     out["f_off"], out["f_ids"] = d2.cmap_offsets, d2.cmap_ids
+    out["f_nodes"], out["f_adj_off"], out["f_adj_ids"], out["f_poses"] = d2.nodes, d2.adj_offsets, d2.adj_ids, d2.poses
     rng = np.random.default_rng(5)
     maps = []
     for case in range(20):
@@ -216,6 +217,11 @@ def gen_drm(C):
     g3 = C.drm.Grid(np.array([-0.75, -1.02, -0.36]), 0.06, (25, 34, 26))
     d3 = C.drm.build_drm(rw7.model, rw7.checker(), rw7.model.lower, rw7.model.upper, 300, 10, 10.0, 10.0, g3, seed=0)
     out["g_nodes"], out["g_off"], out["g_ids"] = d3.nodes, d3.cmap_offsets, d3.cmap_ids
+    out["g_adj_off"], out["g_adj_ids"], out["g_poses"] = d3.adj_offsets, d3.adj_ids, d3.poses
+    # a build with binding d_cs / d_ts filters (drm.py:226-229) and a small k
+    d4 = C.drm.build_drm(rw7.model, rw7.checker(), rw7.model.lower, rw7.model.upper, 400, 4, 2.5, 0.35, g3, seed=5)
+    out["h_nodes"], out["h_adj_off"], out["h_adj_ids"], out["h_poses"] = d4.nodes, d4.adj_offsets, d4.adj_ids, d4.poses
+    out["h_off"], out["h_ids"] = d4.cmap_offsets, d4.cmap_ids
     cloud = fx.cloud10k()
     pts = cloud.centers()
     vm_same = C.world.voxelize_point_cloud(pts, 0.06, g3.origin)

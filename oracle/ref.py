@@ -432,3 +432,32 @@ def node_voxel_pairs(model, nodes, grid_origin, grid_side, extents):
         cols.append(vi)
     pairs = np.unique(np.stack([np.concatenate(rows), np.concatenate(cols)], axis=1), axis=0)
     return pairs[:, 0], pairs[:, 1]
+
+
+def roadmap_adjacency(nodes, ee_pos, k, d_cs, d_ts):
+    """drm.py:219-248: k nearest-first edges under the d_cs / d_ts rules, symmetrised CSR."""
+    n = nodes.shape[0]
+    k_query = min(n, 4 * k + 1)
+    dists, idx = cKDTree(nodes).query(nodes, k=k_query)
+    rows, cols = [], []
+    for i in range(n):
+        picked = 0
+        for j_pos in range(1, k_query):
+            j = int(idx[i, j_pos])
+            if dists[i, j_pos] > d_cs:
+                break
+            if np.linalg.norm(ee_pos[i] - ee_pos[j]) > d_ts:
+                continue
+            rows.append(i)
+            cols.append(j)
+            picked += 1
+            if picked >= k:
+                break
+    rows = np.asarray(rows, dtype=np.int64)
+    cols = np.asarray(cols, dtype=np.int64)
+    und = np.unique(np.stack([np.concatenate([rows, cols]), np.concatenate([cols, rows])], axis=1), axis=0)
+    order = np.lexsort((und[:, 1], und[:, 0]))
+    r, c = und[order, 0], und[order, 1]
+    off = np.zeros(n + 1, dtype=np.int64)
+    np.cumsum(np.bincount(r, minlength=n), out=off[1:])
+    return off, c.astype(np.int32)

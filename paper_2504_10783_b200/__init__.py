@@ -15,8 +15,8 @@ from .errors import (CorridorError, DimensionMismatch, EmptyChord, GradientUndef
 from .model import (BOX, FIXED, PRISMATIC, REVOLUTE, SPHERE, Geometry, Joint, Link, RigidTransform,
                     RobotModel, fk_batch, forward_kinematics, pose_vector, rotation_about_axis)
 from .polytope import HPolytope, SampleBatch, hit_and_run_device, hit_and_run_sample
-from .roadmap import (CollisionSet, DeviceRoadmap, Drm, Grid, PwlPath, build_collision_map, collision_set, load_drm,
-                      sample_free_nodes, save_drm)
+from .roadmap import (CollisionSet, DeviceRoadmap, Drm, Grid, PwlPath, build_collision_map, build_drm, collision_set,
+                      load_drm, pose_rows, sample_free_configurations, sample_free_nodes, save_drm)
 from .rng import child_seed
 from .scene import (VoxelMap, World, load_point_cloud, load_scene, save_point_cloud, save_scene,
                     voxelize_point_cloud)

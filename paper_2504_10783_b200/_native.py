@@ -86,6 +86,8 @@ SIGNATURES = {
                                   C.POINTER(c_vp)]),
     "ez_roadmap_destroy": (c_i32, [c_vp]),
     "ez_roadmap_build": (c_i32, [c_vp, c_vp, c_i64, c_i32, P_dbl, c_dbl, P_i32, c_vp, C.POINTER(c_vp)]),
+    "ez_roadmap_adjacency": (c_i32, [c_vp, c_i64, c_i32, c_vp, c_i32, c_i32, c_dbl, c_dbl, c_vp, c_vp, P_i64,
+                                     c_vp]),
     "ez_roadmap_info": (c_i32, [c_vp, P_i64, P_i64, P_i64]),
     "ez_roadmap_export": (c_i32, [c_vp, P_i64, P_i32]),
     "ez_collision_set": (c_i32, [c_vp, c_vp, c_i64, P_dbl, c_dbl, c_i32, c_vp, P_i64, c_vp]),

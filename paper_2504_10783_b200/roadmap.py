@@ -245,6 +245,86 @@ def build_collision_map(world_or_model, nodes, grid: Grid):
     return DeviceRoadmap.build(world_or_model, nodes, grid).export()
 
 
+def sample_free_configurations(checker, lower, upper, count: int, rng, budget_factor: int = 1000) -> np.ndarray:
+    """Uniform rejection sampling of free configurations, draw for draw the reference's
+    (drm.py:147-167): the same ``rng.uniform`` chunks, each chunk checked in one
+    ``checker.check_batch`` call (one GPU launch for a GPU checker)."""
+    lower = np.asarray(lower, dtype=float)
+    upper = np.asarray(upper, dtype=float)
+    out, have, drawn = [], 0, 0
+    budget = budget_factor * count
+    while have < count:
+        chunk = min(max(count - have, 256) * 2, budget - drawn)
+        if chunk <= 0:
+            from .errors import SamplingExhausted
+
+            raise SamplingExhausted(f"rejection budget {budget} exhausted with {have}/{count} samples")
+        Q = rng.uniform(lower, upper, size=(chunk, lower.shape[0]))
+        drawn += chunk
+        good = Q[np.asarray(checker.check_batch(Q), dtype=bool)]
+        out.append(good)
+        have += good.shape[0]
+    return np.concatenate(out)[:count]
+
+
+def pose_rows(model, nodes: np.ndarray) -> np.ndarray:
+    """``pose_vector(forward_kinematics(model, q)[1])`` for every node (drm.py:217), the
+    end-effector (last link) frames from one batched GPU FK launch."""
+    from .model import fk_batch
+
+    rots, trans = fk_batch(model, nodes)
+    R, t = rots[-1], trans[-1]
+    if model.dim == 2:
+        return np.concatenate([t, np.arctan2(R[:, 1, 0], R[:, 0, 0])[:, None]], axis=1)
+    tr = R[:, 0, 0] + R[:, 1, 1] + R[:, 2, 2]
+    w = 0.5 * np.sqrt(np.maximum(0.0, 1.0 + tr))
+    with np.errstate(divide="ignore", invalid="ignore"):
+        q = np.stack([w, (R[:, 2, 1] - R[:, 1, 2]) / (4 * w), (R[:, 0, 2] - R[:, 2, 0]) / (4 * w),
+                      (R[:, 1, 0] - R[:, 0, 1]) / (4 * w)], axis=1)
+    near_pi = ~(w > 1e-9)
+    if near_pi.any():  # the reference's dominant-diagonal branch (world.py:253-262), row by row
+        from .model import RigidTransform, pose_vector
+
+        for r in np.flatnonzero(near_pi):
+            q[r] = pose_vector(RigidTransform(R[r], t[r]))[3:]
+    return np.concatenate([t, q], axis=1)
+
+
+def build_drm(model, base_checker, lower, upper, n_nodes: int, k: int, d_cs: float, d_ts: float, grid: Grid,
+              seed: int = 0) -> Drm:
+    """Drop-in for ``corridor.drm.build_drm`` (drm.py:207-255), every bulk step on the GPU.
+
+    * nodes: ``sample_free_configurations`` with ``default_rng(seed)`` (the reference's draws;
+      each rejection chunk is one check launch of ``base_checker``);
+    * poses: end-effector pose rows from one FK launch (``pose_rows``);
+    * adjacency: ``ez_roadmap_adjacency`` (nearest 4k+1 by configuration distance, d_cs / d_ts
+      filters, k per node, symmetrised CSR);
+    * collision map: ``ez_roadmap_build`` (node x voxel sweep, CSR by voxel).
+    """
+    import torch
+
+    if n_nodes < 2:
+        raise ValueError("need at least two nodes")
+    if k < 1:
+        raise ValueError("k must be >= 1")
+    rng = np.random.default_rng(seed)
+    nodes = sample_free_configurations(base_checker, lower, upper, n_nodes, rng)
+    poses = pose_rows(model, nodes)
+    dev = torch_device()
+    dn = torch.as_tensor(np.ascontiguousarray(nodes, dtype=np.float64), device=dev)
+    de = torch.as_tensor(np.ascontiguousarray(poses[:, :model.dim], dtype=np.float64), device=dev)
+    off = torch.empty(n_nodes + 1, dtype=torch.int64, device=dev)
+    ids = torch.empty(max(1, 2 * k * n_nodes), dtype=torch.int32, device=dev)
+    nnz = C.c_int64(0)
+    N.check(N.lib().ez_roadmap_adjacency(dn.data_ptr(), n_nodes, model.dof, de.data_ptr(), model.dim, int(k),
+                                         float(d_cs), float(d_ts), off.data_ptr(), ids.data_ptr(), C.byref(nnz),
+                                         stream_handle()))
+    adj_off = off.cpu().numpy()
+    adj_ids = ids[: nnz.value].cpu().numpy()
+    cmap_off, cmap_ids = DeviceRoadmap.build(model, nodes, grid).export()
+    return Drm(nodes, adj_off, adj_ids, cmap_off, cmap_ids, poses, grid, d_cs=d_cs, d_ts=d_ts)
+
+
 def sample_free_nodes(world, n: int, seed: int = 0, batch: int = 1 << 20) -> np.ndarray:
     """Uniform collision-free configurations of ``world`` (rejection sampling, GPU checks).
 

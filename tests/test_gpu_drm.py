@@ -114,3 +114,54 @@ def test_free_node_sampling():
     assert nodes.shape == (5000, 7)
     assert np.all(w.checker().check_batch(nodes))
     assert np.all(nodes >= w.lower) and np.all(nodes <= w.upper)
+
+
+@pytest.mark.parametrize("which", ["forest", "franka", "franka_filtered"])
+def test_build_drm_matches_reference(which):
+    """The drop-in build_drm (drm.py:207-255) against the reference's own builds: the same
+    nodes (same draws, GPU fp64 checks), poses to 1e-12, adjacency and collision map exact."""
+    from paper_2504_10783_b200 import fixtures as fx
+    from paper_2504_10783_b200.roadmap import build_drm
+    from paper_2504_10783_b200.scene import World
+
+    z = golden("drm.npz")
+    if which == "forest":
+        model = fx.point_robot_model()
+        world = World(model)
+        grid = Grid(np.array([-5.0, -5.0]), 0.25, (40, 40))
+        args, seed, key = (200, 10, 10.0, 10.0), 8, "f"
+    else:
+        world = fx.franka7_world(False)
+        model = world.model
+        grid = Grid(np.array([-0.75, -1.02, -0.36]), 0.06, (25, 34, 26))
+        args, seed, key = ((300, 10, 10.0, 10.0), 0, "g") if which == "franka" else ((400, 4, 2.5, 0.35), 5, "h")
+    d = build_drm(model, world.checker(precision="fp64"), model.lower, model.upper, *args, grid, seed=seed)
+    assert np.array_equal(d.nodes, z[f"{key}_nodes"])
+    assert d.poses.shape == z[f"{key}_poses"].shape
+    assert np.allclose(d.poses, z[f"{key}_poses"], atol=1e-12)
+    assert np.array_equal(d.adj_offsets, z[f"{key}_adj_off"])
+    assert np.array_equal(d.adj_ids, z[f"{key}_adj_ids"])
+    off_key, ids_key = (f"{key}_off", f"{key}_ids")
+    assert np.array_equal(d.cmap_offsets, z[off_key]) and np.array_equal(d.cmap_ids, z[ids_key])
+    # reference properties (test_drm.py:30-66): symmetric adjacency, free nodes
+    for i in range(d.n_nodes):
+        for j in d.neighbors(i):
+            assert i in set(int(v) for v in d.neighbors(int(j)))
+    assert world.checker(precision="fp64").check_batch(d.nodes).all()
+
+
+def test_build_drm_two_nodes_and_validation():
+    """test_drm.py:45-51: two nodes with k = 1 give one undirected edge; bad sizes raise."""
+    from paper_2504_10783_b200 import fixtures as fx
+    from paper_2504_10783_b200.roadmap import build_drm
+    from paper_2504_10783_b200.scene import World
+
+    base = World(fx.point_robot_model())
+    grid = Grid(np.array([-5.0, -5.0]), 0.25, (40, 40))
+    d = build_drm(base.model, base.checker(), base.lower, base.upper, 2, 1, 100.0, 100.0, grid, seed=1)
+    assert d.adj_ids.shape[0] == 2
+    assert set(d.neighbors(0)) == {1} and set(d.neighbors(1)) == {0}
+    with pytest.raises(ValueError):
+        build_drm(base.model, base.checker(), base.lower, base.upper, 1, 1, 1.0, 1.0, grid)
+    with pytest.raises(ValueError):
+        build_drm(base.model, base.checker(), base.lower, base.upper, 10, 0, 1.0, 1.0, grid)

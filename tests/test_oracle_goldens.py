@@ -170,3 +170,11 @@ def test_oracle_region7_segment_and_counters():
     A, b = z["A"], z["b"]
     assert A.shape[0] == 14 + int(z["hyperplanes_added"])
     assert np.all(A @ v1 <= b + 1e-9) and np.all(A @ v2 <= b + 1e-9)
+
+
+@pytest.mark.parametrize("key,k,d_cs,d_ts", [("f", 10, 10.0, 10.0), ("g", 10, 10.0, 10.0), ("h", 4, 2.5, 0.35)])
+def test_oracle_roadmap_adjacency_matches_reference(key, k, d_cs, d_ts):
+    z = golden("drm.npz")
+    dim = 2 if key == "f" else 3
+    off, ids = ref.roadmap_adjacency(z[f"{key}_nodes"], z[f"{key}_poses"][:, :dim], k, d_cs, d_ts)
+    assert np.array_equal(off, z[f"{key}_adj_off"]) and np.array_equal(ids, z[f"{key}_adj_ids"])
