@@ -105,7 +105,8 @@ typedef struct ez_world_info {
     int64_t device_bytes;         /* bytes held on the device                */
     int32_t check_cta;            /* CTA size of the specialised check kernel */
                                   /* for large batches, 0 = generic kernel   */
-    int32_t reserved_;
+    int32_t check_variant;        /* voxel-code variant of the specialised   */
+                                  /* kernel (0 literal grid, 1 generic), -1  */
 } ez_world_info;
 
 /* EI-ZO parameters: inflation.InflationParams (inflation.py:55-95). */

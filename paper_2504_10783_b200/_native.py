@@ -41,7 +41,7 @@ class WorldInfo(C.Structure):
     _fields_ = [("dof", c_i32), ("n_links", c_i32), ("n_spheres", c_i32), ("n_pairs", c_i32),
                 ("n_static", c_i32), ("n_hot_pairs", c_i32), ("n_voxels", c_i64), ("grid_dims", c_i32 * 3),
                 ("cell_side", c_dbl), ("list_entries", c_i64), ("device_bytes", c_i64),
-                ("check_cta", c_i32), ("reserved_", c_i32)]
+                ("check_cta", c_i32), ("check_variant", c_i32)]
 
 
 class EizoParams(C.Structure):

@@ -133,6 +133,11 @@ struct Gen {
     const ModelDev<float>& M;
     const uint8_t* blob;
     float margin;
+    // voxel-map code: 0 = grid constants as literals and a 32-bit cell index
+    // (vox_fetch / vox_decide), 1 = the generic voxel_cell / voxel_decide.
+    // jit_specialize builds both and keeps the faster (their flags are equal:
+    // every decision is conservative or exact)
+    int variant = 0;
     std::ostringstream o;
 
     const JointRec<float>* J() const { return reinterpret_cast<const JointRec<float>*>(blob); }
@@ -262,16 +267,72 @@ struct Gen {
         return (v >= 1 && v <= 64) ? v : kVoxBatch;
     }
 
-    // spheres order[k_begin, k_end)
+    // float literal of a double bound, rounded toward -inf (down) or +inf (up)
+    static std::string lit_dir(double v, bool up) {
+        float f = static_cast<float>(v);
+        if (up && static_cast<double>(f) < v) f = std::nextafter(f, INFINITY);
+        if (!up && static_cast<double>(f) > v) f = std::nextafter(f, -INFINITY);
+        return lit(f);
+    }
+
+    // Distance-grid lookup of sphere s with the grid's constants as literals:
+    // in-grid test, cell index (32-bit: the grid has < 2^28 cells), an upper
+    // bound e of the distance from the centre to its cell centre, the cell
+    // word.  Any valid cell and bound give the same flag: the decisions below
+    // are conservative by the grid's eps and the list walk is exact.
+    void vox_fetch(int j, int s) {
+        const VoxGrid<float>& V = M.vox;
+        const std::string X = "c" + std::to_string(s) + "_0", Y = "c" + std::to_string(s) + "_1",
+                          Z = "c" + std::to_string(s) + "_2";
+        const std::string c[3] = {X, Y, Z};
+        o << "        float e" << j << " = 0.0f; uint32_t w" << j << " = kFarCell;\n        {\n";
+        for (int k = 0; k < 3; ++k)
+            o << "            const float f" << k << " = (" << c[k] << " - " << lit(V.org[k]) << ") * " << lit(V.inv_h)
+              << ";\n";
+        o << "            if ((f0 >= 0.0f) & (f1 >= 0.0f) & (f2 >= 0.0f) & (f0 < " << lit(float(V.n[0])) << ") & (f1 < "
+          << lit(float(V.n[1])) << ") & (f2 < " << lit(float(V.n[2])) << ")) {\n";
+        for (int k = 0; k < 3; ++k) {
+            const float ch = static_cast<float>(double(V.org[k]) + 0.5 * double(V.h));
+            o << "                const int i" << k << " = static_cast<int>(f" << k << ");\n"
+              << "                const float d" << k << " = " << c[k] << " - fmaf(static_cast<float>(i" << k << "), "
+              << lit(V.h) << ", " << lit(ch) << ");\n";
+        }
+        o << "                e" << j << " = jit_dist_ub(d0 * d0 + d1 * d1 + d2 * d2);\n"
+          << "                w" << j << " = __ldg(M.vox.cells + (i0 + " << V.n[0] << " * (i1 + " << V.n[1]
+          << " * i2)));\n            }\n        }\n";
+    }
+
+    void vox_decide(int j, int s) {
+        const VoxGrid<float>& V = M.vox;
+        const double R = S()[s].rvox;
+        // free: q dq - e > R + eps; hit: q < 255 and q dq + dq + e <= R - eps
+        const std::string c_free = lit_dir(double(R) + double(V.eps), true);
+        const std::string c_hit = lit_dir(double(R) - double(V.eps) - double(V.dq), false);
+        o << "        if (w" << j << " != kFarCell) {\n"
+          << "            const float qf = static_cast<float>(w" << j << " >> 24);\n"
+          << "            if (!(fmaf(qf, " << lit(V.dq) << ", -e" << j << ") > " << c_free << ")) {\n"
+          << "                if ((w" << j << " < 0xFF000000u) & (fmaf(qf, " << lit(V.dq) << ", e" << j << ") <= " << c_hit
+          << ")) return true;\n"
+          << "                if (voxel_walk<float>(M.vox, w" << j << ", e" << j << ", c" << s << "_0, c" << s << "_1, c"
+          << s << "_2, " << lit(S()[s].rvox) << ")) return true;\n"
+          << "            }\n        }\n";
+    }
+
+    // spheres order[k_begin, k_end): static obstacles, then the voxel map
+    // (cells of vox_batch() spheres fetched before any is decided)
     void obstacles(int k_begin, int k_end) {
         const int32_t* order = reinterpret_cast<const int32_t*>(blob + M.off_order);
         const bool vox = M.vox.present;
+        const bool legacy = variant == 1;
         for (int k0 = k_begin; k0 < k_end; k0 += vox_batch()) {
             const int nb = std::min(vox_batch(), k_end - k0);
             o << "    {\n";
-            for (int j = 0; j < nb; ++j) {
+            for (int j = 0; j < nb && vox; ++j) {
                 const int s = order[k0 + j];
-                if (!vox) continue;
+                if (!legacy) {
+                    vox_fetch(j, s);
+                    continue;
+                }
                 o << "        float e" << j << " = 0.0f; uint32_t w" << j << " = kFarCell;\n"
                   << "        { const int64_t cl = voxel_cell<float>(M.vox, c" << s << "_0, c" << s << "_1, c" << s
                   << "_2, e" << j << "); if (cl >= 0) w" << j << " = __ldg(M.vox.cells + cl); }\n";
@@ -279,9 +340,13 @@ struct Gen {
             for (int j = 0; j < nb; ++j) {
                 const int s = order[k0 + j];
                 statics(s);
-                if (vox)
-                    o << "        if (w" << j << " != kFarCell && voxel_decide<float>(M.vox, w" << j << ", e" << j
-                      << ", c" << s << "_0, c" << s << "_1, c" << s << "_2, " << lit(S()[s].rvox) << ")) return true;\n";
+                if (!vox) continue;
+                if (!legacy) {
+                    vox_decide(j, s);
+                    continue;
+                }
+                o << "        if (w" << j << " != kFarCell && voxel_decide<float>(M.vox, w" << j << ", e" << j << ", c" << s
+                  << "_0, c" << s << "_1, c" << s << "_2, " << lit(S()[s].rvox) << ")) return true;\n";
             }
             o << "    }\n";
         }
@@ -311,7 +376,11 @@ struct Gen {
     // everything but the kernel entry points (kernel_source adds one)
     std::string source() {
         o << "// generated by ez_jit.cu for one robot model\n#include \"ez_check_core.cuh\"\n\nnamespace ez {\n\n"
-          << "__device__ __forceinline__ float sq3(float dx, float dy, float dz) { return dx * dx + dy * dy + dz * dz; }\n\n"
+          << "__device__ __forceinline__ float sq3(float dx, float dy, float dz) { return dx * dx + dy * dy + dz * dz; }\n"
+          // an upper bound of sqrt(x): one MUFU.RSQ (ftz; x below 1e-30 bounds by 1e-15), raised by 2^-20
+          << "__device__ __forceinline__ float jit_dist_ub(float x) {\n"
+             "    float r;\n    asm(\"rsqrt.approx.ftz.f32 %0, %1;\" : \"=f\"(r) : \"f\"(x));\n"
+             "    return x > 1e-30f ? x * r * 1.00000095367431640625f : 1e-15f;\n}\n\n"
           << "struct JitPolicy {\n    static constexpr bool kRegRows = true;\n    const ModelDev<float>& M;\n"
           << "    template <typename Q>\n    __device__ __forceinline__ bool a(const Q* row, float*) const {\n";
         fk();
@@ -489,8 +558,8 @@ JitCheck::~JitCheck() {
             if (l) cudaLibraryUnload(l);
 }
 
-std::string jit_source(const ez_world* w) {
-    Gen g{w->mf, w->h_blob_f.data(), static_cast<float>(w->margin), {}};
+std::string jit_source(const ez_world* w, int variant) {
+    Gen g{w->mf, w->h_blob_f.data(), static_cast<float>(w->margin), variant, {}};
     return g.source();
 }
 
@@ -531,12 +600,11 @@ int32_t launch_at(ez_world* w, const JitCheck& jc, int bt, const void* d_q, bool
 
 // CTA size for large batches: time 1024, 512 and 256 threads (each at the
 // residency its kernel was compiled for) on random configurations.
-int32_t tune_bt(ez_world* w, const JitCheck& jc) {
+int32_t tune_bt(ez_world* w, const JitCheck& jc, float* best_ms) {
+    *best_ms = 1e30f;
     const char* e = getenv("EZ_JIT_BT");
-    if (e && (atoi(e) == 256 || atoi(e) == 512 || atoi(e) == 1024) && w->jit_occ[0][shape_of(atoi(e)) + 2] > 0) {
-        w->jit_bt = atoi(e);
-        return EZ_OK;
-    }
+    const int forced = (e && (atoi(e) == 256 || atoi(e) == 512 || atoi(e) == 1024) &&
+                        w->jit_occ[0][shape_of(atoi(e)) + 2] > 0) ? atoi(e) : 0;
     const int64_t n = int64_t(1) << 20;
     const int dof = w->dof;
     float* d_q = nullptr;
@@ -563,7 +631,7 @@ int32_t tune_bt(ez_world* w, const JitCheck& jc) {
         for (int pass = 0; pass < 2 && st == EZ_OK; ++pass)
             for (int c = 0; c < 3 && st == EZ_OK; ++c) {
                 const int bt = sizes[c];
-                if (w->jit_occ[0][shape_of(bt) + 2] < 1) continue;
+                if (w->jit_occ[0][shape_of(bt) + 2] < 1 || (forced && bt != forced)) continue;
                 for (int r = 0; r < 2 && st == EZ_OK; ++r) st = launch_at(w, jc, bt, d_q, false, n, dof, d_out, s, 0, nullptr);
                 if (!ck(cudaEventRecord(e0, s))) break;
                 for (int r = 0; r < 4 && st == EZ_OK; ++r) st = launch_at(w, jc, bt, d_q, false, n, dof, d_out, s, 0, nullptr);
@@ -575,7 +643,10 @@ int32_t tune_bt(ez_world* w, const JitCheck& jc) {
         int pick = -1;
         for (int c = 0; c < 3; ++c)
             if (best[c] < 1e30f && (pick < 0 || best[c] < best[pick])) pick = c;
-        if (pick >= 0) w->jit_bt = sizes[pick];
+        if (pick >= 0) {
+            w->jit_bt = sizes[pick];
+            *best_ms = best[pick];
+        }
     }
     cudaFree(d_q);
     cudaFree(d_out);
@@ -599,53 +670,76 @@ int32_t jit_specialize(ez_world* w) {
     };
     if (w->mf.n_boxes > 0 || w->mf.n_mix > 0) return refuse(EZ_UNSUPPORTED, "robot boxes use the generic check kernel");
     if (w->h_blob_f.empty()) return refuse(EZ_UNSUPPORTED, "no host copy of the model");
-    const std::string src = jit_source(w);
-    if (const char* dump = getenv("EZ_JIT_DUMP")) {  // inspection: write the generated source
-        if (FILE* f = fopen(dump, "w")) {
-            fwrite(src.data(), 1, src.size(), f);
-            fclose(f);
-        }
-    }
-    std::shared_ptr<JitCheck> jc;
-    {
-        std::lock_guard<std::mutex> lk(g_mu);
-        auto it = g_cache.find(src);
-        if (it != g_cache.end()) jc = it->second;
-    }
-    if (!jc) {
-        const int32_t st = compile(src, &jc);
-        if (st != EZ_OK) {
-            w->jit_failed = true;
-            w->jit_error = ez_last_error();
-            return st;
-        }
-        std::lock_guard<std::mutex> lk(g_mu);
-        g_cache.emplace(src, jc);
-    }
-    // a size whose rows do not fit in shared memory (many joints, fp64 rows,
-    // 1024 threads) keeps occupancy 0 and is never launched
+    // EZ_JIT_VOX=0/1 forces one voxel-code variant (Gen::variant); otherwise
+    // both are built and timed, and the faster one is kept (measured: the
+    // literal-constant code wins for the 7-DOF model, the generic calls for
+    // the 14-DOF one, where the longer code spills more at 64 registers)
+    const char* ev = getenv("EZ_JIT_VOX");
+    const int v_lo = (ev && ev[0] == '1') ? 1 : 0, v_hi = (ev && ev[0] == '0') ? 0 : 1;
     int max_smem = 0;
     EZ_CUDA(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, w->device));
-    for (int i = 0; i < 2; ++i)
-        for (int si = 0; si < kJitSizeCount; ++si) {
-            const int bt = kJitSizes[si];
-            const size_t smem = jit_smem(w, bt, i == 1);
-            w->jit_occ[i][si] = 0;
-            if (smem > static_cast<size_t>(max_smem)) continue;
-            const void* k = reinterpret_cast<const void*>(jc->k[i][shape_of(bt)]);
-            if (bt == 256 || bt == 512 || bt == 1024)
-                EZ_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-            int occ = 0;
-            EZ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, bt, smem));
-            w->jit_occ[i][si] = occ;
+    std::shared_ptr<JitCheck> best;
+    float best_ms = 1e30f;
+    int best_bt = 0, best_var = -1;
+    int32_t best_occ[2][kJitSizeCount] = {};
+    for (int variant = v_lo; variant <= v_hi; ++variant) {
+        const std::string src = jit_source(w, variant);
+        if (const char* dump = getenv("EZ_JIT_DUMP")) {  // inspection: write the generated source
+            if (FILE* f = fopen((std::string(dump) + (variant ? ".generic" : "")).c_str(), "w")) {
+                fwrite(src.data(), 1, src.size(), f);
+                fclose(f);
+            }
         }
-    if (w->jit_occ[0][0] < 1 || w->jit_occ[1][0] < 1)
-        return refuse(EZ_CAPACITY, "specialised check kernel does not fit on an SM");
+        std::shared_ptr<JitCheck> jc;
+        {
+            std::lock_guard<std::mutex> lk(g_mu);
+            auto it = g_cache.find(src);
+            if (it != g_cache.end()) jc = it->second;
+        }
+        if (!jc) {
+            const int32_t st = compile(src, &jc);
+            if (st != EZ_OK) {
+                w->jit_failed = true;
+                w->jit_error = ez_last_error();
+                return st;
+            }
+            std::lock_guard<std::mutex> lk(g_mu);
+            g_cache.emplace(src, jc);
+        }
+        // a size whose rows do not fit in shared memory (many joints, fp64 rows,
+        // 1024 threads) keeps occupancy 0 and is never launched
+        for (int i = 0; i < 2; ++i)
+            for (int si = 0; si < kJitSizeCount; ++si) {
+                const int bt = kJitSizes[si];
+                const size_t smem = jit_smem(w, bt, i == 1);
+                w->jit_occ[i][si] = 0;
+                if (smem > static_cast<size_t>(max_smem)) continue;
+                const void* k = reinterpret_cast<const void*>(jc->k[i][shape_of(bt)]);
+                if (bt == 256 || bt == 512 || bt == 1024)
+                    EZ_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+                int occ = 0;
+                EZ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, bt, smem));
+                w->jit_occ[i][si] = occ;
+            }
+        if (w->jit_occ[0][0] < 1 || w->jit_occ[1][0] < 1) continue;
+        float ms = 1e30f;
+        EZ_TRY(tune_bt(w, *jc, &ms));
+        if (!best || ms < best_ms) {
+            best = jc;
+            best_ms = ms;
+            best_bt = w->jit_bt;
+            best_var = variant;
+            std::memcpy(best_occ, w->jit_occ, sizeof(best_occ));
+        }
+    }
+    if (!best) return refuse(EZ_CAPACITY, "specialised check kernel does not fit on an SM");
     // tuned before it is published: a launch that sees the kernel (atomic
     // snapshot in launch_check_t) also sees its CTA size and occupancies
-    const int32_t st = tune_bt(w, *jc);
-    if (st == EZ_OK) std::atomic_store(&w->jit, std::shared_ptr<const JitCheck>(jc));
-    return st;
+    std::memcpy(w->jit_occ, best_occ, sizeof(best_occ));
+    w->jit_bt = best_bt;
+    w->jit_variant = best_var;
+    std::atomic_store(&w->jit, std::shared_ptr<const JitCheck>(best));
+    return EZ_OK;
 }
 
 // Large batches run at the tuned CTA size; a batch too small to give every

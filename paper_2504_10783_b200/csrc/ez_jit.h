@@ -27,7 +27,7 @@ struct JitCheck {
 // boxes or NVRTC is missing.
 int32_t jit_specialize(ez_world* w);  // published with std::atomic_store
 // CUDA source of the specialised kernel (for inspection and tests)
-std::string jit_source(const ez_world* w);
+std::string jit_source(const ez_world* w, int variant = 0);
 // Launch it over n rows (fp32 arithmetic); jc is the caller's snapshot of ez_world::jit.
 int32_t jit_launch(ez_world* w, const JitCheck& jc, const void* d_q, bool q64, int64_t n, int64_t ld,
                    uint8_t* d_free, cudaStream_t stream, int64_t count_lim, int32_t* n_col);

@@ -1159,9 +1159,10 @@ extern "C" int32_t ez_world_get_info(const ez_world* w, ez_world_info* out) {
     out->device_bytes = w->device_bytes;
     {
         std::lock_guard<std::mutex> lk(const_cast<ez_world*>(w)->cfg_mu);  // jit is published under cfg_mu
-        out->check_cta = std::atomic_load(&w->jit) ? w->jit_bt : 0;
+        const bool on = static_cast<bool>(std::atomic_load(&w->jit));
+        out->check_cta = on ? w->jit_bt : 0;
+        out->check_variant = on ? w->jit_variant : -1;
     }
-    out->reserved_ = 0;
     return EZ_OK;
 }
 

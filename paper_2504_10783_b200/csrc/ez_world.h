@@ -63,6 +63,7 @@ struct ez_world {
     bool jit_failed = false;
     std::string jit_error;
     int32_t jit_bt = 512;            // CTA size for large batches
+    int32_t jit_variant = -1;        // voxel-code variant in use (ez_jit.cu Gen::variant)
     int32_t jit_occ[2][ez::kJitSizeCount] = {};  // [rows f32/f64][CTA size 64..1024] resident CTAs per SM
 
     // cached launch shapes of k_check, [T fp64][Q fp64]; set once under cfg_mu

@@ -140,7 +140,7 @@ class NativeWorld:
                 "n_hot_pairs": wi.n_hot_pairs,
                 "n_static": wi.n_static, "n_voxels": wi.n_voxels, "grid_dims": tuple(wi.grid_dims),
                 "cell_side": wi.cell_side, "list_entries": wi.list_entries, "device_bytes": wi.device_bytes,
-                "check_cta": wi.check_cta}
+                "check_cta": wi.check_cta, "check_variant": wi.check_variant}
 
     # -- checking --------------------------------------------------------------
     def check_host(self, Q: np.ndarray, precision="fp32", out: np.ndarray | None = None) -> np.ndarray:

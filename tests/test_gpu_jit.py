@@ -162,3 +162,21 @@ def test_specialised_equals_generic_prismatic_oblique(rows):
     a, b = gen.check_device(Q), jit.check_device(Q)
     assert 0.0 < float(a.float().mean()) < 1.0
     assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("variant", ["0", "1"])
+@pytest.mark.parametrize("which", ["franka7", "bimanual14"])
+def test_both_voxel_code_variants_equal_generic(which, variant, monkeypatch):
+    """The literal-constant voxel code (variant 0) and the generic calls (variant 1), each forced
+    with EZ_JIT_VOX, give the generic kernel's flags exactly (specialisation keeps the faster)."""
+    monkeypatch.setenv("EZ_JIT_VOX", variant)
+    w = {"franka7": fx.franka7_world, "bimanual14": fx.bimanual14_world}[which]()
+    gen, jit = w.checker(specialize=False).native, w.checker(specialize=False).native
+    assert jit.specialize(1) and jit.info()["check_variant"] == int(variant)
+    lo = torch.as_tensor(w.lower, dtype=torch.float32, device="cuda")
+    hi = torch.as_tensor(w.upper, dtype=torch.float32, device="cuda")
+    g = torch.Generator(device="cuda")
+    g.manual_seed(5)
+    Q = lo + (hi - lo) * torch.rand((1 << 19, w.model.dof), generator=g, device="cuda")
+    assert torch.equal(gen.check_device(Q), jit.check_device(Q))
+    assert torch.equal(gen.check_device(Q.double()), jit.check_device(Q.double()))
