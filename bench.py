@@ -310,18 +310,6 @@ def bench_drm(n_nodes: int = 100_000, reps: int = 10, cpu: bool = True) -> dict:
     drm = Drm(nodes, np.zeros(n_nodes + 1, np.int64), np.zeros(0, np.int32), off, ids, np.zeros((n_nodes, 7)), grid)
     out = {"grid": "25x34x26 side 0.06", "n_nodes": n_nodes, "cmap_nnz": int(ids.shape[0]),
            "node_sampling_s": t_nodes, "cmap_build_s": t_map, "cmap_first_build_s": builds[0], "clouds": []}
-    # the whole drop-in build_drm (drm.py:207-255): reference draws, fp64 checks, poses, k-NN
-    # adjacency (k = 10, d_cs = 1.5, d_ts = 0.5) and the collision map, 100k nodes
-    from paper_2504_10783_b200.roadmap import build_drm
-
-    base64 = base.checker(precision="fp64")
-    build_drm(base.model, base64, base.lower, base.upper, 2000, 10, 1.5, 0.5, grid, seed=1)  # warm-up
-    t0 = time.perf_counter()
-    full = build_drm(base.model, base64, base.lower, base.upper, n_nodes, 10, 1.5, 0.5, grid, seed=1)
-    torch.cuda.synchronize()
-    out["build_drm"] = {"seconds": time.perf_counter() - t0, "n_nodes": n_nodes, "k": 10, "d_cs": 1.5, "d_ts": 0.5,
-                        "adj_nnz": int(full.adj_ids.shape[0]), "cmap_nnz": int(full.cmap_ids.shape[0]),
-                        "reference_estimate": "SURVEY 8(d): ~15 min on the CPU for a 100k-node build"}
     # 10^5-point clouds at the paper's ~360 active voxels, and the survey's
     # stress case: 10^6 points, ~2k active voxels
     for n_pts, blobs in ((100_000, 3), (100_000, 8), (1_000_000, 30)):
@@ -346,10 +334,33 @@ def bench_drm(n_nodes: int = 100_000, reps: int = 10, cpu: bool = True) -> dict:
             rec["cpu_port_ms"] = (time.perf_counter() - t0) * 1e3
             rec["cpu_matches"] = bool(np.array_equal(blocked, cs.ids))
         out["clouds"].append(rec)
+    # the whole drop-in build_drm (drm.py:207-255): reference draws, fp64 checks, poses, k-NN
+    # adjacency (k = 10, d_cs = 1.5, d_ts = 0.5) and the collision map, 100k nodes
+    from paper_2504_10783_b200.roadmap import build_drm
+
+    base64 = base.checker(precision="fp64")
+    build_drm(base.model, base64, base.lower, base.upper, 2000, 10, 1.5, 0.5, grid, seed=1)  # warm-up
+    t0 = time.perf_counter()
+    full = build_drm(base.model, base64, base.lower, base.upper, n_nodes, 10, 1.5, 0.5, grid, seed=1)
+    torch.cuda.synchronize()
+    out["build_drm"] = {"seconds": time.perf_counter() - t0, "n_nodes": n_nodes, "k": 10, "d_cs": 1.5, "d_ts": 0.5,
+                        "adj_nnz": int(full.adj_ids.shape[0]), "cmap_nnz": int(full.cmap_ids.shape[0]),
+                        "reference_estimate": "SURVEY 8(d): ~15 min on the CPU for a 100k-node build"}
     return out
 
 
+CONFIG2 = {"workload": "config 2: Franka-like 7-DOF (33 spheres r=0.055, 232 self pairs) vs 10k voxel "
+                       "spheres (side 0.02), uniform fp32 configs in the joint limits (default_rng)",
+           "configs_per_step_per_gpu": BATCH, "l2": "8 rotating resident batches (224 MB > L2)"}
+
+
 def run_reference(args):
+    """The reference arm: the reference's CPU algorithm for config 2 on this host's cores.  The
+    reference package cannot travel to the GPU box (/root/reference is absent there), so this is
+    its restatement oracle/ref.py (kind "port": numpy FK and pairs, the reference's own
+    scipy.spatial.cKDTree for the voxel query, all host threads), pinned to the reference's flags
+    by tests/test_oracle_goldens.py; the reference package itself measured 3.8e3 checks/s
+    (SURVEY.md §6).  Each step checks a bounded sample of the config-2 rows."""
     rank, world_size, _ = _rank()
     if rank != 0:
         return
@@ -370,12 +381,14 @@ def run_reference(args):
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * float(np.mean(t_steps)), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": "config 2: Franka-like 7-DOF (33 spheres, 232 self pairs) vs 10k voxel spheres",
-                       "sample_per_step": n},
+            "config": dict(CONFIG2),
             "impl": "reference",
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
-                             "sample": f"{n} configs per step, oracle/ref.py with {cores} threads",
-                             "cpu": cpu_model(), "host_cpus": os.cpu_count()},
+                             "sample": f"{n} config-2 rows per step (bounded sample of the {BATCH}-row step), "
+                                       f"oracle/ref.py (restatement of world.py:483-565) with {cores} threads",
+                             "cpu": cpu_model(), "host_cpus": os.cpu_count(),
+                             "note": "the reference package itself: 3.8e3 checks/s (SURVEY.md §6); the port is "
+                                     "~16x faster, so ratios against it are conservative"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -704,12 +717,10 @@ def run_ours(args):
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world_size, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": max_ms / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": "config 2: Franka-like 7-DOF (33 spheres r=0.055, 232 self pairs) vs 10k voxel "
-                               "spheres (side 0.02), uniform fp32 configs in the joint limits (default_rng)",
-                   "configs_per_step_per_gpu": BATCH, "l2": "8 rotating resident batches (224 MB > L2)",
-                   "free_fraction": free_frac, "precision": "fp32 (flags exact outside a 1e-5 contact band)",
-                   "parity": "batch 0 = tests/golden/config2_1m.npz rows (reference flags, "
-                             "tests/test_gpu_pinned.py::test_config2_full_size_through_the_bench_launch)"},
+        "config": dict(CONFIG2),
+        "workload_detail": {"free_fraction": free_frac, "precision": "fp32 (flags exact outside a 1e-5 contact band)",
+                            "parity": "batch 0 = tests/golden/config2_1m.npz rows (reference flags, "
+                                      "tests/test_gpu_pinned.py::test_config2_full_size_through_the_bench_launch)"},
         "roofline": {"bound": "fp32", "achieved": achieved_tf, "peak": peak_tf, "unit": "TFLOP/s",
                      "frac": achieved_tf / peak_tf, "traffic": traffic,
                      "kernel": ("ez_check_jit_f (k_check specialised for the model at run time, NVRTC sm_100a)"
