@@ -20,10 +20,12 @@
 #include <sys/stat.h>
 #include <unistd.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <map>
 #include <memory>
 #include <mutex>
@@ -134,9 +136,10 @@ struct Gen {
     const uint8_t* blob;
     float margin;
     // voxel-map code: 0 = grid constants as literals and a 32-bit cell index
-    // (vox_fetch / vox_decide), 1 = the generic voxel_cell / voxel_decide.
-    // jit_specialize builds both and keeps the faster (their flags are equal:
-    // every decision is conservative or exact)
+    // (vox_fetch / vox_decide), 1 = the generic voxel_cell / voxel_decide,
+    // 2 = variant 0's lookups streamed with the FK (phase B below).
+    // jit_specialize builds them all and keeps the fastest (their flags are
+    // equal: every decision is conservative or exact)
     int variant = 0;
     std::ostringstream o;
 
@@ -154,7 +157,8 @@ struct Gen {
     }
 
     // joint chain: frame of link j in R{j}_k / t{j}_k, sphere s in c{s}_k
-    void fk() {
+    // after_link(j), if set, is emitted right after link j's sphere centres
+    void fk(const std::function<void(int)>& after_link = nullptr) {
         for (int j = 0; j < M.n_joints; ++j) {
             const JointRec<float>& jr = J()[j];
             float jR[9], jt[3];
@@ -221,6 +225,7 @@ struct Gen {
                       << ");\n";
                 }
             }
+            if (after_link) after_link(j);
         }
     }
 
@@ -388,8 +393,39 @@ struct Gen {
         obstacles(0, a_obst());
         o << "    return false;\n    }\n"
           << "    template <typename Q>\n    __device__ __forceinline__ bool b(const Q* row, float*) const {\n";
-        fk();
-        obstacles(a_obst(), M.n_spheres);
+        if (variant == 2 && M.vox.present && a_obst() == 0) {
+            // variant 2: the obstacle tests stream with the kinematics (a link's
+            // spheres are tested as soon as its frame exists, in link order, and
+            // their centres die there); the pair blocks then recompute the FK
+            // with every centre live.  Trades one FK for fewer live registers
+            // during the grid lookups.
+            const int32_t* order = reinterpret_cast<const int32_t*>(blob + M.off_order);
+            std::vector<int> rank(M.n_spheres);
+            for (int k = 0; k < M.n_spheres; ++k) rank[order[k]] = k;
+            o << "    {\n";
+            fk([&](int j) {
+                const JointRec<float>& jr = J()[j];
+                std::vector<int> sph;
+                for (int t = jr.sph_begin; t < jr.sph_end; ++t) sph.push_back(t);
+                // within a link, the calibrated (most-hit-first) order
+                std::sort(sph.begin(), sph.end(), [&](int x, int y) { return rank[x] < rank[y]; });
+                for (size_t k0 = 0; k0 < sph.size(); k0 += vox_batch()) {
+                    const size_t nb = std::min<size_t>(vox_batch(), sph.size() - k0);
+                    o << "    {\n";
+                    for (size_t u = 0; u < nb; ++u) vox_fetch(static_cast<int>(u), sph[k0 + u]);
+                    for (size_t u = 0; u < nb; ++u) {
+                        statics(sph[k0 + u]);
+                        vox_decide(static_cast<int>(u), sph[k0 + u]);
+                    }
+                    o << "    }\n";
+                }
+            });
+            o << "    }\n";
+            fk();
+        } else {
+            fk();
+            obstacles(a_obst(), M.n_spheres);
+        }
         blocks();
         o << "    return false;\n    }\n};\n\n";
         // dynamic shared memory = rows, then the survivor ring of 2 * bt entries
@@ -675,7 +711,8 @@ int32_t jit_specialize(ez_world* w) {
     // literal-constant code wins for the 7-DOF model, the generic calls for
     // the 14-DOF one, where the longer code spills more at 64 registers)
     const char* ev = getenv("EZ_JIT_VOX");
-    const int v_lo = (ev && ev[0] == '1') ? 1 : 0, v_hi = (ev && ev[0] == '0') ? 0 : 1;
+    const int forced = (ev && ev[0] >= '0' && ev[0] <= '2') ? ev[0] - '0' : -1;
+    const int v_lo = forced >= 0 ? forced : 0, v_hi = forced >= 0 ? forced : (w->mf.vox.present ? 2 : 0);
     int max_smem = 0;
     EZ_CUDA(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, w->device));
     std::shared_ptr<JitCheck> best;
@@ -685,7 +722,7 @@ int32_t jit_specialize(ez_world* w) {
     for (int variant = v_lo; variant <= v_hi; ++variant) {
         const std::string src = jit_source(w, variant);
         if (const char* dump = getenv("EZ_JIT_DUMP")) {  // inspection: write the generated source
-            if (FILE* f = fopen((std::string(dump) + (variant ? ".generic" : "")).c_str(), "w")) {
+            if (FILE* f = fopen((std::string(dump) + (variant ? ".v" + std::to_string(variant) : std::string())).c_str(), "w")) {
                 fwrite(src.data(), 1, src.size(), f);
                 fclose(f);
             }

@@ -164,10 +164,11 @@ def test_specialised_equals_generic_prismatic_oblique(rows):
     assert torch.equal(a, b)
 
 
-@pytest.mark.parametrize("variant", ["0", "1"])
+@pytest.mark.parametrize("variant", ["0", "1", "2"])
 @pytest.mark.parametrize("which", ["franka7", "bimanual14"])
 def test_both_voxel_code_variants_equal_generic(which, variant, monkeypatch):
-    """The literal-constant voxel code (variant 0) and the generic calls (variant 1), each forced
+    """The literal-constant voxel code (variant 0), the generic calls (variant 1) and the lookups
+    streamed with the FK (variant 2), each forced
     with EZ_JIT_VOX, give the generic kernel's flags exactly (specialisation keeps the faster)."""
     monkeypatch.setenv("EZ_JIT_VOX", variant)
     w = {"franka7": fx.franka7_world, "bimanual14": fx.bimanual14_world}[which]()
