@@ -130,16 +130,19 @@ struct HModel {
     int dof = 0, n_store = 0;
 };
 
-// calibrated hot self pairs tested in phase A: 16, or one per 40 pairs up to
-// 32 for large models (measured: 7-DOF / 248 pairs best at 16, 14-DOF / 1,264
-// pairs +8% at 32); EZ_HOT_PAIRS overrides, for tuning
+// calibrated hot self pairs tested in phase A.  Measured with the round-2
+// specialised kernels (2^20 rows, tools/time_check.py): the 7-DOF model (232
+// pairs) is fastest at 4 (11.1e9 checks/s; 16: 10.6e9, 2: 8.0e9), the 14-DOF
+// model (1,248 pairs) at 48 (5.13e9; 31: 5.05e9, 96: 3.9e9): 4 below 400
+// pairs, else one per 26 pairs in [16, 48].  EZ_HOT_PAIRS overrides.
 int hot_pairs(int n_pairs) {
     static const int v = [] {
         const char* e = getenv("EZ_HOT_PAIRS");
         const int x = e ? atoi(e) : -1;
         return (x >= 0 && x <= 256) ? x : -1;
     }();
-    return v >= 0 ? v : std::max(16, std::min(32, n_pairs / 40));
+    if (v >= 0) return v;
+    return n_pairs < 400 ? 4 : std::max(16, std::min(48, n_pairs / 26));
 }
 constexpr int kMinBlock = 3;   // smaller link-pair blocks are tested without the bounding-sphere skip
 
