@@ -50,6 +50,37 @@ def _rank():
     return int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("LOCAL_RANK", "0"))
 
 
+_BACKEND = {"name": "nccl"}
+
+
+def _max_over_ranks(x: float, world_size: int) -> float:
+    """Max of a host scalar over ranks (NCCL: on the device; gloo test mode: on the host)."""
+    if world_size == 1:
+        return float(x)
+    import torch
+    import torch.distributed as dist
+
+    dev = "cuda" if _BACKEND["name"] == "nccl" else "cpu"
+    t = torch.tensor([float(x)], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def _barrier(world_size: int) -> None:
+    if world_size > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+
+
+def _comm(world_size: int):
+    from paper_2504_10783_b200.distributed import LocalComm, TorchComm
+
+    if world_size == 1:
+        return LocalComm()
+    return TorchComm() if _BACKEND["name"] == "nccl" else TorchComm(device="cpu")
+
+
 class ClockSampler:
     """nvidia-smi clocks / throttle reasons, sampled every 100 ms over a window of untimed steps
     that brackets the (millisecond-long) timed region."""
@@ -490,21 +521,15 @@ def bench_config3(world, ck, comm, world_size: int, rank: int) -> dict:
     from paper_2504_10783_b200.polytope import HPolytope
     from paper_2504_10783_b200.roadmap import PwlPath
 
-    dist = torch.distributed if world_size > 1 else None
     path = PwlPath(fx.random_free_path(world, 10, seed=3))
     dom = HPolytope.from_bounds(world.lower, world.upper)
     params = InflationParams(**fx.FRANKA_PARAMS)
 
     def max_over_ranks(x):
-        if world_size == 1:
-            return x
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
+        return _max_over_ranks(x, world_size)
 
     def barrier():
-        if world_size > 1:
-            dist.barrier()
+        _barrier(world_size)
         torch.cuda.synchronize()
 
     out = {"segments": 10, "path": "10 chained 0.6-long segments, free with margin 0.02 (default_rng(3))"}
@@ -552,18 +577,14 @@ def bench_e2e(ck, host_batches, world_size: int, steps: int) -> dict:
         while n_w < 3 or time.perf_counter() - t_w < 1.0:  # copies run slower in a buffer's first second
             ck.check_batch(batches[n_w % len(batches)])
             n_w += 1
-        if world_size > 1:
-            dist.barrier()
+        _barrier(world_size)
         groups = []
         for _ in range(3):
             t_e = time.perf_counter()
             for i in range(steps):
                 ck.check_batch(batches[i % len(batches)])
             groups.append(time.perf_counter() - t_e)
-        t = torch.tensor([float(np.median(groups))], dtype=torch.float64, device="cuda")
-        if world_size > 1:
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return BATCH * steps * world_size / float(t.item())
+        return BATCH * steps * world_size / _max_over_ranks(float(np.median(groups)), world_size)
 
     pageable = host_batches
     pinned32 = []
@@ -589,15 +610,19 @@ def run_ours(args):
     rank, world_size, local_rank = _rank()
     if world_size != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world_size}")
-    torch.cuda.set_device(local_rank)
-    dev = torch.device("cuda", local_rank)
+    # one GPU per rank; the gloo test mode (--dist-backend gloo) may put several ranks on one GPU
+    gpu = local_rank % max(1, torch.cuda.device_count())
+    torch.cuda.set_device(gpu)
+    dev = torch.device("cuda", gpu)
+    _BACKEND["name"] = args.dist_backend
     if world_size > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group("gloo")
 
     from paper_2504_10783_b200 import _native as N
     from paper_2504_10783_b200 import fixtures as fx
-    from paper_2504_10783_b200.distributed import LocalComm, TorchComm
-
     world = fx.franka7_world()
     t_jit = time.perf_counter()
     ck = world.checker()  # "auto": the model-specialised kernel is compiled with the device world
@@ -620,8 +645,7 @@ def run_ours(args):
         step(i)
     torch.cuda.synchronize()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    if world_size > 1:
-        dist.barrier()
+    _barrier(world_size)
     torch.cuda.synchronize()
 
     def busy(seconds: float) -> None:
@@ -636,11 +660,10 @@ def run_ours(args):
                 torch.cuda.synchronize()
         torch.cuda.synchronize()
 
-    with ClockSampler(local_rank) as clk:
+    with ClockSampler(gpu) as clk:
         clk.wait_first()
         busy(0.4)
-        if world_size > 1:
-            dist.barrier()
+        _barrier(world_size)
         torch.cuda.synchronize()
         t0 = torch.cuda.Event(enable_timing=True)
         t1 = torch.cuda.Event(enable_timing=True)
@@ -651,17 +674,12 @@ def run_ours(args):
             ev[i][1].record(stream)
         t1.record(stream)
         torch.cuda.synchronize()
-        if world_size > 1:
-            dist.barrier()
+        _barrier(world_size)
         busy(0.4)
-    if world_size > 1:
-        dist.barrier()
+    _barrier(world_size)
     total_ms = t0.elapsed_time(t1)
     launch_ms = [a.elapsed_time(b) for a, b in ev]
-    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
-    if world_size > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    max_ms = float(t.item())
+    max_ms = _max_over_ranks(total_ms, world_size)
     checks = BATCH * args.steps * world_size
     value = checks / (max_ms * 1e-3)
     step(0)
@@ -677,8 +695,8 @@ def run_ours(args):
     fp64_rate = 4 * BATCH / (e64a.elapsed_time(e64b) * 1e-3)
 
     e2e = bench_e2e(ck, host_batches, world_size, max(3, min(args.steps, 10)))
-    comm = TorchComm() if world_size > 1 else LocalComm()
-    fp64_peak = _peak("ez_fp64_tc_peak", local_rank) if rank == 0 else 0.0
+    comm = _comm(world_size)
+    fp64_peak = _peak("ez_fp64_tc_peak", gpu)
     eizo = None if args.skip_eizo else bench_eizo7(world, ck, cpu=(world_size == 1 and not args.skip_cpu),
                                                    fp64_peak=fp64_peak)
     config3 = None if args.skip_eizo else bench_config3(world, ck, comm, world_size, rank)
@@ -691,7 +709,7 @@ def run_ours(args):
             dist.destroy_process_group()
         return
 
-    peak_tf = _peak("ez_fp32_peak", local_rank)
+    peak_tf = _peak("ez_fp32_peak", gpu)
     avg_launch_ms = float(np.mean(launch_ms))
     achieved_tf = FLOP_PER_CHECK * BATCH / (avg_launch_ms * 1e-3) / 1e12
     traffic = None
@@ -769,13 +787,12 @@ def bench_config4_sharded(comm, world_size: int) -> dict:
     v1, v2 = fx.random_free_segment(world, seed=3)
     dom = HPolytope.from_bounds(world.lower, world.upper)
     params = InflationParams(**fx.FRANKA_PARAMS)
-    torch.distributed.barrier()
+    _barrier(world_size)
     t0 = time.perf_counter()
     rep = inflate_edge_sharded(Segment(v1, v2), dom, params, ck, seed=7, comm=comm)
     torch.cuda.synchronize()
-    t = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device="cuda")
-    torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-    return {"ms_wall_max_over_ranks": float(t.item()) * 1e3, "iterations": rep.iterations,
+    dt = _max_over_ranks(time.perf_counter() - t0, world_size)
+    return {"ms_wall_max_over_ranks": dt * 1e3, "iterations": rep.iterations,
             "faces": rep.hyperplanes_added, "collision_checks": rep.collision_checks,
             "collectives": comm.collectives, "ranks": world_size}
 
@@ -803,6 +820,8 @@ def main():
     ap.add_argument("--skip-cpu", action="store_true")
     ap.add_argument("--skip-extra", action="store_true", help="skip the config-4 and config-5 (DRM) sections")
     ap.add_argument("--cpu-sample", type=int, default=30_000)
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="gloo: host-staged collectives, ranks may share a GPU (tests of the multi-rank path)")
     args = ap.parse_args()
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         _relaunch_under_torchrun(args)

@@ -114,3 +114,19 @@ def test_native_sessions_two_processes_equal_single_gpu():
             assert len(got) == len(want.sets)
             for (a_, b_), P in zip(got, want.sets):
                 assert np.array_equal(a_, P.A) and np.array_equal(b_, P.b)
+
+
+def test_bench_two_ranks_gloo_mode():
+    """`bench.py --gpus 2` outside torchrun re-launches itself under torch.distributed.run and
+    prints one JSON line from rank 0 with n_gpus 2 (gloo test mode: both ranks on cuda:0)."""
+    import json
+    import subprocess
+
+    r = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--gpus", "2", "--steps", "3", "--warmup", "3",
+                        "--dist-backend", "gloo", "--skip-extra", "--skip-eizo", "--skip-cpu"],
+                       capture_output=True, text=True, timeout=900, cwd=str(ROOT))
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["steps"] == 3 and d["value"] > 0 and d["e2e"]["value"] > 0
