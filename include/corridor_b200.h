@@ -210,6 +210,9 @@ int32_t ez_eizo_session_begin(ez_world* world, const double* h_v1, const double*
 int32_t ez_eizo_session_end(ez_eizo_session* session);
 int32_t ez_eizo_session_sample(ez_eizo_session* session, int32_t k, uint64_t walk_begin, int64_t count,
                                int64_t m_local, int32_t* n_col_m, int32_t* n_cand);
+/* Optional hint: make the draws of iteration k's walks [walk_begin, +count)
+ * ahead on the session's side stream (overlapping the current iteration). */
+int32_t ez_eizo_session_prefetch(ez_eizo_session* session, int32_t k, uint64_t walk_begin, int64_t count);
 int32_t ez_eizo_session_bisect(ez_eizo_session* session, int32_t k, int32_t n_take, double* d_star,
                                double* d_pstar, double* d_dstar);
 int32_t ez_eizo_session_place(ez_eizo_session* session, int32_t k, const double* d_star, const double* d_pstar,

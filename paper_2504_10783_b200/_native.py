@@ -76,6 +76,7 @@ SIGNATURES = {
                                       c_i32, c_i32, C.POINTER(c_vp)]),
     "ez_eizo_session_end": (c_i32, [c_vp]),
     "ez_eizo_session_sample": (c_i32, [c_vp, c_i32, c_u64, c_i64, c_i64, P_i32, P_i32]),
+    "ez_eizo_session_prefetch": (c_i32, [c_vp, c_i32, c_u64, c_i64]),
     "ez_eizo_session_bisect": (c_i32, [c_vp, c_i32, c_i32, c_vp, c_vp, c_vp]),
     "ez_eizo_session_place": (c_i32, [c_vp, c_i32, c_vp, c_vp, c_vp, c_i32, P_i32, P_i32]),
     "ez_eizo_session_result": (c_i32, [c_vp, P_dbl, P_dbl, c_i32, P_i32]),

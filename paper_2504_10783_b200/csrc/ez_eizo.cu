@@ -9,6 +9,7 @@
 // Samples, candidates and faces stay in device memory; the host reads one
 // 32-byte status record per iteration.
 #include <algorithm>
+#include <chrono>
 #include <climits>
 #include <cmath>
 #include <mutex>
@@ -1286,38 +1287,46 @@ static int32_t ws_create(ez_eizo_ws** out) {
     return EZ_OK;
 }
 
+// Take a free workspace of device `dev` from its pool (creating one if all are
+// busy) / give it back.
+static int32_t ws_acquire(int dev, ez_eizo_ws** out) {
+    WsPool& P = g_pool[dev & 63];
+    std::lock_guard<std::mutex> lk(P.mu);
+    for (size_t i = 0; i < P.all.size(); ++i)
+        if (!P.busy[i]) {
+            P.busy[i] = true;
+            *out = P.all[i];
+            return EZ_OK;
+        }
+    ez_eizo_ws* n = nullptr;
+    const int32_t st = ws_create(&n);
+    if (st != EZ_OK) {
+        eizo_ws_free(n);
+        return st;
+    }
+    P.all.push_back(n);
+    P.busy.push_back(true);
+    *out = n;
+    return EZ_OK;
+}
+
+static void ws_release(int dev, ez_eizo_ws* ws) {
+    if (!ws) return;
+    WsPool& P = g_pool[dev & 63];
+    std::lock_guard<std::mutex> lk(P.mu);
+    for (size_t i = 0; i < P.all.size(); ++i)
+        if (P.all[i] == ws) P.busy[i] = false;
+}
+
 // A workspace of the current device for the duration of one call.
 struct WsLease {
     int device = 0;
     ez_eizo_ws* ws = nullptr;
     int32_t acquire(int dev) {
         device = dev;
-        WsPool& P = g_pool[dev & 63];
-        std::lock_guard<std::mutex> lk(P.mu);
-        for (size_t i = 0; i < P.all.size(); ++i)
-            if (!P.busy[i]) {
-                P.busy[i] = true;
-                ws = P.all[i];
-                return EZ_OK;
-            }
-        ez_eizo_ws* n = nullptr;
-        const int32_t st = ws_create(&n);
-        if (st != EZ_OK) {
-            eizo_ws_free(n);
-            return st;
-        }
-        P.all.push_back(n);
-        P.busy.push_back(true);
-        ws = n;
-        return EZ_OK;
+        return ws_acquire(dev, &ws);
     }
-    ~WsLease() {
-        if (!ws) return;
-        WsPool& P = g_pool[device & 63];
-        std::lock_guard<std::mutex> lk(P.mu);
-        for (size_t i = 0; i < P.all.size(); ++i)
-            if (P.all[i] == ws) P.busy[i] = false;
-    }
+    ~WsLease() { ws_release(device, ws); }
 };
 
 static int32_t ws_reserve(ez_eizo_ws* ws, int d, int64_t n, int32_t c, int32_t f, int n_ms) {

@@ -161,6 +161,10 @@ class EizoSession:
                                             C.byref(nc))
         return st, int(ncm.value), int(nc.value)
 
+    def prefetch(self, k: int, walk_begin: int, count: int) -> None:
+        """Make iteration k's draws ahead on the session's side stream (a hint)."""
+        N.check(N.lib().ez_eizo_session_prefetch(self._h, int(k), int(walk_begin), int(count)))
+
     def bisect(self, k: int, n_take: int):
         torch = self.torch
         star = torch.empty((n_take, self.d), dtype=torch.float64, device=self.dev)
@@ -234,16 +238,46 @@ def inflate_edge_sharded(seg: Segment, domain: HPolytope, params: InflationParam
     my_shards = [comm.rank * local + j for j in range(local)]
     make = session_factory or (lambda: EizoSession(checker, seg, domain, params, n_b, seed, rng))
     sessions = [make() for _ in my_shards]
+    def n_of(k):
+        return max(params.n_p, required_batch_size(k, params))
+
+    def prefetch(k, offset):
+        # iteration k's draws on each session's side stream, two iterations ahead
+        # (the loop's own walks are pipelined one iteration ahead of the host)
+        if params.n_it is not None and k > params.n_it:
+            return
+        for g, S in zip(my_shards, sessions):
+            if hasattr(S, "prefetch"):
+                lo, hi = shard_range(n_of(k), W, g)
+                S.prefetch(k, offset + lo, hi - lo)
+
+    import os
+    import time
+
+    prof = {} if os.environ.get("EZ_SHARD_PROFILE") else None
+
+    def tick(name, t0):
+        if prof is not None:
+            prof[name] = prof.get(name, 0.0) + time.perf_counter() - t0
+        return time.perf_counter()
+
     try:
         k, walk_offset, checks, hyper = 1, 0, 0, 0
+        prefetch(1, 0)
+        prefetch(2, n_of(1))
         while True:
             m = required_batch_size(k, params)
             n_s = max(params.n_p, m)
             mine = []
+            t0 = time.perf_counter()
             for g, S in zip(my_shards, sessions):
                 lo, hi = shard_range(n_s, W, g)
                 mine.extend(S.sample(k, walk_offset + lo, hi - lo, max(0, min(hi, m) - lo)))
+            t0 = tick("sample", t0)
+            prefetch(k + 2, walk_offset + n_s + n_of(k + 1))
+            t0 = tick("prefetch", t0)
             info = comm.all_gather_i64(mine).reshape(W, 3)  # collective 1
+            t0 = tick("collective1", t0)
             _raise_worst(info[:, 0])
             n_col_m = int(info[:, 1].sum())
             walk_offset += n_s
@@ -257,6 +291,7 @@ def inflate_edge_sharded(seg: Segment, domain: HPolytope, params: InflationParam
             per_rank = (local + width * takes.reshape(comm.world_size, local).sum(axis=1))
             L = int(per_rank.max())
             parts = []
+            t0 = time.perf_counter()
             for g, S in zip(my_shards, sessions):
                 st, star, pstar, dstar = S.bisect(k, int(takes[g]))
                 head = torch.tensor([float(st)], dtype=torch.float64, device=star.device if star is not None else "cpu")
@@ -268,21 +303,27 @@ def inflate_edge_sharded(seg: Segment, domain: HPolytope, params: InflationParam
             buf = torch.cat([p.to(parts[0].device) for p in parts])
             if buf.numel() < L:
                 buf = torch.cat([buf, buf.new_zeros(L - buf.numel())])
+            t0 = tick("bisect+pack", t0)
             allbuf = comm.all_gather_f64(buf)  # collective 2
-            stats, rows = [], []
+            t0 = tick("collective2", t0)
+            heads, rows = [], []
             for r in range(comm.world_size):
                 off = 0
                 for j in range(local):
                     t = int(takes[r * local + j])
-                    stats.append(int(allbuf[r, off].item()))
+                    heads.append((r, off))
                     rows.append(allbuf[r, off + 1: off + 1 + t * width].reshape(t, width))
                     off += 1 + t * width
-            _raise_worst(stats)
+            hr = torch.tensor([h[0] for h in heads], device=allbuf.device)
+            hc = torch.tensor([h[1] for h in heads], device=allbuf.device)
+            _raise_worst(allbuf[hr, hc].cpu().numpy().astype(np.int64))  # one read of every status
             rows = torch.cat(rows)
             C_tot = int(rows.shape[0])
             checks += C_tot * (1 + n_b)
             star, pstar, dstar = rows[:, :d], rows[:, d:2 * d], rows[:, 2 * d]
+            t0 = tick("unpack", t0)
             outs = [S.place(k, star, pstar, dstar) for S in sessions]
+            t0 = tick("place", t0)
             # placement is deterministic and identical on every rank: no exchange
             _raise_worst([o[0] for o in outs])
             hyper += outs[0][1]
@@ -291,6 +332,8 @@ def inflate_edge_sharded(seg: Segment, domain: HPolytope, params: InflationParam
                 break
             k += 1
         poly = sessions[0].result()
+        if prof is not None:
+            print("inflate_edge_sharded phases (s):", {k_: round(v, 4) for k_, v in prof.items()}, flush=True)
         checker.calls += checks
         return InflationReport(poly, k, hyper, checks, terminated)
     finally:
