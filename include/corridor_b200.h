@@ -195,6 +195,11 @@ int32_t ez_inflate_edge(ez_world* world, const double* h_v1, const double* h_v2,
                         int32_t rng, ez_eizo_report* report, double* h_A_out, double* h_b_out,
                         int32_t face_cap);
 
+/* If the polytope has more than face_cap rows, ez_inflate_edge fills the
+ * report (n_faces included), keeps the rows for the calling thread and returns
+ * EZ_CAPACITY; ez_inflate_edge_result copies them out (count, then copy). */
+int32_t ez_inflate_edge_result(double* h_A_out, double* h_b_out, int32_t face_cap, int32_t* n_faces);
+
 /* In-segment batch sharding: EI-ZO as resumable steps.  Each
  * rank runs a session over the same segment/domain/seed; per iteration k the
  * caller (torch.distributed over NCCL) all-reduces the first-m collision

@@ -72,6 +72,7 @@ SIGNATURES = {
                                c_vp, c_vp]),
     "ez_inflate_edge": (c_i32, [c_vp, P_dbl, P_dbl, c_i32, P_dbl, P_dbl, c_i32, C.POINTER(EizoParams),
                                 c_u64, c_i32, c_i32, C.POINTER(EizoReport), P_dbl, P_dbl, c_i32]),
+    "ez_inflate_edge_result": (c_i32, [P_dbl, P_dbl, c_i32, P_i32]),
     "ez_eizo_session_begin": (c_i32, [c_vp, P_dbl, P_dbl, c_i32, P_dbl, P_dbl, c_i32, C.POINTER(EizoParams), c_u64,
                                       c_i32, c_i32, C.POINTER(c_vp)]),
     "ez_eizo_session_end": (c_i32, [c_vp]),

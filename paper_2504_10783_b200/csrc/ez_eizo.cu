@@ -12,6 +12,7 @@
 #include <chrono>
 #include <climits>
 #include <cmath>
+#include <cstring>
 #include <mutex>
 #include <type_traits>
 #include <vector>
@@ -1602,6 +1603,10 @@ extern "C" int32_t ez_hit_and_run(const double* d_A, const double* d_b, int32_t 
     return EZ_OK;
 }
 
+// the polytope of the last ez_inflate_edge on this thread that overflowed face_cap
+static thread_local std::vector<double> g_last_faces;
+static thread_local int g_last_dim = 0;
+
 // required_batch_size (inflation.py:156-161)
 static int64_t batch_size(int k, const ez_eizo_params& p) {
     const double pi = 3.14159265358979311599796346854;  // math.pi
@@ -1782,16 +1787,44 @@ extern "C" int32_t ez_inflate_edge(ez_world* w, const double* h_v1, const double
     EZ_CUDA(cudaEventSynchronize(ws->ev1));  // also drains the void look-ahead iteration
     float ms = 0.f;
     cudaEventElapsedTime(&ms, ws->ev0, ws->ev1);
-    if (F > face_cap) return fail(EZ_CAPACITY, "face_cap smaller than the result polytope");
-    EZ_CUDA(cudaMemcpyAsync(h_A_out, ws->A, sizeof(double) * F * d, cudaMemcpyDeviceToHost, s));
-    EZ_CUDA(cudaMemcpyAsync(h_b_out, ws->b, sizeof(double) * F, cudaMemcpyDeviceToHost, s));
-    EZ_CUDA(cudaStreamSynchronize(s));
     report->iterations = k;
     report->hyperplanes_added = hyper;
     report->collision_checks = checks;
     report->terminated_by = terminated;
     report->n_faces = F;
     report->device_ms = ms;
+    if (F > face_cap) {
+        // count, then copy: the polytope is kept for this thread and
+        // ez_inflate_edge_result hands it out, so a short buffer never loses
+        // the device work (the report above is complete)
+        std::vector<double>& keep = g_last_faces;
+        keep.resize(static_cast<size_t>(F) * (d + 1));
+        EZ_CUDA(cudaMemcpyAsync(keep.data(), ws->A, sizeof(double) * F * d, cudaMemcpyDeviceToHost, s));
+        EZ_CUDA(cudaMemcpyAsync(keep.data() + static_cast<size_t>(F) * d, ws->b, sizeof(double) * F,
+                                cudaMemcpyDeviceToHost, s));
+        EZ_CUDA(cudaStreamSynchronize(s));
+        g_last_dim = d;
+        return fail(EZ_CAPACITY, "face_cap smaller than the result polytope: report->n_faces rows are kept for "
+                                 "ez_inflate_edge_result");
+    }
+    EZ_CUDA(cudaMemcpyAsync(h_A_out, ws->A, sizeof(double) * F * d, cudaMemcpyDeviceToHost, s));
+    EZ_CUDA(cudaMemcpyAsync(h_b_out, ws->b, sizeof(double) * F, cudaMemcpyDeviceToHost, s));
+    EZ_CUDA(cudaStreamSynchronize(s));
+    return EZ_OK;
+}
+
+// The polytope of this thread's last ez_inflate_edge that returned EZ_CAPACITY.
+extern "C" int32_t ez_inflate_edge_result(double* h_A_out, double* h_b_out, int32_t face_cap, int32_t* n_faces) {
+    if (!n_faces) return fail(EZ_INVALID_ARGUMENT, "null argument");
+    const int d = g_last_dim;
+    const int F = d > 0 ? static_cast<int>(g_last_faces.size() / (d + 1)) : 0;
+    *n_faces = F;
+    if (F == 0) return fail(EZ_INVALID_ARGUMENT, "no kept polytope on this thread");
+    if (F > face_cap || !h_A_out || !h_b_out) return fail(EZ_CAPACITY, "face_cap smaller than the kept polytope");
+    std::memcpy(h_A_out, g_last_faces.data(), sizeof(double) * F * d);
+    std::memcpy(h_b_out, g_last_faces.data() + static_cast<size_t>(F) * d, sizeof(double) * F);
+    g_last_faces.clear();
+    g_last_dim = 0;
     return EZ_OK;
 }
 

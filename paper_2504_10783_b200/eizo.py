@@ -236,9 +236,15 @@ def inflate_edge(seg: Segment, domain: HPolytope, params: InflationParams, check
     rep = N.EizoReport()
     from .native_world import precision_code
 
-    N.check(N.lib().ez_inflate_edge(native.handle, N.ptr(v1), N.ptr(v2), d, N.ptr(A0), N.ptr(b0), domain.n_faces,
-                                    C.byref(p), int(seed) & (2**64 - 1), precision_code(checker.precision),
-                                    rng_mode(rng), C.byref(rep), N.ptr(A_out), N.ptr(b_out), cap))
+    st = N.lib().ez_inflate_edge(native.handle, N.ptr(v1), N.ptr(v2), d, N.ptr(A0), N.ptr(b0), domain.n_faces,
+                                 C.byref(p), int(seed) & (2**64 - 1), precision_code(checker.precision),
+                                 rng_mode(rng), C.byref(rep), N.ptr(A_out), N.ptr(b_out), cap)
+    if st == 11 and rep.n_faces > cap:  # EZ_CAPACITY: count, then copy (the device run is not repeated)
+        cap = rep.n_faces
+        A_out, b_out = np.empty((cap, d)), np.empty(cap)
+        nf = C.c_int32(0)
+        st = N.lib().ez_inflate_edge_result(N.ptr(A_out), N.ptr(b_out), cap, C.byref(nf))
+    N.check(st)
     with _CALLS_LOCK:  # inflations of several segments may run in threads
         checker.calls += int(rep.collision_checks)
     F = rep.n_faces

@@ -212,3 +212,35 @@ def test_franka7_region_eps_audit_independent_sampler():
 
 
 FRANKA_EPS = fx.FRANKA_PARAMS["eps"]
+
+
+def test_face_cap_overflow_counts_then_copies():
+    """ez_inflate_edge with a face_cap below the result: EZ_CAPACITY with a complete report, the
+    rows kept for ez_inflate_edge_result (count, then copy), equal to a normal call's."""
+    import ctypes as C
+
+    from paper_2504_10783_b200 import _native as N
+    from paper_2504_10783_b200.eizo import default_bisection_steps
+
+    world = fx.disc_world([[0.0, 1.2], [0.0, -1.2], [2.0, 1.2]], 0.5)
+    seg = Segment(np.array([-1.0, 0.0]), np.array([1.0, 0.0]))
+    dom = HPolytope.from_bounds(world.lower, world.upper)
+    params = InflationParams()
+    ck = world.checker()
+    full = inflate_edge(seg, dom, params, ck, seed=4)
+    assert full.polytope.n_faces > 5
+    p = N.EizoParams(params.delta, params.eps, params.tau, params.delta_max, params.t_col, params.n_p, params.n_f,
+                     default_bisection_steps(dom, params.delta_max), params.n_ms, 0)
+    rep = N.EizoReport()
+    small = 2
+    A_out, b_out = np.empty((small, 2)), np.empty(small)
+    v1, v2 = np.ascontiguousarray(seg.v1), np.ascontiguousarray(seg.v2)
+    A0, b0 = np.ascontiguousarray(dom.A), np.ascontiguousarray(dom.b)
+    st = N.lib().ez_inflate_edge(ck.native.handle, N.ptr(v1), N.ptr(v2), 2, N.ptr(A0), N.ptr(b0), dom.n_faces,
+                                 C.byref(p), 4, 0, 0, C.byref(rep), N.ptr(A_out), N.ptr(b_out), small)
+    assert st == 11 and rep.n_faces == full.polytope.n_faces and rep.iterations == full.iterations
+    A2, b2 = np.empty((rep.n_faces, 2)), np.empty(rep.n_faces)
+    nf = C.c_int32(0)
+    assert N.lib().ez_inflate_edge_result(N.ptr(A2), N.ptr(b2), rep.n_faces, C.byref(nf)) == 0
+    assert nf.value == rep.n_faces
+    assert np.array_equal(A2, full.polytope.A) and np.array_equal(b2, full.polytope.b)
