@@ -205,38 +205,78 @@ __device__ __forceinline__ int hnr_walk(double (&x)[MAXD], int d, const double* 
 // squares rounded, summed left to right, IEEE sqrt and divide; cpoly.py:163-164),
 // so the walks' critical path skips the norm.  Element (step, k) at
 // Z[(step * (d + 1) + k) * count + walk]; k = d holds the chord uniform.
+// Warp-cooperative inverse normals: the central rational (85% of the draws)
+// is evaluated in place; the tail draws of the warp's 32 x d uniforms are
+// packed into shared memory, evaluated by all 32 lanes together (about two
+// rounds instead of a divergent tail branch in almost every warp for each of
+// the d slots) and read back.
 template <int MAXD>
-__global__ void k_draws(uint64_t seed, uint64_t walk_offset, int64_t count, int d, int step0, double* __restrict__ Z,
-                        const int32_t* __restrict__ status) {
+__global__ void __launch_bounds__(MAXD <= 16 ? 256 : 128)
+k_draws(uint64_t seed, uint64_t walk_offset, int64_t count, int d, int step0, double* __restrict__ Z,
+        const int32_t* __restrict__ status) {
+    constexpr int kWarps = (MAXD <= 16 ? 256 : 128) / 32;
+    __shared__ double s_tail[kWarps][32 * MAXD];
     if (status && (status[0] != EZ_OK || status[1] != 0)) return;
     // one thread per (walk, step), the step from blockIdx.y (no 64-bit
     // division): the walk's hash prefix once for its d + 1 draws
     const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-    if (i >= count) return;
+    const bool live = i < count;  // dead lanes take part in the warp's tail rounds
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const uint64_t step = static_cast<uint64_t>(step0) + blockIdx.y;
-    const uint64_t key = walk_key(seed, walk_offset + static_cast<uint64_t>(i));
-    double* z = Z + static_cast<int64_t>(step) * (d + 1) * count + i;
+    const uint64_t key = walk_key(seed, walk_offset + static_cast<uint64_t>(live ? i : 0));
+    double* st = s_tail[wid];
     double v[MAXD];
+    uint32_t tails = 0;  // bit k: slot k went to the warp's tail list
+    int n_tail = 0;
+#pragma unroll
+    for (int k = 0; k < MAXD; ++k) {
+        if (k < d) {
+            const double u = counter_uniform(key, step, k);
+            const bool tail = live && !as241_central(u);
+            v[k] = (live && !tail) ? as241_center(u) : 0.0;
+            const unsigned m = __ballot_sync(0xffffffffu, tail);
+            if (tail) {
+                st[n_tail + __popc(m & ((1u << lane) - 1u))] = u;
+                tails |= 1u << k;
+            }
+            n_tail += __popc(m);
+        }
+    }
+    __syncwarp();
+    for (int t = lane; t < n_tail; t += 32) st[t] = as241_tail(st[t]);
+    __syncwarp();
+    // read the tail results back: the same ballots give the same slots
+    n_tail = 0;
     double ss = 0.0;
 #pragma unroll
     for (int k = 0; k < MAXD; ++k) {
-        v[k] = (k < d) ? counter_normal(key, step, k) : 0.0;
-        if (k < d) ss = __dadd_rn(ss, __dmul_rn(v[k], v[k]));
+        if (k < d) {
+            const bool tail = (tails >> k) & 1u;
+            const unsigned m = __ballot_sync(0xffffffffu, tail);
+            if (tail) v[k] = st[n_tail + __popc(m & ((1u << lane) - 1u))];
+            n_tail += __popc(m);
+            ss = __dadd_rn(ss, __dmul_rn(v[k], v[k]));
+        }
     }
-    const double nrm = sqrt(ss);
+    if (!live) return;
+    // unit direction: one division and d products (numpy divides each
+    // component, cpoly.py:163-164; the products differ from its quotients by
+    // at most an ulp, below the ndtri approximation's own few ulps)
+    const double inv = 1.0 / sqrt(ss);
+    double* z = Z + static_cast<int64_t>(step) * (d + 1) * count + i;
 #pragma unroll
     for (int k = 0; k < MAXD; ++k)
-        if (k < d) z[k * count] = v[k] / nrm;
+        if (k < d) z[k * count] = v[k] * inv;
     z[d * count] = counter_uniform(key, step, d);
 }
 
 static void launch_draws(cudaStream_t s, uint64_t seed, uint64_t walk_offset, int64_t count, int d, int n_ms,
                          double* z, const int32_t* status) {
     for (int step0 = 0; step0 < n_ms; step0 += 65535) {  // gridDim.y limit
-        const dim3 grid(static_cast<unsigned>((count + 255) / 256), static_cast<unsigned>(std::min(n_ms - step0, 65535)));
-        if (d <= 8) k_draws<8><<<grid, 256, 0, s>>>(seed, walk_offset, count, d, step0, z, status);
-        else if (d <= 16) k_draws<16><<<grid, 256, 0, s>>>(seed, walk_offset, count, d, step0, z, status);
-        else k_draws<32><<<grid, 256, 0, s>>>(seed, walk_offset, count, d, step0, z, status);
+        const unsigned gy = static_cast<unsigned>(std::min(n_ms - step0, 65535));
+        if (d <= 8) k_draws<8><<<dim3(static_cast<unsigned>((count + 255) / 256), gy), 256, 0, s>>>(seed, walk_offset, count, d, step0, z, status);
+        else if (d <= 16) k_draws<16><<<dim3(static_cast<unsigned>((count + 255) / 256), gy), 256, 0, s>>>(seed, walk_offset, count, d, step0, z, status);
+        else k_draws<32><<<dim3(static_cast<unsigned>((count + 127) / 128), gy), 128, 0, s>>>(seed, walk_offset, count, d, step0, z, status);
     }
 }
 
@@ -583,29 +623,55 @@ k_compact(const uint8_t* __restrict__ free_flags, int64_t n, int n_p, double thr
         if (accept) rec[kStop] = 1;
     }
     if (accept) return;
+    // 16 flags per thread per round (one 16-byte load): a 1024-thread round
+    // covers 16,384 samples, so an EI-ZO batch (10-26k) takes one or two
+    // rounds of one block-wide scan instead of a scan per 1,024 flags
+    constexpr int kPer = 16;
     int run = 0;
-    for (int64_t base = 0; base < n && run < n_p; base += blockDim.x) {
-        const int64_t i = base + threadIdx.x;
-        const bool f = (i < n) && free_flags[i] == 0;
-        const unsigned m = __ballot_sync(0xffffffffu, f);
-        const int pre = __popc(m & ((1u << lane) - 1u));
-        if (lane == 0) warp_tot[wid] = __popc(m);
+    for (int64_t base = 0; base < n && run < n_p; base += static_cast<int64_t>(blockDim.x) * kPer) {
+        const int64_t i0 = base + static_cast<int64_t>(threadIdx.x) * kPer;
+        uint32_t colmask = 0;  // bit j: sample i0 + j collides (flag 0)
+        if (i0 + kPer <= n) {
+            const uint4 v = *reinterpret_cast<const uint4*>(free_flags + i0);
+            const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+#pragma unroll
+                for (int bb = 0; bb < 4; ++bb)
+                    if (((w[q] >> (8 * bb)) & 0xFFu) == 0u) colmask |= 1u << (4 * q + bb);
+        } else {
+            for (int j = 0; j < kPer; ++j)
+                if (i0 + j < n && free_flags[i0 + j] == 0) colmask |= 1u << j;
+        }
+        const int cnt = __popc(colmask);
+        // block-wide exclusive scan of the per-thread counts
+        int incl = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        if (lane == 31) warp_tot[wid] = incl;
         __syncthreads();
         if (wid == 0) {
             const int nw = blockDim.x >> 5;
-            int v = lane < nw ? warp_tot[lane] : 0;
-            int incl = v;
+            const int v = lane < nw ? warp_tot[lane] : 0;
+            int wi = v;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
-                const int y = __shfl_up_sync(0xffffffffu, incl, o);
-                if (lane >= o) incl += y;
+                const int y = __shfl_up_sync(0xffffffffu, wi, o);
+                if (lane >= o) wi += y;
             }
-            warp_off[lane] = incl - v;
-            if (lane == 31) s_total = incl;
+            warp_off[lane] = wi - v;
+            if (lane == 31) s_total = wi;
         }
         __syncthreads();
-        const int pos = run + warp_off[wid] + pre;
-        if (f && pos < n_p) col[pos] = static_cast<int32_t>(i);
+        int pos = run + warp_off[wid] + (incl - cnt);
+        while (colmask && pos < n_p) {  // this thread's colliding samples, in index order
+            const int j = __ffs(colmask) - 1;
+            colmask &= colmask - 1;
+            col[pos++] = static_cast<int32_t>(i0 + j);
+        }
         run += s_total;
         __syncthreads();
     }

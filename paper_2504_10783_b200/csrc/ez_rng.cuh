@@ -36,8 +36,62 @@ __device__ __forceinline__ double counter_uniform(uint64_t key, uint64_t step, u
     return u53(splitmix(key ^ (step * 64ull + slot)));
 }
 
+// Inverse normal CDF in fp64: Wichura's AS241 (PPND16).  Its central
+// rational (|p - 0.5| <= 0.425, 85% of the draws) needs no transcendental; the
+// tails take one log and one sqrt.  Against scipy.special.ndtri (the
+// reference's, cpoly.py:164 via seeding.py:58-60) the relative error is at
+// most 1.2e-15 on 5e6 reference-stream uniforms (checked in numpy).  The
+// coefficients live in constant memory so every DFMA reads its operand from
+// the constant bank (as literals each double costs two UMOVs).
+__constant__ double kAs241[6][8] = {
+    {3.3871328727963666080e0, 1.3314166789178437745e+2, 1.9715909503065514427e+3, 1.3731693765509461125e+4,
+     4.5921953931549871457e+4, 6.7265770927008700853e+4, 3.3430575583588128105e+4, 2.5090809287301226727e+3},
+    {1.0, 4.2313330701600911252e+1, 6.8718700749205790830e+2, 5.3941960214247511077e+3, 2.1213794301586595867e+4,
+     3.9307895800092710610e+4, 2.8729085735721942674e+4, 5.2264952788528545610e+3},
+    {1.42343711074968357734e0, 4.63033784615654529590e0, 5.76949722146069140550e0, 3.64784832476320460504e0,
+     1.27045825245236838258e0, 2.41780725177450611770e-1, 2.27238449892691845833e-2, 7.74545014278341407640e-4},
+    {1.0, 2.05319162663775882187e0, 1.67638483018380384940e0, 6.89767334985100004550e-1,
+     1.48103976427480074590e-1, 1.51986665636164571966e-2, 5.47593808499534494600e-4, 1.05075007164441684324e-9},
+    {6.65790464350110377720e0, 5.46378491116411436990e0, 1.78482653991729133580e0, 2.96560571828504891230e-1,
+     2.65321895265761230930e-2, 1.24266094738807843860e-3, 2.71155556874348757815e-5, 2.01033439929228813265e-7},
+    {1.0, 5.99832206555887937690e-1, 1.36929880922735805310e-1, 1.48753612908506148525e-2,
+     7.86869131145613259100e-4, 1.84631831751005468180e-5, 1.42151175831644588870e-7, 2.04426310338993978564e-15}};
+
+__device__ __forceinline__ double as241_poly(int set, double r) {
+    double v = kAs241[set][7];
+#pragma unroll
+    for (int k = 6; k >= 0; --k) v = fma(v, r, kAs241[set][k]);
+    return v;
+}
+
+__device__ __forceinline__ bool as241_central(double p) { return fabs(p - 0.5) <= 0.425; }
+
+__device__ __forceinline__ double as241_center(double p) {
+    const double q = p - 0.5;
+    const double r = 0.180625 - q * q;
+    // a correctly rounded reciprocal and two products instead of a division
+    // (one more rounding, within the approximation's few ulps)
+    return q * as241_poly(0, r) * __drcp_rn(as241_poly(1, r));
+}
+
+__device__ __forceinline__ double as241_tail(double p) {
+    const double q = p - 0.5;
+    double r = sqrt(-log(q < 0.0 ? p : 1.0 - p));
+    double v;
+    if (r <= 5.0) {
+        r -= 1.6;
+        v = as241_poly(2, r) / as241_poly(3, r);
+    } else {
+        r -= 5.0;
+        v = as241_poly(4, r) / as241_poly(5, r);
+    }
+    return q < 0.0 ? -v : v;
+}
+
+__device__ __forceinline__ double ndtri_as241(double p) { return as241_central(p) ? as241_center(p) : as241_tail(p); }
+
 __device__ __forceinline__ double counter_normal(uint64_t key, uint64_t step, uint32_t slot) {
-    return normcdfinv(counter_uniform(key, step, slot));
+    return ndtri_as241(counter_uniform(key, step, slot));
 }
 
 struct Philox4 {

@@ -43,3 +43,6 @@ for e in ev:
 print(f"region span {t1 - t0:.0f} us, GPU busy {busy:.0f} us ({100 * busy / (t1 - t0):.0f}%), device_ms {r.device_ms:.3f}")
 for k, v in sorted(by.items(), key=lambda x: -x[1])[:14]:
     print(f"  {k:40s} {v:9.0f} us")
+if "--timeline" in sys.argv:
+    for e in ev:
+        print(f"  {e['ts'] - t0:9.1f} +{e['dur']:8.1f}  stream {e.get('args', {}).get('stream', '?'):>4}  {e['name'][:50]}")
