@@ -253,7 +253,7 @@ def bench_boxes(checks_n: int = 1 << 20) -> dict:
             "workload": "8 robot boxes + 1 sphere, 20 self pairs (box-box SAT, sphere-box), 1 static box, 10k voxels"}
 
 
-def bench_config4(checks_n: int = 1 << 20, cpu: bool = True) -> dict:
+def bench_config4(checks_n: int = 1 << 20, cpu: bool = True, fp64_peak: float = 0.0) -> dict:
     """Config 4: 14-DOF bimanual (66 spheres, 1,248 pairs): checks/s and one EI-ZO region."""
     import torch
 
@@ -296,6 +296,10 @@ def bench_config4(checks_n: int = 1 << 20, cpu: bool = True) -> dict:
            "eizo_roofline": {"bound": "FP64 tensor (DMMA) in the walk", "flop_per_region": flop,
                              "walk_gemm_flop": walk_gemm,
                              "achieved_tflops": flop / (rep.device_ms * 1e-3) / 1e12,
+                             "peak_tflops": fp64_peak,
+                             "walk_dmma_bound_ms": walk_gemm / (fp64_peak * 1e12) * 1e3 if fp64_peak else None,
+                             "frac_of_dmma_bound": (walk_gemm / (fp64_peak * 1e12)) / (rep.device_ms * 1e-3)
+                             if fp64_peak else None,
                              "note": "93% of the region is the walk over up to 1,860 faces; an LP analysis "
                                      "(tools/redundancy.py) finds <3% of the faces redundant"},
            "workload": "14-DOF bimanual sphere model vs 10k voxels; EI-ZO single segment, Franka (eps, delta)"}
@@ -726,7 +730,7 @@ def run_ours(args):
     extra = {}
     if world_size == 1 and not args.skip_extra:
         extra["config1"] = bench_config1(cpu=not args.skip_cpu)
-        extra["config4"] = bench_config4(cpu=not args.skip_cpu)
+        extra["config4"] = bench_config4(cpu=not args.skip_cpu, fp64_peak=fp64_peak)
         extra["boxes"] = bench_boxes()
         extra["drm"] = bench_drm(cpu=not args.skip_cpu)
     if config4_sharded is not None:
