@@ -33,6 +33,8 @@ int32_t retain_async_pool();  // keep the current device's default mem pool cach
 // fn(lo, hi) over [0, n) split across a persistent host thread pool (parts of
 // at least min_per_part items); returns when every part is done
 void host_parallel(int64_t n, int64_t min_per_part, const std::function<void(int64_t, int64_t)>& fn);
+// n bytes into (write-combined) pinned staging memory with streaming stores
+void copy_to_staging(void* dst, const void* src, size_t n);
 #endif
 
 #define EZ_CUDA(call)                                                        \

@@ -1266,7 +1266,7 @@ extern "C" int32_t ez_check_batch_host(ez_world* w, const void* h_q, int32_t q_d
         } else {
             char* dst = static_cast<char*>(w->h_stage_in[st]);
             if (ld == dof) {
-                std::memcpy(dst, src, row_bytes * rows);
+                copy_to_staging(dst, src, row_bytes * rows);
             } else {
                 for (int64_t r = 0; r < rows; ++r) std::memcpy(dst + r * row_bytes, src + r * ld * es, row_bytes);
             }
