@@ -1191,7 +1191,8 @@ extern "C" int32_t ez_check_batch(ez_world* w, const void* d_q, int32_t q_dtype,
 //    never wait on one another, so the host moves of some chunks overlap the
 //    DMA and kernels of others (one thread moving pageable rows runs far below
 //    the PCIe rate).
-// Stages are allocated on first use, so small batches hold little memory.
+// Stage buffers are allocated on first use at the path's chunk size (pinned
+// callers never touch the host stages), so small batches hold little memory.
 extern "C" int32_t ez_check_batch_host(ez_world* w, const void* h_q, int32_t q_dtype, int64_t n, int64_t ld,
                                        uint8_t* h_free, int32_t precision) {
     if (!w) return fail(EZ_INVALID_ARGUMENT, "null world");
@@ -1208,10 +1209,11 @@ extern "C" int32_t ez_check_batch_host(ez_world* w, const void* h_q, int32_t q_d
         const int64_t v = e ? atoll(e) : dflt;
         return std::min(hi, std::max(lo, v));
     };
-    static const int64_t stage_cap = env_i("EZ_HOST_CHUNK_MAX", int64_t(1) << 16, 1024, int64_t(1) << 22);
-    static const int64_t chunk_pg = std::min(stage_cap, env_i("EZ_HOST_CHUNK", int64_t(1) << 16, 1024, int64_t(1) << 22));
-    static const int64_t chunk_pin = std::min(stage_cap, env_i("EZ_HOST_CHUNK_PINNED", int64_t(1) << 16, 1024, int64_t(1) << 22));
-    static const int lanes_pin = static_cast<int>(env_i("EZ_HOST_LANES_PINNED", 4, 1, NL));
+    static const int64_t chunk_max = env_i("EZ_HOST_CHUNK_MAX", int64_t(1) << 22, 1024, int64_t(1) << 22);
+    static const int64_t chunk_pg = std::min(chunk_max, env_i("EZ_HOST_CHUNK", int64_t(1) << 16, 1024, int64_t(1) << 22));
+    static const int64_t chunk_pin =
+        std::min(chunk_max, env_i("EZ_HOST_CHUNK_PINNED", int64_t(1) << 17, 1024, int64_t(1) << 22));
+    static const int lanes_pin = static_cast<int>(env_i("EZ_HOST_LANES_PINNED", 2, 1, NL));
     static const int lanes_pg = static_cast<int>(env_i("EZ_HOST_LANES", NL, 1, NL));
     static const bool wc = !getenv("EZ_HOST_NO_WC");
     cudaPointerAttributes attr{};
@@ -1219,21 +1221,45 @@ extern "C" int32_t ez_check_batch_host(ez_world* w, const void* h_q, int32_t q_d
     cudaGetLastError();
     const bool pinned_out = cudaPointerGetAttributes(&attr, h_free) == cudaSuccess && attr.type == cudaMemoryTypeHost;
     cudaGetLastError();
-    const int64_t chunk = pinned_in ? chunk_pin : chunk_pg;
+    const int64_t chunk = std::min<int64_t>(pinned_in ? chunk_pin : chunk_pg, n);
+    // stage capacity: a power of two >= 4096 rows, so a run of growing small
+    // batches reallocates O(log) times
+    int64_t cap = 4096;
+    while (cap < chunk) cap <<= 1;
     const int64_t nchunks = (n + chunk - 1) / chunk;
     const int lanes = static_cast<int>(std::min<int64_t>(pinned_in ? lanes_pin : lanes_pg, nchunks));
     for (int i = 0; i < lanes; ++i)
         if (!w->hstream[i]) EZ_CUDA(cudaStreamCreateWithFlags(&w->hstream[i], cudaStreamNonBlocking));
+    // Only the buffers this call's path uses are allocated, at (at least) its
+    // chunk size; every stage is idle here (each call drains all of its stages).
     for (int i = 0; i < 2 * lanes; ++i) {
-        if (w->h_stage_in[i]) continue;
-        // write-combined: the host only streams rows into it and the DMA engine
-        // reads it (no cache snooping, streaming stores)
-        EZ_CUDA(cudaHostAlloc(&w->h_stage_in[i], sizeof(double) * stage_cap * dof,
-                              wc ? cudaHostAllocWriteCombined : cudaHostAllocDefault));
-        EZ_CUDA(cudaMallocHost(reinterpret_cast<void**>(&w->h_stage_out[i]), stage_cap));
-        EZ_CUDA(cudaMalloc(&w->d_stage_in[i], sizeof(double) * stage_cap * dof));
-        EZ_CUDA(cudaMalloc(reinterpret_cast<void**>(&w->d_stage_out[i]), stage_cap));
-        EZ_CUDA(cudaEventCreateWithFlags(&w->stage_done[i], cudaEventDisableTiming));
+        if (!w->stage_done[i]) EZ_CUDA(cudaEventCreateWithFlags(&w->stage_done[i], cudaEventDisableTiming));
+        if (w->d_rows[i] < chunk) {
+            cudaFree(w->d_stage_in[i]);
+            cudaFree(w->d_stage_out[i]);
+            w->d_stage_in[i] = w->d_stage_out[i] = nullptr;
+            w->d_rows[i] = 0;
+            EZ_CUDA(cudaMalloc(&w->d_stage_in[i], sizeof(double) * cap * dof));
+            EZ_CUDA(cudaMalloc(reinterpret_cast<void**>(&w->d_stage_out[i]), cap));
+            w->d_rows[i] = cap;
+        }
+        if (!pinned_in && w->h_in_rows[i] < chunk) {
+            cudaFreeHost(w->h_stage_in[i]);
+            w->h_stage_in[i] = nullptr;
+            w->h_in_rows[i] = 0;
+            // write-combined: the host only streams rows into it and the DMA
+            // engine reads it (no cache snooping, streaming stores)
+            EZ_CUDA(cudaHostAlloc(&w->h_stage_in[i], sizeof(double) * cap * dof,
+                                  wc ? cudaHostAllocWriteCombined : cudaHostAllocDefault));
+            w->h_in_rows[i] = cap;
+        }
+        if (!pinned_out && w->h_out_rows[i] < chunk) {
+            cudaFreeHost(w->h_stage_out[i]);
+            w->h_stage_out[i] = nullptr;
+            w->h_out_rows[i] = 0;
+            EZ_CUDA(cudaMallocHost(reinterpret_cast<void**>(&w->h_stage_out[i]), cap));
+            w->h_out_rows[i] = cap;
+        }
     }
     const char* q = static_cast<const char*>(h_q);
     static const bool prof = getenv("EZ_HOST_PROFILE") != nullptr;

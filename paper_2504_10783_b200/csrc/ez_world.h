@@ -50,6 +50,8 @@ struct ez_world {
     uint8_t* h_stage_out[kHostStages] = {};
     void* d_stage_in[kHostStages] = {};
     uint8_t* d_stage_out[kHostStages] = {};
+    // capacities in rows (buffers grow on demand; all idle between calls)
+    int64_t h_in_rows[kHostStages] = {}, h_out_rows[kHostStages] = {}, d_rows[kHostStages] = {};
 
     ez_eizo_ws* eizo = nullptr;
 
