@@ -1667,6 +1667,18 @@ static int32_t launch_bisect(ez_world* w, ez_eizo_ws* ws, int precision, cudaStr
                              int d, double ee,
                              int n_b, double t_col) {
     if (precision == EZ_F64) return launch_bisect_t<double, MAXD>(w, ws, w->md, s, it, n_p, d, ee, n_b, t_col);
+    // fp32 checks on a specialised world: the bisection on the model's own
+    // code, one thread per checked point (ez_bisect_core.cuh; same points,
+    // decisions and rows as k_bisect2).  EZ_BISECT_JIT=0 (read per call)
+    // keeps k_bisect2.
+    const char* bj = getenv("EZ_BISECT_JIT");
+    const char* b1 = getenv("EZ_BISECT1");
+    if (d == w->dof && !(bj && bj[0] == '0') && !(b1 && b1[0] == '1')) {
+        const std::shared_ptr<const JitCheck> jc = std::atomic_load(&w->jit);
+        if (jc && jc->bk)
+            return jit_bisect_launch(w, *jc, ws->X, ws->col, ws->rec, it + kNumCand, n_p, ws->seg, ee, n_b, t_col,
+                                     ws->star, ws->pstar, ws->dstar, s);
+    }
     return launch_bisect_t<float, MAXD>(w, ws, w->mf, s, it, n_p, d, ee, n_b, t_col);
 }
 

@@ -455,6 +455,25 @@ std::string kernel_source(const std::string& body, char qt, int shp) {
     return o.str();
 }
 
+// the bisection entry point (one program; fp64 rows, fp32 checks).  128
+// threads at <= 128 registers: 16 warps per SM (7-DOF: 143 registers
+// uncapped, one 256-thread CTA per SM)
+constexpr int kBisectThreads = 128;
+constexpr int kBisectMinBlocks = 4;
+std::string bisect_source(const std::string& body, int dof) {
+    std::ostringstream o;
+    o << body << "#include \"ez_bisect_core.cuh\"\n\nextern \"C\" __global__ void __launch_bounds__(" << kBisectThreads
+      << ", " << kBisectMinBlocks
+      << ") ez_bisect_jit(const __grid_constant__ ez::ModelDev<float> M, const double* __restrict__ X, "
+         "const int32_t* __restrict__ col, int32_t* __restrict__ rec, const int32_t* __restrict__ n_cand, "
+         "const double* __restrict__ seg, double ee, int n_b, double t_col, double* __restrict__ star, "
+         "double* __restrict__ pstar, double* __restrict__ dstar, int64_t resident, int forced_l) {\n"
+         "    const ez::JitPolicy pol{M};\n    ez::bisect_points<ez::JitPolicy, "
+      << dof << ", " << kBisectThreads
+      << ">(pol, X, col, rec, n_cand, seg, ee, n_b, t_col, star, pstar, dstar, resident, forced_l);\n}\n";
+    return o.str();
+}
+
 // ---------------------------------------------------------------------------
 // compile + load, cached by source text (same model and margin -> one module)
 // ---------------------------------------------------------------------------
@@ -542,46 +561,50 @@ int32_t nvrtc_cubin(const std::string& src, std::vector<char>* cubin) {
 
 // The six programs compile concurrently (one host thread each; NVRTC is
 // thread-safe per program), each cached on disk under its own key.
-int32_t compile(const std::string& body, std::shared_ptr<JitCheck>* out) {
+int32_t compile(const std::string& body, int dof, std::shared_ptr<JitCheck>* out) {
     struct Job {
         std::string src, path, error;
         std::vector<char> cubin;
         int32_t st = EZ_OK;
         bool cached = false;
     };
-    Job jobs[2][kShapes];
+    constexpr int kJobs = 2 * kShapes + 1;  // check kernels [rows][shape], then the bisection
+    Job jobs[kJobs];
     std::vector<std::thread> threads;
-    for (int i = 0; i < 2; ++i)
-        for (int v = 0; v < kShapes; ++v) {
-            Job& j = jobs[i][v];
-            j.src = kernel_source(body, i ? 'd' : 'f', v);
-            j.path = cache_path(j.src);
-            j.cached = read_file(j.path, &j.cubin);
-            if (!j.cached)
-                threads.emplace_back([&j] {
-                    j.st = nvrtc_cubin(j.src, &j.cubin);
-                    if (j.st != EZ_OK) j.error = ez_last_error();
-                });
-        }
+    for (int n = 0; n < kJobs; ++n) {
+        Job& j = jobs[n];
+        j.src = n < 2 * kShapes ? kernel_source(body, n / kShapes ? 'd' : 'f', n % kShapes) : bisect_source(body, dof);
+        j.path = cache_path(j.src);
+        j.cached = read_file(j.path, &j.cubin);
+        if (!j.cached)
+            threads.emplace_back([&j] {
+                j.st = nvrtc_cubin(j.src, &j.cubin);
+                if (j.st != EZ_OK) j.error = ez_last_error();
+            });
+    }
     for (auto& t : threads) t.join();
     auto jc = std::make_shared<JitCheck>();
-    for (int i = 0; i < 2; ++i)
-        for (int v = 0; v < kShapes; ++v) {
-            Job& j = jobs[i][v];
-            if (j.st != EZ_OK) return fail(j.st, j.error);
-            bool loaded = cudaLibraryLoadData(&jc->lib[i][v], j.cubin.data(), nullptr, nullptr, 0, nullptr, nullptr,
-                                              0) == cudaSuccess;
-            if (!loaded && j.cached) {  // a cached cubin that does not load is rebuilt
-                cudaGetLastError();
-                EZ_TRY(nvrtc_cubin(j.src, &j.cubin));
-                j.cached = false;
-                loaded = cudaLibraryLoadData(&jc->lib[i][v], j.cubin.data(), nullptr, nullptr, 0, nullptr, nullptr,
-                                             0) == cudaSuccess;
-            }
-            if (!loaded) EZ_CUDA(cudaGetLastError());
-            if (!j.cached) write_file(j.path, j.cubin);
-            EZ_CUDA(cudaLibraryGetKernel(&jc->k[i][v], jc->lib[i][v], kernel_name(i ? 'd' : 'f', v).c_str()));
+    for (int n = 0; n < kJobs; ++n) {
+        Job& j = jobs[n];
+        if (j.st != EZ_OK) return fail(j.st, j.error);
+        const bool bis = n == 2 * kShapes;
+        cudaLibrary_t* lib = bis ? &jc->blib : &jc->lib[n / kShapes][n % kShapes];
+        bool loaded = cudaLibraryLoadData(lib, j.cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0) == cudaSuccess;
+        if (!loaded && j.cached) {  // a cached cubin that does not load is rebuilt
+            cudaGetLastError();
+            EZ_TRY(nvrtc_cubin(j.src, &j.cubin));
+            j.cached = false;
+            loaded = cudaLibraryLoadData(lib, j.cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0) == cudaSuccess;
         }
+        if (!loaded) EZ_CUDA(cudaGetLastError());
+        if (!j.cached) write_file(j.path, j.cubin);
+        if (bis) {
+            EZ_CUDA(cudaLibraryGetKernel(&jc->bk, jc->blib, "ez_bisect_jit"));
+            EZ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&jc->b_occ, reinterpret_cast<const void*>(jc->bk),
+                                                                  kBisectThreads, 0));
+        }
+        else EZ_CUDA(cudaLibraryGetKernel(&jc->k[n / kShapes][n % kShapes], *lib, kernel_name(n / kShapes ? 'd' : 'f', n % kShapes).c_str()));
+    }
     *out = jc;
     return EZ_OK;
 }
@@ -592,6 +615,7 @@ JitCheck::~JitCheck() {
     for (auto& row : lib)
         for (cudaLibrary_t l : row)
             if (l) cudaLibraryUnload(l);
+    if (blib) cudaLibraryUnload(blib);
 }
 
 std::string jit_source(const ez_world* w, int variant) {
@@ -734,7 +758,7 @@ int32_t jit_specialize(ez_world* w) {
             if (it != g_cache.end()) jc = it->second;
         }
         if (!jc) {
-            const int32_t st = compile(src, &jc);
+            const int32_t st = compile(src, w->dof, &jc);
             if (st != EZ_OK) {
                 w->jit_failed = true;
                 w->jit_error = ez_last_error();
@@ -794,6 +818,26 @@ int32_t jit_launch(ez_world* w, const JitCheck& jc, const void* d_q, bool q64, i
         }
     }
     return launch_at(w, jc, bt, d_q, q64, n, ld, d_free, stream, count_lim, n_col);
+}
+
+// EZ_BISECT_LEVELS=1..4 (read per call) forces the binary steps per round;
+// otherwise the kernel picks from the device-side candidate count.
+int32_t jit_bisect_launch(ez_world* w, const JitCheck& jc, const double* X, const int32_t* col, int32_t* rec,
+                          const int32_t* n_cand, int n_p, const double* seg, double ee, int n_b, double t_col,
+                          double* star, double* pstar, double* dstar, cudaStream_t stream) {
+    if (n_p <= 0) return EZ_OK;
+    int forced_l = 0;
+    if (const char* e = getenv("EZ_BISECT_LEVELS"))
+        if (e[0] >= '1' && e[0] <= '4') forced_l = e[0] - '0';
+    int64_t resident = static_cast<int64_t>(w->num_sms) * std::max(jc.b_occ, 1) * kBisectThreads;
+    ModelDev<float> M = w->mf;
+    void* args[] = {&M, const_cast<double**>(&X), const_cast<int32_t**>(&col), &rec, const_cast<int32_t**>(&n_cand),
+                    const_cast<double**>(&seg), &ee, &n_b, &t_col, &star, &pstar, &dstar, &resident, &forced_l};
+    const int64_t threads = static_cast<int64_t>(n_p) << 4;  // up to 16 threads per candidate
+    EZ_CUDA(cudaLaunchKernel(reinterpret_cast<const void*>(jc.bk),
+                             dim3(static_cast<unsigned>((threads + kBisectThreads - 1) / kBisectThreads)),
+                             dim3(kBisectThreads), args, 0, stream));
+    return EZ_OK;
 }
 
 }  // namespace ez

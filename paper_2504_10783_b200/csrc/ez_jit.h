@@ -18,6 +18,10 @@ constexpr int kJitSizeCount = 5;  // 64, 128, 256, 512, 1024
 struct JitCheck {
     cudaLibrary_t lib[2][3] = {};
     cudaKernel_t k[2][3] = {};
+    // the EI-ZO bisection on the same model code (ez_bisect_core.cuh)
+    cudaLibrary_t blib = nullptr;
+    cudaKernel_t bk = nullptr;
+    int b_occ = 0;  // its resident CTAs per SM
     ~JitCheck();
 };
 
@@ -31,5 +35,12 @@ std::string jit_source(const ez_world* w, int variant = 0);
 // Launch it over n rows (fp32 arithmetic); jc is the caller's snapshot of ez_world::jit.
 int32_t jit_launch(ez_world* w, const JitCheck& jc, const void* d_q, bool q64, int64_t n, int64_t ld,
                    uint8_t* d_free, cudaStream_t stream, int64_t count_lim, int32_t* n_col);
+
+// The EI-ZO bisection of the first *n_cand (<= n_p) candidates on the
+// specialised check (ez_bisect_core.cuh; same arguments as ez_eizo.cu's
+// k_bisect2, rec = status / stop words, d = the world's dof).
+int32_t jit_bisect_launch(ez_world* w, const JitCheck& jc, const double* X, const int32_t* col, int32_t* rec,
+                          const int32_t* n_cand, int n_p, const double* seg, double ee, int n_b, double t_col,
+                          double* star, double* pstar, double* dstar, cudaStream_t stream);
 
 }  // namespace ez

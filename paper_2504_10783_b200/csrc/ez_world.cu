@@ -1214,7 +1214,7 @@ extern "C" int32_t ez_check_batch_host(ez_world* w, const void* h_q, int32_t q_d
     static const int64_t chunk_pin =
         std::min(chunk_max, env_i("EZ_HOST_CHUNK_PINNED", int64_t(1) << 17, 1024, int64_t(1) << 22));
     static const int lanes_pin = static_cast<int>(env_i("EZ_HOST_LANES_PINNED", 2, 1, NL));
-    static const int lanes_pg = static_cast<int>(env_i("EZ_HOST_LANES", NL, 1, NL));
+    static const int lanes_pg = static_cast<int>(env_i("EZ_HOST_LANES", 12, 1, NL));
     static const bool wc = !getenv("EZ_HOST_NO_WC");
     cudaPointerAttributes attr{};
     const bool pinned_in = cudaPointerGetAttributes(&attr, h_q) == cudaSuccess && attr.type == cudaMemoryTypeHost;

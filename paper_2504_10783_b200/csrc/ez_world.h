@@ -42,7 +42,7 @@ struct ez_world {
     std::mutex mu;
     // kHostLanes lanes (a host thread and a stream each) with two stages per
     // lane: pinned/device row and flag buffers plus a reuse event per stage
-    static constexpr int kHostLanes = 8;
+    static constexpr int kHostLanes = 16;
     static constexpr int kHostStages = 2 * kHostLanes;
     cudaStream_t hstream[kHostLanes] = {};
     cudaEvent_t stage_done[kHostStages] = {};

@@ -181,3 +181,67 @@ def test_both_voxel_code_variants_equal_generic(which, variant, monkeypatch):
     Q = lo + (hi - lo) * torch.rand((1 << 19, w.model.dof), generator=g, device="cuda")
     assert torch.equal(gen.check_device(Q), jit.check_device(Q))
     assert torch.equal(gen.check_device(Q.double()), jit.check_device(Q.double()))
+
+
+@pytest.mark.parametrize("which", ["franka7", "bimanual14", "arm3"])
+def test_specialised_bisection_equals_cooperative(which, monkeypatch):
+    """The EI-ZO bisection on the specialised check (ez_bisect_core.cuh: one thread per point,
+    three binary steps per round) forms the same points as k_bisect2 (EZ_BISECT_JIT=0) and so
+    takes the same decisions wherever the specialised and generic fp32 checks agree; they can
+    differ only inside the fp32 contact band (next test), which these regions never hit:
+    identical regions and counters."""
+    from paper_2504_10783_b200.eizo import InflationParams, Segment, inflate_edge
+    from paper_2504_10783_b200.polytope import HPolytope
+
+    w = {"franka7": fx.franka7_world, "bimanual14": fx.bimanual14_world, "arm3": fx.arm3_world}[which]()
+    ck = w.checker()
+    assert ck.native.specialize(1)
+    dom = HPolytope.from_bounds(w.lower, w.upper)
+    if which == "arm3":
+        v1, v2 = fx.ARM3_SEGMENT
+        p = InflationParams()
+    else:
+        v1, v2 = fx.random_free_segment(w, seed=3)
+        p = InflationParams(**{**fx.FRANKA_PARAMS, "n_it": 3 if which == "bimanual14" else None})
+    reps = []
+    for flag in ("0", "1"):
+        monkeypatch.setenv("EZ_BISECT_JIT", flag)
+        reps += [inflate_edge(Segment(np.asarray(v1), np.asarray(v2)), dom, p, ck, seed=s) for s in (7, 8)]
+    for a, b in zip(reps[:2], reps[2:]):
+        assert (a.iterations, a.hyperplanes_added, a.collision_checks, a.terminated_by) == \
+               (b.iterations, b.hyperplanes_added, b.collision_checks, b.terminated_by)
+        assert np.array_equal(a.polytope.A, b.polytope.A) and np.array_equal(a.polytope.b, b.polytope.b)
+
+
+def test_specialised_flags_differ_only_inside_contact_band():
+    """Near collision boundaries (points along free-to-colliding segments and their bisection
+    points) the specialised and generic fp32 checks round differently in a few configurations;
+    every such configuration lies inside the contact band the fp32 contract exempts (the
+    reference's fp64 clearance |c| < 1e-5)."""
+    from oracle import ref
+
+    w = fx.franka7_world()
+    gen, jit = w.checker(specialize=False).native, w.checker(specialize=False).native
+    assert jit.specialize(1)
+    lo = torch.as_tensor(w.lower, dtype=torch.float64, device="cuda")
+    hi = torch.as_tensor(w.upper, dtype=torch.float64, device="cuda")
+    g = torch.Generator(device="cuda")
+    g.manual_seed(11)
+    Q = lo + (hi - lo) * torch.rand((1 << 16, 7), generator=g, device="cuda", dtype=torch.float64)
+    f = gen.check_device(Q).bool()
+    a, b = Q[f][: 1 << 13], Q[~f][: 1 << 13]
+    n = min(len(a), len(b))
+    a, b = a[:n], b[:n]
+    pts = []
+    for _ in range(24):  # bisection on the generic check, every visited point kept
+        m = 0.5 * (a + b)
+        fm = gen.check_device(m).bool()
+        a = torch.where(fm[:, None], m, a)
+        b = torch.where(fm[:, None], b, m)
+        pts.append(m)
+    P = torch.cat(pts)
+    mism = (gen.check_device(P) != jit.check_device(P)).nonzero().flatten()
+    X = P[mism[:256]].cpu().numpy()
+    if len(X):
+        clr = ref.OracleChecker(w).clearance(X)
+        assert np.abs(clr).max() < BAND
