@@ -49,10 +49,11 @@ __device__ __forceinline__ double project_point(const double (&c)[D], const doub
 // CTA of CTA threads; each group's bracket [lo, hi] lives in shared memory
 // (thread t owns components t, t + 2^L, ...), so only the thread's own point is
 // live in registers across the check (14-DOF: 28 instead of 84 registers).
-// L trades dependent rounds for speculative checks (2^L per L steps).  The
-// bisection is latency-bound for the 7- and 14-DOF models alike; measured per
-// region (7-DOF / 14-DOF): L = 2 473 us / 53.7 ms, L = 3 336 us / 37.7 ms,
-// L = 4 348 us / 30.8 ms (4 wins once the candidates fit in one wave).
+// L trades dependent rounds for speculative checks (2^L per L steps);
+// measured per region (7-DOF / 14-DOF): L = 2 473 us / 53.7 ms, L = 3 336 us
+// / 37.7 ms, L = 4 348 us / 30.8 ms (4 wins once the candidates fit in one
+// wave), against k_bisect2's 534 us / 24.0 ms: the 14-DOF model keeps
+// k_bisect2 (ez_eizo.cu launch_bisect).
 //
 // L is chosen per launch from the device-side C: 4 when C * 16 threads fit in
 // `resident` (the GPU's resident threads for this kernel), else 3; forced_l in

@@ -1667,13 +1667,16 @@ static int32_t launch_bisect(ez_world* w, ez_eizo_ws* ws, int precision, cudaStr
                              int d, double ee,
                              int n_b, double t_col) {
     if (precision == EZ_F64) return launch_bisect_t<double, MAXD>(w, ws, w->md, s, it, n_p, d, ee, n_b, t_col);
-    // fp32 checks on a specialised world: the bisection on the model's own
-    // code, one thread per checked point (ez_bisect_core.cuh; same points,
-    // decisions and rows as k_bisect2).  EZ_BISECT_JIT=0 (read per call)
-    // keeps k_bisect2.
+    // fp32 checks on a specialised world with a light model: the bisection on
+    // the model's own code, one thread per checked point (ez_bisect_core.cuh;
+    // same points as k_bisect2).  A heavy model's single-thread check is too
+    // long a chain: the 14-DOF bisection (1,248 pairs) takes 24.0 ms per region
+    // in k_bisect2's 8-lane cooperative checks against 32.5 ms here (7-DOF:
+    // 534 -> 329 us).  EZ_BISECT_JIT=0 / 1 (read per call) forces either way.
     const char* bj = getenv("EZ_BISECT_JIT");
     const char* b1 = getenv("EZ_BISECT1");
-    if (d == w->dof && !(bj && bj[0] == '0') && !(b1 && b1[0] == '1')) {
+    const bool use_jit = bj && (bj[0] == '0' || bj[0] == '1') ? bj[0] == '1' : w->n_pairs <= 600;
+    if (d == w->dof && use_jit && !(b1 && b1[0] == '1')) {
         const std::shared_ptr<const JitCheck> jc = std::atomic_load(&w->jit);
         if (jc && jc->bk)
             return jit_bisect_launch(w, *jc, ws->X, ws->col, ws->rec, it + kNumCand, n_p, ws->seg, ee, n_b, t_col,
