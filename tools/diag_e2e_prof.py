@@ -1,3 +1,4 @@
+"""Host-side costs of the pageable check_batch path: numpy copy rate and EZ_HOST_PROFILE call times."""
 import sys, time
 from pathlib import Path
 import numpy as np

@@ -1,3 +1,4 @@
+"""Cost of registering (cudaHostRegister) a pageable 28 MB row array instead of copying it into pinned stages (DESIGN: slower than copying)."""
 import time, numpy as np, torch
 cr = torch.cuda.cudart()
 torch.cuda.init()

@@ -1,3 +1,4 @@
+"""Session prefetch: 14-DOF EI-ZO iterations through EizoSession with and without walking the next iterations ahead."""
 import sys, time
 from pathlib import Path
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))

@@ -1,3 +1,4 @@
+"""Write the generated specialised-check source of the 7- or 14-DOF model (EZ_JIT_DUMP): python tools/dump_jit.py 7|14 [path]."""
 import os, sys
 from pathlib import Path
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
