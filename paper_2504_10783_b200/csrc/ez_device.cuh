@@ -51,32 +51,25 @@ template <typename T> __device__ __forceinline__ T tsqrt(T x);
 template <> __device__ __forceinline__ float tsqrt<float>(float x) { return sqrtf(x); }
 template <> __device__ __forceinline__ double tsqrt<double>(double x) { return sqrt(x); }
 
-// fp32 sin and cos of a joint value: one three-constant Cody-Waite reduction
-// by pi/2 and the minimax polynomials of [-pi/4, pi/4] (max error 1.5 ulp,
-// 9e-8 absolute, against sincosf's 0.5 ulp at about half the instructions).
-// Beyond |x| = 128 rad the library routine takes over.
+// fp32 sin and cos of a joint value: a two-constant reduction by 2 pi into
+// [-pi, pi] and the SFU's sin / cos (MUFU.SIN / MUFU.COS, absolute error
+// about 2^-21.4 there).  Near contact this moves the fp32 decisions by at most
+// 2.8e-7 in fp64 clearance (tools/diag_fp32_contact.py, 27k boundary points
+// per model; 1.3e-7 with the 1.5-ulp minimax polynomials used before, at
+// about 4x the instructions), far inside the 1e-5 contact band of the fp32
+// contract (tests/test_gpu_check.py::test_fp32_disagreements_hug_contact).
+// Config 2: 87.8 -> 81.1 us per 2^20.  Beyond |x| = 128 rad the library
+// routine takes over.
 __device__ __forceinline__ void sincos_f32(float x, float& s, float& c) {
     if (!(fabsf(x) <= 128.0f)) {
         sincosf(x, &s, &c);
         return;
     }
-    const float k = rintf(x * 0.636619772367581f);
-    float r = fmaf(k, -1.5703125f, x);
-    r = fmaf(k, -4.837512969970703125e-4f, r);
-    r = fmaf(k, -7.54978995489188216e-8f, r);
-    const float z = r * r;
-    float ps = fmaf(z, -1.9515295891e-4f, 8.3321608736e-3f);
-    ps = fmaf(ps, z, -1.6666654611e-1f);
-    const float sr = fmaf(ps * z, r, r);
-    float pc = fmaf(z, 2.443315711809948e-5f, -1.388731625493765e-3f);
-    pc = fmaf(pc, z, 4.166664568298827e-2f);
-    const float cr = fmaf(pc * z, z, fmaf(-0.5f, z, 1.0f));
-    const int q = static_cast<int>(k);
-    const bool swap = q & 1;
-    s = swap ? cr : sr;
-    c = swap ? sr : cr;
-    if (q & 2) s = -s;
-    if ((q + 1) & 2) c = -c;
+    const float k = rintf(x * 0.159154943091895336f);
+    float r = fmaf(k, -6.28318548202514648f, x);  // 2 pi rounded to fp32
+    r = fmaf(k, 1.74845553e-7f, r);                 // minus its rounding error
+    s = __sinf(r);
+    c = __cosf(r);
 }
 
 // sin/cos of a joint value.  fp32 arithmetic on an fp64 input keeps the

@@ -677,24 +677,35 @@ int32_t tune_bt(ez_world* w, const JitCheck& jc, float* best_ms) {
         if (r != cudaSuccess && st == EZ_OK) st = cuda_fail(r, "CTA-size pick", __FILE__, __LINE__);
         return st == EZ_OK;
     };
-    if (ck(cudaMalloc(&d_q, sizeof(float) * n * dof)) && ck(cudaMalloc(&d_out, n)) &&
+    // rotating batches larger than twice the L2 (as the workloads it is tuned
+    // for): on one L2-resident batch the 14-DOF model timed 512 threads
+    // faster, on the streamed batches 1024 is (193 vs 214 us per 2^20)
+    const int nb = static_cast<int>(std::min<int64_t>(8, (int64_t(256) << 20) / (sizeof(float) * n * dof) + 1));
+    auto qb = [&](int r) { return d_q + static_cast<int64_t>(r % nb) * n * dof; };
+    if (ck(cudaMalloc(&d_q, sizeof(float) * n * dof * nb)) && ck(cudaMalloc(&d_out, n)) &&
         ck(cudaMalloc(&d_box, sizeof(double) * 2 * dof)) &&
         ck(cudaMemcpy(d_box, w->q_lo.data(), sizeof(double) * dof, cudaMemcpyHostToDevice)) &&
         ck(cudaMemcpy(d_box + dof, w->q_hi.data(), sizeof(double) * dof, cudaMemcpyHostToDevice)) &&
         ck(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking)) && ck(cudaEventCreate(&e0)) &&
         ck(cudaEventCreate(&e1))) {
-        k_fill_box<<<256, 256, 0, s>>>(d_q, n, dof, d_box, d_box + dof, 0x7E57ull);
-        // two interleaved passes, best time per size: the first launches of a
-        // fresh process can run while the clocks are still ramping
+        k_fill_box<<<1024, 256, 0, s>>>(d_q, n * nb, dof, d_box, d_box + dof, 0x7E57ull);
+        // a warm-up of ~30 launches (the GPU idled through the NVRTC compile
+        // and its clocks ramp back up), then three interleaved passes, best
+        // time per size (with two and no warm-up the 14-DOF model sometimes
+        // kept 512 threads: 224 against 193 us per 2^20)
         const int sizes[3] = {1024, 512, 256};
         float best[3] = {1e30f, 1e30f, 1e30f};
-        for (int pass = 0; pass < 2 && st == EZ_OK; ++pass)
+        for (int r = 0; r < 30 && st == EZ_OK; ++r)
+            if (w->jit_occ[0][shape_of(sizes[r % 3]) + 2] > 0)
+                st = launch_at(w, jc, sizes[r % 3], qb(r), false, n, dof, d_out, s, 0, nullptr);
+        for (int pass = 0; pass < 3 && st == EZ_OK; ++pass)
             for (int c = 0; c < 3 && st == EZ_OK; ++c) {
                 const int bt = sizes[c];
                 if (w->jit_occ[0][shape_of(bt) + 2] < 1 || (forced && bt != forced)) continue;
-                for (int r = 0; r < 2 && st == EZ_OK; ++r) st = launch_at(w, jc, bt, d_q, false, n, dof, d_out, s, 0, nullptr);
+                for (int r = 0; r < 2 && st == EZ_OK; ++r) st = launch_at(w, jc, bt, qb(r), false, n, dof, d_out, s, 0, nullptr);
                 if (!ck(cudaEventRecord(e0, s))) break;
-                for (int r = 0; r < 4 && st == EZ_OK; ++r) st = launch_at(w, jc, bt, d_q, false, n, dof, d_out, s, 0, nullptr);
+                for (int r = 0; r < 2 * nb && st == EZ_OK; ++r)
+                    st = launch_at(w, jc, bt, qb(r + 2), false, n, dof, d_out, s, 0, nullptr);
                 float ms = 0.f;
                 if (!ck(cudaEventRecord(e1, s)) || !ck(cudaEventSynchronize(e1)) || !ck(cudaEventElapsedTime(&ms, e0, e1)))
                     break;
@@ -703,6 +714,9 @@ int32_t tune_bt(ez_world* w, const JitCheck& jc, float* best_ms) {
         int pick = -1;
         for (int c = 0; c < 3; ++c)
             if (best[c] < 1e30f && (pick < 0 || best[c] < best[pick])) pick = c;
+        if (getenv("EZ_JIT_TUNE_LOG"))
+            fprintf(stderr, "tune_bt dof %d: 1024 %.4f 512 %.4f 256 %.4f ms (%d launches)\n", dof, best[0], best[1], best[2],
+                    2 * nb);
         if (pick >= 0) {
             w->jit_bt = sizes[pick];
             *best_ms = best[pick];
