@@ -59,7 +59,11 @@ __device__ __forceinline__ void check_tiles_reg(const P& pol, int dof, int32_t* 
     const int qcap = 2 * bt;
     auto wrap = [&](int x) { return BT > 0 ? x % qcap : (x & (qcap - 1)); };
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#ifdef EZ_CHECK_NO_PF
+    const bool pre = false;
+#else
     const bool pre = dof <= kPrefetch;  // prefetch the next tile's row in registers
+#endif
     int qhead = 0, qn = 0;
     const int64_t tiles = (n + bt - 1) / bt;
     Q nxt[kPrefetch];

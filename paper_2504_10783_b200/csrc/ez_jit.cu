@@ -266,6 +266,31 @@ struct Gen {
 
     // obstacles in calibrated order, cells of kVoxBatch spheres fetched together
     // distance-grid cells fetched together per batch of spheres (EZ_JIT_VOXB)
+    // Deferred list walks (EZ_JIT_DEFER=0: walk in place).  An undecided
+    // sphere's (cell word, bound, centre, radius) go to a per-thread queue and
+    // the out-of-line walks run after every other test.  A call in the middle
+    // of the straight-line tests made each fetched cell word live across it,
+    // so it was stored to the stack right after its load: the store waited on
+    // the load and the batched fetches lost their overlap.
+    bool defer() const {
+        static const bool on = [] {
+            const char* e = getenv("EZ_JIT_DEFER");
+            return !(e && e[0] == '0');
+        }();
+        return on && M.vox.present && variant != 1;
+    }
+    void walk_queue() {
+        if (!defer()) return;
+        const int nq = std::max(1, M.n_spheres);
+        o << "    uint32_t wq_w[" << nq << "]; float wq_e[" << nq << "], wq_x[" << nq << "], wq_y[" << nq << "], wq_z["
+          << nq << "], wq_r[" << nq << "]; int nwq = 0;\n";
+    }
+    void walk_flush() {
+        if (!defer()) return;
+        o << "    for (int i = 0; i < nwq; ++i)\n"
+             "        if (voxel_walk<float>(M.vox, wq_w[i], wq_e[i], wq_x[i], wq_y[i], wq_z[i], wq_r[i])) return true;\n";
+    }
+
     static int vox_batch() {
         const char* e = getenv("EZ_JIT_VOXB");
         const int v = e ? atoi(e) : kVoxBatch;
@@ -318,9 +343,14 @@ struct Gen {
           << "            if (!(fmaf(qf, " << lit(V.dq) << ", -e" << j << ") > " << c_free << ")) {\n"
           << "                if ((w" << j << " < 0xFF000000u) & (fmaf(qf, " << lit(V.dq) << ", e" << j << ") <= " << c_hit
           << ")) return true;\n"
-          << "                if (voxel_walk<float>(M.vox, w" << j << ", e" << j << ", c" << s << "_0, c" << s << "_1, c"
-          << s << "_2, " << lit(S()[s].rvox) << ")) return true;\n"
-          << "            }\n        }\n";
+          ;
+        if (defer())
+            o << "                wq_w[nwq] = w" << j << "; wq_e[nwq] = e" << j << "; wq_x[nwq] = c" << s << "_0; wq_y[nwq] = c"
+              << s << "_1; wq_z[nwq] = c" << s << "_2; wq_r[nwq] = " << lit(S()[s].rvox) << "; ++nwq;\n";
+        else
+            o << "                if (voxel_walk<float>(M.vox, w" << j << ", e" << j << ", c" << s << "_0, c" << s << "_1, c"
+              << s << "_2, " << lit(S()[s].rvox) << ")) return true;\n";
+        o << "            }\n        }\n";
     }
 
     // spheres order[k_begin, k_end): static obstacles, then the voxel map
@@ -380,7 +410,9 @@ struct Gen {
 
     // everything but the kernel entry points (kernel_source adds one)
     std::string source() {
-        o << "// generated by ez_jit.cu for one robot model\n#include \"ez_check_core.cuh\"\n\nnamespace ez {\n\n"
+        o << "// generated by ez_jit.cu for one robot model\n"
+          << (getenv("EZ_JIT_NOPF") ? "#define EZ_CHECK_NO_PF 1\n" : "")
+          << "#include \"ez_check_core.cuh\"\n\nnamespace ez {\n\n"
           << "__device__ __forceinline__ float sq3(float dx, float dy, float dz) { return dx * dx + dy * dy + dz * dz; }\n"
           // an upper bound of sqrt(x): one MUFU.RSQ (ftz; x below 1e-30 bounds by 1e-15), raised by 2^-20
           << "__device__ __forceinline__ float jit_dist_ub(float x) {\n"
@@ -388,11 +420,14 @@ struct Gen {
              "    return x > 1e-30f ? x * r * 1.00000095367431640625f : 1e-15f;\n}\n\n"
           << "struct JitPolicy {\n    static constexpr bool kRegRows = true;\n    const ModelDev<float>& M;\n"
           << "    template <typename Q>\n    __device__ __forceinline__ bool a(const Q* row, float*) const {\n";
+        if (a_obst() > 0) walk_queue();
         fk();
         hot();
         obstacles(0, a_obst());
+        if (a_obst() > 0) walk_flush();
         o << "    return false;\n    }\n"
           << "    template <typename Q>\n    __device__ __forceinline__ bool b(const Q* row, float*) const {\n";
+        walk_queue();
         if (variant == 2 && M.vox.present && a_obst() == 0) {
             // variant 2: the obstacle tests stream with the kinematics (a link's
             // spheres are tested as soon as its frame exists, in link order, and
@@ -427,6 +462,7 @@ struct Gen {
             obstacles(a_obst(), M.n_spheres);
         }
         blocks();
+        walk_flush();
         o << "    return false;\n    }\n};\n\n";
         // dynamic shared memory = rows, then the survivor ring of 2 * bt entries
         o << "template <typename Q, int BT>\n__device__ __forceinline__ void jit_body(const ModelDev<float>& M, const Q* q, "
