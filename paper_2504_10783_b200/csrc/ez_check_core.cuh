@@ -50,8 +50,20 @@ __device__ __forceinline__ void check_phase_b(const P& pol, int dof, const Q* __
 // tile publish the per-warp survivor counts and then the queue; a thread that
 // passes the first one of the next tile knows every thread has finished this
 // tile's rounds, so queue slots and s_warp are never overwritten early.
+//
+// s_pf (bt rows of dof, or nullptr): the next tile's row is prefetched with
+// cp.async into the thread's own shared-memory slot, so it occupies no
+// registers while this tile is checked.  (Held in registers across phase B
+// at 64 registers, the prefetched row was spilled right after its load, and
+// the spill store waited for the load: 4% of the stall samples.)
+template <typename Q>
+__device__ __forceinline__ void cp_async_elem(Q* dst, const Q* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(smem_u32(dst)), "l"(src), "n"(sizeof(Q))
+                 : "memory");
+}
+
 template <typename T, typename Q, int BT, class P>
-__device__ __forceinline__ void check_tiles_reg(const P& pol, int dof, int32_t* s_queue, int* s_warp,
+__device__ __forceinline__ void check_tiles_reg(const P& pol, int dof, int32_t* s_queue, int* s_warp, Q* s_pf,
                                                 const Q* __restrict__ q, int64_t n, int64_t ld,
                                                 uint8_t* __restrict__ out, int64_t count_lim,
                                                 int32_t* __restrict__ n_col) {
@@ -62,7 +74,7 @@ __device__ __forceinline__ void check_tiles_reg(const P& pol, int dof, int32_t* 
 #ifdef EZ_CHECK_NO_PF
     const bool pre = false;
 #else
-    const bool pre = dof <= kPrefetch;  // prefetch the next tile's row in registers
+    const bool pre = s_pf == nullptr && dof <= kPrefetch;  // prefetch the next tile's row in registers
 #endif
     int qhead = 0, qn = 0;
     const int64_t tiles = (n + bt - 1) / bt;
@@ -75,7 +87,18 @@ __device__ __forceinline__ void check_tiles_reg(const P& pol, int dof, int32_t* 
                 if (k < dof) nxt[k] = q[r * ld + k];
         }
     };
+    Q* my_pf = s_pf != nullptr ? s_pf + threadIdx.x * dof : nullptr;
+    auto prefetch_sm = [&](int64_t tile) {
+        const int64_t r = tile * bt + threadIdx.x;
+        if (tile < tiles && r < n) {
+#pragma unroll
+            for (int k = 0; k < 32; ++k)
+                if (k < dof) cp_async_elem(my_pf + k, q + r * ld + k);
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
     if (pre) prefetch(blockIdx.x);
+    if (my_pf != nullptr) prefetch_sm(blockIdx.x);
     for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
         const int64_t base = tile * bt;
         const int nr = static_cast<int>(min(static_cast<int64_t>(bt), n - base));
@@ -83,16 +106,22 @@ __device__ __forceinline__ void check_tiles_reg(const P& pol, int dof, int32_t* 
         bool col = false;
         if (valid) {
             Q row[32];
-            if (pre) {
+            if (my_pf != nullptr) {
+                asm volatile("cp.async.wait_group 0;" ::: "memory");  // this thread's own copies
+#pragma unroll
+                for (int k = 0; k < 32; ++k)
+                    if (k < dof) row[k] = my_pf[k];
+                prefetch_sm(tile + gridDim.x);  // lands while this tile is checked
+            } else if (pre) {
 #pragma unroll
                 for (int k = 0; k < kPrefetch; ++k)
                     if (k < dof) row[k] = nxt[k];
+                prefetch(tile + gridDim.x);  // lands while this tile is checked
             } else {
 #pragma unroll
                 for (int k = 0; k < 32; ++k)
                     if (k < dof) row[k] = q[(base + threadIdx.x) * ld + k];
             }
-            if (pre) prefetch(tile + gridDim.x);  // lands while this tile is checked
             col = pol.a(row, static_cast<T*>(nullptr));
             if (col) out[base + threadIdx.x] = 0;
         }

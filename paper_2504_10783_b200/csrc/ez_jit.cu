@@ -45,6 +45,19 @@
 namespace ez {
 namespace {
 
+// The next tile's rows are prefetched into shared memory with cp.async
+// (check_tiles_reg's s_pf) for up to 8 joints (7-DOF: 78.9 -> 76.7 us per
+// 2^20); EZ_JIT_PFSM=0 prefetches into registers.  More joints prefetch
+// nothing (14-DOF: 188 us without, 201 us with the 57 KB of staged rows,
+// which also shrink the L1 the grid lookups hit).
+bool prefetch_sm(int dof) {
+    static const bool on = [] {
+        const char* e = getenv("EZ_JIT_PFSM");
+        return !(e && e[0] == '0');
+    }();
+    return on && dof <= 8;
+}
+
 // ---------------------------------------------------------------------------
 // NVRTC, opened at run time (no link-time dependency)
 // ---------------------------------------------------------------------------
@@ -470,8 +483,9 @@ struct Gen {
           << "    extern __shared__ __align__(16) uint8_t smem[];\n"
           << "    __shared__ int s_warp[32];\n"
           << "    const JitPolicy pol{M};\n"
-          << "    check_tiles_reg<float, Q, BT>(pol, " << M.dof
-          << ", reinterpret_cast<int32_t*>(smem), s_warp, q, n, ld, out, count_lim, n_col);\n}\n\n"
+          << "    check_tiles_reg<float, Q, BT>(pol, " << M.dof << ", reinterpret_cast<int32_t*>(smem), s_warp, "
+          << (prefetch_sm(M.dof) ? "reinterpret_cast<Q*>(smem + 8 * (BT > 0 ? BT : blockDim.x))" : "static_cast<Q*>(nullptr)")
+          << ", q, n, ld, out, count_lim, n_col);\n}\n\n"
           << "}  // namespace ez\n\n";
         return o.str();
     }
@@ -663,7 +677,11 @@ namespace {
 
 // dynamic shared memory: the survivor ring of 2 * bt entries (rows live in
 // registers, check_tiles_reg)
-size_t jit_smem(const ez_world*, int bt, bool) { return 2 * static_cast<size_t>(bt) * sizeof(int32_t); }
+size_t jit_smem(const ez_world* w, int bt, bool q64) {
+    // the survivor ring of 2 bt indices, then (prefetch_sm) one row per thread
+    return 2 * static_cast<size_t>(bt) * sizeof(int32_t) +
+           (prefetch_sm(w->dof) ? static_cast<size_t>(bt) * w->dof * (q64 ? sizeof(double) : sizeof(float)) : 0);
+}
 
 // random rows in the joint box for the CTA-size pick
 __global__ void k_fill_box(float* q, int64_t n, int dof, const double* lo, const double* hi, uint64_t seed) {
