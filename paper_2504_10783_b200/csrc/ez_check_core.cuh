@@ -226,12 +226,15 @@ __device__ __forceinline__ void check_tiles(const P& pol, int dof, T* my_cen, Q*
         const unsigned sm = __ballot_sync(0xffffffffu, surv);
         if (lane == 0) s_warp[wid] = __popc(sm);
         __syncthreads();
-        // survivors in earlier warps (off) and in the tile (add): lane l reads
-        // warp l's count, two warp reductions (a per-thread loop over the 32
-        // counts was ~95 instructions per thread per tile)
-        const int wc = lane < bt / 32 ? s_warp[lane] : 0;
-        const int off = static_cast<int>(__reduce_add_sync(0xffffffffu, static_cast<unsigned>(lane < wid ? wc : 0)));
-        const int add = static_cast<int>(__reduce_add_sync(0xffffffffu, static_cast<unsigned>(wc)));
+        // (the generic kernels keep the per-thread loop over the warp counts:
+        // with the two warp reductions of check_tiles_reg the fp64 kernel ran
+        // 479 -> 614 us per 2^20)
+        int off = 0, add = 0;
+        for (int w = 0; w < bt / 32; ++w) {
+            const int c = s_warp[w];
+            off += (w < wid) ? c : 0;
+            add += c;
+        }
         if (surv)
             s_queue[wrap(qhead + qn + off + __popc(sm & ((1u << lane) - 1u)))] = static_cast<int32_t>(base + threadIdx.x);
         qn += add;
