@@ -1096,10 +1096,12 @@ k_place(double* __restrict__ A, double* __restrict__ b, int32_t* __restrict__ re
 // L2 bandwidth bound it: ~4 us per round at 10^4 x 7 anchors).  Here CTA r
 // owns the contiguous candidate range [r C / K, (r + 1) C / K): its rows,
 // distances and alive bytes are staged in its shared memory once; per round
-// each CTA takes its arg-min, rank 0 reduces the K results through
-// distributed shared memory, builds the face exactly as k_place does and
-// broadcasts it; two cluster barriers per round.  Same decisions and bits as
-// k_place (global index tie-break, same dot-product order).
+// each CTA takes its arg-min and writes it into every CTA's shared memory
+// (distributed shared memory); after one cluster barrier every CTA reduces the
+// K results and builds the face exactly as k_place does (rank 0 stores it).
+// One cluster barrier per round (two, with rank 0 broadcasting the face, cost
+// 185 us per 7-DOF region).  Same decisions and bits as k_place (global index
+// tie-break, same dot-product order).
 #ifndef EZ_PLACE_CL
 #define EZ_PLACE_CL 8
 #endif
@@ -1123,8 +1125,8 @@ k_place_cl(double* __restrict__ A, double* __restrict__ b, int32_t* __restrict__
     extern __shared__ __align__(16) uint8_t smem_pcl[];
     __shared__ double s_bd[32];
     __shared__ int s_bi[32];
-    __shared__ double s_cbd[kPlaceCl];  // rank 0: the CTAs' results
-    __shared__ int s_cbi[kPlaceCl];
+    __shared__ double s_cbd[2][kPlaceCl];  // every CTA's result, by round parity
+    __shared__ int s_cbi[2][kPlaceCl];
     __shared__ double s_a[32];
     __shared__ double s_rhs;
     __shared__ int s_best;
@@ -1149,6 +1151,7 @@ k_place_cl(double* __restrict__ A, double* __restrict__ b, int32_t* __restrict__
     const double* e = seg + d;
     double rhs = 0.0;
     for (int r = 0; r < n_f; ++r) {
+        const int par = r & 1;
         __syncthreads();
         double bd = INFINITY;
         int bi = INT_MAX;
@@ -1196,15 +1199,21 @@ k_place_cl(double* __restrict__ A, double* __restrict__ b, int32_t* __restrict__
                     bi = oi;
                 }
             }
-            if (lane == 0) {
-                *cluster.map_shared_rank(&s_cbd[rank], 0) = bd;
-                *cluster.map_shared_rank(&s_cbi[rank], 0) = bi;
+            // this CTA's result into slot `rank` of every CTA (lane q writes CTA q)
+            bd = __shfl_sync(0xffffffffu, bd, 0);
+            bi = __shfl_sync(0xffffffffu, bi, 0);
+            if (lane < kPlaceCl) {
+                *cluster.map_shared_rank(&s_cbd[par][rank], lane) = bd;
+                *cluster.map_shared_rank(&s_cbi[par][rank], lane) = bi;
             }
         }
+        // One cluster barrier per round: every CTA reduces the same K results
+        // and builds the same face (slots alternate by round parity, so a CTA
+        // one round ahead never overwrites values another is still reading)
         cluster.sync();
-        if (rank == 0 && wid == 0) {
-            bd = lane < kPlaceCl ? s_cbd[lane] : INFINITY;
-            bi = lane < kPlaceCl ? s_cbi[lane] : INT_MAX;
+        if (wid == 0) {
+            bd = lane < kPlaceCl ? s_cbd[par][lane] : INFINITY;
+            bi = lane < kPlaceCl ? s_cbi[par][lane] : INT_MAX;
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) {
                 const double od = __shfl_down_sync(0xffffffffu, bd, o);
@@ -1218,7 +1227,7 @@ k_place_cl(double* __restrict__ A, double* __restrict__ b, int32_t* __restrict__
             bd = __shfl_sync(0xffffffffu, bd, 0);  // = dstar[best]
             int best = (bi == INT_MAX) ? -1 : bi;
             if (best >= 0 && bd <= 1e-12) {
-                if (lane == 0) set_status(rec + kStatus, EZ_GRADIENT_UNDEFINED);  // inflation.py:423-424
+                if (lane == 0 && rank == 0) set_status(rec + kStatus, EZ_GRADIENT_UNDEFINED);  // inflation.py:423-424
                 best = -1;
             }
             double ak = 0.0, rh = 0.0;
@@ -1250,19 +1259,18 @@ k_place_cl(double* __restrict__ A, double* __restrict__ b, int32_t* __restrict__
                     ak /= norm;
                     rh /= norm;
                 }
-                if (lane < d) A[static_cast<int64_t>(F) * d + lane] = ak;
-                if (lane == 0) b[F] = rh;
-            }
-            // broadcast the face (or the stop) to every CTA of the cluster
-            for (int q = 0; q < kPlaceCl; ++q) {
-                if (best >= 0 && lane < d) *cluster.map_shared_rank(&s_a[lane], q) = ak;
-                if (lane == 0) {
-                    *cluster.map_shared_rank(&s_rhs, q) = rh;
-                    *cluster.map_shared_rank(&s_best, q) = best;
+                if (rank == 0) {
+                    if (lane < d) A[static_cast<int64_t>(F) * d + lane] = ak;
+                    if (lane == 0) b[F] = rh;
                 }
+                if (lane < d) s_a[lane] = ak;
+            }
+            if (lane == 0) {
+                s_rhs = rh;
+                s_best = best;
             }
         }
-        cluster.sync();
+        __syncthreads();
         if (s_best < 0) break;
         ++F;
         ++placed;
