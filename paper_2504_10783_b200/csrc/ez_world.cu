@@ -1226,7 +1226,17 @@ extern "C" int32_t ez_check_batch_host(ez_world* w, const void* h_q, int32_t q_d
     // batches reallocates O(log) times
     int64_t cap = 4096;
     while (cap < chunk) cap <<= 1;
-    const int64_t nchunks = (n + chunk - 1) / chunk;
+    // Chunk boundaries.  Pageable rows ramp up: chunk c holds min(chunk,
+    // (c + 1) chunk / 8) rows, so the lanes' first host copies finish one after
+    // another and the first H2D starts after a small copy instead of all lanes
+    // finishing full-size copies at once while the DMA engine idles.
+    std::vector<int64_t> cstart{0};
+    while (cstart.back() < n) {
+        const int64_t c = static_cast<int64_t>(cstart.size()) - 1;
+        const int64_t sz = pinned_in ? chunk : std::min(chunk, std::max<int64_t>(1024, (c + 1) * (chunk / 8)));
+        cstart.push_back(std::min(n, cstart.back() + sz));
+    }
+    const int64_t nchunks = static_cast<int64_t>(cstart.size()) - 1;
     const int lanes = static_cast<int>(std::min<int64_t>(pinned_in ? lanes_pin : lanes_pg, nchunks));
     for (int i = 0; i < lanes; ++i)
         if (!w->hstream[i]) EZ_CUDA(cudaStreamCreateWithFlags(&w->hstream[i], cudaStreamNonBlocking));
@@ -1266,11 +1276,15 @@ extern "C" int32_t ez_check_batch_host(ez_world* w, const void* h_q, int32_t q_d
     const auto tcall = std::chrono::steady_clock::now();
     // pending[stage]: chunk whose flags sit in the stage's pinned output
     std::vector<int64_t> pending(2 * lanes, -1);
+    static const bool prof2 = prof && getenv("EZ_HOST_PROFILE")[0] == '2';
+    std::atomic<int64_t> t_copy{0}, t_api{0}, t_wait{0};
     auto drain = [&](int st) -> int32_t {
+        const auto tw0 = std::chrono::steady_clock::now();
         EZ_CUDA(cudaEventSynchronize(w->stage_done[st]));
+        if (prof2) t_wait += std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now() - tw0).count();
         if (pending[st] >= 0) {
-            const int64_t pr0 = pending[st] * chunk;
-            std::memcpy(h_free + pr0, w->h_stage_out[st], std::min(chunk, n - pr0));
+            const int64_t pr0 = cstart[pending[st]];
+            std::memcpy(h_free + pr0, w->h_stage_out[st], cstart[pending[st] + 1] - pr0);
             pending[st] = -1;
         }
         return EZ_OK;
@@ -1279,8 +1293,8 @@ extern "C" int32_t ez_check_batch_host(ez_world* w, const void* h_q, int32_t q_d
         const int lane = static_cast<int>(c % lanes);
         const int st = 2 * lane + static_cast<int>((c / lanes) & 1);
         cudaStream_t s = w->hstream[lane];
-        const int64_t r0 = c * chunk;
-        const int64_t rows = std::min(chunk, n - r0);
+        const int64_t r0 = cstart[c];
+        const int64_t rows = cstart[c + 1] - r0;
         const char* src = q + r0 * ld * es;
         const size_t row_bytes = es * dof;
         EZ_TRY(drain(st));  // the stage's previous chunk is done (and its flags delivered)
@@ -1291,13 +1305,16 @@ extern "C" int32_t ez_check_batch_host(ez_world* w, const void* h_q, int32_t q_d
                                       cudaMemcpyHostToDevice, s));
         } else {
             char* dst = static_cast<char*>(w->h_stage_in[st]);
+            const auto tc0 = std::chrono::steady_clock::now();
             if (ld == dof) {
                 copy_to_staging(dst, src, row_bytes * rows);
             } else {
                 for (int64_t r = 0; r < rows; ++r) std::memcpy(dst + r * row_bytes, src + r * ld * es, row_bytes);
             }
+            if (prof2) t_copy += std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now() - tc0).count();
             EZ_CUDA(cudaMemcpyAsync(w->d_stage_in[st], dst, row_bytes * rows, cudaMemcpyHostToDevice, s));
         }
+        const auto ta0 = std::chrono::steady_clock::now();
         EZ_TRY(launch_check(w, w->d_stage_in[st], q_dtype, rows, dof, w->d_stage_out[st], precision, s));
         if (pinned_out) {
             EZ_CUDA(cudaMemcpyAsync(h_free + r0, w->d_stage_out[st], rows, cudaMemcpyDeviceToHost, s));
@@ -1306,6 +1323,7 @@ extern "C" int32_t ez_check_batch_host(ez_world* w, const void* h_q, int32_t q_d
             pending[st] = c;
         }
         EZ_CUDA(cudaEventRecord(w->stage_done[st], s));
+        if (prof2) t_api += std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now() - ta0).count();
         return EZ_OK;
     };
     int32_t status = EZ_OK;
@@ -1340,9 +1358,11 @@ extern "C" int32_t ez_check_batch_host(ez_world* w, const void* h_q, int32_t q_d
         return status;
     }
     if (prof)
-        fprintf(stderr, "ez_check_batch_host n=%lld chunks=%lld lanes=%d pinned=%d: call %.3f ms\n",
+        fprintf(stderr, "ez_check_batch_host n=%lld chunks=%lld lanes=%d pinned=%d: call %.3f ms (summed over lanes: "
+                "copy %.3f, kernel+D2H+event calls %.3f, stage waits %.3f ms)\n",
                 static_cast<long long>(n), static_cast<long long>(nchunks), lanes, int(pinned_in),
-                1e3 * std::chrono::duration<double>(std::chrono::steady_clock::now() - tcall).count());
+                1e3 * std::chrono::duration<double>(std::chrono::steady_clock::now() - tcall).count(), t_copy * 1e-6,
+                t_api * 1e-6, t_wait * 1e-6);
     return EZ_OK;
 }
 
