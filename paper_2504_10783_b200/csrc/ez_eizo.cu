@@ -433,6 +433,9 @@ __device__ __forceinline__ void chord_merge(double& S, double& H, double os, dou
 #ifndef EZ_HNR_MINB
 #define EZ_HNR_MINB 8
 #endif
+#ifndef EZ_HNR_SWP_KC
+#define EZ_HNR_SWP_KC 2
+#endif
 template <int KC>
 __global__ void __launch_bounds__(64, KC >= 8 ? 8 : EZ_HNR_MINB)
 k_hnr_mma(const double* __restrict__ Ap, const int32_t* __restrict__ F_dev, int F, int d,
@@ -494,7 +497,8 @@ k_hnr_mma(const double* __restrict__ Ap, const int32_t* __restrict__ F_dev, int 
         // until the merge below (7-DOF walk -2%; at d >= 8 the registers cost
         // more than the chains: 14-DOF +4%, so one chain)
         constexpr int TPR = EZ_HNR_TPR;
-        constexpr int NCH = KC <= 2 ? TPR : 1;
+        constexpr bool SWP = KC >= EZ_HNR_SWP_KC;  // software-pipelined single-tile rounds
+        constexpr int NCH = SWP ? 1 : (KC <= 2 ? TPR : 1);
         double cs[NCH][2][2], ch[NCH][2][2];
 #pragma unroll
         for (int u = 0; u < NCH; ++u)
@@ -506,6 +510,47 @@ k_hnr_mma(const double* __restrict__ Ap, const int32_t* __restrict__ F_dev, int 
                     ch[u][s2][e] = (SG && e) ? -1.0 : 1.0;
                 }
         bool outside = false;
+        if constexpr (SWP) {
+            // Software-pipelined tiles (one per round): the DMMAs of tile t are
+            // issued before the chord updates of tile t - 1, which then run
+            // while the tensor pipe works (the 14-DOF walk waited on each
+            // tile's DMMA results before its compare-selects could start)
+            double va[KC], vn[KC], gp[2] = {0.0, 0.0}, hp[2] = {0.0, 0.0};
+#pragma unroll
+            for (int j = 0; j < KC; ++j) va[j] = (0 < tiles) ? __ldg(arow + 4 * j) : 0.0;
+            for (int t = 0; t < tiles; ++t) {
+#pragma unroll
+                for (int j = 0; j < KC; ++j)
+                    vn[j] = (t + 1 < tiles) ? __ldg(arow + static_cast<int64_t>(t + 1) * 8 * KP + 4 * j) : 0.0;
+                double g[2] = {0.0, 0.0}, h[2] = {0.0, 0.0};
+#pragma unroll
+                for (int j = 0; j < KC; ++j) {
+                    dmma_8x8x4(g[0], g[1], va[j], x[j]);
+                    dmma_8x8x4(h[0], h[1], va[j], dr[j]);
+                }
+                if (t > 0) {
+#pragma unroll
+                    for (int s2 = 0; s2 < 2; ++s2) {
+                        outside |= check_seed && step == 0 && gp[s2] > kMemberTol;
+                        chord_update<SG>(gp[s2], hp[s2], cs[0][s2], ch[0][s2]);
+                    }
+                }
+#pragma unroll
+                for (int s2 = 0; s2 < 2; ++s2) {
+                    gp[s2] = g[s2];
+                    hp[s2] = h[s2];
+                }
+#pragma unroll
+                for (int j = 0; j < KC; ++j) va[j] = vn[j];
+            }
+            if (tiles > 0) {
+#pragma unroll
+                for (int s2 = 0; s2 < 2; ++s2) {
+                    outside |= check_seed && step == 0 && gp[s2] > kMemberTol;
+                    chord_update<SG>(gp[s2], hp[s2], cs[0][s2], ch[0][s2]);
+                }
+            }
+        } else {
         double va[TPR][KC], vn[TPR][KC];
 #pragma unroll
         for (int u = 0; u < TPR; ++u)
@@ -540,6 +585,7 @@ k_hnr_mma(const double* __restrict__ Ap, const int32_t* __restrict__ F_dev, int 
             for (int u = 0; u < TPR; ++u)
 #pragma unroll
                 for (int j = 0; j < KC; ++j) va[u][j] = vn[u][j];
+        }
         }
         // Reduce over the 8 face rows (lane bits 2-4) as a reduce-scatter: the
         // 4 running ends (slot s2, end e) halve at each butterfly level, so
