@@ -436,6 +436,9 @@ __device__ __forceinline__ void chord_merge(double& S, double& H, double os, dou
 #ifndef EZ_HNR_SWP_KC
 #define EZ_HNR_SWP_KC 2
 #endif
+#ifndef EZ_HNR_SP2
+#define EZ_HNR_SP2 1
+#endif
 template <int KC>
 __global__ void __launch_bounds__(64, KC >= 8 ? 8 : EZ_HNR_MINB)
 k_hnr_mma(const double* __restrict__ Ap, const int32_t* __restrict__ F_dev, int F, int d,
@@ -497,8 +500,9 @@ k_hnr_mma(const double* __restrict__ Ap, const int32_t* __restrict__ F_dev, int 
         // until the merge below (7-DOF walk -2%; at d >= 8 the registers cost
         // more than the chains: 14-DOF +4%, so one chain)
         constexpr int TPR = EZ_HNR_TPR;
-        constexpr bool SWP = KC >= EZ_HNR_SWP_KC;  // software-pipelined single-tile rounds
-        constexpr int NCH = SWP ? 1 : (KC <= 2 ? TPR : 1);
+        constexpr bool SWP = KC >= EZ_HNR_SWP_KC;  // software-pipelined rounds
+        constexpr int SP = KC <= 2 ? EZ_HNR_SP2 : 1;  // tiles per pipelined round
+        constexpr int NCH = SWP ? (KC <= 2 ? SP : 1) : (KC <= 2 ? TPR : 1);
         double cs[NCH][2][2], ch[NCH][2][2];
 #pragma unroll
         for (int u = 0; u < NCH; ++u)
@@ -511,44 +515,62 @@ k_hnr_mma(const double* __restrict__ Ap, const int32_t* __restrict__ F_dev, int 
                 }
         bool outside = false;
         if constexpr (SWP) {
-            // Software-pipelined tiles (one per round): the DMMAs of tile t are
-            // issued before the chord updates of tile t - 1, which then run
-            // while the tensor pipe works (the 14-DOF walk waited on each
-            // tile's DMMA results before its compare-selects could start)
-            double va[KC], vn[KC], gp[2] = {0.0, 0.0}, hp[2] = {0.0, 0.0};
+            // Software-pipelined rounds of SP tiles: the DMMAs of round r are
+            // issued before the chord updates of round r - 1, which then run
+            // while the tensor pipe works (the walk waited on each round's
+            // DMMA results before its compare-selects could start)
+            double va[SP][KC], vn[SP][KC], gp[SP][2], hp[SP][2];
 #pragma unroll
-            for (int j = 0; j < KC; ++j) va[j] = (0 < tiles) ? __ldg(arow + 4 * j) : 0.0;
-            for (int t = 0; t < tiles; ++t) {
+            for (int u = 0; u < SP; ++u) {
+                gp[u][0] = gp[u][1] = hp[u][0] = hp[u][1] = 0.0;
 #pragma unroll
                 for (int j = 0; j < KC; ++j)
-                    vn[j] = (t + 1 < tiles) ? __ldg(arow + static_cast<int64_t>(t + 1) * 8 * KP + 4 * j) : 0.0;
-                double g[2] = {0.0, 0.0}, h[2] = {0.0, 0.0};
+                    va[u][j] = (u < tiles) ? __ldg(arow + static_cast<int64_t>(u) * 8 * KP + 4 * j) : 0.0;
+            }
+            for (int t = 0; t < tiles; t += SP) {
 #pragma unroll
-                for (int j = 0; j < KC; ++j) {
-                    dmma_8x8x4(g[0], g[1], va[j], x[j]);
-                    dmma_8x8x4(h[0], h[1], va[j], dr[j]);
-                }
+                for (int u = 0; u < SP; ++u)
+#pragma unroll
+                    for (int j = 0; j < KC; ++j)
+                        vn[u][j] = (t + SP + u < tiles) ? __ldg(arow + static_cast<int64_t>(t + SP + u) * 8 * KP + 4 * j) : 0.0;
+                double g[SP][2], h[SP][2];
+#pragma unroll
+                for (int u = 0; u < SP; ++u) g[u][0] = g[u][1] = h[u][0] = h[u][1] = 0.0;
+#pragma unroll
+                for (int j = 0; j < KC; ++j)
+#pragma unroll
+                    for (int u = 0; u < SP; ++u) {
+                        dmma_8x8x4(g[u][0], g[u][1], va[u][j], x[j]);
+                        dmma_8x8x4(h[u][0], h[u][1], va[u][j], dr[j]);
+                    }
                 if (t > 0) {
 #pragma unroll
+                    for (int u = 0; u < SP; ++u)
+#pragma unroll
+                        for (int s2 = 0; s2 < 2; ++s2) {
+                            outside |= check_seed && step == 0 && gp[u][s2] > kMemberTol;
+                            chord_update<SG>(gp[u][s2], hp[u][s2], cs[u % NCH][s2], ch[u % NCH][s2]);
+                        }
+                }
+#pragma unroll
+                for (int u = 0; u < SP; ++u) {
+#pragma unroll
                     for (int s2 = 0; s2 < 2; ++s2) {
-                        outside |= check_seed && step == 0 && gp[s2] > kMemberTol;
-                        chord_update<SG>(gp[s2], hp[s2], cs[0][s2], ch[0][s2]);
+                        gp[u][s2] = g[u][s2];
+                        hp[u][s2] = h[u][s2];
                     }
-                }
 #pragma unroll
-                for (int s2 = 0; s2 < 2; ++s2) {
-                    gp[s2] = g[s2];
-                    hp[s2] = h[s2];
+                    for (int j = 0; j < KC; ++j) va[u][j] = vn[u][j];
                 }
-#pragma unroll
-                for (int j = 0; j < KC; ++j) va[j] = vn[j];
             }
             if (tiles > 0) {
 #pragma unroll
-                for (int s2 = 0; s2 < 2; ++s2) {
-                    outside |= check_seed && step == 0 && gp[s2] > kMemberTol;
-                    chord_update<SG>(gp[s2], hp[s2], cs[0][s2], ch[0][s2]);
-                }
+                for (int u = 0; u < SP; ++u)
+#pragma unroll
+                    for (int s2 = 0; s2 < 2; ++s2) {
+                        outside |= check_seed && step == 0 && gp[u][s2] > kMemberTol;
+                        chord_update<SG>(gp[u][s2], hp[u][s2], cs[u % NCH][s2], ch[u % NCH][s2]);
+                    }
             }
         } else {
         double va[TPR][KC], vn[TPR][KC];
