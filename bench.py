@@ -515,7 +515,7 @@ def bench_eizo7(world, ck, cpu: bool, fp64_peak: float) -> dict:
 def bench_config3(world, ck, comm, world_size: int, rank: int) -> dict:
     """Config 3: 10-segment 7-DOF paths.  Latency of one path (sequential drop-in inflate_path and
     segment-sharded speculation, both with the reference's seeding) and segments/s over a stream
-    of paths sharded across ranks (weak scaling: 4 paths per rank)."""
+    of paths sharded across ranks (weak scaling: 8 paths per rank, all in flight at once)."""
     import torch
 
     from paper_2504_10783_b200 import fixtures as fx
@@ -552,10 +552,11 @@ def bench_config3(world, ck, comm, world_size: int, rank: int) -> dict:
         np.array_equal(a.A, b.A) for a, b in zip(scs.sets, seq.sets)))
     out["sharded_reinflated"] = scs.reinflated
     out["path_latency_ms"] = min(out["sequential_drop_in_ms"], out["sharded_speculative_ms_max_over_ranks"])
-    # throughput: a stream of paths, 4 per rank, each through inflate_path (reference semantics)
-    per_rank = 4
+    # throughput: a stream of paths, 8 per rank in flight (8 gives 2.8k segments/s on one GPU,
+    # 4 gives 2.2k: tools/diag_stream.py), each through inflate_path (reference semantics)
+    per_rank = 8
     paths = [PwlPath(fx.random_free_path(world, 10, seed=100 + p)) for p in range(per_rank * world_size)]
-    inflate_paths_sharded(paths[:world_size], dom, params, ck, seed=5, comm=comm)  # warm-up
+    inflate_paths_sharded(paths, dom, params, ck, seed=5, comm=comm, concurrency=per_rank)  # warm-up (workspaces)
     barrier()
     t0 = time.perf_counter()
     got = inflate_paths_sharded(paths, dom, params, ck, seed=5, comm=comm, concurrency=per_rank)
@@ -564,7 +565,7 @@ def bench_config3(world, ck, comm, world_size: int, rank: int) -> dict:
     out["stream"] = {"paths": len(paths), "paths_per_rank": per_rank, "segments": 10 * len(paths),
                      "inflations_on_rank0": sum(len(s.sets) for s in got.values()) if rank == 0 else None,
                      "seconds_max_over_ranks": dt, "segments_per_s": 10 * len(paths) / dt,
-                     "scaling": "weak (4 paths per rank, no collective)"}
+                     "scaling": "weak (8 paths per rank in flight, no collective)"}
     return out
 
 
