@@ -154,20 +154,24 @@ np.savez({path!r}, *out)
 
 
 def test_two_level_bisection_equals_one_step(tmp_path):
-    """k_bisect2 (two binary levels per round) against the one-step loop (EZ_BISECT1=1): same regions."""
+    """The bisection kernels against the one-step loop (`k_bisect`, EZ_BISECT1=1): `k_bisect2`
+    (two binary levels per round of 8-lane checks, EZ_BISECT_JIT=0) and, for the specialised
+    fp32 world, `ez_bisect_jit` (3-4 levels per round of single-thread checks, the default):
+    same regions."""
     import os, subprocess, sys
     from pathlib import Path
     root = str(Path(__file__).resolve().parents[1])
     res = []
-    for flag in ("0", "1"):
-        path = str(tmp_path / f"b{flag}.npz")
-        env = dict(os.environ, EZ_BISECT1=flag)
+    for flag, extra in (("1", {}), ("0", {"EZ_BISECT_JIT": "0"}), ("0", {})):
+        path = str(tmp_path / f"b{flag}{len(extra)}.npz")
+        env = dict(os.environ, EZ_BISECT1=flag, **extra)
         subprocess.run([sys.executable, "-c", _BISECT_CHILD.format(root=root, path=path)], env=env, check=True,
                        timeout=600)
         z = np.load(path)
         res.append([z[k] for k in sorted(z.files, key=lambda s: int(s.split("_")[1]))])
-    for a, b in zip(*res):
-        assert np.array_equal(a, b)
+    for other in res[1:]:
+        for a, b in zip(res[0], other):
+            assert np.array_equal(a, b)
 
 
 @pytest.mark.parametrize("which", ["franka7", "bimanual14"])
