@@ -53,7 +53,9 @@ __device__ __forceinline__ double project_point(const double (&c)[D], const doub
 // measured per region (7-DOF / 14-DOF): L = 2 473 us / 53.7 ms, L = 3 336 us
 // / 37.7 ms, L = 4 348 us / 30.8 ms (4 wins once the candidates fit in one
 // wave), against k_bisect2's 534 us / 24.0 ms: the 14-DOF model keeps
-// k_bisect2 (ez_eizo.cu launch_bisect).
+// k_bisect2 (ez_eizo.cu launch_bisect).  Each point runs the policy's full()
+// (one FK; a() then b() computed it three times for a free point): 7-DOF
+// 289 -> 234 us per region, 14-DOF 29.8 ms.
 //
 // L is chosen per launch from the device-side C: 4 when C * 16 threads fit in
 // `resident` (the GPU's resident threads for this kernel), else 3; forced_l in
@@ -112,7 +114,11 @@ __device__ __forceinline__ void bisect_points(const P& pol, const double* __rest
                 }
                 pt[k] = t == 0 ? a : 0.5 * (a + b);
             }
+#ifdef EZ_BISECT_AB
             fr = !pol.a(pt, static_cast<float*>(nullptr)) && !pol.b(pt, static_cast<float*>(nullptr));
+#else
+            fr = !pol.full(pt, static_cast<float*>(nullptr));  // one FK per point
+#endif
         }
         const unsigned bal = (__ballot_sync(gm, fr) >> sh) & kGroup;
         if (first) {

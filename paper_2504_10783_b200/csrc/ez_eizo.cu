@@ -1746,9 +1746,9 @@ static int32_t launch_bisect(ez_world* w, ez_eizo_ws* ws, int precision, cudaStr
     // fp32 checks on a specialised world with a light model: the bisection on
     // the model's own code, one thread per checked point (ez_bisect_core.cuh;
     // same points as k_bisect2).  A heavy model's single-thread check is too
-    // long a chain: the 14-DOF bisection (1,248 pairs) takes 24.0 ms per region
-    // in k_bisect2's 8-lane cooperative checks against 32.5 ms here (7-DOF:
-    // 534 -> 329 us).  EZ_BISECT_JIT=0 / 1 (read per call) forces either way.
+    // long a chain: the 14-DOF bisection (1,248 pairs) takes 24.1 ms per region
+    // in k_bisect2's 8-lane cooperative checks against 29.8 ms here (7-DOF:
+    // 534 -> 234 us).  EZ_BISECT_JIT=0 / 1 (read per call) forces either way.
     const char* bj = getenv("EZ_BISECT_JIT");
     const char* b1 = getenv("EZ_BISECT1");
     const bool use_jit = bj && (bj[0] == '0' || bj[0] == '1') ? bj[0] == '1' : w->n_pairs <= 600;

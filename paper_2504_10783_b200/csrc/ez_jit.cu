@@ -425,6 +425,7 @@ struct Gen {
     std::string source() {
         o << "// generated by ez_jit.cu for one robot model\n"
           << (getenv("EZ_JIT_NOPF") ? "#define EZ_CHECK_NO_PF 1\n" : "")
+          << (getenv("EZ_JIT_BISECT_AB") ? "#define EZ_BISECT_AB 1\n" : "")
           << "#include \"ez_check_core.cuh\"\n\nnamespace ez {\n\n"
           << "__device__ __forceinline__ float sq3(float dx, float dy, float dz) { return dx * dx + dy * dy + dz * dz; }\n"
           // an upper bound of sqrt(x): one MUFU.RSQ (ftz; x below 1e-30 bounds by 1e-15), raised by 2^-20
@@ -474,6 +475,17 @@ struct Gen {
             fk();
             obstacles(a_obst(), M.n_spheres);
         }
+        blocks();
+        walk_flush();
+        o << "    return false;\n    }\n";
+        // the whole check with one FK (the bisection's single-thread checks,
+        // which run at up to 128 registers: a() then b() computed the FK three
+        // times for a free configuration)
+        o << "    template <typename Q>\n    __device__ __forceinline__ bool full(const Q* row, float*) const {\n";
+        walk_queue();
+        fk();
+        hot();
+        obstacles(0, M.n_spheres);
         blocks();
         walk_flush();
         o << "    return false;\n    }\n};\n\n";
