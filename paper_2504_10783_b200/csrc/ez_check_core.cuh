@@ -162,6 +162,26 @@ __device__ __forceinline__ void check_tiles_reg(const P& pol, int dof, int32_t* 
     }
 }
 
+// Small batches (the EI-ZO loop's 10-15k samples): one row per thread, the
+// policy's full() check (one FK), no survivor queue.  The tile loop's phase B
+// recomputes the FK (twice in the streamed variant) and meets at barriers,
+// which costs latency when every thread has a single row.
+template <typename Q, class P>
+__device__ __forceinline__ void check_rows_full(const P& pol, int dof, const Q* __restrict__ q, int64_t n, int64_t ld,
+                                                uint8_t* __restrict__ out, int64_t count_lim,
+                                                int32_t* __restrict__ n_col) {
+    for (int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; r < n;
+         r += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        Q row[32];
+#pragma unroll
+        for (int k = 0; k < 32; ++k)
+            if (k < dof) row[k] = q[r * ld + k];
+        const bool col = pol.full(row, static_cast<float*>(nullptr));
+        out[r] = col ? 0 : 1;
+        if (n_col != nullptr && col && r < count_lim) atomicAdd(n_col, 1);
+    }
+}
+
 // rows: bt * dof staging slots in shared memory; s_queue: 2 * bt entries;
 // s_warp: bt / 32 entries; cen: this thread's centre store.  The CTA size bt
 // is BT, or blockDim.x for BT = 0 (one kernel launched at several sizes).

@@ -45,6 +45,16 @@
 namespace ez {
 namespace {
 
+// Batches up to this many rows on the small-CTA kernel run check_rows_full
+// (EZ_JIT_FULL_ROWS, 0 = never).
+long long full_rows() {
+    static const long long v = [] {
+        const char* e = getenv("EZ_JIT_FULL_ROWS");
+        return e ? atoll(e) : 32768LL;
+    }();
+    return v;
+}
+
 // The next tile's rows are prefetched into shared memory with cp.async
 // (check_tiles_reg's s_pf) for up to 8 joints (7-DOF: 78.9 -> 76.7 us per
 // 2^20); EZ_JIT_PFSM=0 prefetches into registers.  More joints prefetch
@@ -304,6 +314,14 @@ struct Gen {
              "        if (voxel_walk<float>(M.vox, wq_w[i], wq_e[i], wq_x[i], wq_y[i], wq_z[i], wq_r[i])) return true;\n";
     }
 
+    // full(): cells of this many spheres fetched together (its callers run at
+    // >= 128 registers with one row per thread, where the chain of grid-cell
+    // round trips is the latency; EZ_JIT_FULL_VOXB)
+    static int full_vox_batch() {
+        const char* e = getenv("EZ_JIT_FULL_VOXB");
+        const int v = e ? atoi(e) : 12;  // 7-DOF region: 8, 12, 16, 33 within noise (12 kept)
+        return (v >= 1 && v <= 64) ? v : 12;
+    }
     static int vox_batch() {
         const char* e = getenv("EZ_JIT_VOXB");
         const int v = e ? atoi(e) : kVoxBatch;
@@ -368,12 +386,13 @@ struct Gen {
 
     // spheres order[k_begin, k_end): static obstacles, then the voxel map
     // (cells of vox_batch() spheres fetched before any is decided)
-    void obstacles(int k_begin, int k_end) {
+    void obstacles(int k_begin, int k_end, int batch = 0) {
+        const int vb = batch > 0 ? batch : vox_batch();
         const int32_t* order = reinterpret_cast<const int32_t*>(blob + M.off_order);
         const bool vox = M.vox.present;
         const bool legacy = variant == 1;
-        for (int k0 = k_begin; k0 < k_end; k0 += vox_batch()) {
-            const int nb = std::min(vox_batch(), k_end - k0);
+        for (int k0 = k_begin; k0 < k_end; k0 += vb) {
+            const int nb = std::min(vb, k_end - k0);
             o << "    {\n";
             for (int j = 0; j < nb && vox; ++j) {
                 const int s = order[k0 + j];
@@ -485,7 +504,7 @@ struct Gen {
         walk_queue();
         fk();
         hot();
-        obstacles(0, M.n_spheres);
+        obstacles(0, M.n_spheres, full_vox_batch());
         blocks();
         walk_flush();
         o << "    return false;\n    }\n};\n\n";
@@ -495,6 +514,8 @@ struct Gen {
           << "    extern __shared__ __align__(16) uint8_t smem[];\n"
           << "    __shared__ int s_warp[32];\n"
           << "    const JitPolicy pol{M};\n"
+          << "    if (BT == 0 && n <= " << full_rows() << ") {  // small batch: one row per thread, one FK\n"
+          << "        check_rows_full<Q>(pol, " << M.dof << ", q, n, ld, out, count_lim, n_col);\n        return;\n    }\n"
           << "    check_tiles_reg<float, Q, BT>(pol, " << M.dof << ", reinterpret_cast<int32_t*>(smem), s_warp, "
           << (prefetch_sm(M.dof) ? "reinterpret_cast<Q*>(smem + 8 * (BT > 0 ? BT : blockDim.x))" : "static_cast<Q*>(nullptr)")
           << ", q, n, ld, out, count_lim, n_col);\n}\n\n"
