@@ -245,3 +245,21 @@ def test_specialised_flags_differ_only_inside_contact_band():
     if len(X):
         clr = ref.OracleChecker(w).clearance(X)
         assert np.abs(clr).max() < BAND
+
+
+@pytest.mark.parametrize("which", ["franka7", "bimanual14"])
+def test_small_batch_full_path_equals_generic(which):
+    """Batches up to 32k rows run one row per thread through the policy's full() (one FK, no
+    survivor queue): the generic kernel's flags exactly, for fp32 and fp64 rows and with the
+    EI-ZO loop's collision count."""
+    w = {"franka7": fx.franka7_world, "bimanual14": fx.bimanual14_world}[which]()
+    gen, jit = w.checker(specialize=False).native, w.checker(specialize=False).native
+    assert jit.specialize(1)
+    lo = torch.as_tensor(w.lower, dtype=torch.float32, device="cuda")
+    hi = torch.as_tensor(w.upper, dtype=torch.float32, device="cuda")
+    g = torch.Generator(device="cuda")
+    g.manual_seed(9)
+    for n in (1, 100, 10_000, 32_768):
+        Q = lo + (hi - lo) * torch.rand((n, w.model.dof), generator=g, device="cuda")
+        assert torch.equal(gen.check_device(Q), jit.check_device(Q))
+        assert torch.equal(gen.check_device(Q.double()), jit.check_device(Q.double()))
