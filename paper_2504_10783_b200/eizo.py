@@ -11,6 +11,7 @@ step back, batch size) are host helpers of the public API.
 from __future__ import annotations
 
 import ctypes as C
+import functools
 import math
 import threading
 from dataclasses import dataclass
@@ -188,7 +189,13 @@ def compute_step_back(a, b_raw: float, seg: Segment, delta_max: float) -> float:
 
 def default_bisection_steps(domain: HPolytope, delta_max: float) -> int:
     """ceil(log2(L / delta_max)) with L the domain box diagonal (inflation.py:219-229)."""
-    A, b = domain.A, domain.b
+    return _bisection_steps(domain.A.tobytes(), domain.b.tobytes(), domain.A.shape, float(delta_max))
+
+
+@functools.lru_cache(maxsize=64)
+def _bisection_steps(a_bytes: bytes, b_bytes: bytes, shape, delta_max: float) -> int:
+    A = np.frombuffer(a_bytes, dtype=float).reshape(shape)
+    b = np.frombuffer(b_bytes, dtype=float)
     with np.errstate(divide="ignore", invalid="ignore"):
         R = b[:, None] / A
     hi = np.where(A > 1e-12, R, np.inf).min(axis=0, initial=np.inf)
@@ -248,7 +255,7 @@ def inflate_edge(seg: Segment, domain: HPolytope, params: InflationParams, check
     with _CALLS_LOCK:  # inflations of several segments may run in threads
         checker.calls += int(rep.collision_checks)
     F = rep.n_faces
-    poly = HPolytope(A_out[:F], b_out[:F])
+    poly = HPolytope._from_unit_rows(A_out[:F], b_out[:F])  # the device normalised them (cpoly.py:32-38)
     return InflationReport(poly, rep.iterations, rep.hyperplanes_added, int(rep.collision_checks),
                            TERMINATED_ACCEPTED if rep.terminated_by == 0 else TERMINATED_MAX_ITER,
                            float(rep.device_ms))
