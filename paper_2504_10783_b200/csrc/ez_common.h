@@ -67,6 +67,23 @@ struct DeviceGuard {
 #define EZ_ON_DEVICE(dev)                                                    \
     ::ez::DeviceGuard _ez_dg(dev);                                           \
     EZ_CUDA(_ez_dg.err)
+
+// Allow a kernel the current device's whole opt-in dynamic shared memory.
+// Launch sizes differ by call (faces, candidates, models, grids) and calls run
+// on several host threads: setting the attribute to each launch's own size
+// let another thread lower it between that set and this launch.  The maximum
+// is the same for every caller, so concurrent sets agree.
+template <typename K>
+inline int32_t allow_max_dyn_smem(K kern) {
+    int dev = 0, optin = 0;
+    EZ_CUDA(cudaGetDevice(&dev));
+    EZ_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+    cudaFuncAttributes fa{};
+    EZ_CUDA(cudaFuncGetAttributes(&fa, reinterpret_cast<const void*>(kern)));
+    EZ_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(kern), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 optin - static_cast<int>(fa.sharedSizeBytes)));
+    return EZ_OK;
+}
 #endif
 
 // ---------------------------------------------------------------------------

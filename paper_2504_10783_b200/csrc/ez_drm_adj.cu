@@ -193,8 +193,7 @@ extern "C" int32_t ez_roadmap_adjacency(const double* d_nodes, int64_t n_nodes, 
         ck(cudaMallocAsync(&d_cnt, sizeof(unsigned long long), s), "alloc count") &&
         ck(cudaMallocAsync(&d_nuniq, sizeof(int64_t), s), "alloc count") &&
         ck(cudaMemsetAsync(d_cnt, 0, sizeof(unsigned long long), s), "memset") &&
-        ck(cudaFuncSetAttribute(k_knn_edges, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)),
-           "smem attribute")) {
+        (st = allow_max_dyn_smem(k_knn_edges)) == EZ_OK) {
         const unsigned grid = static_cast<unsigned>((n_nodes + kKnnWarps - 1) / kKnnWarps);
         k_knn_edges<<<grid, 32 * kKnnWarps, smem, s>>>(d_nodes, n_nodes, dof, d_ee, ee_dim, K, k, d_cs, d_ts, keys,
                                                        d_cnt);

@@ -196,8 +196,8 @@ extern "C" int32_t ez_roadmap_build(ez_world* w, const double* d_nodes, int64_t 
     while (warps > 1 && smem_for(warps) > 160 * 1024) warps /= 2;
     const size_t smem = smem_for(warps);
     if (smem > static_cast<size_t>(w->smem_optin) - 2048) return fail(EZ_CAPACITY, "roadmap grid bitmap exceeds shared memory");
-    EZ_CUDA(cudaFuncSetAttribute(k_node_voxels<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    EZ_CUDA(cudaFuncSetAttribute(k_node_voxels<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    EZ_TRY(allow_max_dyn_smem(k_node_voxels<false>));
+    EZ_TRY(allow_max_dyn_smem(k_node_voxels<true>));
     const unsigned grid = static_cast<unsigned>(std::min<int64_t>((n_nodes + warps - 1) / warps, 148 * 8));
     // temporaries come from the stream-ordered pool (kept mapped between builds)
     EZ_TRY(retain_async_pool());

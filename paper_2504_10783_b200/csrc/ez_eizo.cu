@@ -1557,7 +1557,7 @@ static int32_t launch_hnr_t(cudaStream_t s, const double* A, const double* b, co
     auto k = k_hnr<MAXD, RNG, LPW, BT>;
     const int lda = hnr_lda(d);
     const size_t smem = static_cast<size_t>(smem_faces) * (lda + 1) * sizeof(double);
-    if (smem > 48 * 1024) EZ_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    if (smem > 48 * 1024) EZ_TRY(allow_max_dyn_smem(k));
     const int64_t threads = count * LPW;
     const unsigned grid = static_cast<unsigned>((threads + BT - 1) / BT);
     k<<<grid, BT, smem, s>>>(A, b, F_dev, F, d, seeds, n_seeds, seg, count, n_ms, seed, walk_offset, out, status,
@@ -1730,7 +1730,7 @@ static int32_t launch_bisect_t(ez_world* w, ez_eizo_ws* ws, const ModelDev<T>& M
     auto kern = one_step ? k_bisect<T, MAXD, G> : k_bisect2<T, MAXD>;
     const int cpb = one_step ? CPB : 128 / 32;
     if (smem > static_cast<size_t>(w->smem_optin) - 1024) return fail(EZ_CAPACITY, "robot model too large for one bisection CTA");
-    if (smem > 48 * 1024) EZ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    if (smem > 48 * 1024) EZ_TRY(allow_max_dyn_smem(kern));
     kern<<<static_cast<unsigned>((n_p + cpb - 1) / cpb), 128, smem, s>>>(M, static_cast<T>(w->margin), ws->X, d, ws->col,
                                                                      ws->rec, it, ws->seg, ee, n_b, t_col, ws->star,
                                                                      ws->pstar, ws->dstar);
@@ -1861,13 +1861,11 @@ extern "C" int32_t ez_inflate_edge(ez_world* w, const double* h_v1, const double
     const int place_dcap = place_dist_cap(p.n_p);
     const size_t place_smem = place_smem_bytes(p.n_p, place_dcap);
     if (place_smem > 48 * 1024)
-        EZ_CUDA(cudaFuncSetAttribute(k_place, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(place_smem)));
+        EZ_TRY(allow_max_dyn_smem(k_place));
     // the cluster placement when a CTA's share of the anchors fits in shared memory
     const size_t place_cl_smem = place_cl_smem_bytes(p.n_p, d);
     const bool place_cl = place_cl_smem <= 200 * 1024 && !getenv("EZ_PLACE_1CTA");
-    if (place_cl && place_cl_smem > 48 * 1024)
-        EZ_CUDA(cudaFuncSetAttribute(k_place_cl, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     static_cast<int>(place_cl_smem)));
+    if (place_cl && place_cl_smem > 48 * 1024) EZ_TRY(allow_max_dyn_smem(k_place_cl));
 
     // One iteration = hit-and-run, check (+ first-M count), compaction/test,
     // bisection, placement, and a 128-byte record copy.  Iteration k+1 is
@@ -2069,7 +2067,7 @@ extern "C" int32_t ez_refine_set(ez_world* w, const double* h_v1, const double* 
     const int place_dcap = place_dist_cap(static_cast<int>(n_cols));
     const size_t place_smem = place_smem_bytes(static_cast<int>(n_cols), place_dcap);
     if (place_smem > 48 * 1024)
-        EZ_CUDA(cudaFuncSetAttribute(k_place, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(place_smem)));
+        EZ_TRY(allow_max_dyn_smem(k_place));
     k_place<<<1, 1024, place_smem, s>>>(ws->A, ws->b, ws->rec, ws->rec + slot_offset(0), d, ws->star, ws->pstar,
                                         ws->dstar, ws->seg, delta_max, n_cols, ws->X, place_dcap);
     EZ_CUDA(cudaGetLastError());

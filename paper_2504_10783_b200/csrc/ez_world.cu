@@ -776,7 +776,7 @@ static int32_t calibrate_layout(ez_world* w, HModel& hm, const double* lower, co
     const int threads = check_block_threads<float>(w, w->mf.blob_bytes, w->mf.cen_words, dof * 4, &smem);
     if (threads == 0) return fail(EZ_CAPACITY, "robot model too large for one checking CTA");
     if (smem > 48 * 1024)
-        EZ_CUDA(cudaFuncSetAttribute(k_calibrate, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+        EZ_TRY(allow_max_dyn_smem(k_calibrate));
     k_calibrate<<<(n + threads - 1) / threads, threads, smem>>>(w->mf, d_lh, d_lh + dof, n, 0x5EEDC0DEull,
                                                                 static_cast<float>(w->margin), d_cnt, d_cnt + np);
     EZ_CUDA(cudaGetLastError());
