@@ -909,6 +909,15 @@ int32_t jit_specialize(ez_world* w) {
 // drops to the largest size that does, down to 64 threads.
 int32_t jit_launch(ez_world* w, const JitCheck& jc, const void* d_q, bool q64, int64_t n, int64_t ld, uint8_t* d_free,
                    cudaStream_t stream, int64_t count_lim, int32_t* n_col) {
+    // the survivor queue holds int32 row indices: launches of at most 2^30 rows
+    const int64_t kMaxRows = int64_t(1) << 30;
+    if (n > kMaxRows) {
+        const size_t es = q64 ? sizeof(double) : sizeof(float);
+        for (int64_t r0 = 0; r0 < n; r0 += kMaxRows)
+            EZ_TRY(jit_launch(w, jc, static_cast<const char*>(d_q) + r0 * ld * es, q64, std::min(kMaxRows, n - r0), ld,
+                              d_free + r0, stream, count_lim - r0, n_col));
+        return EZ_OK;
+    }
     int bt = 64;
     for (int si = kJitSizeCount - 1; si >= 0; --si) {
         const int cand = kJitSizes[si];

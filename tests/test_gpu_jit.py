@@ -263,3 +263,22 @@ def test_small_batch_full_path_equals_generic(which):
         Q = lo + (hi - lo) * torch.rand((n, w.model.dof), generator=g, device="cuda")
         assert torch.equal(gen.check_device(Q), jit.check_device(Q))
         assert torch.equal(gen.check_device(Q.double()), jit.check_device(Q.double()))
+
+
+def test_batch_beyond_int32_queue_indices():
+    """A device batch of 2^31 + 4096 rows (60 GB of fp32 rows; row indices past int32) runs as
+    launches of at most 2^30 rows (the survivor queue holds int32 row indices): the rows on both
+    sides of every split get the flags a small batch of the same rows gets."""
+    w = fx.franka7_world()
+    nat = w.checker().native
+    n = (1 << 31) + 4096
+    lo = torch.as_tensor(w.lower, dtype=torch.float32, device="cuda")
+    hi = torch.as_tensor(w.upper, dtype=torch.float32, device="cuda")
+    Q = torch.empty((n, 7), dtype=torch.float32, device="cuda")
+    Q.uniform_()
+    Q.mul_(hi - lo).add_(lo)
+    flags = nat.check_device(Q)
+    for a, b in ((0, 4096), ((1 << 30) - 4096, (1 << 30) + 4096), ((1 << 31) - 4096, n)):
+        assert torch.equal(flags[a:b], nat.check_device(Q[a:b].clone()))
+    del Q, flags
+    torch.cuda.empty_cache()
