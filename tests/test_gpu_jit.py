@@ -66,9 +66,10 @@ def test_robot_boxes_stay_generic():
     assert not ck.native.specialize(0)
 
 
-def test_specialisation_only_at_world_creation():
+def test_specialisation_only_at_world_creation(monkeypatch):
     """no NVRTC compile or CTA-size tuning inside a check call.  Large robots get the
     specialised kernel when their device world is created ("auto"); specialize=False never."""
+    monkeypatch.delenv("EZ_JIT", raising=False)  # the default behaviour ("auto" on)
     w = fx.franka7_world()
     assert w.checker().native.specialize(0)
     assert w.checker().native.info()["check_cta"] in (256, 512, 1024)
